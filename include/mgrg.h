@@ -1,0 +1,156 @@
+/*
+ * mgrg.h -- C ABI of the B200-native multigrid refactoring path.
+ *
+ * This is the binary drop-in boundary under the reference's C++ entry points
+ * (/root/reference/proj/include/mgr/refactor.hpp).  The reference's public
+ * API is header-only templates, so the source-level drop-in is
+ * include/mgr_b200/refactor.hpp (namespace mgr, same names/types), which calls
+ * the functions below; ctypes / cgo-style bindings call them directly.
+ *
+ * Layout conventions (identical to the reference):
+ *   - values: row-major, dimension 0 fastest (ndarray.hpp:16-26);
+ *   - classes: ONE buffer of N elements; class 0 (coarsest nodal values,
+ *     packed row-major) at offset 0, class l (level-l coefficients in class
+ *     order, grid.hpp:136-164) at offset N_{l-1} = number of level-(l-1)
+ *     nodes.  This equals the concatenation of RefactoredData::classes
+ *     (refactor.hpp:18-32) and the MGRF payload order (pipeline.cpp:197-200);
+ *   - coords: NULL for uniform coordinates i/(n-1) (grid.cpp:7-12), else the
+ *     per-dimension coordinate arrays concatenated, dimension 0 first.
+ *
+ * Numerics: every kernel evaluates the reference's expressions in the same
+ * order with IEEE round-to-nearest and no FMA contraction, so classes and
+ * reconstructions are bit-identical to the reference CPU path.
+ *
+ * Threading: a plan owns its device workspace and must not be used by two
+ * calls concurrently; distinct plans are independent.  The last
+ * error message is thread-local.
+ *
+ * Errors: every function returns an mgrg_status; the codes map 1:1 onto the
+ * reference's exception types (errors.hpp:27-37).
+ */
+#ifndef MGRG_H
+#define MGRG_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum mgrg_status {
+  MGRG_OK = 0,
+  MGRG_INVALID_GRID = 1,      /* mgr::InvalidGrid    (grid.cpp:17-34)        */
+  MGRG_INVALID_LEVEL = 2,     /* mgr::InvalidLevel   (refactor.hpp:480-482)  */
+  MGRG_SHAPE_ERROR = 3,       /* mgr::ShapeError     (grid.hpp:44-47)        */
+  MGRG_INVALID_FUSION = 4,    /* mgr::InvalidFusion  (kernels.hpp:337-338)   */
+  MGRG_SINGULAR_SYSTEM = 5,   /* mgr::SingularSystem (kernels.hpp:121-131)   */
+  MGRG_TOO_MANY_WORKERS = 6,  /* mgr::TooManyWorkers                         */
+  MGRG_WORKER_FAILURE = 7,    /* mgr::WorkerFailure  (parallel_impl.hpp:845) */
+  MGRG_CORRUPT_FILE = 8,      /* mgr::CorruptFile                            */
+  MGRG_MISSING_CLASS = 9,     /* mgr::MissingClass   (refactor.hpp:483-485)  */
+  MGRG_INVALID_BOUND = 10,    /* mgr::InvalidBound                           */
+  MGRG_IO_ERROR = 11,         /* mgr::IoError                                */
+  MGRG_CUDA_ERROR = 12,       /* device failure (no reference equivalent)   */
+  MGRG_NCCL_ERROR = 13,       /* collective failure                          */
+  MGRG_UNSUPPORTED = 14,      /* e.g. 4-D grids (spatiotemporal, out of scope)*/
+  MGRG_INVALID_ARGUMENT = 15, /* null pointer, bad dtype, ...                */
+  MGRG_OUT_OF_MEMORY = 16
+} mgrg_status;
+
+typedef enum mgrg_dtype { MGRG_F32 = 4, MGRG_F64 = 8 } mgrg_dtype;
+
+/* Grid description: TensorGrid minus the values (grid.hpp:19-26) plus
+ * RefactorOptions::levels (refactor.hpp:71-76). */
+typedef struct mgrg_grid_desc {
+  int32_t ndims;         /* 1..3 (the reference allows 4; see MGRG_UNSUPPORTED) */
+  int32_t dtype;         /* mgrg_dtype */
+  uint64_t shape[4];     /* finest-level extents, dim 0 fastest */
+  const double *coords;  /* NULL = uniform; else sum(shape) doubles */
+  int32_t levels;        /* 0 = full depth, else the RefactorOptions cap */
+  int32_t device;        /* CUDA device ordinal the plan lives on */
+} mgrg_grid_desc;
+
+typedef struct mgrg_plan mgrg_plan;
+
+/* Plan = build_hierarchy (grid.cpp:78-112) with min_extent 2 as decompose
+ * validates it (refactor.hpp:465-466), per-level class layouts
+ * (grid.cpp:140-165), Thomas factors built in the working precision
+ * (kernels.hpp:107-135), geometry uploaded to the device, and the device
+ * workspace (about N/4 elements).  All allocation happens here. */
+mgrg_status mgrg_plan_create(const mgrg_grid_desc *desc, mgrg_plan **plan);
+mgrg_status mgrg_plan_destroy(mgrg_plan *plan);
+
+/* Hierarchy depth L (RefactoredData::levels). */
+mgrg_status mgrg_plan_levels(const mgrg_plan *plan, int32_t *levels);
+/* offsets[0..L+1]: class l occupies [offsets[l], offsets[l+1]); offsets[0]=0,
+ * offsets[L+1] = N. */
+mgrg_status mgrg_plan_class_offsets(const mgrg_plan *plan, uint64_t *offsets);
+/* Level-l extents, ndims entries (GridHierarchy::level_shape). */
+mgrg_status mgrg_plan_level_shape(const mgrg_plan *plan, int32_t level,
+                                  uint64_t *extents);
+/* Total element count N and device workspace bytes owned by the plan. */
+mgrg_status mgrg_plan_sizes(const mgrg_plan *plan, uint64_t *num_elements,
+                            uint64_t *workspace_bytes);
+
+/* ---- whole-path entry points (device buffers) --------------------------
+ * mgr::decompose (refactor.hpp:462-474): d_values (N elements, not
+ * modified) -> d_classes (N elements, class layout above).  Asynchronous on
+ * `stream` (a cudaStream_t; NULL = legacy default stream). */
+mgrg_status mgrg_decompose(mgrg_plan *plan, const void *d_values,
+                           void *d_classes, void *stream);
+
+/* mgr::recompose (refactor.hpp:476-496): classes 0..classes_used are read,
+ * classes above it are treated as zero (never read).  classes_used > L ->
+ * MGRG_INVALID_LEVEL. */
+mgrg_status mgrg_recompose(mgrg_plan *plan, const void *d_classes,
+                           int32_t classes_used, void *d_values, void *stream);
+
+/* ---- host-buffer entry points (what the reference's callers pass) -------
+ * Same semantics; host -> device copy, the device path, device -> host copy,
+ * synchronous.  Pinned host memory gives full PCIe bandwidth. */
+mgrg_status mgrg_decompose_host(mgrg_plan *plan, const void *h_values,
+                                void *h_classes);
+mgrg_status mgrg_recompose_host(mgrg_plan *plan, const void *h_classes,
+                                int32_t classes_used, void *h_values);
+
+/* ---- unit-level kernels (kernels.hpp), device buffers, for parity ---------
+ * compute_coefficients / restore_coefficients (kernels.hpp:284-310): in place
+ * on a packed level-`level` array. */
+mgrg_status mgrg_gpk(mgrg_plan *plan, int32_t level, int32_t inverse,
+                     void *d_level_values, void *stream);
+/* masstrans_apply (kernels.hpp:328-412): input extents
+ * masstrans_input_shape(level, dim) (kernels.hpp:314-320), output the same
+ * with `dim` reduced; fused_copy (dim 0 only, else MGRG_INVALID_FUSION) also
+ * writes the level's class (class order) into d_coef. */
+mgrg_status mgrg_masstrans(mgrg_plan *plan, int32_t level, int32_t dim,
+                           const void *d_in, void *d_out, int32_t fused_copy,
+                           void *d_coef, void *stream);
+/* solve_correction (kernels.hpp:417-448): in place on the level-(l-1)
+ * lattice; identity when `dim` does not refine. */
+mgrg_status mgrg_solve(mgrg_plan *plan, int32_t level, int32_t dim, void *d_f,
+                       void *stream);
+/* apply_correction (kernels.hpp:451-464): values += sign * z. */
+mgrg_status mgrg_apply_correction(mgrg_plan *plan, uint64_t count,
+                                  void *d_values, const void *d_z, int32_t sign,
+                                  void *stream);
+/* reorder (grid.hpp:177-196) of one packed level-`level` array: direction 0 =
+ * to_hierarchical (coarse nodes first, then class order), 1 = to_natural. */
+mgrg_status mgrg_reorder(mgrg_plan *plan, int32_t level, int32_t direction,
+                         const void *d_in, void *d_out, void *stream);
+
+/* ---- diagnostics ------------------------------------------------------- */
+/* Thread-local message of the last failing call ("" if none). */
+const char *mgrg_last_error(void);
+/* Status name as the reference spells the exception ("InvalidGrid", ...). */
+const char *mgrg_status_name(mgrg_status status);
+/* Kernel launches the last decompose/recompose issued on this plan. */
+mgrg_status mgrg_plan_last_launches(const mgrg_plan *plan, uint64_t *launches);
+/* Library version string. */
+const char *mgrg_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* MGRG_H */

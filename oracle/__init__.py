@@ -1,0 +1,287 @@
+"""CPU oracle for the decompose/recompose path -- TEST INFRASTRUCTURE ONLY.
+
+Only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline / reference
+legs may import this package, and only as the checker (never as the thing
+measured or shipped).  The product (paper_2105_12764_b200) never imports it.
+
+Two CPU implementations behind one numpy interface:
+
+* ``impl="oracle"``: oracle/libmgr_oracle.so, the plain-C restatement
+  (mgr_oracle.c / mgr_oracle_engine.inc, each function citing the reference
+  file:line it restates);
+* ``impl="ref"``: oracle/_ref/libmgr_ref.so, the UNMODIFIED reference
+  (/root/reference/proj) compiled from its own sources by oracle/Makefile.
+  Present wherever ``make -C oracle`` ran with /root/reference mounted (the
+  built .so travels to the GPU box with the repo snapshot).
+
+Parity pinned: tests/test_oracle.py asserts the restatement is bit-identical
+to the reference on every case and matches the reference tests' golden
+vectors (tests/golden/).
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+ORACLE_SO = os.path.join(_HERE, "libmgr_oracle.so")
+REF_SO = os.path.join(_HERE, "_ref", "libmgr_ref.so")
+
+_libs: dict[str, ctypes.CDLL] = {}
+
+
+class OracleError(RuntimeError):
+    def __init__(self, code: int, what: str):
+        super().__init__(f"{what}: status {code}")
+        self.code = code
+
+
+def build(quiet: bool = True) -> None:
+    """Compile the oracle (and oracle/_ref when /root/reference exists)."""
+    import subprocess
+
+    subprocess.run(["make", "-C", _HERE, "-s"], check=True,
+                   stdout=subprocess.DEVNULL if quiet else None)
+
+
+def available(impl: str = "oracle") -> bool:
+    return os.path.exists(ORACLE_SO if impl == "oracle" else REF_SO)
+
+
+def _lib(impl: str) -> ctypes.CDLL:
+    if impl not in _libs:
+        path = ORACLE_SO if impl == "oracle" else REF_SO
+        if not os.path.exists(path):
+            raise FileNotFoundError(f"{path} not built (make -C oracle)")
+        _libs[impl] = ctypes.CDLL(path)
+    return _libs[impl]
+
+
+def _prefix(impl: str) -> str:
+    return "mgro_" if impl == "oracle" else "mgrref_"
+
+
+def _sfx(dtype) -> str:
+    dt = np.dtype(dtype)
+    if dt == np.float64:
+        return "f64"
+    if dt == np.float32:
+        return "f32"
+    raise TypeError(f"unsupported dtype {dt}")
+
+
+def _shape_arr(shape):
+    return (ctypes.c_uint64 * len(shape))(*[int(s) for s in shape])
+
+
+def _coords_arr(shape, coords):
+    if coords is None:
+        return None, None
+    flat = np.ascontiguousarray(np.concatenate([np.asarray(c, dtype=np.float64)
+                                                for c in coords]))
+    if flat.size != sum(int(s) for s in shape):
+        raise OracleError(1, "coordinate arrays do not match the shape")
+    return flat, flat.ctypes.data_as(ctypes.c_void_p)
+
+
+def _ptr(a: np.ndarray):
+    return a.ctypes.data_as(ctypes.c_void_p)
+
+
+def _check(st: int, what: str) -> None:
+    if st != 0:
+        raise OracleError(st, what)
+
+
+def hierarchy(shape, coords=None, levels_cap: int = 0, min_extent: int = 2):
+    """(L, extents[L+1][ndims]) of build_hierarchy (grid.cpp:78-112)."""
+    lib = _lib("oracle")
+    nd = len(shape)
+    ext = (ctypes.c_uint64 * (65 * nd))()
+    lv = ctypes.c_int()
+    keep, cp = _coords_arr(shape, coords)
+    lib.mgro_hierarchy.argtypes = [ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p,
+                                   ctypes.c_int, ctypes.c_int,
+                                   ctypes.POINTER(ctypes.c_int), ctypes.c_void_p]
+    _check(lib.mgro_hierarchy(nd, _shape_arr(shape), cp, levels_cap, min_extent,
+                              ctypes.byref(lv), ext), "hierarchy")
+    L = lv.value
+    return L, [[int(ext[l * nd + d]) for d in range(nd)] for l in range(L + 1)]
+
+
+def class_offsets(shape, levels: int):
+    """offsets[0..L+1]: class l starts at offsets[l] = N_{l-1}."""
+    lib = _lib("oracle")
+    off = (ctypes.c_uint64 * (levels + 2))()
+    lib.mgro_class_offsets.argtypes = [ctypes.c_int, ctypes.c_void_p, ctypes.c_int,
+                                       ctypes.c_void_p]
+    _check(lib.mgro_class_offsets(len(shape), _shape_arr(shape), levels, off),
+           "class_offsets")
+    return [int(x) for x in off]
+
+
+def class_layout(shape, levels: int, level: int):
+    lib = _lib("oracle")
+    nd = len(shape)
+    base = (ctypes.c_uint64 * (1 << nd))()
+    ext = (ctypes.c_uint64 * ((1 << nd) * nd))()
+    lib.mgro_class_layout.argtypes = [ctypes.c_int, ctypes.c_void_p, ctypes.c_int,
+                                      ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p]
+    _check(lib.mgro_class_layout(nd, _shape_arr(shape), levels, level, base, ext),
+           "class_layout")
+    return ([int(b) for b in base],
+            [[int(ext[m * nd + d]) for d in range(nd)] for m in range(1 << nd)])
+
+
+def decompose(values: np.ndarray, shape, coords=None, levels_cap: int = 0,
+              impl: str = "oracle"):
+    """mgr::decompose (refactor.hpp:462-474).  Returns (classes, L) with all
+    classes in one flat array, class l at offset N_{l-1}."""
+    lib = _lib(impl)
+    values = np.ascontiguousarray(values)
+    out = np.empty(values.size, dtype=values.dtype)
+    fn = getattr(lib, _prefix(impl) + "decompose_" + _sfx(values.dtype))
+    fn.argtypes = [ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int,
+                   ctypes.c_void_p, ctypes.c_void_p, ctypes.POINTER(ctypes.c_int)]
+    keep, cp = _coords_arr(shape, coords)
+    lv = ctypes.c_int()
+    _check(fn(len(shape), _shape_arr(shape), cp, levels_cap, _ptr(values),
+              _ptr(out), ctypes.byref(lv)), "decompose")
+    return out, lv.value
+
+
+def recompose(classes: np.ndarray, shape, levels: int, classes_used: int,
+              coords=None, impl: str = "oracle") -> np.ndarray:
+    """mgr::recompose (refactor.hpp:476-496) from the flat class buffer."""
+    lib = _lib(impl)
+    classes = np.ascontiguousarray(classes)
+    out = np.empty(classes.size, dtype=classes.dtype)
+    fn = getattr(lib, _prefix(impl) + "recompose_" + _sfx(classes.dtype))
+    fn.argtypes = [ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int,
+                   ctypes.c_void_p, ctypes.c_int, ctypes.c_void_p]
+    keep, cp = _coords_arr(shape, coords)
+    _check(fn(len(shape), _shape_arr(shape), cp, levels, _ptr(classes),
+              classes_used, _ptr(out)), "recompose")
+    return out
+
+
+def gpk(values: np.ndarray, shape, level: int, inverse: bool = False,
+        coords=None, levels_cap: int = 0, impl: str = "oracle") -> np.ndarray:
+    """compute_coefficients / restore_coefficients (kernels.hpp:284-310) on a
+    packed level array; returns a new array."""
+    lib = _lib(impl)
+    v = np.array(values, copy=True, order="C")
+    fn = getattr(lib, _prefix(impl) + "gpk_" + _sfx(v.dtype))
+    fn.argtypes = [ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int,
+                   ctypes.c_int, ctypes.c_int, ctypes.c_void_p]
+    keep, cp = _coords_arr(shape, coords)
+    _check(fn(len(shape), _shape_arr(shape), cp, levels_cap, level, int(inverse),
+              _ptr(v)), "gpk")
+    return v
+
+
+def masstrans(inp: np.ndarray, shape, level: int, dim: int, out_size: int,
+              fused_copy: bool = False, class_size: int = 0, coords=None,
+              levels_cap: int = 0, impl: str = "oracle"):
+    """masstrans_apply (kernels.hpp:328-412); returns (out, coef_out|None)."""
+    lib = _lib(impl)
+    inp = np.ascontiguousarray(inp)
+    out = np.empty(out_size, dtype=inp.dtype)
+    coef = np.zeros(class_size, dtype=inp.dtype) if fused_copy else None
+    fn = getattr(lib, _prefix(impl) + "masstrans_" + _sfx(inp.dtype))
+    fn.argtypes = [ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int,
+                   ctypes.c_int, ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p,
+                   ctypes.c_int, ctypes.c_void_p]
+    keep, cp = _coords_arr(shape, coords)
+    _check(fn(len(shape), _shape_arr(shape), cp, levels_cap, level, dim, _ptr(inp),
+              _ptr(out), int(fused_copy), _ptr(coef) if coef is not None else None),
+           "masstrans")
+    return out, coef
+
+
+def solve(f: np.ndarray, shape, level: int, dim: int, coords=None,
+          levels_cap: int = 0, impl: str = "oracle") -> np.ndarray:
+    """solve_correction (kernels.hpp:417-448) on the level-(l-1) lattice."""
+    lib = _lib(impl)
+    v = np.array(f, copy=True, order="C")
+    fn = getattr(lib, _prefix(impl) + "solve_" + _sfx(v.dtype))
+    fn.argtypes = [ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int,
+                   ctypes.c_int, ctypes.c_int, ctypes.c_void_p]
+    keep, cp = _coords_arr(shape, coords)
+    _check(fn(len(shape), _shape_arr(shape), cp, levels_cap, level, dim, _ptr(v)),
+           "solve")
+    return v
+
+
+def reorder(values: np.ndarray, shape, level: int, to_natural: bool = False,
+            coords=None, levels_cap: int = 0) -> np.ndarray:
+    """reorder (grid.hpp:177-196), f64."""
+    lib = _lib("oracle")
+    v = np.ascontiguousarray(values, dtype=np.float64)
+    out = np.empty_like(v)
+    lib.mgro_reorder_f64.argtypes = [ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p,
+                                     ctypes.c_int, ctypes.c_int, ctypes.c_int,
+                                     ctypes.c_void_p, ctypes.c_void_p]
+    keep, cp = _coords_arr(shape, coords)
+    _check(lib.mgro_reorder_f64(len(shape), _shape_arr(shape), cp, levels_cap, level,
+                                int(to_natural), _ptr(v), _ptr(out)), "reorder")
+    return out
+
+
+def embarrassing_roundtrip_f32(values: np.ndarray, shape, nblocks: int,
+                               workers: int):
+    """Reference embarrassing_decompose (parallel_impl.hpp:810-847) + threaded
+    recompose of nblocks independent blocks; returns (t_dec, t_rec) seconds."""
+    lib = _lib("ref")
+    v = np.ascontiguousarray(values, dtype=np.float32)
+    fn = lib.mgrref_embarrassing_roundtrip_f32
+    fn.argtypes = [ctypes.c_int, ctypes.c_void_p, ctypes.c_int, ctypes.c_int,
+                   ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
+                   ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_double)]
+    td, tr = ctypes.c_double(), ctypes.c_double()
+    _check(fn(len(shape), _shape_arr(shape), nblocks, workers, _ptr(v), None, None,
+              ctypes.byref(td), ctypes.byref(tr)), "embarrassing_roundtrip")
+    return td.value, tr.value
+
+
+# ---- deterministic data (tests/oracle.cpp:167-186, acceptance.cpp:383-393) --
+
+def smooth_field(shape, coords=None) -> np.ndarray:
+    """The reference's smooth test field S(x) evaluated in fp64 on the grid
+    (acceptance.cpp:383-393; 2-D drops z, 1-D drops y,z)."""
+    axes = []
+    for d, n in enumerate(shape):
+        axes.append(np.asarray(coords[d], dtype=np.float64) if coords is not None
+                    else np.arange(n, dtype=np.float64) / (n - 1))
+    c1 = (0.35, 0.4, 0.45)
+    c2 = (0.7, 0.65, 0.6)
+    # arrays indexed [..., x] with x fastest -> reverse axis order for meshgrid
+    grids = np.meshgrid(*axes[::-1], indexing="ij")[::-1]
+    r1 = sum((g - c1[d]) ** 2 for d, g in enumerate(grids))
+    r2 = sum((g - c2[d]) ** 2 for d, g in enumerate(grids))
+    s = np.ones_like(grids[0])
+    for g in grids:
+        s = s * np.sin(2 * np.pi * g)
+    return (np.exp(-30 * r1) + 0.6 * np.exp(-25 * r2) + 0.2 * s).reshape(-1)
+
+
+def ref_random_vector(n: int, seed: int, lo: float = 0.0, hi: float = 1.0):
+    """oracle::random_vector of the reference tests (tests/oracle.cpp:167-174)."""
+    lib = _lib("ref")
+    out = np.empty(n, dtype=np.float64)
+    lib.mgrref_random_vector.argtypes = [ctypes.c_uint64, ctypes.c_uint, ctypes.c_double,
+                                         ctypes.c_double, ctypes.c_void_p]
+    lib.mgrref_random_vector(n, seed, lo, hi, _ptr(out))
+    return out
+
+
+def ref_random_increasing_coords(n: int, seed: int):
+    """oracle::random_increasing_coords (tests/oracle.cpp:176-186)."""
+    lib = _lib("ref")
+    out = np.empty(n, dtype=np.float64)
+    lib.mgrref_random_increasing_coords.argtypes = [ctypes.c_uint64, ctypes.c_uint,
+                                                    ctypes.c_void_p]
+    lib.mgrref_random_increasing_coords(n, seed, _ptr(out))
+    return out

@@ -1,0 +1,293 @@
+// ref_harness.cpp -- C ABI around the UNMODIFIED reference implementation
+// (TEST INFRASTRUCTURE).  Compiled by oracle/Makefile together with
+// /root/reference/proj/src/grid.cpp and refactor.cpp (read in place, never
+// copied) into oracle/_ref/libmgr_ref.so, with the reference's own flags
+// (-std=gnu++20 -O3 -DNDEBUG, no -march: no FMA contraction).  Used to pin
+// the C restatement (mgr_oracle.c) and as bench.py's reference arm.
+//
+// Same argument conventions and status codes as mgr_oracle.h.
+#include <cstdint>
+#include <cstring>
+#include <exception>
+#include <optional>
+#include <thread>
+#include <vector>
+
+#include "mgr/parallel.hpp"
+#include "mgr/refactor.hpp"
+#include "oracle.hpp" // reference tests/oracle.hpp: deterministic data helpers
+
+namespace {
+
+int code_of(const mgr::Error &e) {
+  static const char *names[] = {"",           "InvalidGrid",   "InvalidLevel",
+                                "ShapeError", "InvalidFusion", "SingularSystem",
+                                "TooManyWorkers", "WorkerFailure", "CorruptFile",
+                                "MissingClass", "InvalidBound",  "IoError"};
+  for (int i = 1; i < 12; ++i)
+    if (e.code() == names[i])
+      return i;
+  return 15;
+}
+
+mgr::Shape to_shape(int nd, const uint64_t *shape) {
+  return mgr::Shape(shape, shape + nd);
+}
+
+std::vector<std::vector<double>> to_coords(int nd, const uint64_t *shape,
+                                           const double *coords) {
+  std::vector<std::vector<double>> c;
+  for (int d = 0; d < nd; ++d) {
+    if (coords) {
+      c.emplace_back(coords, coords + shape[d]);
+      coords += shape[d];
+    } else {
+      c.push_back(mgr::uniform_coords(shape[d]));
+    }
+  }
+  return c;
+}
+
+template <typename Real>
+int decompose_impl(int nd, const uint64_t *shape, const double *coords,
+                   int levels_cap, const Real *values, Real *classes,
+                   int *levels_out) {
+  try {
+    mgr::TensorGrid<Real> g;
+    g.shape = to_shape(nd, shape);
+    g.coords = to_coords(nd, shape, coords);
+    g.values.assign(values, values + mgr::num_elements(g.shape));
+    mgr::RefactorOptions opt;
+    if (levels_cap > 0)
+      opt.levels = std::size_t(levels_cap);
+    const auto r = mgr::decompose(g, opt);
+    std::size_t off = 0;
+    for (const auto &c : r.classes) {
+      std::memcpy(classes + off, c.data(), c.size() * sizeof(Real));
+      off += c.size();
+    }
+    if (levels_out)
+      *levels_out = int(r.levels);
+    return 0;
+  } catch (const mgr::Error &e) {
+    return code_of(e);
+  } catch (...) {
+    return 15;
+  }
+}
+
+template <typename Real>
+int recompose_impl(int nd, const uint64_t *shape, const double *coords,
+                   int levels, const Real *classes, int k, Real *values) {
+  try {
+    mgr::RefactoredData<Real> r;
+    r.shape = to_shape(nd, shape);
+    r.coords = to_coords(nd, shape, coords);
+    r.levels = std::size_t(levels);
+    const auto hier = mgr::build_hierarchy(r.shape, r.coords,
+                                           std::optional<std::size_t>(levels), 2);
+    std::size_t off = 0;
+    for (std::size_t l = 0; l <= r.levels; ++l) {
+      const std::size_t sz =
+          l == 0 ? hier.num_nodes(0) : hier.num_nodes(l) - hier.num_nodes(l - 1);
+      r.classes.emplace_back(classes + off, classes + off + sz);
+      off += sz;
+    }
+    if (k < 0)
+      return 2;
+    const auto g = mgr::recompose(r, std::size_t(k));
+    std::memcpy(values, g.values.data(), g.values.size() * sizeof(Real));
+    return 0;
+  } catch (const mgr::Error &e) {
+    return code_of(e);
+  } catch (...) {
+    return 15;
+  }
+}
+
+template <typename Real>
+int gpk_impl(int nd, const uint64_t *shape, const double *coords, int cap,
+             int level, int inverse, Real *values) {
+  try {
+    std::optional<std::size_t> lv;
+    if (cap > 0)
+      lv = std::size_t(cap);
+    const auto hier =
+        mgr::build_hierarchy(to_shape(nd, shape), to_coords(nd, shape, coords), lv);
+    const std::size_t n = hier.num_nodes(std::size_t(level));
+    std::span<Real> s(values, n);
+    if (inverse)
+      mgr::restore_coefficients<Real>(s, hier, std::size_t(level));
+    else
+      mgr::compute_coefficients<Real>(s, hier, std::size_t(level));
+    return 0;
+  } catch (const mgr::Error &e) {
+    return code_of(e);
+  } catch (...) {
+    return 15;
+  }
+}
+
+template <typename Real>
+int masstrans_impl(int nd, const uint64_t *shape, const double *coords, int cap,
+                   int level, int dim, const Real *in, Real *out, int fused,
+                   Real *coef) {
+  try {
+    std::optional<std::size_t> lv;
+    if (cap > 0)
+      lv = std::size_t(cap);
+    const auto hier =
+        mgr::build_hierarchy(to_shape(nd, shape), to_coords(nd, shape, coords), lv);
+    mgr::NdBuffer<Real> b(mgr::masstrans_input_shape(hier, std::size_t(level),
+                                                     std::size_t(dim)));
+    b.data.assign(in, in + b.data.size());
+    std::vector<Real> cv;
+    const auto o = mgr::masstrans_apply(b, hier, std::size_t(level),
+                                        std::size_t(dim), fused != 0,
+                                        coef ? &cv : nullptr);
+    std::memcpy(out, o.data.data(), o.data.size() * sizeof(Real));
+    if (coef && fused)
+      std::memcpy(coef, cv.data(), cv.size() * sizeof(Real));
+    return 0;
+  } catch (const mgr::Error &e) {
+    return code_of(e);
+  } catch (...) {
+    return 15;
+  }
+}
+
+template <typename Real>
+int solve_impl(int nd, const uint64_t *shape, const double *coords, int cap,
+               int level, int dim, Real *f) {
+  try {
+    std::optional<std::size_t> lv;
+    if (cap > 0)
+      lv = std::size_t(cap);
+    const auto hier =
+        mgr::build_hierarchy(to_shape(nd, shape), to_coords(nd, shape, coords), lv);
+    mgr::NdBuffer<Real> b(hier.level_shape(std::size_t(level) - 1));
+    b.data.assign(f, f + b.data.size());
+    mgr::solve_correction(b, hier, std::size_t(level), std::size_t(dim));
+    std::memcpy(f, b.data.data(), b.data.size() * sizeof(Real));
+    return 0;
+  } catch (const mgr::Error &e) {
+    return code_of(e);
+  } catch (...) {
+    return 15;
+  }
+}
+
+} // namespace
+
+extern "C" {
+
+int mgrref_decompose_f64(int nd, const uint64_t *shape, const double *coords,
+                         int cap, const double *v, double *c, int *lo) {
+  return decompose_impl<double>(nd, shape, coords, cap, v, c, lo);
+}
+int mgrref_decompose_f32(int nd, const uint64_t *shape, const double *coords,
+                         int cap, const float *v, float *c, int *lo) {
+  return decompose_impl<float>(nd, shape, coords, cap, v, c, lo);
+}
+int mgrref_recompose_f64(int nd, const uint64_t *shape, const double *coords,
+                         int levels, const double *c, int k, double *v) {
+  return recompose_impl<double>(nd, shape, coords, levels, c, k, v);
+}
+int mgrref_recompose_f32(int nd, const uint64_t *shape, const double *coords,
+                         int levels, const float *c, int k, float *v) {
+  return recompose_impl<float>(nd, shape, coords, levels, c, k, v);
+}
+int mgrref_gpk_f64(int nd, const uint64_t *s, const double *c, int cap, int l,
+                   int inv, double *v) {
+  return gpk_impl<double>(nd, s, c, cap, l, inv, v);
+}
+int mgrref_gpk_f32(int nd, const uint64_t *s, const double *c, int cap, int l,
+                   int inv, float *v) {
+  return gpk_impl<float>(nd, s, c, cap, l, inv, v);
+}
+int mgrref_masstrans_f64(int nd, const uint64_t *s, const double *c, int cap,
+                         int l, int dim, const double *in, double *out,
+                         int fused, double *coef) {
+  return masstrans_impl<double>(nd, s, c, cap, l, dim, in, out, fused, coef);
+}
+int mgrref_masstrans_f32(int nd, const uint64_t *s, const double *c, int cap,
+                         int l, int dim, const float *in, float *out, int fused,
+                         float *coef) {
+  return masstrans_impl<float>(nd, s, c, cap, l, dim, in, out, fused, coef);
+}
+int mgrref_solve_f64(int nd, const uint64_t *s, const double *c, int cap, int l,
+                     int dim, double *f) {
+  return solve_impl<double>(nd, s, c, cap, l, dim, f);
+}
+int mgrref_solve_f32(int nd, const uint64_t *s, const double *c, int cap, int l,
+                     int dim, float *f) {
+  return solve_impl<float>(nd, s, c, cap, l, dim, f);
+}
+
+// embarrassing_decompose (parallel_impl.hpp:810-847) + recompose of every
+// block, each block an independent 3-D grid of the same shape; `workers`
+// threads.  Used by bench.py --impl reference to time the reference on all
+// host cores.  values/classes: nblocks * N elements back to back.
+int mgrref_embarrassing_roundtrip_f32(int nd, const uint64_t *shape,
+                                      int nblocks, int workers,
+                                      const float *values, float *classes,
+                                      float *recomposed, double *t_dec,
+                                      double *t_rec) {
+  try {
+    const mgr::Shape s = to_shape(nd, shape);
+    const std::size_t n = mgr::num_elements(s);
+    std::vector<mgr::TensorGrid<float>> blocks(nblocks);
+    for (int b = 0; b < nblocks; ++b) {
+      blocks[b].shape = s;
+      blocks[b].coords = to_coords(nd, shape, nullptr);
+      blocks[b].values.assign(values + b * n, values + (b + 1) * n);
+    }
+    const auto t0 = std::chrono::steady_clock::now();
+    const auto out = mgr::embarrassing_decompose(blocks, workers);
+    const auto t1 = std::chrono::steady_clock::now();
+    // recompose: the reference has no parallel recompose driver; use the
+    // same pool shape (one std::thread per worker, blocks dealt in order).
+    std::vector<std::thread> th;
+    std::vector<mgr::TensorGrid<float>> rec(nblocks);
+    const int pool = std::max(1, std::min(workers, nblocks));
+    for (int w = 0; w < pool; ++w)
+      th.emplace_back([&, w] {
+        for (int b = w; b < nblocks; b += pool)
+          rec[b] = mgr::recompose(out[b], out[b].levels);
+      });
+    for (auto &t : th)
+      t.join();
+    const auto t2 = std::chrono::steady_clock::now();
+    for (int b = 0; b < nblocks; ++b) {
+      std::size_t off = b * n;
+      for (const auto &c : out[b].classes) {
+        if (classes)
+          std::memcpy(classes + off, c.data(), c.size() * sizeof(float));
+        off += c.size();
+      }
+      if (recomposed)
+        std::memcpy(recomposed + b * n, rec[b].values.data(), n * sizeof(float));
+    }
+    *t_dec = std::chrono::duration<double>(t1 - t0).count();
+    *t_rec = std::chrono::duration<double>(t2 - t1).count();
+    return 0;
+  } catch (const mgr::Error &e) {
+    return code_of(e);
+  } catch (...) {
+    return 15;
+  }
+}
+
+// Deterministic test data exactly as the reference tests generate it
+// (tests/oracle.cpp:167-186).
+void mgrref_random_vector(uint64_t n, unsigned seed, double lo, double hi,
+                          double *out) {
+  const auto v = oracle::random_vector(n, seed, lo, hi);
+  std::memcpy(out, v.data(), n * sizeof(double));
+}
+void mgrref_random_increasing_coords(uint64_t n, unsigned seed, double *out) {
+  const auto v = oracle::random_increasing_coords(n, seed);
+  std::memcpy(out, v.data(), n * sizeof(double));
+}
+
+} // extern "C"

@@ -1,0 +1,25 @@
+"""B200-native multigrid data refactoring (arXiv 2105.12764).
+
+The hot path -- MGARD-style multilevel decompose / recompose of structured
+1-D/2-D/3-D grids -- runs in hand-written sm_100a kernels (csrc/) behind the
+C ABI include/mgrg.h.  This package is the host-side mirror of the
+reference's C++ API (refactor.py), the device-level plan handle (plan.py) and
+the multi-GPU block driver (parallel.py)."""
+from . import errors
+from .errors import (CorruptFile, Error, InvalidBound, InvalidFusion, InvalidGrid,
+                     InvalidLevel, IoError, MissingClass, ShapeError, SingularSystem,
+                     TooManyWorkers, WorkerFailure)
+from .plan import Plan
+from .refactor import (LevelPassStats, PassStats, PhaseCounters, ReconstructionReport,
+                       RefactoredData, RefactorOptions, TensorGrid, decompose, make_grid,
+                       recompose, recompose_with_report, uniform_coords, value_range,
+                       weighted_l2_norm)
+
+__all__ = [
+    "Plan", "TensorGrid", "RefactoredData", "RefactorOptions", "PassStats",
+    "LevelPassStats", "PhaseCounters", "ReconstructionReport", "decompose", "recompose",
+    "recompose_with_report", "make_grid", "uniform_coords", "value_range",
+    "weighted_l2_norm", "errors", "Error", "InvalidGrid", "InvalidLevel", "ShapeError",
+    "InvalidFusion", "SingularSystem", "TooManyWorkers", "WorkerFailure", "CorruptFile",
+    "MissingClass", "InvalidBound", "IoError",
+]

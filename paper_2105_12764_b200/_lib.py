@@ -1,0 +1,94 @@
+"""ctypes binding of the C ABI (include/mgrg.h) -- libmgrg.so, built in-tree.
+
+The library is the product: there is no CPU fallback.  If it is missing the
+import of anything that computes fails loudly (MissingExtension)."""
+from __future__ import annotations
+
+import ctypes
+import os
+
+from . import errors
+
+PKG_DIR = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(PKG_DIR, "libmgrg.so")
+HEADER = os.path.join(os.path.dirname(PKG_DIR), "include", "mgrg.h")
+
+MGRG_F32 = 4
+MGRG_F64 = 8
+
+# Every function include/mgrg.h declares (checked by tests/test_capi.py).
+EXPORTS = (
+    "mgrg_plan_create", "mgrg_plan_destroy", "mgrg_plan_levels",
+    "mgrg_plan_class_offsets", "mgrg_plan_level_shape", "mgrg_plan_sizes",
+    "mgrg_decompose", "mgrg_recompose", "mgrg_decompose_host",
+    "mgrg_recompose_host", "mgrg_gpk", "mgrg_masstrans", "mgrg_solve",
+    "mgrg_apply_correction", "mgrg_reorder", "mgrg_last_error",
+    "mgrg_status_name", "mgrg_plan_last_launches", "mgrg_version",
+)
+
+
+class MissingExtension(ImportError):
+    pass
+
+
+class GridDesc(ctypes.Structure):
+    _fields_ = [
+        ("ndims", ctypes.c_int32),
+        ("dtype", ctypes.c_int32),
+        ("shape", ctypes.c_uint64 * 4),
+        ("coords", ctypes.c_void_p),
+        ("levels", ctypes.c_int32),
+        ("device", ctypes.c_int32),
+    ]
+
+
+_lib = None
+
+
+def lib() -> ctypes.CDLL:
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise MissingExtension(
+                f"{LIB_PATH} is not built; run __graft_entry__.build() "
+                "(the refactoring path has no CPU fallback)")
+        L = ctypes.CDLL(LIB_PATH)
+        vp, i32, u64 = ctypes.c_void_p, ctypes.c_int32, ctypes.c_uint64
+        sig = {
+            "mgrg_plan_create": [ctypes.POINTER(GridDesc), ctypes.POINTER(vp)],
+            "mgrg_plan_destroy": [vp],
+            "mgrg_plan_levels": [vp, ctypes.POINTER(i32)],
+            "mgrg_plan_class_offsets": [vp, vp],
+            "mgrg_plan_level_shape": [vp, i32, vp],
+            "mgrg_plan_sizes": [vp, ctypes.POINTER(u64), ctypes.POINTER(u64)],
+            "mgrg_decompose": [vp, vp, vp, vp],
+            "mgrg_recompose": [vp, vp, i32, vp, vp],
+            "mgrg_decompose_host": [vp, vp, vp],
+            "mgrg_recompose_host": [vp, vp, i32, vp],
+            "mgrg_gpk": [vp, i32, i32, vp, vp],
+            "mgrg_masstrans": [vp, i32, i32, vp, vp, i32, vp, vp],
+            "mgrg_solve": [vp, i32, i32, vp, vp],
+            "mgrg_apply_correction": [vp, u64, vp, vp, i32, vp],
+            "mgrg_reorder": [vp, i32, i32, vp, vp, vp],
+            "mgrg_plan_last_launches": [vp, ctypes.POINTER(u64)],
+        }
+        for name, args in sig.items():
+            fn = getattr(L, name)
+            fn.argtypes = args
+            fn.restype = ctypes.c_int
+        L.mgrg_last_error.restype = ctypes.c_char_p
+        L.mgrg_last_error.argtypes = []
+        L.mgrg_status_name.restype = ctypes.c_char_p
+        L.mgrg_status_name.argtypes = [ctypes.c_int]
+        L.mgrg_version.restype = ctypes.c_char_p
+        L.mgrg_version.argtypes = []
+        _lib = L
+    return _lib
+
+
+def check(status: int) -> None:
+    """Raise the reference-named exception for a non-zero mgrg_status."""
+    if status != 0:
+        L = lib()
+        msg = L.mgrg_last_error().decode() or L.mgrg_status_name(status).decode()
+        raise errors.from_status(status, msg)

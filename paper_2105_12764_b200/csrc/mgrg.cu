@@ -1,0 +1,901 @@
+// mgrg.cu -- plan, level loop and C ABI (include/mgrg.h) of the B200 path.
+//
+// Host side of the drop-in boundary: the reference engine
+// (RefactorEngine<Real>, /root/reference/proj/include/mgr/refactor.hpp:153-458)
+// becomes a plan (hierarchy + geometry + workspace on the device) and a level
+// loop that launches, per level,
+//   decompose: dec_level -> thomas(d) for every refining d (last one fused
+//              with apply_pack, writing the packed level-(l-1) array);
+//   recompose: rec_load -> thomas(d) (last fused with unapply_expand) ->
+//              rec_gpk (scatter_class + GPK inverse, writing the level-l
+//              array).
+// Level arrays live in HBM packed row-major (paper §III.C "stride always
+// one"); the class buffer is the single N-element output.
+#include <algorithm>
+#include <array>
+#include <cstdlib>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include <cuda_runtime.h>
+
+#include "../../include/mgrg.h"
+#include "kernels.cuh"
+
+using namespace mgrg;
+
+namespace {
+
+thread_local std::string g_last_error;
+
+mgrg_status fail(mgrg_status st, const std::string &msg) {
+  g_last_error = msg;
+  return st;
+}
+
+#define CUDA_TRY(expr)                                                         \
+  do {                                                                         \
+    cudaError_t e_ = (expr);                                                   \
+    if (e_ != cudaSuccess)                                                     \
+      return fail(MGRG_CUDA_ERROR, std::string(#expr) + ": " +                 \
+                                       cudaGetErrorString(e_));                \
+  } while (0)
+
+constexpr int kMaxLevels = 40;
+
+// RAII current-device switch: the C ABI may be called from threads whose
+// current device differs from the plan's.
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int dev) {
+    cudaGetDevice(&prev);
+    if (prev != dev)
+      cudaSetDevice(dev);
+  }
+  ~DeviceGuard() {
+    int cur = -1;
+    cudaGetDevice(&cur);
+    if (prev >= 0 && cur != prev)
+      cudaSetDevice(prev);
+  }
+};
+
+uint64_t coarse_extent(uint64_t n) { return n / 2 + 1; } // grid.hpp:77
+
+// Host hierarchy: build_hierarchy / build_dim_levels (grid.cpp:40-112) with
+// the validation of validate_grid_geometry (grid.cpp:14-36).
+struct Hierarchy {
+  int nd = 0;
+  int L = 0;
+  uint64_t shape[4] = {1, 1, 1, 1};
+  std::vector<std::vector<uint64_t>> ext;             // [l][d]
+  std::vector<std::vector<std::vector<double>>> h, r; // [d][l][i]
+};
+
+mgrg_status build_hierarchy(const mgrg_grid_desc &desc, Hierarchy &H) {
+  const int nd = desc.ndims;
+  if (nd < 1 || nd > 4)
+    return fail(MGRG_INVALID_GRID, "grid must have 1..4 dimensions, got " +
+                                       std::to_string(nd));
+  if (nd == 4)
+    return fail(MGRG_UNSUPPORTED,
+                "4-D (spatiotemporal) grids are outside this path's scope");
+  H.nd = nd;
+  std::vector<std::vector<double>> coords(nd);
+  const double *cp = desc.coords;
+  for (int d = 0; d < nd; ++d) {
+    const uint64_t n = desc.shape[d];
+    H.shape[d] = n;
+    if (n < 2)
+      return fail(MGRG_INVALID_GRID, "dimension " + std::to_string(d) + " has " +
+                                         std::to_string(n) +
+                                         " nodes; need at least 2");
+    if (n > (uint64_t(1) << 31))
+      return fail(MGRG_UNSUPPORTED, "extent too large");
+    coords[d].resize(n);
+    for (uint64_t i = 0; i < n; ++i)
+      coords[d][i] = cp ? cp[i] : (n > 1 ? double(i) / double(n - 1) : 0.0);
+    if (cp)
+      cp += n;
+    for (uint64_t i = 0; i + 1 < n; ++i)
+      if (!(coords[d][i] < coords[d][i + 1]))
+        return fail(MGRG_INVALID_GRID, "coordinates of dimension " +
+                                           std::to_string(d) +
+                                           " are not strictly increasing at index " +
+                                           std::to_string(i));
+  }
+  int levels = 0;
+  bool any = false;
+  for (int d = 0; d < nd; ++d) {
+    const uint64_t e = desc.shape[d];
+    if (e < 3)
+      continue;
+    const int depth = int(std::floor(std::log2(double(e - 1))));
+    levels = any ? std::min(levels, depth) : depth;
+    any = true;
+  }
+  if (!any)
+    return fail(MGRG_INVALID_GRID, "no dimension has at least 3 nodes");
+  if (desc.levels < 0)
+    return fail(MGRG_INVALID_LEVEL, "level count must be at least 1");
+  if (desc.levels > 0)
+    levels = std::min(levels, int(desc.levels));
+  if (levels > kMaxLevels)
+    return fail(MGRG_UNSUPPORTED, "too many levels");
+  H.L = levels;
+  H.ext.assign(levels + 1, std::vector<uint64_t>(nd));
+  H.h.assign(nd, {});
+  H.r.assign(nd, {});
+  for (int d = 0; d < nd; ++d) {
+    std::vector<std::vector<uint64_t>> idx(levels + 1);
+    idx[levels].resize(desc.shape[d]);
+    for (uint64_t i = 0; i < desc.shape[d]; ++i)
+      idx[levels][i] = i;
+    for (int l = levels - 1; l >= 0; --l) {
+      const auto &fine = idx[l + 1];
+      auto &c = idx[l];
+      for (size_t p = 0; p < fine.size(); p += 2)
+        c.push_back(fine[p]);
+      if (c.back() != fine.back())
+        c.push_back(fine.back());
+    }
+    H.h[d].resize(levels + 1);
+    H.r[d].resize(levels + 1);
+    for (int l = 0; l <= levels; ++l) {
+      const auto &ids = idx[l];
+      H.ext[l][d] = ids.size();
+      auto &h = H.h[d][l];
+      auto &r = H.r[d][l];
+      h.resize(ids.size() - 1);
+      for (size_t i = 0; i + 1 < ids.size(); ++i)
+        h[i] = coords[d][ids[i + 1]] - coords[d][ids[i]];
+      if (h.size() >= 2) {
+        r.resize(h.size() - 1);
+        for (size_t i = 0; i + 1 < h.size(); ++i)
+          r[i] = h[i] / (h[i] + h[i + 1]);
+      }
+    }
+  }
+  return MGRG_OK;
+}
+
+// Tile shapes of the level kernels (coarse outputs per CTA along x, y).
+enum class TileKind { t32x8, t128x1 };
+
+struct LaunchCount {
+  uint64_t n = 0;
+};
+
+template <typename R> struct PlanT {
+  std::vector<LevelGeom<R>> geom;                 // [l], l = 1..L
+  std::vector<std::array<ThomasGeom<R>, 3>> thom; // [l][kd] (level-(l-1) factors)
+  R *d_geom = nullptr;
+};
+
+} // namespace
+
+struct mgrg_plan {
+  int device = 0;
+  int dtype = MGRG_F32;
+  int esize = 4;
+  Hierarchy H;
+  int kmap[3] = {0, -1, -1};              // kernel dim -> user dim (-1 = pad)
+  std::vector<std::array<uint32_t, 3>> kext; // [l][kd] padded extents
+  std::vector<uint64_t> nodes;            // N_l
+  uint32_t refine = 0;                    // kernel-dim refine mask (same at every level)
+  int refine_dims[3];
+  int nrefine = 0;
+  TileKind tile = TileKind::t32x8;
+  uint32_t zchunk = 32;
+  mgrg_status deferred = MGRG_OK;         // SingularSystem found at build time
+  std::string deferred_msg;
+  PlanT<float> pf;
+  PlanT<double> pd;
+  void *d_geom = nullptr;
+  size_t geom_bytes = 0;
+  void *d_ws = nullptr; // [A: N_{L-1}][B: N_{L-2}][F: N_{L-1}]
+  size_t ws_bytes = 0;
+  uint64_t offA = 0, offB = 0, offF = 0; // element offsets inside d_ws
+  void *d_stage = nullptr;               // host-API staging (2N elements), lazy
+  cudaStream_t own_stream = nullptr;
+  uint64_t last_launches = 0;
+};
+
+namespace {
+
+template <typename R> PlanT<R> &pt(mgrg_plan *p);
+template <> PlanT<float> &pt<float>(mgrg_plan *p) { return p->pf; }
+template <> PlanT<double> &pt<double>(mgrg_plan *p) { return p->pd; }
+
+// make_class_layout (grid.cpp:140-165) on the padded 3-D lattice.
+template <typename R>
+void fill_layout(LevelGeom<R> &g) {
+  uint64_t off = 0;
+  g.tbase[0] = 0;
+  g.tex[0] = g.tey[0] = 0;
+  for (unsigned mask = 1; mask < 8; ++mask) {
+    uint64_t e[3], count = 1;
+    for (int d = 0; d < 3; ++d) {
+      const uint64_t n = g.n[d];
+      e[d] = ((mask >> d) & 1) ? n - coarse_extent(n) : coarse_extent(n);
+      count *= e[d];
+    }
+    g.tbase[mask] = off;
+    g.tex[mask] = uint32_t(e[0]);
+    g.tey[mask] = uint32_t(e[1]);
+    off += count;
+  }
+}
+
+// TridiagonalOperator::build (kernels.hpp:107-135) in the working precision.
+template <typename R>
+bool thomas_factors(const std::vector<double> &hd, std::vector<R> &h,
+                    std::vector<R> &fwd, std::vector<R> &ip, std::string &err) {
+  const size_t n = hd.size() + 1;
+  h.resize(hd.size());
+  for (size_t i = 0; i < hd.size(); ++i)
+    h[i] = R(hd[i]);
+  fwd.assign(n, R(0));
+  ip.assign(n, R(0));
+  R pivot = R(2) * h[0];
+  if (!(pivot > R(0))) {
+    err = "nonpositive leading pivot";
+    return false;
+  }
+  ip[0] = R(1) / pivot;
+  for (size_t i = 1; i < n; ++i) {
+    const R sub = h[i - 1];
+    fwd[i] = -sub * ip[i - 1];
+    const R diag = i + 1 < n ? R(2) * (h[i - 1] + h[i]) : R(2) * h[i - 1];
+    pivot = diag + fwd[i] * sub;
+    if (!(pivot > R(0))) {
+      err = "nonpositive pivot at row " + std::to_string(i);
+      return false;
+    }
+    ip[i] = R(1) / pivot;
+  }
+  return true;
+}
+
+template <typename R> mgrg_status upload_geometry(mgrg_plan *p) {
+  const Hierarchy &H = p->H;
+  const int L = H.L;
+  // host staging of every per-level array in R, then one upload
+  std::vector<R> buf;
+  struct Ref {
+    size_t h[3], r[3], th[3], tf[3], ti[3];
+  };
+  std::vector<Ref> refs(L + 1);
+  auto push = [&](const std::vector<R> &v) {
+    size_t off = buf.size();
+    buf.insert(buf.end(), v.begin(), v.end());
+    buf.resize((buf.size() + 31) & ~size_t(31), R(0)); // 256-byte alignment
+    return off;
+  };
+  std::vector<std::array<ThomasGeom<R>, 3>> thom(L + 1);
+  for (int l = 1; l <= L; ++l) {
+    for (int kd = 0; kd < 3; ++kd) {
+      refs[l].h[kd] = refs[l].r[kd] = refs[l].th[kd] = refs[l].tf[kd] =
+          refs[l].ti[kd] = size_t(-1);
+      const int ud = p->kmap[kd];
+      if (ud < 0)
+        continue;
+      std::vector<R> h(H.h[ud][l].begin(), H.h[ud][l].end());
+      std::vector<R> r(H.r[ud][l].begin(), H.r[ud][l].end());
+      refs[l].h[kd] = push(h);
+      refs[l].r[kd] = push(r);
+      if (H.ext[l - 1][ud] < H.ext[l][ud]) {
+        std::vector<R> th, tf, ti;
+        std::string err;
+        if (!thomas_factors<R>(H.h[ud][l - 1], th, tf, ti, err) &&
+            p->deferred == MGRG_OK) {
+          p->deferred = MGRG_SINGULAR_SYSTEM;
+          p->deferred_msg = err;
+        }
+        if (th.empty())
+          th.push_back(R(0));
+        refs[l].th[kd] = push(th);
+        refs[l].tf[kd] = push(tf);
+        refs[l].ti[kd] = push(ti);
+      }
+    }
+  }
+  if (buf.empty())
+    buf.resize(32, R(0));
+  p->geom_bytes = buf.size() * sizeof(R);
+  CUDA_TRY(cudaMalloc(&p->d_geom, p->geom_bytes));
+  CUDA_TRY(cudaMemcpy(p->d_geom, buf.data(), p->geom_bytes, cudaMemcpyHostToDevice));
+  R *base = static_cast<R *>(p->d_geom);
+  PlanT<R> &P = pt<R>(p);
+  P.geom.assign(L + 1, LevelGeom<R>{});
+  P.thom.assign(L + 1, {});
+  for (int l = 1; l <= L; ++l) {
+    LevelGeom<R> &g = P.geom[l];
+    g.refine = 0;
+    for (int kd = 0; kd < 3; ++kd) {
+      g.n[kd] = p->kext[l][kd];
+      g.m[kd] = p->kext[l - 1][kd];
+      if (g.m[kd] < g.n[kd])
+        g.refine |= 1u << kd;
+      g.h[kd] = refs[l].h[kd] == size_t(-1) ? nullptr : base + refs[l].h[kd];
+      g.r[kd] = refs[l].r[kd] == size_t(-1) ? nullptr : base + refs[l].r[kd];
+      ThomasGeom<R> &t = P.thom[l][kd];
+      t.m = g.m[kd];
+      t.h = refs[l].th[kd] == size_t(-1) ? nullptr : base + refs[l].th[kd];
+      t.fwd = refs[l].tf[kd] == size_t(-1) ? nullptr : base + refs[l].tf[kd];
+      t.ip = refs[l].ti[kd] == size_t(-1) ? nullptr : base + refs[l].ti[kd];
+    }
+    fill_layout(g);
+  }
+  return MGRG_OK;
+}
+
+template <typename R, int CX, int CY> void set_smem_attrs() {
+  static bool done = false; // per instantiation; attribute is per device too
+  (void)done;
+  cudaFuncSetAttribute(dec_level_kernel<R, CX, CY>,
+                       cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       int(dec_level_smem<R, CX, CY>()));
+  cudaFuncSetAttribute(rec_load_kernel<R, CX, CY>,
+                       cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       int(rec_load_smem<R, CX, CY>()));
+  cudaFuncSetAttribute(rec_gpk_kernel<R, CX, CY>,
+                       cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       int(rec_gpk_smem<R, CX, CY>()));
+}
+
+template <typename R, int CX, int CY>
+dim3 level_grid(const LevelGeom<R> &g, uint32_t zchunk) {
+  return dim3((g.m[0] + CX - 1) / CX, (g.m[1] + CY - 1) / CY,
+              (g.m[2] + zchunk - 1) / zchunk);
+}
+
+template <typename R, int CX, int CY>
+void launch_dec_level(const LevelGeom<R> &g, const R *in, R *cls, R *P, R *f,
+                      uint32_t zchunk, cudaStream_t s) {
+  dec_level_kernel<R, CX, CY><<<level_grid<R, CX, CY>(g, zchunk), CX * CY,
+                                dec_level_smem<R, CX, CY>(), s>>>(g, in, cls, P, f,
+                                                                  zchunk);
+}
+template <typename R, int CX, int CY>
+void launch_rec_load(const LevelGeom<R> &g, const R *cls, R *f, uint32_t zchunk,
+                     cudaStream_t s) {
+  rec_load_kernel<R, CX, CY><<<level_grid<R, CX, CY>(g, zchunk), CX * CY,
+                               rec_load_smem<R, CX, CY>(), s>>>(g, cls, f, zchunk);
+}
+template <typename R, int CX, int CY>
+void launch_rec_gpk(const LevelGeom<R> &g, const R *coarse, const R *cls, R *out,
+                    uint32_t zchunk, cudaStream_t s) {
+  rec_gpk_kernel<R, CX, CY><<<level_grid<R, CX, CY>(g, zchunk), CX * CY,
+                              rec_gpk_smem<R, CX, CY>(), s>>>(g, coarse, cls, out,
+                                                              zchunk);
+}
+
+// Batched Thomas along kernel dim kd of the m-lattice `g.m`.
+template <typename R>
+void launch_thomas(const LevelGeom<R> &g, const ThomasGeom<R> &t, int kd, R *f,
+                   Epi epi, const R *base, R *out, cudaStream_t s) {
+  const uint64_t mx = g.m[0], my = g.m[1], mz = g.m[2];
+  if (kd == 0) {
+    const uint64_t nf = my * mz;
+    const uint64_t warps = (nf + 31) / 32;
+    thomas_x_kernel<R><<<unsigned((warps + 3) / 4), 128, 0, s>>>(f, t, nf, epi, base,
+                                                                 out);
+  } else {
+    const uint64_t S = kd == 1 ? mx : mx * my;
+    const uint64_t ostride = kd == 1 ? mx * my : mx; // the remaining dim
+    const uint64_t nf = mx * (kd == 1 ? mz : my);
+    thomas_strided_kernel<R><<<unsigned((nf + 127) / 128), 128, 0, s>>>(
+        f, t, S, uint32_t(mx), ostride, nf, epi, base, out);
+  }
+}
+
+template <typename R> R *ws(mgrg_plan *p, uint64_t off) {
+  return static_cast<R *>(p->d_ws) + off;
+}
+// Buffer holding the packed level-j array, 1 <= j <= L-1 (ping-pong A/B).
+template <typename R> R *level_buf(mgrg_plan *p, int j) {
+  return ((p->H.L - 1 - j) % 2 == 0) ? ws<R>(p, p->offA) : ws<R>(p, p->offB);
+}
+
+template <typename R>
+mgrg_status run_decompose(mgrg_plan *p, const R *d_in, R *d_cls, cudaStream_t s) {
+  PlanT<R> &P = pt<R>(p);
+  const int L = p->H.L;
+  R *F = ws<R>(p, p->offF);
+  uint64_t launches = 0;
+  for (int l = L; l >= 1; --l) {
+    const LevelGeom<R> &g = P.geom[l];
+    const R *a = l == L ? d_in : level_buf<R>(p, l);
+    R *Pout = l == 1 ? d_cls : level_buf<R>(p, l - 1);
+    R *cls = d_cls + p->nodes[l - 1];
+    if (p->tile == TileKind::t32x8)
+      launch_dec_level<R, 32, 8>(g, a, cls, Pout, F, p->zchunk, s);
+    else
+      launch_dec_level<R, 128, 1>(g, a, cls, Pout, F, p->zchunk, s);
+    ++launches;
+    for (int i = 0; i < p->nrefine; ++i) {
+      const int kd = p->refine_dims[i];
+      const bool last = i == p->nrefine - 1;
+      launch_thomas<R>(g, P.thom[l][kd], kd, F, last ? Epi::add : Epi::none, Pout,
+                       Pout, s);
+      ++launches;
+    }
+  }
+  CUDA_TRY(cudaGetLastError());
+  p->last_launches = launches;
+  return MGRG_OK;
+}
+
+template <typename R>
+mgrg_status run_recompose(mgrg_plan *p, const R *d_cls, int k, R *d_out,
+                          cudaStream_t s) {
+  PlanT<R> &P = pt<R>(p);
+  const int L = p->H.L;
+  R *F = ws<R>(p, p->offF);
+  uint64_t launches = 0;
+  for (int l = 1; l <= L; ++l) {
+    const LevelGeom<R> &g = P.geom[l];
+    const R *prev = l == 1 ? d_cls : level_buf<R>(p, l - 1);
+    R *out = l == L ? d_out : level_buf<R>(p, l);
+    const R *cls = d_cls + p->nodes[l - 1];
+    if (l <= k) {
+      if (p->tile == TileKind::t32x8)
+        launch_rec_load<R, 32, 8>(g, cls, F, p->zchunk, s);
+      else
+        launch_rec_load<R, 128, 1>(g, cls, F, p->zchunk, s);
+      ++launches;
+      for (int i = 0; i < p->nrefine; ++i) {
+        const int kd = p->refine_dims[i];
+        const bool last = i == p->nrefine - 1;
+        launch_thomas<R>(g, P.thom[l][kd], kd, F, last ? Epi::sub : Epi::none, prev,
+                         F, s);
+        ++launches;
+      }
+      if (p->tile == TileKind::t32x8)
+        launch_rec_gpk<R, 32, 8>(g, F, cls, out, p->zchunk, s);
+      else
+        launch_rec_gpk<R, 128, 1>(g, F, cls, out, p->zchunk, s);
+    } else {
+      // classes above classes_used are zero: f = 0, z = +0 exactly, so the
+      // coarse values are a_{l-1} unchanged and the fine ones interp + 0.
+      if (p->tile == TileKind::t32x8)
+        launch_rec_gpk<R, 32, 8>(g, prev, nullptr, out, p->zchunk, s);
+      else
+        launch_rec_gpk<R, 128, 1>(g, prev, nullptr, out, p->zchunk, s);
+    }
+    ++launches;
+  }
+  CUDA_TRY(cudaGetLastError());
+  p->last_launches = launches;
+  return MGRG_OK;
+}
+
+mgrg_status check_plan(const mgrg_plan *p) {
+  if (!p)
+    return fail(MGRG_INVALID_ARGUMENT, "null plan");
+  return MGRG_OK;
+}
+
+} // namespace
+
+extern "C" {
+
+const char *mgrg_version(void) { return "mgrg-b200 0.1 (sm_100a)"; }
+
+const char *mgrg_last_error(void) { return g_last_error.c_str(); }
+
+const char *mgrg_status_name(mgrg_status st) {
+  switch (st) {
+  case MGRG_OK: return "Ok";
+  case MGRG_INVALID_GRID: return "InvalidGrid";
+  case MGRG_INVALID_LEVEL: return "InvalidLevel";
+  case MGRG_SHAPE_ERROR: return "ShapeError";
+  case MGRG_INVALID_FUSION: return "InvalidFusion";
+  case MGRG_SINGULAR_SYSTEM: return "SingularSystem";
+  case MGRG_TOO_MANY_WORKERS: return "TooManyWorkers";
+  case MGRG_WORKER_FAILURE: return "WorkerFailure";
+  case MGRG_CORRUPT_FILE: return "CorruptFile";
+  case MGRG_MISSING_CLASS: return "MissingClass";
+  case MGRG_INVALID_BOUND: return "InvalidBound";
+  case MGRG_IO_ERROR: return "IoError";
+  case MGRG_CUDA_ERROR: return "CudaError";
+  case MGRG_NCCL_ERROR: return "NcclError";
+  case MGRG_UNSUPPORTED: return "Unsupported";
+  case MGRG_INVALID_ARGUMENT: return "InvalidArgument";
+  case MGRG_OUT_OF_MEMORY: return "OutOfMemory";
+  }
+  return "Unknown";
+}
+
+mgrg_status mgrg_plan_create(const mgrg_grid_desc *desc, mgrg_plan **out) {
+  g_last_error.clear();
+  if (!desc || !out)
+    return fail(MGRG_INVALID_ARGUMENT, "null argument");
+  *out = nullptr;
+  if (desc->dtype != MGRG_F32 && desc->dtype != MGRG_F64)
+    return fail(MGRG_INVALID_ARGUMENT, "dtype must be MGRG_F32 or MGRG_F64");
+  std::unique_ptr<mgrg_plan> p(new mgrg_plan());
+  p->device = desc->device;
+  p->dtype = desc->dtype;
+  p->esize = desc->dtype;
+  if (mgrg_status st = build_hierarchy(*desc, p->H))
+    return st;
+  const Hierarchy &H = p->H;
+  const int nd = H.nd, L = H.L;
+  // kernel dims: user dims in order, padded to 3
+  for (int kd = 0; kd < 3; ++kd)
+    p->kmap[kd] = kd < nd ? kd : -1;
+  p->kext.assign(L + 1, {1, 1, 1});
+  p->nodes.assign(L + 1, 1);
+  for (int l = 0; l <= L; ++l)
+    for (int kd = 0; kd < 3; ++kd) {
+      const int ud = p->kmap[kd];
+      p->kext[l][kd] = ud < 0 ? 1 : uint32_t(H.ext[l][ud]);
+      p->nodes[l] *= p->kext[l][kd];
+    }
+  p->refine = 0;
+  p->nrefine = 0;
+  for (int kd = 0; kd < 3; ++kd)
+    if (p->kext[L - 1][kd] < p->kext[L][kd]) {
+      p->refine |= 1u << kd;
+      p->refine_dims[p->nrefine++] = kd;
+    }
+  p->tile = nd == 1 ? TileKind::t128x1 : TileKind::t32x8;
+  p->zchunk = nd == 3 ? 32 : 1;
+  if (const char *zc = std::getenv("MGRG_ZCHUNK"))
+    if (nd == 3 && std::atoi(zc) > 0)
+      p->zchunk = uint32_t(std::atoi(zc));
+
+  DeviceGuard guard(p->device);
+  mgrg_status st = p->dtype == MGRG_F32 ? upload_geometry<float>(p.get())
+                                        : upload_geometry<double>(p.get());
+  if (st)
+    return st;
+  // workspace: A = N_{L-1}, B = N_{L-2}, F = N_{L-1}
+  const uint64_t nA = p->nodes[L - 1];
+  const uint64_t nB = L >= 2 ? p->nodes[L - 2] : 1;
+  auto al = [](uint64_t n) { return (n + 63) & ~uint64_t(63); };
+  p->offA = 0;
+  p->offB = al(nA);
+  p->offF = p->offB + al(nB);
+  p->ws_bytes = (p->offF + al(nA)) * p->esize;
+  cudaError_t e = cudaMalloc(&p->d_ws, p->ws_bytes);
+  if (e != cudaSuccess) {
+    cudaFree(p->d_geom);
+    return fail(e == cudaErrorMemoryAllocation ? MGRG_OUT_OF_MEMORY : MGRG_CUDA_ERROR,
+                std::string("workspace allocation: ") + cudaGetErrorString(e));
+  }
+  if (p->dtype == MGRG_F32) {
+    set_smem_attrs<float, 32, 8>();
+    set_smem_attrs<float, 128, 1>();
+  } else {
+    set_smem_attrs<double, 32, 8>();
+    set_smem_attrs<double, 128, 1>();
+  }
+  CUDA_TRY(cudaGetLastError());
+  *out = p.release();
+  return MGRG_OK;
+}
+
+mgrg_status mgrg_plan_destroy(mgrg_plan *p) {
+  if (!p)
+    return MGRG_OK;
+  {
+    DeviceGuard guard(p->device);
+    cudaFree(p->d_geom);
+    cudaFree(p->d_ws);
+    cudaFree(p->d_stage);
+    if (p->own_stream)
+      cudaStreamDestroy(p->own_stream);
+  }
+  delete p;
+  return MGRG_OK;
+}
+
+mgrg_status mgrg_plan_levels(const mgrg_plan *p, int32_t *levels) {
+  if (mgrg_status st = check_plan(p))
+    return st;
+  if (!levels)
+    return fail(MGRG_INVALID_ARGUMENT, "null output");
+  *levels = p->H.L;
+  return MGRG_OK;
+}
+
+mgrg_status mgrg_plan_class_offsets(const mgrg_plan *p, uint64_t *offsets) {
+  if (mgrg_status st = check_plan(p))
+    return st;
+  if (!offsets)
+    return fail(MGRG_INVALID_ARGUMENT, "null output");
+  offsets[0] = 0;
+  for (int l = 0; l <= p->H.L; ++l)
+    offsets[l + 1] = p->nodes[l];
+  return MGRG_OK;
+}
+
+mgrg_status mgrg_plan_level_shape(const mgrg_plan *p, int32_t level,
+                                  uint64_t *extents) {
+  if (mgrg_status st = check_plan(p))
+    return st;
+  if (level < 0 || level > p->H.L)
+    return fail(MGRG_INVALID_LEVEL, "level " + std::to_string(level) +
+                                        " outside [0, " + std::to_string(p->H.L) + "]");
+  for (int d = 0; d < p->H.nd; ++d)
+    extents[d] = p->H.ext[level][d];
+  return MGRG_OK;
+}
+
+mgrg_status mgrg_plan_sizes(const mgrg_plan *p, uint64_t *n, uint64_t *wsb) {
+  if (mgrg_status st = check_plan(p))
+    return st;
+  if (n)
+    *n = p->nodes[p->H.L];
+  if (wsb)
+    *wsb = p->ws_bytes + p->geom_bytes;
+  return MGRG_OK;
+}
+
+mgrg_status mgrg_plan_last_launches(const mgrg_plan *p, uint64_t *launches) {
+  if (mgrg_status st = check_plan(p))
+    return st;
+  *launches = p->last_launches;
+  return MGRG_OK;
+}
+
+mgrg_status mgrg_decompose(mgrg_plan *p, const void *d_values, void *d_classes,
+                           void *stream) {
+  g_last_error.clear();
+  if (mgrg_status st = check_plan(p))
+    return st;
+  if (!d_values || !d_classes)
+    return fail(MGRG_INVALID_ARGUMENT, "null device buffer");
+  if (p->deferred)
+    return fail(p->deferred, p->deferred_msg);
+  DeviceGuard guard(p->device);
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  return p->dtype == MGRG_F32
+             ? run_decompose<float>(p, static_cast<const float *>(d_values),
+                                    static_cast<float *>(d_classes), s)
+             : run_decompose<double>(p, static_cast<const double *>(d_values),
+                                     static_cast<double *>(d_classes), s);
+}
+
+mgrg_status mgrg_recompose(mgrg_plan *p, const void *d_classes, int32_t k,
+                           void *d_values, void *stream) {
+  g_last_error.clear();
+  if (mgrg_status st = check_plan(p))
+    return st;
+  if (k < 0 || k > p->H.L)
+    return fail(MGRG_INVALID_LEVEL, "requested " + std::to_string(k) +
+                                        " classes; container has " +
+                                        std::to_string(p->H.L));
+  if (!d_values || !d_classes)
+    return fail(MGRG_INVALID_ARGUMENT, "null device buffer");
+  if (p->deferred)
+    return fail(p->deferred, p->deferred_msg);
+  DeviceGuard guard(p->device);
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  return p->dtype == MGRG_F32
+             ? run_recompose<float>(p, static_cast<const float *>(d_classes), k,
+                                    static_cast<float *>(d_values), s)
+             : run_recompose<double>(p, static_cast<const double *>(d_classes), k,
+                                     static_cast<double *>(d_values), s);
+}
+
+static mgrg_status ensure_stage(mgrg_plan *p) {
+  if (p->d_stage)
+    return MGRG_OK;
+  const uint64_t n = p->nodes[p->H.L];
+  cudaError_t e = cudaMalloc(&p->d_stage, 2 * n * p->esize);
+  if (e != cudaSuccess)
+    return fail(e == cudaErrorMemoryAllocation ? MGRG_OUT_OF_MEMORY : MGRG_CUDA_ERROR,
+                std::string("staging allocation: ") + cudaGetErrorString(e));
+  CUDA_TRY(cudaStreamCreateWithFlags(&p->own_stream, cudaStreamNonBlocking));
+  return MGRG_OK;
+}
+
+mgrg_status mgrg_decompose_host(mgrg_plan *p, const void *h_values, void *h_classes) {
+  g_last_error.clear();
+  if (mgrg_status st = check_plan(p))
+    return st;
+  if (!h_values || !h_classes)
+    return fail(MGRG_INVALID_ARGUMENT, "null host buffer");
+  DeviceGuard guard(p->device);
+  if (mgrg_status st = ensure_stage(p))
+    return st;
+  const uint64_t bytes = p->nodes[p->H.L] * p->esize;
+  char *din = static_cast<char *>(p->d_stage), *dout = din + bytes;
+  CUDA_TRY(cudaMemcpyAsync(din, h_values, bytes, cudaMemcpyHostToDevice, p->own_stream));
+  if (mgrg_status st = mgrg_decompose(p, din, dout, p->own_stream))
+    return st;
+  CUDA_TRY(cudaMemcpyAsync(h_classes, dout, bytes, cudaMemcpyDeviceToHost, p->own_stream));
+  CUDA_TRY(cudaStreamSynchronize(p->own_stream));
+  return MGRG_OK;
+}
+
+mgrg_status mgrg_recompose_host(mgrg_plan *p, const void *h_classes, int32_t k,
+                                void *h_values) {
+  g_last_error.clear();
+  if (mgrg_status st = check_plan(p))
+    return st;
+  if (!h_values || !h_classes)
+    return fail(MGRG_INVALID_ARGUMENT, "null host buffer");
+  if (k < 0 || k > p->H.L)
+    return fail(MGRG_INVALID_LEVEL, "requested " + std::to_string(k) +
+                                        " classes; container has " +
+                                        std::to_string(p->H.L));
+  DeviceGuard guard(p->device);
+  if (mgrg_status st = ensure_stage(p))
+    return st;
+  const uint64_t bytes = p->nodes[p->H.L] * p->esize;
+  char *din = static_cast<char *>(p->d_stage), *dout = din + bytes;
+  // only classes 0..k are read (refactor.hpp:483-485): copy that prefix
+  const uint64_t used = p->nodes[k] * p->esize;
+  CUDA_TRY(cudaMemcpyAsync(din, h_classes, used, cudaMemcpyHostToDevice, p->own_stream));
+  if (mgrg_status st = mgrg_recompose(p, din, k, dout, p->own_stream))
+    return st;
+  CUDA_TRY(cudaMemcpyAsync(h_values, dout, bytes, cudaMemcpyDeviceToHost, p->own_stream));
+  CUDA_TRY(cudaStreamSynchronize(p->own_stream));
+  return MGRG_OK;
+}
+
+// ---- unit-level kernels ------------------------------------------------
+
+static mgrg_status check_level(const mgrg_plan *p, int32_t level) {
+  if (level < 1 || level > p->H.L)
+    return fail(MGRG_INVALID_LEVEL, "level " + std::to_string(level) + " outside [1, " +
+                                        std::to_string(p->H.L) + "]");
+  return MGRG_OK;
+}
+
+extern "C++" {
+template <typename R>
+static mgrg_status gpk_t(mgrg_plan *p, int level, int inverse, void *d, cudaStream_t s) {
+  const LevelGeom<R> &g = pt<R>(p).geom[level];
+  const uint64_t n = g.nodes();
+  gpk_inplace_kernel<R><<<unsigned((n + 255) / 256), 256, 0, s>>>(g, static_cast<R *>(d),
+                                                                   inverse);
+  CUDA_TRY(cudaGetLastError());
+  return MGRG_OK;
+}
+} // extern "C++"
+
+mgrg_status mgrg_gpk(mgrg_plan *p, int32_t level, int32_t inverse, void *d, void *stream) {
+  g_last_error.clear();
+  if (mgrg_status st = check_plan(p))
+    return st;
+  if (mgrg_status st = check_level(p, level))
+    return st;
+  if (!d)
+    return fail(MGRG_INVALID_ARGUMENT, "null device buffer");
+  DeviceGuard guard(p->device);
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  return p->dtype == MGRG_F32 ? gpk_t<float>(p, level, inverse, d, s)
+                              : gpk_t<double>(p, level, inverse, d, s);
+}
+
+extern "C++" {
+template <typename R>
+static mgrg_status masstrans_t(mgrg_plan *p, int level, int kd, const void *in, void *out,
+                               int fused, void *coef, cudaStream_t s) {
+  const LevelGeom<R> &g = pt<R>(p).geom[level];
+  uint32_t e[3];
+  for (int d = 0; d < 3; ++d)
+    e[d] = d < kd ? g.m[d] : g.n[d];
+  uint64_t total = 1;
+  for (int d = 0; d < 3; ++d)
+    total *= d == kd ? g.m[d] : e[d];
+  masstrans_kernel<R><<<unsigned((total + 255) / 256), 256, 0, s>>>(
+      g, kd, e[0], e[1], e[2], static_cast<const R *>(in), static_cast<R *>(out));
+  if (fused && coef) {
+    const uint64_t n = g.nodes();
+    class_copy_kernel<R><<<unsigned((n + 255) / 256), 256, 0, s>>>(
+        g, static_cast<const R *>(in), static_cast<R *>(coef));
+  }
+  CUDA_TRY(cudaGetLastError());
+  return MGRG_OK;
+}
+} // extern "C++"
+
+mgrg_status mgrg_masstrans(mgrg_plan *p, int32_t level, int32_t dim, const void *d_in,
+                           void *d_out, int32_t fused, void *d_coef, void *stream) {
+  g_last_error.clear();
+  if (mgrg_status st = check_plan(p))
+    return st;
+  if (mgrg_status st = check_level(p, level))
+    return st;
+  if (dim < 0 || dim >= p->H.nd)
+    return fail(MGRG_SHAPE_ERROR, "dimension " + std::to_string(dim) + " out of range");
+  if (fused && dim != 0)
+    return fail(MGRG_INVALID_FUSION, "coefficient copy can only fuse with dimension 0");
+  if (!d_in || !d_out)
+    return fail(MGRG_INVALID_ARGUMENT, "null device buffer");
+  DeviceGuard guard(p->device);
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  return p->dtype == MGRG_F32 ? masstrans_t<float>(p, level, dim, d_in, d_out, fused, d_coef, s)
+                              : masstrans_t<double>(p, level, dim, d_in, d_out, fused, d_coef, s);
+}
+
+extern "C++" {
+template <typename R>
+static mgrg_status solve_t(mgrg_plan *p, int level, int kd, void *f, cudaStream_t s) {
+  const LevelGeom<R> &g = pt<R>(p).geom[level];
+  if (!((g.refine >> kd) & 1))
+    return MGRG_OK; // identity transfer (kernels.hpp:434-435)
+  launch_thomas<R>(g, pt<R>(p).thom[level][kd], kd, static_cast<R *>(f), Epi::none,
+                   nullptr, nullptr, s);
+  CUDA_TRY(cudaGetLastError());
+  return MGRG_OK;
+}
+} // extern "C++"
+
+mgrg_status mgrg_solve(mgrg_plan *p, int32_t level, int32_t dim, void *d_f, void *stream) {
+  g_last_error.clear();
+  if (mgrg_status st = check_plan(p))
+    return st;
+  if (mgrg_status st = check_level(p, level))
+    return st;
+  if (dim < 0 || dim >= p->H.nd)
+    return fail(MGRG_SHAPE_ERROR, "dimension " + std::to_string(dim) + " out of range");
+  if (!d_f)
+    return fail(MGRG_INVALID_ARGUMENT, "null device buffer");
+  if (p->deferred)
+    return fail(p->deferred, p->deferred_msg);
+  DeviceGuard guard(p->device);
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  return p->dtype == MGRG_F32 ? solve_t<float>(p, level, dim, d_f, s)
+                              : solve_t<double>(p, level, dim, d_f, s);
+}
+
+mgrg_status mgrg_apply_correction(mgrg_plan *p, uint64_t count, void *d_v, const void *d_z,
+                                  int32_t sign, void *stream) {
+  g_last_error.clear();
+  if (mgrg_status st = check_plan(p))
+    return st;
+  if (!d_v || !d_z)
+    return fail(MGRG_INVALID_ARGUMENT, "null device buffer");
+  if (count == 0)
+    return MGRG_OK;
+  DeviceGuard guard(p->device);
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const unsigned blocks = unsigned((count + 255) / 256);
+  if (p->dtype == MGRG_F32)
+    apply_kernel<float><<<blocks, 256, 0, s>>>(count, static_cast<float *>(d_v),
+                                               static_cast<const float *>(d_z), sign);
+  else
+    apply_kernel<double><<<blocks, 256, 0, s>>>(count, static_cast<double *>(d_v),
+                                                static_cast<const double *>(d_z), sign);
+  CUDA_TRY(cudaGetLastError());
+  return MGRG_OK;
+}
+
+mgrg_status mgrg_reorder(mgrg_plan *p, int32_t level, int32_t dir, const void *d_in,
+                         void *d_out, void *stream) {
+  g_last_error.clear();
+  if (mgrg_status st = check_plan(p))
+    return st;
+  if (mgrg_status st = check_level(p, level))
+    return st;
+  if (!d_in || !d_out)
+    return fail(MGRG_INVALID_ARGUMENT, "null device buffer");
+  DeviceGuard guard(p->device);
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const uint64_t n = p->nodes[level];
+  const unsigned blocks = unsigned((n + 255) / 256);
+  if (p->dtype == MGRG_F32)
+    reorder_kernel<float><<<blocks, 256, 0, s>>>(p->pf.geom[level], dir,
+                                                 static_cast<const float *>(d_in),
+                                                 static_cast<float *>(d_out));
+  else
+    reorder_kernel<double><<<blocks, 256, 0, s>>>(p->pd.geom[level], dir,
+                                                  static_cast<const double *>(d_in),
+                                                  static_cast<double *>(d_out));
+  CUDA_TRY(cudaGetLastError());
+  return MGRG_OK;
+}
+
+} // extern "C"
