@@ -1,0 +1,464 @@
+#!/usr/bin/env python3
+"""Benchmark of the B200 decompose/recompose path (BASELINE.json config 4).
+
+Workload: one independent 3-D 1025^3 fp32 block per GPU (weak scaling,
+BASELINE.json configs[3]; the paper's embarrassingly parallel mode), the
+reference's smooth field S(x) (acceptance.cpp:383-393) evaluated on
+((x+gx)/2, (y+gy)/2, (z+gz)/2) for rank g.  One step = decompose of the block
+followed by the full recompose (classes_used = L), plus -- when N > 1 -- one
+NCCL all_gather of the fixed-size per-block metadata record (the only
+collective on the path).  The 4.3 GB input is 34x the 126 MB L2, so no L2
+flush is needed between iterations.
+
+Reported: value = aggregate refactoring throughput, GB/s of field data
+processed (each step processes every block twice: decompose + recompose)
+over the max-over-ranks device time; decompose / recompose GB/s separately;
+the dominant kernel's roofline (live CUDA-event timing of every launch over
+the timed region against its algorithmic bytes); the end-to-end number
+through the host-buffer C ABI entry points (H2D + device path + D2H); the
+reference CPU implementation on this box's cores (cpu_baseline).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+SHAPE = (1025, 1025, 1025)
+DTYPE = "float32"
+METRIC = "decompose/recompose GB/s (aggregate over GPUs)"
+WORKLOAD = "3D 1025^3 fp32 per GPU, block-sharded weak scaling (BASELINE configs[3])"
+FALLBACK_HBM_GBS = 6650.0
+
+
+def env_int(name, default):
+    try:
+        return int(os.environ.get(name, default))
+    except ValueError:
+        return default
+
+
+# ---------------------------------------------------------------------------
+# synthetic data
+# ---------------------------------------------------------------------------
+def field_factors(shape, rank):
+    """1-D fp64 factors of the separable smooth field for block `rank`."""
+    off = (rank & 1, (rank >> 1) & 1, (rank >> 2) & 1)
+    c1, c2 = (0.35, 0.4, 0.45), (0.7, 0.65, 0.6)
+    fac = []
+    for d, n in enumerate(shape):
+        x = (np.arange(n, dtype=np.float64) / (n - 1) + off[d]) / 2.0
+        fac.append((np.exp(-30 * (x - c1[d]) ** 2), np.exp(-25 * (x - c2[d]) ** 2),
+                    np.sin(2 * np.pi * x)))
+    return fac
+
+
+def make_field_device(shape, rank, device, dtype):
+    """S = e1x e1y e1z + 0.6 e2x e2y e2z + 0.2 sx sy sz on the device (fp64,
+    cast to the run dtype), row-major with x fastest."""
+    import torch
+
+    fac = field_factors(shape, rank)
+    t = [[torch.from_numpy(f).to(device) for f in fd] for fd in fac]
+    nx, ny, nz = shape
+    out = torch.empty(nz, ny, nx, dtype=getattr(torch, dtype), device=device)
+    for z0 in range(0, nz, 64):
+        z1 = min(nz, z0 + 64)
+        acc = None
+        for term, w in ((0, 1.0), (1, 0.6), (2, 0.2)):
+            fx, fy, fz = t[0][term], t[1][term], t[2][term][z0:z1]
+            p = w * fz[:, None, None] * fy[None, :, None] * fx[None, None, :]
+            acc = p if acc is None else acc + p
+        out[z0:z1] = acc.to(out.dtype)
+    return out.reshape(-1)
+
+
+# ---------------------------------------------------------------------------
+# clocks sampled during the timed region
+# ---------------------------------------------------------------------------
+class ClockSampler:
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "50"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self._t = threading.Thread(target=self._read, daemon=True)
+            self._t.start()
+        except (OSError, FileNotFoundError):
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        time.sleep(0.12)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        self._t.join(timeout=2)
+        sm, smax, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown",
+                 "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                smax = float(parts[1])
+            except ValueError:
+                continue
+            for nm, val in zip(names, parts[3:7]):
+                if val.lower() in ("active", "1", "yes"):
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": smax,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def hbm_peak():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(p) as f:
+            return float(json.load(f)["hbm_gbs"]), "measured"
+    except (OSError, KeyError, ValueError):
+        return FALLBACK_HBM_GBS, "fallback"
+
+
+def ncu_traffic():
+    """dram bytes per launch from the committed ncu --set full capture."""
+    p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    try:
+        with open(p) as f:
+            return json.load(f)
+    except (OSError, ValueError):
+        return {}
+
+
+# ---------------------------------------------------------------------------
+# CPU legs (test-infrastructure oracle: the reference compiled from its own
+# sources, oracle/_ref; else the C restatement)
+# ---------------------------------------------------------------------------
+def cpu_threads():
+    n = os.cpu_count() or 1
+    try:
+        n = len(os.sched_getaffinity(0))
+    except AttributeError:
+        pass
+    return max(1, min(n, 64))
+
+
+def cpu_sample(block_n: int, threads: int):
+    """decompose + recompose of `threads` independent block_n^3 fp32 blocks of
+    the same smooth-field family, one per thread; returns (GB/s, kind, secs)."""
+    import oracle
+
+    shape = (block_n,) * 3
+    blocks = []
+    for b in range(threads):
+        fac = field_factors(shape, b % 8)
+        v = np.zeros(shape[::-1], dtype=np.float64)
+        for term, w in ((0, 1.0), (1, 0.6), (2, 0.2)):
+            v += w * np.einsum("k,j,i->kji", fac[2][term], fac[1][term], fac[0][term])
+        blocks.append(v.astype(np.float32).reshape(-1))
+    nbytes = threads * blocks[0].nbytes
+    if oracle.available("ref"):
+        allv = np.concatenate(blocks)
+        td, tr = oracle.embarrassing_roundtrip_f32(allv, shape, threads, threads)
+        return 2 * nbytes / (td + tr) / 1e9, "reference", td + tr
+
+    # the C restatement, one ctypes call per block on its own thread (ctypes
+    # releases the GIL)
+    def one(v):
+        c, L = oracle.decompose(v, shape)
+        oracle.recompose(c, shape, L, L)
+
+    ths = [threading.Thread(target=one, args=(v,)) for v in blocks]
+    t0 = time.perf_counter()
+    for t in ths:
+        t.start()
+    for t in ths:
+        t.join()
+    dt = time.perf_counter() - t0
+    return 2 * nbytes / dt / 1e9, "port", dt
+
+
+# ---------------------------------------------------------------------------
+def run_reference(args, rank, world):
+    if rank != 0:
+        return
+    threads = cpu_threads()
+    block_n = 129
+    for _ in range(args.warmup):
+        cpu_sample(block_n, threads)
+    vals, secs = [], 0.0
+    kind = "reference"
+    for _ in range(args.steps):
+        v, kind, dt = cpu_sample(block_n, threads)
+        vals.append(v)
+        secs += dt
+    value = statistics.median(vals)
+    sample = (f"per step: {threads} independent {block_n}^3 fp32 blocks of the same "
+              f"smooth field, decompose+recompose, one per thread")
+    out = {
+        "impl": "reference", "metric": METRIC, "value": round(value, 4), "unit": "GB/s",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": round(1000 * secs / max(1, args.steps), 3),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "f32", "data": "synthetic",
+        "config": {"workload": WORKLOAD, "sample": sample},
+        "cpu_baseline": {"value": round(value, 4), "unit": "GB/s", "cores": threads,
+                         "kind": kind, "sample": sample},
+        "e2e": {"value": round(value, 4), "unit": "GB/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(out), flush=True)
+
+
+def run_e2e(plan, d_in, d_out, N, nbytes, L, K, dist, device, world):
+    """End to end through the host-buffer C ABI entry points (pinned host
+    memory): H2D of the inputs, the device path, D2H of the result, every
+    step."""
+    import torch
+
+    h_in = torch.empty(N, dtype=torch.float32, pin_memory=True)
+    h_in.copy_(d_in)
+    h_cls = torch.empty(N, dtype=torch.float32, pin_memory=True)
+    h_out = torch.empty(N, dtype=torch.float32, pin_memory=True)
+    hin, hcls, hout = h_in.numpy(), h_cls.numpy(), h_out.numpy()
+    plan.decompose_host(hin, hcls)  # warm (allocates the staging buffers)
+    plan.recompose_host(hcls, L, hout)
+    E = max(1, min(K, 3))
+    if dist is not None:
+        dist.barrier()
+    t0 = time.perf_counter()
+    for _ in range(E):
+        plan.decompose_host(hin, hcls)
+        plan.recompose_host(hcls, L, hout)
+    e2e_s = (time.perf_counter() - t0) / E
+    t = torch.tensor([e2e_s], dtype=torch.float64, device=device)
+    if dist is not None:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    e2e_s = t.item()
+    e2e_ok = bool(np.array_equal(hout, d_out.cpu().numpy()))
+    e2e = {"value": round(world * 2 * nbytes / e2e_s / 1e9, 3), "unit": "GB/s",
+           "h2d_bytes_per_step": 2 * nbytes, "d2h_bytes_per_step": 2 * nbytes,
+           "ms_per_step": round(1000 * e2e_s, 2), "steps": E,
+           "matches_device_path": e2e_ok}
+    return e2e
+
+def run_ours(args, rank, world, local_rank):
+    import torch
+
+    from paper_2105_12764_b200 import Plan
+
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+    device = torch.device("cuda", local_rank)
+    torch.cuda.set_device(device)
+    N = int(np.prod(SHAPE))
+    esize = 4
+    nbytes = N * esize
+
+    d_in = make_field_device(SHAPE, rank, device, DTYPE)
+    plan = Plan(SHAPE, DTYPE, device=local_rank)
+    L = plan.levels
+    d_cls = torch.empty(N, dtype=torch.float32, device=device)
+    d_out = torch.empty(N, dtype=torch.float32, device=device)
+    stream = torch.cuda.current_stream(device)
+
+    # per-block metadata record (gathered with NCCL every step when N > 1):
+    # block id, origin[3], shape[3], dtype bytes, L, class offsets 0..L+1
+    meta = np.zeros(64, dtype=np.int64)
+    meta[0] = rank
+    meta[1:4] = [1024 * (rank & 1), 1024 * ((rank >> 1) & 1), 1024 * ((rank >> 2) & 1)]
+    meta[4:7] = SHAPE
+    meta[7] = esize
+    meta[8] = L
+    offs = plan.class_offsets
+    meta[9:9 + len(offs)] = offs
+    d_meta = torch.from_numpy(meta).to(device)
+    d_meta_all = torch.empty(world * meta.size, dtype=torch.int64, device=device)
+
+    def step(ev_d=None, ev_r=None):
+        plan.decompose(d_in, d_cls, stream)
+        if ev_d is not None:
+            ev_d.record(stream)
+        plan.recompose(d_cls, L, d_out, stream)
+        if ev_r is not None:
+            ev_r.record(stream)
+        if dist is not None:
+            dist.all_gather_into_tensor(d_meta_all, d_meta)
+
+    for _ in range(max(3, args.warmup)):
+        step()
+    torch.cuda.synchronize()
+    # size-independent correctness of what is being timed: lossless round trip
+    diff = (d_out - d_in).abs().max().item()
+    rng = (d_in.max() - d_in.min()).item()
+    rt_err = diff / rng
+
+    K = args.steps
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+           for _ in range(K)]
+    e_start = torch.cuda.Event(enable_timing=True)
+    e_end = torch.cuda.Event(enable_timing=True)
+    plan.set_profiling(True)
+    sampler = ClockSampler(local_rank)
+    sampler.start()
+    time.sleep(0.2)
+    if dist is not None:
+        dist.barrier()
+    torch.cuda.synchronize()
+    e_start.record(stream)
+    prev = e_start
+    dec_ms, rec_ms = [], []
+    for i in range(K):
+        step(evs[i][0], evs[i][1])
+    e_end.record(stream)
+    torch.cuda.synchronize()
+    if dist is not None:
+        dist.barrier()
+    clocks = sampler.stop()
+    total_ms = e_start.elapsed_time(e_end)
+    for i in range(K):
+        dec_ms.append(prev.elapsed_time(evs[i][0]))
+        rec_ms.append(evs[i][0].elapsed_time(evs[i][1]))
+        prev = evs[i][1]
+    prof = plan.profile(reset=True)
+    plan.set_profiling(False)
+    launches_per_step = len(prof) // K if K else 0
+
+    t = torch.tensor([total_ms, statistics.median(dec_ms), statistics.median(rec_ms)],
+                     dtype=torch.float64, device=device)
+    if dist is not None:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    total_ms, dmed, rmed = t.tolist()
+    ms_step = total_ms / K
+    value = world * 2 * nbytes / (ms_step * 1e-3) / 1e9
+    dec_gbs = world * nbytes / (dmed * 1e-3) / 1e9
+    rec_gbs = world * nbytes / (rmed * 1e-3) / 1e9
+
+    # roofline of the dominant kernel launch (largest total device time)
+    peak, peak_kind = hbm_peak()
+    groups = {}
+    for kname, lvl, ms, by in prof:
+        g = groups.setdefault((kname, lvl), [0.0, 0, by])
+        g[0] += ms
+        g[1] += 1
+    (dk, dl), (dtot, dcnt, dbytes) = max(groups.items(), key=lambda kv: kv[1][0])
+    davg = dtot / dcnt
+    achieved = dbytes / (davg * 1e-3) / 1e9
+    step_dev_ms = sum(g[0] for g in groups.values()) / K
+    alg_step = sum(g[2] * g[1] for g in groups.values()) / K
+    traffic = ncu_traffic().get(f"{dk}/L{dl}")
+    roofline = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak,
+                "unit": "GB/s", "frac": round(achieved / peak, 4),
+                "traffic": traffic, "kernel": f"{dk} level {dl}",
+                "algorithmic_bytes_per_launch": dbytes,
+                "avg_launch_ms": round(davg, 4), "share_of_step": round(dtot / K / step_dev_ms, 3),
+                "peak_source": f"{peak_kind} (MEASURED_PEAKS.json hbm_gbs)"
+                if peak_kind == "measured" else "fallback 6.65 TB/s (B200_PROFILING.md)"}
+    step_roofline = {"algorithmic_bytes_per_step": alg_step,
+                     "achieved_GBps": round(alg_step / (ms_step * 1e-3) / 1e9, 1),
+                     "frac": round(alg_step / (ms_step * 1e-3) / 1e9 / peak, 4)}
+    per_kernel = {}
+    for (kname, lvl), (tot, cnt, by) in sorted(groups.items(), key=lambda kv: -kv[1][0])[:12]:
+        per_kernel[f"{kname}/L{lvl}"] = {"ms": round(tot / cnt, 4),
+                                         "GBps": round(by / (tot / cnt * 1e-3) / 1e9, 1)}
+
+    e2e = None
+    if not args.no_e2e:
+        e2e = run_e2e(plan, d_in, d_out, N, nbytes, L, K, dist, device, world)
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        threads = cpu_threads()
+        bn = 257
+        v, kind, dt = cpu_sample(bn, threads)
+        cpu = {"value": round(v, 4), "unit": "GB/s", "cores": threads, "kind": kind,
+               "sample": f"{threads} independent {bn}^3 fp32 smooth-field blocks, "
+                         f"decompose+recompose, one per thread ({dt:.1f} s wall)"}
+
+    if rank == 0:
+        out = {
+            "metric": METRIC, "value": round(value, 2), "unit": "GB/s", "n_gpus": world,
+            "steps": K, "warmup": max(3, args.warmup), "ms_per_step": round(ms_step, 4),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "f32", "data": "synthetic",
+            "config": {"workload": WORKLOAD, "shape": list(SHAPE), "levels": L,
+                       "blocks_per_gpu": 1, "step": "decompose + full recompose"
+                       + (" + NCCL all_gather of per-block metadata" if world > 1 else ""),
+                       "l2": "inputs (4.3 GB) larger than L2; no flush",
+                       "parallelism": f"embarrassing x{world}"},
+            "decompose_GBps": round(dec_gbs, 2), "recompose_GBps": round(rec_gbs, 2),
+            "roundtrip_rel_err": rt_err,
+            "roofline": roofline, "step_roofline": step_roofline,
+            "per_kernel": per_kernel,
+            "cpu_baseline": cpu, "e2e": e2e,
+            "gpu_launches": launches_per_step * K,
+            "clocks": clocks,
+        }
+        print(json.dumps(out), flush=True)
+    plan.close()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=100)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    ap.add_argument("--no-e2e", action="store_true", help="skip the host-buffer leg")
+    args = ap.parse_args()
+    world = env_int("WORLD_SIZE", 1)
+    rank = env_int("RANK", 0)
+    local_rank = env_int("LOCAL_RANK", 0)
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+
+        torch.cuda.set_device(local_rank)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    try:
+        run_ours(args, rank, world, local_rank)
+    finally:
+        if world > 1:
+            import torch.distributed as dist
+
+            dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

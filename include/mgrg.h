@@ -146,6 +146,26 @@ const char *mgrg_last_error(void);
 const char *mgrg_status_name(mgrg_status status);
 /* Kernel launches the last decompose/recompose issued on this plan. */
 mgrg_status mgrg_plan_last_launches(const mgrg_plan *plan, uint64_t *launches);
+/* Per-launch device timing.  With profiling on, every kernel the plan
+ * launches is bracketed by CUDA events on its stream (records accumulate
+ * across calls until reset).  mgrg_plan_profile_read waits for the recorded
+ * work, then fills up to `cap` entries: kernel kind (mgrg_kernel_kind),
+ * level, device milliseconds and the algorithmic HBM bytes of that launch
+ * (SURVEY.md §8(d) accounting); *count receives the number recorded. */
+typedef enum mgrg_kernel_kind {
+  MGRG_K_DEC_LEVEL = 0, /* GPK + class store + R*M (decompose)      */
+  MGRG_K_THOMAS_X = 1,  /* Thomas along dim 0 (+1, +2: dims 1, 2)   */
+  MGRG_K_THOMAS_Y = 2,
+  MGRG_K_THOMAS_Z = 3,
+  MGRG_K_REC_LOAD = 4,  /* class gather + R*M (recompose)           */
+  MGRG_K_REC_GPK = 5    /* coarse + class -> level array (recompose) */
+} mgrg_kernel_kind;
+mgrg_status mgrg_plan_set_profiling(mgrg_plan *plan, int32_t enable);
+mgrg_status mgrg_plan_profile_reset(mgrg_plan *plan);
+mgrg_status mgrg_plan_profile_read(mgrg_plan *plan, uint64_t cap, int32_t *kinds,
+                                   int32_t *levels, float *ms, uint64_t *bytes,
+                                   uint64_t *count);
+
 /* Library version string. */
 const char *mgrg_version(void);
 

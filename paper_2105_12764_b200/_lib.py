@@ -24,7 +24,11 @@ EXPORTS = (
     "mgrg_recompose_host", "mgrg_gpk", "mgrg_masstrans", "mgrg_solve",
     "mgrg_apply_correction", "mgrg_reorder", "mgrg_last_error",
     "mgrg_status_name", "mgrg_plan_last_launches", "mgrg_version",
+    "mgrg_plan_set_profiling", "mgrg_plan_profile_reset", "mgrg_plan_profile_read",
 )
+
+KERNEL_KINDS = {0: "dec_level", 1: "thomas_x", 2: "thomas_y", 3: "thomas_z",
+                4: "rec_load", 5: "rec_gpk"}
 
 
 class MissingExtension(ImportError):
@@ -71,6 +75,9 @@ def lib() -> ctypes.CDLL:
             "mgrg_apply_correction": [vp, u64, vp, vp, i32, vp],
             "mgrg_reorder": [vp, i32, i32, vp, vp, vp],
             "mgrg_plan_last_launches": [vp, ctypes.POINTER(u64)],
+            "mgrg_plan_set_profiling": [vp, i32],
+            "mgrg_plan_profile_reset": [vp],
+            "mgrg_plan_profile_read": [vp, u64, vp, vp, vp, vp, ctypes.POINTER(u64)],
         }
         for name, args in sig.items():
             fn = getattr(L, name)

@@ -13,7 +13,7 @@ LIB = os.path.join(PKG, "libmgrg.so")
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
     "-O3", "-lineinfo", "-std=c++17",
-    "-Xcompiler", "-fPIC,-O2", "-shared",
+    "-Xcompiler", "-fPIC,-O2,-ffp-contract=off", "-shared",
     "-I", os.path.join(ROOT, "include"),
 ]
 

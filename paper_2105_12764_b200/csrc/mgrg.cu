@@ -25,6 +25,7 @@
 
 #include "../../include/mgrg.h"
 #include "kernels.cuh"
+#include "kernels2.cuh"
 
 using namespace mgrg;
 
@@ -173,6 +174,7 @@ struct LaunchCount {
 template <typename R> struct PlanT {
   std::vector<LevelGeom<R>> geom;                 // [l], l = 1..L
   std::vector<std::array<ThomasGeom<R>, 3>> thom; // [l][kd] (level-(l-1) factors)
+  std::vector<std::array<const Stencil<R> *, 3>> sten; // [l][kd] merged R*M tables
   R *d_geom = nullptr;
 };
 
@@ -190,6 +192,7 @@ struct mgrg_plan {
   int refine_dims[3];
   int nrefine = 0;
   TileKind tile = TileKind::t32x8;
+  bool pair_path = false; // x and y refine: pair-lane kernels (kernels2.cuh)
   uint32_t zchunk = 32;
   mgrg_status deferred = MGRG_OK;         // SingularSystem found at build time
   std::string deferred_msg;
@@ -203,6 +206,16 @@ struct mgrg_plan {
   void *d_stage = nullptr;               // host-API staging (2N elements), lazy
   cudaStream_t own_stream = nullptr;
   uint64_t last_launches = 0;
+  // per-launch profiling (mgrg_plan_set_profiling)
+  bool profiling = false;
+  struct Prof {
+    int kind, level;
+    uint64_t bytes;
+    cudaEvent_t e0, e1;
+  };
+  std::vector<Prof> prof;
+  std::vector<cudaEvent_t> event_pool;
+  size_t prof_used = 0;
 };
 
 namespace {
@@ -261,13 +274,60 @@ bool thomas_factors(const std::vector<double> &hd, std::vector<R> &h,
   return true;
 }
 
+// Merged mass-trans coefficients of coarse output c along one dimension of
+// extent n (masstrans_window, kernels.hpp:159-178), computed in the working
+// precision exactly as the reference forms them: h cast to R, then
+// 2*(h[j-1]+h[j]), 2*h[0], 1 - r[q] in R.
+template <typename R>
+Stencil<R> make_stencil(const std::vector<double> &hd, const std::vector<double> &rd,
+                        uint64_t n, uint64_t c, bool allow_shift) {
+  auto h = [&](uint64_t i) { return R(hd[i]); };
+  auto r = [&](uint64_t i) { return R(rd[i]); };
+  auto dd = [&](uint64_t j) { return R(R(2) * R(h(j - 1) + h(j))); };
+  auto coarse = [&](uint64_t p) { return p % 2 == 0 || p == n - 1; };
+  const uint64_t q = std::min<uint64_t>(2 * c, n - 1);
+  Stencil<R> s{};
+  uint32_t fl = ST_VALID;
+  if (q == 0) {
+    fl |= ST_LEFT;
+    s.d0 = R(R(2) * h(0));
+    s.h0 = h(0);
+  } else if (q == n - 1) {
+    fl |= ST_RIGHT;
+    s.hm1 = h(n - 2);
+    s.d0 = R(R(2) * h(n - 2));
+  } else {
+    s.hm1 = h(q - 1);
+    s.d0 = dd(q);
+    s.h0 = h(q);
+  }
+  if (q >= 1 && !coarse(q - 1)) {
+    fl |= ST_HASL;
+    s.hm2 = h(q - 2);
+    s.dm1 = dd(q - 1);
+    s.hm1 = h(q - 1);
+    s.cl = r(q - 2);
+  }
+  if (q + 1 < n && !coarse(q + 1)) {
+    fl |= ST_HASR;
+    s.h0 = h(q);
+    s.dp1 = dd(q + 1);
+    s.hp1 = h(q + 1);
+    s.cr = R(R(1) - r(q));
+  }
+  if (allow_shift && q != 2 * c)
+    fl |= ST_SHIFT;
+  s.flags = fl;
+  return s;
+}
+
 template <typename R> mgrg_status upload_geometry(mgrg_plan *p) {
   const Hierarchy &H = p->H;
   const int L = H.L;
   // host staging of every per-level array in R, then one upload
   std::vector<R> buf;
   struct Ref {
-    size_t h[3], r[3], th[3], tf[3], ti[3];
+    size_t h[3], r[3], th[3], tf[3], ti[3], st[3];
   };
   std::vector<Ref> refs(L + 1);
   auto push = [&](const std::vector<R> &v) {
@@ -280,7 +340,7 @@ template <typename R> mgrg_status upload_geometry(mgrg_plan *p) {
   for (int l = 1; l <= L; ++l) {
     for (int kd = 0; kd < 3; ++kd) {
       refs[l].h[kd] = refs[l].r[kd] = refs[l].th[kd] = refs[l].tf[kd] =
-          refs[l].ti[kd] = size_t(-1);
+          refs[l].ti[kd] = refs[l].st[kd] = size_t(-1);
       const int ud = p->kmap[kd];
       if (ud < 0)
         continue;
@@ -301,6 +361,14 @@ template <typename R> mgrg_status upload_geometry(mgrg_plan *p) {
         refs[l].th[kd] = push(th);
         refs[l].tf[kd] = push(tf);
         refs[l].ti[kd] = push(ti);
+        // stencil table (raw bytes of Stencil<R>, a whole number of R's)
+        const uint64_t n = H.ext[l][ud], m = H.ext[l - 1][ud];
+        std::vector<R> raw(m * (sizeof(Stencil<R>) / sizeof(R)));
+        for (uint64_t c = 0; c < m; ++c) {
+          const Stencil<R> st = make_stencil<R>(H.h[ud][l], H.r[ud][l], n, c, kd < 2);
+          std::memcpy(raw.data() + c * (sizeof(Stencil<R>) / sizeof(R)), &st, sizeof(st));
+        }
+        refs[l].st[kd] = push(raw);
       }
     }
   }
@@ -313,6 +381,7 @@ template <typename R> mgrg_status upload_geometry(mgrg_plan *p) {
   PlanT<R> &P = pt<R>(p);
   P.geom.assign(L + 1, LevelGeom<R>{});
   P.thom.assign(L + 1, {});
+  P.sten.assign(L + 1, {nullptr, nullptr, nullptr});
   for (int l = 1; l <= L; ++l) {
     LevelGeom<R> &g = P.geom[l];
     g.refine = 0;
@@ -328,6 +397,9 @@ template <typename R> mgrg_status upload_geometry(mgrg_plan *p) {
       t.h = refs[l].th[kd] == size_t(-1) ? nullptr : base + refs[l].th[kd];
       t.fwd = refs[l].tf[kd] == size_t(-1) ? nullptr : base + refs[l].tf[kd];
       t.ip = refs[l].ti[kd] == size_t(-1) ? nullptr : base + refs[l].ti[kd];
+      P.sten[l][kd] = refs[l].st[kd] == size_t(-1)
+                          ? nullptr
+                          : reinterpret_cast<const Stencil<R> *>(base + refs[l].st[kd]);
     }
     fill_layout(g);
   }
@@ -375,6 +447,52 @@ void launch_rec_gpk(const LevelGeom<R> &g, const R *coarse, const R *cls, R *out
                                                               zchunk);
 }
 
+static_assert(sizeof(Stencil<float>) % sizeof(float) == 0, "stencil layout");
+static_assert(sizeof(Stencil<double>) % sizeof(double) == 0, "stencil layout");
+
+constexpr uint32_t kZChunk = 32; // coarse-z planes per CTA of the pair-lane kernels
+template <typename R> constexpr int pair_cy() { return sizeof(R) == 4 ? 16 : 8; }
+
+template <typename R, int CY> void set_pair_attrs() {
+  cudaFuncSetAttribute(dec2_kernel<R, CY>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       int(dec2_smem<R, CY>()));
+  cudaFuncSetAttribute(rl2_kernel<R, CY>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       int(rl2_smem<R, CY>()));
+  cudaFuncSetAttribute(rg2_kernel<R, CY>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       int(rg2_smem<R, CY>()));
+}
+
+template <typename R> dim3 pair_grid(const LevelGeom<R> &g, uint32_t cx) {
+  constexpr int CY = pair_cy<R>();
+  const uint32_t ntz = (g.refine & 4) ? (g.m[2] + kZChunk - 1) / kZChunk : g.m[2];
+  return dim3((g.m[0] + cx - 1) / cx, (g.m[1] + CY - 1) / CY, ntz);
+}
+
+template <typename R>
+void launch_dec2(const LevelGeom<R> &g, const std::array<const Stencil<R> *, 3> &st,
+                 const R *in, R *cls, R *P, R *f, cudaStream_t s) {
+  constexpr int CY = pair_cy<R>();
+  const dim3 grid = pair_grid(g, 30);
+  dec2_kernel<R, CY><<<grid, 256, dec2_smem<R, CY>(), s>>>(g, st[0], st[1], st[2], in, cls,
+                                                           P, f, grid.x, grid.y, grid.z);
+}
+template <typename R>
+void launch_rl2(const LevelGeom<R> &g, const std::array<const Stencil<R> *, 3> &st,
+                const R *cls, R *f, cudaStream_t s) {
+  constexpr int CY = pair_cy<R>();
+  const dim3 grid = pair_grid(g, 30);
+  rl2_kernel<R, CY><<<grid, 256, rl2_smem<R, CY>(), s>>>(g, st[0], st[1], st[2], cls, f,
+                                                         grid.x, grid.y, grid.z);
+}
+template <typename R>
+void launch_rg2(const LevelGeom<R> &g, const R *coarse, const R *cls, R *out,
+                cudaStream_t s) {
+  constexpr int CY = pair_cy<R>();
+  const dim3 grid = pair_grid(g, 32);
+  rg2_kernel<R, CY><<<grid, 256, rg2_smem<R, CY>(), s>>>(g, coarse, cls, out, grid.x,
+                                                         grid.y, grid.z);
+}
+
 // Batched Thomas along kernel dim kd of the m-lattice `g.m`.
 template <typename R>
 void launch_thomas(const LevelGeom<R> &g, const ThomasGeom<R> &t, int kd, R *f,
@@ -402,32 +520,81 @@ template <typename R> R *level_buf(mgrg_plan *p, int j) {
   return ((p->H.L - 1 - j) % 2 == 0) ? ws<R>(p, p->offA) : ws<R>(p, p->offB);
 }
 
+// Launch bookkeeping: counts every kernel of a call and, when profiling is
+// on, brackets each launch with CUDA events on the launch stream so the
+// caller can read per-kernel device time next to the algorithmic bytes.
+struct Recorder {
+  mgrg_plan *p;
+  cudaStream_t s;
+  uint64_t launches = 0;
+  mgrg_status begin(int kind, int level, uint64_t bytes);
+  mgrg_status end();
+};
+
+mgrg_status Recorder::begin(int kind, int level, uint64_t bytes) {
+  ++launches;
+  if (!p->profiling)
+    return MGRG_OK;
+  if (p->prof_used + 2 > p->event_pool.size()) {
+    for (int i = 0; i < 64; ++i) {
+      cudaEvent_t e;
+      CUDA_TRY(cudaEventCreate(&e));
+      p->event_pool.push_back(e);
+    }
+  }
+  mgrg_plan::Prof pr{kind, level, bytes, p->event_pool[p->prof_used],
+                     p->event_pool[p->prof_used + 1]};
+  p->prof_used += 2;
+  CUDA_TRY(cudaEventRecord(pr.e0, s));
+  p->prof.push_back(pr);
+  return MGRG_OK;
+}
+
+mgrg_status Recorder::end() {
+  if (!p->profiling)
+    return MGRG_OK;
+  CUDA_TRY(cudaEventRecord(p->prof.back().e1, s));
+  return MGRG_OK;
+}
+
 template <typename R>
 mgrg_status run_decompose(mgrg_plan *p, const R *d_in, R *d_cls, cudaStream_t s) {
   PlanT<R> &P = pt<R>(p);
   const int L = p->H.L;
   R *F = ws<R>(p, p->offF);
-  uint64_t launches = 0;
+  Recorder rec{p, s};
+  const uint64_t es = sizeof(R);
   for (int l = L; l >= 1; --l) {
     const LevelGeom<R> &g = P.geom[l];
+    const uint64_t Fn = g.nodes(), Cn = g.coarse_nodes();
     const R *a = l == L ? d_in : level_buf<R>(p, l);
     R *Pout = l == 1 ? d_cls : level_buf<R>(p, l - 1);
     R *cls = d_cls + p->nodes[l - 1];
-    if (p->tile == TileKind::t32x8)
+    // read F; write class (F-C) + packed coarse (C) + load vector (C)
+    if (mgrg_status st = rec.begin(MGRG_K_DEC_LEVEL, l, es * (2 * Fn + Cn)))
+      return st;
+    if (p->pair_path)
+      launch_dec2<R>(g, P.sten[l], a, cls, Pout, F, s);
+    else if (p->tile == TileKind::t32x8)
       launch_dec_level<R, 32, 8>(g, a, cls, Pout, F, p->zchunk, s);
     else
       launch_dec_level<R, 128, 1>(g, a, cls, Pout, F, p->zchunk, s);
-    ++launches;
+    if (mgrg_status st = rec.end())
+      return st;
     for (int i = 0; i < p->nrefine; ++i) {
       const int kd = p->refine_dims[i];
       const bool last = i == p->nrefine - 1;
+      // f in + z out; the fused apply also reads the packed coarse values
+      if (mgrg_status st = rec.begin(MGRG_K_THOMAS_X + kd, l, es * Cn * (last ? 3 : 2)))
+        return st;
       launch_thomas<R>(g, P.thom[l][kd], kd, F, last ? Epi::add : Epi::none, Pout,
                        Pout, s);
-      ++launches;
+      if (mgrg_status st = rec.end())
+        return st;
     }
   }
   CUDA_TRY(cudaGetLastError());
-  p->last_launches = launches;
+  p->last_launches = rec.launches;
   return MGRG_OK;
 }
 
@@ -437,41 +604,62 @@ mgrg_status run_recompose(mgrg_plan *p, const R *d_cls, int k, R *d_out,
   PlanT<R> &P = pt<R>(p);
   const int L = p->H.L;
   R *F = ws<R>(p, p->offF);
-  uint64_t launches = 0;
+  Recorder rec{p, s};
+  const uint64_t es = sizeof(R);
   for (int l = 1; l <= L; ++l) {
     const LevelGeom<R> &g = P.geom[l];
+    const uint64_t Fn = g.nodes(), Cn = g.coarse_nodes();
     const R *prev = l == 1 ? d_cls : level_buf<R>(p, l - 1);
     R *out = l == L ? d_out : level_buf<R>(p, l);
     const R *cls = d_cls + p->nodes[l - 1];
     if (l <= k) {
-      if (p->tile == TileKind::t32x8)
+      // read class (F-C); write load vector (C)
+      if (mgrg_status st = rec.begin(MGRG_K_REC_LOAD, l, es * Fn))
+        return st;
+      if (p->pair_path)
+        launch_rl2<R>(g, P.sten[l], cls, F, s);
+      else if (p->tile == TileKind::t32x8)
         launch_rec_load<R, 32, 8>(g, cls, F, p->zchunk, s);
       else
         launch_rec_load<R, 128, 1>(g, cls, F, p->zchunk, s);
-      ++launches;
+      if (mgrg_status st = rec.end())
+        return st;
       for (int i = 0; i < p->nrefine; ++i) {
         const int kd = p->refine_dims[i];
         const bool last = i == p->nrefine - 1;
+        if (mgrg_status st = rec.begin(MGRG_K_THOMAS_X + kd, l, es * Cn * (last ? 3 : 2)))
+          return st;
         launch_thomas<R>(g, P.thom[l][kd], kd, F, last ? Epi::sub : Epi::none, prev,
                          F, s);
-        ++launches;
+        if (mgrg_status st = rec.end())
+          return st;
       }
-      if (p->tile == TileKind::t32x8)
+      // read coarse' (C) + class (F-C); write the level array (F)
+      if (mgrg_status st = rec.begin(MGRG_K_REC_GPK, l, es * 2 * Fn))
+        return st;
+      if (p->pair_path)
+        launch_rg2<R>(g, F, cls, out, s);
+      else if (p->tile == TileKind::t32x8)
         launch_rec_gpk<R, 32, 8>(g, F, cls, out, p->zchunk, s);
       else
         launch_rec_gpk<R, 128, 1>(g, F, cls, out, p->zchunk, s);
     } else {
       // classes above classes_used are zero: f = 0, z = +0 exactly, so the
       // coarse values are a_{l-1} unchanged and the fine ones interp + 0.
-      if (p->tile == TileKind::t32x8)
+      if (mgrg_status st = rec.begin(MGRG_K_REC_GPK, l, es * (Fn + Cn)))
+        return st;
+      if (p->pair_path)
+        launch_rg2<R>(g, prev, nullptr, out, s);
+      else if (p->tile == TileKind::t32x8)
         launch_rec_gpk<R, 32, 8>(g, prev, nullptr, out, p->zchunk, s);
       else
         launch_rec_gpk<R, 128, 1>(g, prev, nullptr, out, p->zchunk, s);
     }
-    ++launches;
+    if (mgrg_status st = rec.end())
+      return st;
   }
   CUDA_TRY(cudaGetLastError());
-  p->last_launches = launches;
+  p->last_launches = rec.launches;
   return MGRG_OK;
 }
 
@@ -546,6 +734,10 @@ mgrg_status mgrg_plan_create(const mgrg_grid_desc *desc, mgrg_plan **out) {
       p->refine_dims[p->nrefine++] = kd;
     }
   p->tile = nd == 1 ? TileKind::t128x1 : TileKind::t32x8;
+  p->pair_path = (p->refine & 3u) == 3u;
+  if (const char *gp = std::getenv("MGRG_GENERIC"))
+    if (std::atoi(gp) != 0)
+      p->pair_path = false;
   p->zchunk = nd == 3 ? 32 : 1;
   if (const char *zc = std::getenv("MGRG_ZCHUNK"))
     if (nd == 3 && std::atoi(zc) > 0)
@@ -573,9 +765,11 @@ mgrg_status mgrg_plan_create(const mgrg_grid_desc *desc, mgrg_plan **out) {
   if (p->dtype == MGRG_F32) {
     set_smem_attrs<float, 32, 8>();
     set_smem_attrs<float, 128, 1>();
+    set_pair_attrs<float, pair_cy<float>()>();
   } else {
     set_smem_attrs<double, 32, 8>();
     set_smem_attrs<double, 128, 1>();
+    set_pair_attrs<double, pair_cy<double>()>();
   }
   CUDA_TRY(cudaGetLastError());
   *out = p.release();
@@ -587,6 +781,8 @@ mgrg_status mgrg_plan_destroy(mgrg_plan *p) {
     return MGRG_OK;
   {
     DeviceGuard guard(p->device);
+    for (cudaEvent_t e : p->event_pool)
+      cudaEventDestroy(e);
     cudaFree(p->d_geom);
     cudaFree(p->d_ws);
     cudaFree(p->d_stage);
@@ -643,6 +839,48 @@ mgrg_status mgrg_plan_last_launches(const mgrg_plan *p, uint64_t *launches) {
   if (mgrg_status st = check_plan(p))
     return st;
   *launches = p->last_launches;
+  return MGRG_OK;
+}
+
+mgrg_status mgrg_plan_set_profiling(mgrg_plan *p, int32_t enable) {
+  if (mgrg_status st = check_plan(p))
+    return st;
+  p->profiling = enable != 0;
+  return MGRG_OK;
+}
+
+mgrg_status mgrg_plan_profile_reset(mgrg_plan *p) {
+  if (mgrg_status st = check_plan(p))
+    return st;
+  p->prof.clear();
+  p->prof_used = 0;
+  return MGRG_OK;
+}
+
+mgrg_status mgrg_plan_profile_read(mgrg_plan *p, uint64_t cap, int32_t *kinds,
+                                   int32_t *levels, float *ms, uint64_t *bytes,
+                                   uint64_t *count) {
+  if (mgrg_status st = check_plan(p))
+    return st;
+  DeviceGuard guard(p->device);
+  if (count)
+    *count = p->prof.size();
+  if (!p->prof.empty())
+    CUDA_TRY(cudaEventSynchronize(p->prof.back().e1));
+  for (uint64_t i = 0; i < p->prof.size() && i < cap; ++i) {
+    const auto &pr = p->prof[i];
+    if (kinds)
+      kinds[i] = pr.kind;
+    if (levels)
+      levels[i] = pr.level;
+    if (bytes)
+      bytes[i] = pr.bytes;
+    if (ms) {
+      float t = 0.f;
+      CUDA_TRY(cudaEventElapsedTime(&t, pr.e0, pr.e1));
+      ms[i] = t;
+    }
+  }
   return MGRG_OK;
 }
 

@@ -116,6 +116,32 @@ class Plan:
         _lib.check(_lib.lib().mgrg_plan_last_launches(self._h, ctypes.byref(n)))
         return n.value
 
+    # -- per-launch profiling ------------------------------------------------------
+    def set_profiling(self, enable: bool = True):
+        _lib.check(_lib.lib().mgrg_plan_set_profiling(self._h, int(enable)))
+        _lib.check(_lib.lib().mgrg_plan_profile_reset(self._h))
+
+    def profile(self, reset: bool = True):
+        """[(kernel, level, ms, algorithmic_bytes)] of the launches recorded
+        since profiling was enabled / last reset (waits for them)."""
+        L = _lib.lib()
+        cnt = ctypes.c_uint64()
+        _lib.check(L.mgrg_plan_profile_read(self._h, 0, None, None, None, None,
+                                            ctypes.byref(cnt)))
+        n = cnt.value
+        kinds = np.empty(n, np.int32)
+        levels = np.empty(n, np.int32)
+        ms = np.empty(n, np.float32)
+        by = np.empty(n, np.uint64)
+        if n:
+            _lib.check(L.mgrg_plan_profile_read(self._h, n, kinds.ctypes.data,
+                                                levels.ctypes.data, ms.ctypes.data,
+                                                by.ctypes.data, ctypes.byref(cnt)))
+        if reset:
+            _lib.check(L.mgrg_plan_profile_reset(self._h))
+        return [(_lib.KERNEL_KINDS[int(k)], int(l), float(t), int(b))
+                for k, l, t, b in zip(kinds, levels, ms, by)]
+
     # -- device entry points (torch CUDA tensors) --------------------------------
     def _torch_dtype(self):
         import torch

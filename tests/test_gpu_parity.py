@@ -16,6 +16,10 @@ SHAPES = [
     (9, 17), (33, 5), (12, 10), (6, 4), (2, 9), (9, 2), (65, 65), (129, 67),
     (9, 9, 9), (17, 9, 5), (12, 10, 9), (5, 7, 4), (3, 3, 3), (9, 2, 5), (2, 5, 9),
     (33, 33, 33), (65, 40, 37), (66, 35, 19), (70, 3, 9),
+    # multi-tile / multi-chunk pair-lane paths (x tiles of 30, y of 8/16,
+    # z chunks of 32 coarse planes), odd and even extents
+    (129, 17, 9), (17, 9, 129), (66, 35, 99), (100, 70, 80), (257, 33, 70),
+    (61, 62, 64), (200, 150), (4097, 5), (5, 300),
 ]
 
 
