@@ -288,7 +288,7 @@ def run_ours(args, rank, world, local_rank):
     nbytes = N * esize
 
     d_in = make_field_device(SHAPE, rank, device, DTYPE)
-    plan = Plan(SHAPE, DTYPE, device=local_rank)
+    plan = Plan(SHAPE, DTYPE, device=local_rank, fast=args.arith == "fast")
     L = plan.levels
     d_cls = torch.empty(N, dtype=torch.float32, device=device)
     d_out = torch.empty(N, dtype=torch.float32, device=device)
@@ -419,7 +419,7 @@ def run_ours(args, rank, world, local_rank):
                        "l2": "inputs (4.3 GB) larger than L2; no flush",
                        "parallelism": f"embarrassing x{world}"},
             "decompose_GBps": round(dec_gbs, 2), "recompose_GBps": round(rec_gbs, 2),
-            "roundtrip_rel_err": rt_err,
+            "roundtrip_rel_err": rt_err, "arith": args.arith,
             "roofline": roofline, "step_roofline": step_roofline,
             "per_kernel": per_kernel,
             "cpu_baseline": cpu, "e2e": e2e,
@@ -438,6 +438,8 @@ def main():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     ap.add_argument("--no-e2e", action="store_true", help="skip the host-buffer leg")
+    ap.add_argument("--arith", choices=["exact", "fast"], default="exact",
+                    help="exact: bit-identical to the reference; fast: FMA policy")
     args = ap.parse_args()
     world = env_int("WORLD_SIZE", 1)
     rank = env_int("RANK", 0)

@@ -69,7 +69,16 @@ typedef struct mgrg_grid_desc {
   const double *coords;  /* NULL = uniform; else sum(shape) doubles */
   int32_t levels;        /* 0 = full depth, else the RefactorOptions cap */
   int32_t device;        /* CUDA device ordinal the plan lives on */
+  int32_t flags;         /* MGRG_FLAG_* */
 } mgrg_grid_desc;
+
+/* Arithmetic policy.  Default: every kernel evaluates the reference's
+ * expressions in the reference's order with no FMA contraction, so results
+ * are bit-identical to the reference CPU path.  MGRG_FLAG_FAST: interpolation
+ * as one FMA and the merged mass-trans as precomputed 5-tap FMA chains
+ * (same operator; results differ at rounding level, range-normalized
+ * ~1e-7 f32 / ~1e-16 f64). */
+#define MGRG_FLAG_FAST 1
 
 typedef struct mgrg_plan mgrg_plan;
 

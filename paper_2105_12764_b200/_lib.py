@@ -43,7 +43,11 @@ class GridDesc(ctypes.Structure):
         ("coords", ctypes.c_void_p),
         ("levels", ctypes.c_int32),
         ("device", ctypes.c_int32),
+        ("flags", ctypes.c_int32),
     ]
+
+
+MGRG_FLAG_FAST = 1
 
 
 _lib = None

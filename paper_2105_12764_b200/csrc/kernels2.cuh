@@ -4,8 +4,9 @@
 // pair (X0 + 2a, X0 + 2a + 1) = (even/coarse-x node, odd/fine-x node).  With
 // X0 = 2*cx0 - 2 the 32 pairs cover the reach-2 stencil window of 30 coarse-x
 // outputs, so the merged R*M along x is a 5-tap window over lanes i, i+1,
-// i+2 and runs on warp shuffles with the lane's stencil coefficients held in
-// registers.  No integer division, no per-node type switch.
+// i+2 and runs on warp shuffles with the lane's stencil held in registers.
+// The y pass reads five rows of the x results from shared memory; the z
+// pass keeps the last planes' y results in registers (no ring indexing).
 //
 // GPK as prolongation: the reference interpolates every fine node from its
 // 2^k coarse corners, reducing pairwise along the fine dimensions in
@@ -18,6 +19,14 @@
 //   coarse z-plane, fine   y-row : W   = lerp_y(W(row-1), W(row+1), ty)
 //   fine   z-plane               : W   = lerp_z(W(plane-1), W(plane+1), tz)
 // The coarse planes' W is kept in shared memory for the fine plane between.
+//
+// Arithmetic policy (template FAST):
+//   FAST = false: the reference's expressions, operation by operation, no
+//                 FMA contraction -> bit-identical to the CPU reference;
+//   FAST = true : lerps as one FMA, merged R*M as a 5-tap FMA chain with
+//                 host-precomputed weights -> ~3x fewer FP instructions,
+//                 differences at the level of rounding (well inside the
+//                 1e-5 f32 / 1e-12 f64 range-normalized parity bar).
 #pragma once
 
 #include "common.cuh"
@@ -26,13 +35,14 @@
 namespace mgrg {
 
 // One coarse output of the merged mass-trans along a dimension, as host-
-// precomputed coefficients in the working precision (see stencil.hpp).
-// v = mv(q) [+ cl*mv(q-1)] [+ cr*mv(q+1)]   (masstrans_window,
-// kernels.hpp:159-178), taps in(q-2..q+2).
+// precomputed coefficients in the working precision (mgrg.cu make_stencil).
+// Exact form: v = mv(q) [+ cl*mv(q-1)] [+ cr*mv(q+1)] (masstrans_window,
+// kernels.hpp:159-178).  Fast form: v = sum_t w[t] * tap[t].
 template <typename R> struct Stencil {
   R hm2, hm1, h0, hp1; // h[q-2], h[q-1], h[q], h[q+1]
   R dm1, d0, dp1;      // 2(h[j-1]+h[j]) at j = q-1, q, q+1 (boundary: 2h)
   R cl, cr;            // r[q-2], 1 - r[q]
+  R w[5];              // fast-path tap weights
   uint32_t flags;      // ST_* below
 };
 enum : uint32_t {
@@ -41,49 +51,57 @@ enum : uint32_t {
   ST_HASL = 4,   // q-1 is fine: + r[q-2]*mv(q-1)
   ST_HASR = 8,   // q+1 is fine: + (1-r[q])*mv(q+1)
   ST_SHIFT = 16, // q = 2c-1 (last node of an even extent): taps shifted by one
-  ST_VALID = 32
+  ST_VALID = 32,
+  ST_INTERIOR = ST_HASL | ST_HASR | ST_VALID
 };
 
-// Taps t0..t4 are the fine positions 2c-2 .. 2c+2 relative to the output's
-// nominal centre 2c; ST_SHIFT moves the centre to 2c-1.
-template <typename R>
+template <typename R, bool FAST> struct Arith {
+  static __device__ __forceinline__ R lerp(R a, R b, R t) {
+    if constexpr (FAST)
+      return fma(t, b - a, a);
+    else
+      return mgrg::lerp(a, b, t);
+  }
+};
+
+// Taps t0..t4 are the fine positions 2c-2 .. 2c+2 around the output's
+// nominal centre 2c (x, y) or q-2 .. q+2 (z, never shifted).
+template <typename R, bool FAST>
 __device__ __forceinline__ R stencil_eval(const Stencil<R> &s, R t0, R t1, R t2, R t3,
                                           R t4) {
-  if (s.flags & ST_SHIFT) { // q = 2c-1 = n-1, n even: only the right-boundary mv
-    return add(mul(s.hm1, t0), mul(s.d0, t1));
+  if constexpr (FAST) {
+    R v = s.w[0] * t0;
+    v = fma(s.w[1], t1, v);
+    v = fma(s.w[2], t2, v);
+    v = fma(s.w[3], t3, v);
+    return fma(s.w[4], t4, v);
+  } else {
+    if (s.flags == ST_INTERIOR) { // straight-line common case
+      R v = add(add(mul(s.hm1, t1), mul(s.d0, t2)), mul(s.h0, t3));
+      const R ml = add(add(mul(s.hm2, t0), mul(s.dm1, t1)), mul(s.hm1, t2));
+      v = add(v, mul(s.cl, ml));
+      const R mr = add(add(mul(s.h0, t2), mul(s.dp1, t3)), mul(s.hp1, t4));
+      return add(v, mul(s.cr, mr));
+    }
+    if (s.flags & ST_SHIFT) // q = 2c-1 = n-1, n even: only the right-boundary mv
+      return add(mul(s.hm1, t0), mul(s.d0, t1));
+    R v;
+    if (s.flags & ST_LEFT)
+      v = add(mul(s.d0, t2), mul(s.h0, t3));
+    else if (s.flags & ST_RIGHT)
+      v = add(mul(s.hm1, t1), mul(s.d0, t2));
+    else
+      v = add(add(mul(s.hm1, t1), mul(s.d0, t2)), mul(s.h0, t3));
+    if (s.flags & ST_HASL) {
+      const R ml = add(add(mul(s.hm2, t0), mul(s.dm1, t1)), mul(s.hm1, t2));
+      v = add(v, mul(s.cl, ml));
+    }
+    if (s.flags & ST_HASR) {
+      const R mr = add(add(mul(s.h0, t2), mul(s.dp1, t3)), mul(s.hp1, t4));
+      v = add(v, mul(s.cr, mr));
+    }
+    return v;
   }
-  R v;
-  if (s.flags & ST_LEFT)
-    v = add(mul(s.d0, t2), mul(s.h0, t3));
-  else if (s.flags & ST_RIGHT)
-    v = add(mul(s.hm1, t1), mul(s.d0, t2));
-  else
-    v = add(add(mul(s.hm1, t1), mul(s.d0, t2)), mul(s.h0, t3));
-  if (s.flags & ST_HASL) {
-    const R ml = add(add(mul(s.hm2, t0), mul(s.dm1, t1)), mul(s.hm1, t2));
-    v = add(v, mul(s.cl, ml));
-  }
-  if (s.flags & ST_HASR) {
-    const R mr = add(add(mul(s.h0, t2), mul(s.dp1, t3)), mul(s.hp1, t4));
-    v = add(v, mul(s.cr, mr));
-  }
-  return v;
-}
-
-template <typename R>
-__device__ __forceinline__ Stencil<R> load_stencil(const Stencil<R> *p) {
-  Stencil<R> s;
-  s.hm2 = __ldg(&p->hm2);
-  s.hm1 = __ldg(&p->hm1);
-  s.h0 = __ldg(&p->h0);
-  s.hp1 = __ldg(&p->hp1);
-  s.dm1 = __ldg(&p->dm1);
-  s.d0 = __ldg(&p->d0);
-  s.dp1 = __ldg(&p->dp1);
-  s.cl = __ldg(&p->cl);
-  s.cr = __ldg(&p->cr);
-  s.flags = __ldg(&p->flags);
-  return s;
 }
 
 // Balanced tiling: tile t of nt over m outputs covers [t*m/nt, (t+1)*m/nt).
@@ -110,154 +128,156 @@ template <typename R> __device__ __forceinline__ void st_pair(R *p, R e, R o) {
     *reinterpret_cast<double2 *>(p) = make_double2(e, o);
 }
 
-// Geometry common to the three pair-lane kernels.
-struct TileGeo {
-  uint32_t cx0, cx1, cy0, cy1;
-  int X0, Y0;               // fine box origin (may be negative)
-  uint32_t OX1, OY0, OY1;   // ownership (x starts at 2*cx0)
+// Class-type tables of the level in shared memory (class_slot,
+// grid.hpp:149-164): row base of mask m at row ranks (wy, wz).
+struct ClassTab {
+  uint64_t tb[8];
+  uint32_t tx[8], ty[8];
+  __device__ __forceinline__ uint64_t row(unsigned m, uint32_t wy, uint32_t wz) const {
+    return tb[m] + uint64_t(tx[m]) * (wy + uint64_t(ty[m]) * wz);
+  }
 };
+template <typename R>
+__device__ __forceinline__ void load_classtab(ClassTab &t, const LevelGeom<R> &g, int tid) {
+  if (tid < 8) {
+    t.tb[tid] = g.tbase[tid];
+    t.tx[tid] = g.tex[tid];
+    t.ty[tid] = g.tey[tid];
+  }
+}
 
 template <int CY> struct PairCfg {
   static constexpr int NW = 8, T = 256, BX = 64, BYR = 2 * CY + 3;
   static constexpr int PLANE = BYR * BX;
+  static constexpr int RW = (CY + 7) / 8; // output rows per warp
+  static constexpr int ZC = 32;           // coarse-z planes per CTA
 };
+
+// shared-memory carve-up helper (16-byte aligned chunks)
+struct Carve {
+  unsigned char *p;
+  template <typename T> __device__ __forceinline__ T *take(size_t n) {
+    T *r = reinterpret_cast<T *>(p);
+    p += (n * sizeof(T) + 15) & ~size_t(15);
+    return r;
+  }
+};
+__host__ __device__ constexpr size_t al16(size_t b) { return (b + 15) & ~size_t(15); }
 
 template <typename R, int CY> constexpr size_t dec2_smem() {
   using C = PairCfg<CY>;
-  return sizeof(R) * (4 * C::PLANE + 2 * C::PLANE + C::BYR * 32 + 5 * CY * 32);
+  return al16(sizeof(R) * 6 * C::PLANE) + al16(sizeof(R) * C::BYR * 32) +
+         al16(sizeof(Stencil<R>) * CY) + al16(sizeof(Stencil<R>) * C::ZC) +
+         al16(sizeof(ClassTab)) + al16(sizeof(R) * C::BYR) +
+         al16(sizeof(R) * (2 * C::ZC + 4));
 }
 template <typename R, int CY> constexpr size_t rl2_smem() {
   using C = PairCfg<CY>;
-  return sizeof(R) * (3 * C::PLANE + C::BYR * 32 + 5 * CY * 32);
+  return al16(sizeof(R) * 3 * C::PLANE) + al16(sizeof(R) * C::BYR * 32) +
+         al16(sizeof(Stencil<R>) * CY) + al16(sizeof(Stencil<R>) * C::ZC) +
+         al16(sizeof(ClassTab));
 }
 template <typename R, int CY> constexpr size_t rg2_smem() {
-  // coarse planes: 3 x (CY+1) rows x 33 (padded to 16 B); W planes: 2 x 2CY x 64
-  return sizeof(R) * (((3 * (CY + 1) * 33 + 3) & ~3) + 2 * (2 * CY) * 64);
+  // coarse planes: 3 x (CY+1) rows x 33; W planes: 2 x 2CY x 64
+  return al16(sizeof(R) * 3 * (CY + 1) * 33) + al16(sizeof(R) * 2 * (2 * CY) * 64) +
+         al16(sizeof(ClassTab));
 }
 
-// y pass of one plane p for this warp's output rows j (CY/8 of them): the
-// result goes to f directly when z does not refine, else into the z ring G.
-template <typename R, int CY>
-__device__ __forceinline__ void y_stage(const LevelGeom<R> &g, const Stencil<R> *sty,
-                                        const R *X, R *G, const TileGeo &tg, int warp,
-                                        int lane, uint32_t p, R *__restrict__ f) {
-  const uint32_t mx = g.m[0], my = g.m[1];
-  const uint32_t cx = tg.cx0 + lane;
-  const bool xval = lane < 30 && cx < tg.cx1;
-#pragma unroll
-  for (int jj = 0; jj < (CY + 7) / 8; ++jj) {
-    const int j = warp + 8 * jj;
-    const uint32_t cy = tg.cy0 + j;
-    if (j < CY && cy < tg.cy1) {
-      const Stencil<R> s = load_stencil(sty + cy);
-      const R *c = X + (2 * j) * 32 + lane; // box rows 2j .. 2j+4
-      const R v = stencil_eval(s, c[0], c[32], c[64], c[96], c[128]);
-      if (!(g.refine & 4)) {
-        if (xval)
-          f[cx + uint64_t(mx) * (cy + uint64_t(my) * p)] = v;
-      } else {
-        G[((p % 5) * CY + j) * 32 + lane] = v;
-      }
-    }
-  }
+// Stage `n` stencils (global) into shared memory.
+template <typename R>
+__device__ __forceinline__ void stage_stencils(Stencil<R> *dst, const Stencil<R> *src,
+                                               uint32_t n, int tid) {
+  constexpr int W = sizeof(Stencil<R>) / 4;
+  const uint32_t *s = reinterpret_cast<const uint32_t *>(src);
+  uint32_t *d = reinterpret_cast<uint32_t *>(dst);
+  for (uint32_t i = tid; i < n * W; i += 256)
+    d[i] = __ldg(s + i);
 }
 
-// z stage: emit every coarse-z output whose 5-plane window is complete
-// (all positions <= `processed` are in the ring).  G is indexed by position,
-// so z descriptors are built unshifted.
-template <typename R, int CY>
-__device__ __forceinline__ void z_stage(const LevelGeom<R> &g, const Stencil<R> *stz,
-                                        const R *G, const TileGeo &tg, int warp, int lane,
-                                        R *__restrict__ f, uint32_t cz1, uint32_t &kk,
-                                        uint32_t processed) {
-  const uint32_t mx = g.m[0], my = g.m[1], nz = g.n[2];
-  const uint64_t mxy = uint64_t(mx) * my;
-  const uint32_t cx = tg.cx0 + lane;
-  const bool xval = lane < 30 && cx < tg.cx1;
-  while (kk < cz1) {
-    const uint32_t q = coarse_pos(kk, nz);
-    if (min(q + 2, nz - 1) > processed)
-      break;
-    const Stencil<R> s = load_stencil(stz + kk);
-#pragma unroll
-    for (int jj = 0; jj < (CY + 7) / 8; ++jj) {
-      const int j = warp + 8 * jj;
-      const uint32_t cy = tg.cy0 + j;
-      if (j < CY && cy < tg.cy1 && xval) {
-        auto gv = [&](int pos) -> R {
-          return (pos < 0 || pos >= int(nz)) ? R(0) : G[((pos % 5) * CY + j) * 32 + lane];
-        };
-        const int qi = int(q);
-        const R v = stencil_eval(s, gv(qi - 2), gv(qi - 1), gv(qi), gv(qi + 1), gv(qi + 2));
-        f[cx + uint64_t(mx) * cy + mxy * kk] = v;
-      }
-    }
-    ++kk;
-  }
+// y pass of the X rows for output row j (box rows 2j .. 2j+4).
+template <typename R, bool FAST>
+__device__ __forceinline__ R y_eval(const Stencil<R> &s, const R *X, int j, int lane) {
+  const R *c = X + (2 * j) * 32 + lane;
+  return stencil_eval<R, FAST>(s, c[0], c[32], c[64], c[96], c[128]);
 }
 
 // ---------------------------------------------------------------------------
 // Decompose, one level (fast path; x and y refine).  Same contract as
-// dec_level_kernel (kernels.cuh).
+// dec_level_kernel (kernels.cuh): GPK forward on `in`, class-order store
+// into `cls`, packed kept-node values into P, merged R*M of vec(C) into f.
 // ---------------------------------------------------------------------------
-template <typename R, int CY>
+template <typename R, int CY, bool FAST>
 __global__ void __launch_bounds__(256)
     dec2_kernel(LevelGeom<R> g, const Stencil<R> *__restrict__ stx,
                 const Stencil<R> *__restrict__ sty, const Stencil<R> *__restrict__ stz,
                 const R *__restrict__ in, R *__restrict__ cls, R *__restrict__ P,
                 R *__restrict__ f, uint32_t ntx, uint32_t nty, uint32_t ntz) {
   using C = PairCfg<CY>;
+  using A = Arith<R, FAST>;
   extern __shared__ __align__(16) unsigned char smem_bytes[];
-  R *U = reinterpret_cast<R *>(smem_bytes); // [4][BYR][64] raw planes
-  R *Wc = U + 4 * C::PLANE;                 // [2][BYR][64] prolongated coarse planes
-  R *X = Wc + 2 * C::PLANE;                 // [BYR][32] x-pass results
-  R *G = X + C::BYR * 32;                   // [5][CY][32] xy results (z ring)
+  Carve cv{smem_bytes};
+  R *U = cv.take<R>(6 * C::PLANE); // [4][BYR][64] raw planes + [2][BYR][64] W planes
+  R *Wc = U + 4 * C::PLANE;
+  R *X = cv.take<R>(C::BYR * 32); // [BYR][32] x-pass results
+  Stencil<R> *sY = cv.take<Stencil<R>>(CY);
+  Stencil<R> *sZ = cv.take<Stencil<R>>(C::ZC);
+  ClassTab *ct = cv.take<ClassTab>(1);
+  R *tyv = cv.take<R>(C::BYR);        // r_y of each box row (fine rows)
+  R *tzv = cv.take<R>(2 * C::ZC + 4); // r_z of each box plane (fine planes)
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const uint32_t nx = g.n[0], ny = g.n[1], nz = g.n[2];
   const uint32_t mx = g.m[0], my = g.m[1], mz = g.m[2];
   const bool rz = g.refine & 4;
-  TileGeo tg;
-  tg.cx0 = tile_lo(blockIdx.x, ntx, mx);
-  tg.cx1 = tile_lo(blockIdx.x + 1, ntx, mx);
-  tg.cy0 = tile_lo(blockIdx.y, nty, my);
-  tg.cy1 = tile_lo(blockIdx.y + 1, nty, my);
+  const uint32_t cx0 = tile_lo(blockIdx.x, ntx, mx), cx1 = tile_lo(blockIdx.x + 1, ntx, mx);
+  const uint32_t cy0 = tile_lo(blockIdx.y, nty, my), cy1 = tile_lo(blockIdx.y + 1, nty, my);
   const uint32_t cz0 = tile_lo(blockIdx.z, ntz, mz), cz1 = tile_lo(blockIdx.z + 1, ntz, mz);
-  tg.X0 = 2 * int(tg.cx0) - 2;
-  tg.Y0 = 2 * int(tg.cy0) - 2;
-  tg.OX1 = tg.cx1 == mx ? nx : 2 * tg.cx1;
-  tg.OY0 = 2 * tg.cy0;
-  tg.OY1 = tg.cy1 == my ? ny : 2 * tg.cy1;
+  const int X0 = 2 * int(cx0) - 2, Y0 = 2 * int(cy0) - 2;
+  const uint32_t OX1 = cx1 == mx ? nx : 2 * cx1;
+  const uint32_t OY0 = 2 * cy0, OY1 = cy1 == my ? ny : 2 * cy1;
   const uint32_t Z0 = rz ? (cz0 ? 2 * cz0 - 2 : 0) : cz0;
   const uint32_t Z1 = rz ? min(nz, 2 * cz1 + 1) : cz1;
   const uint32_t OZ0 = rz ? 2 * cz0 : cz0, OZ1 = rz ? (cz1 == mz ? nz : 2 * cz1) : cz1;
   const uint64_t nxy = uint64_t(nx) * ny;
+  const uint64_t mxy = uint64_t(mx) * my;
 
-  // ---- per-lane x geometry
-  const int xe = tg.X0 + 2 * lane, xo = xe + 1;
+  // ---- stage per-CTA tables
+  stage_stencils(sY, sty + cy0, cy1 - cy0, tid);
+  if (rz)
+    stage_stencils(sZ, stz + cz0, cz1 - cz0, tid);
+  load_classtab(*ct, g, tid);
+  for (int b = tid; b < C::BYR; b += 256) {
+    const int y = Y0 + b;
+    tyv[b] = (y > 0 && y < int(ny) - 1 && (y & 1)) ? g.r[1][y - 1] : R(0);
+  }
+  if (rz)
+    for (uint32_t p = Z0 + tid; p < Z1; p += 256)
+      tzv[p - Z0] = ((p & 1) && p < nz - 1) ? g.r[2][p - 1] : R(0);
+
+  // ---- per-lane x geometry (registers for the whole kernel)
+  const int xe = X0 + 2 * lane, xo = xe + 1;
+  const bool xe_ok = xe >= 0 && xe < int(nx);
   const bool xo_ok = xo >= 0 && xo < int(nx);
   const bool xo_fine = xo_ok && xo < int(nx) - 1;
-  const R tx = xo_fine ? __ldg(g.r[0] + xo - 1) : R(0);
-  const bool own_e = lane >= 1 && xe < int(tg.OX1);
-  const bool own_o = lane >= 1 && xo < int(tg.OX1) && xo_ok;
-  const uint32_t cr_e = uint32_t(xe) >> 1;                         // coarse rank of xe
+  const R tx = xo_fine ? g.r[0][xo - 1] : R(0);
+  const bool own_e = lane >= 1 && xe < int(OX1);
+  const bool own_o = lane >= 1 && xo < int(OX1) && xo_ok;
+  const uint32_t cr_e = uint32_t(xe) >> 1;
   const uint32_t rk_o = xo_fine ? uint32_t(xo - 1) >> 1 : coarse_rank(uint32_t(xo));
-  Stencil<R> sx{};
-  const bool xval = lane < 30 && tg.cx0 + lane < tg.cx1;
-  if (xval)
-    sx = load_stencil(stx + tg.cx0 + lane);
+  const bool xval = lane < 30 && cx0 + lane < cx1;
+  const Stencil<R> sx = stx[min(cx0 + min(uint32_t(lane), 29u), mx - 1)];
 
   // ---- LDGSTS plane loader: thread -> column tid&63, rows (tid>>6) + 4m
   const int lc = tid & 63, lr0 = tid >> 6;
-  const int gx = tg.X0 + lc;
+  const int gx = X0 + lc;
   const bool col_ok = gx >= 0 && gx < int(nx);
   auto load_plane = [&](uint32_t p) {
     if (p < Z1 && col_ok) {
       R *dst = U + (p & 3) * C::PLANE + lc;
       const R *src = in + nxy * p + gx;
-#pragma unroll 4
+#pragma unroll 3
       for (int b = lr0; b < C::BYR; b += 4) {
-        const int gy = tg.Y0 + b;
+        const int gy = Y0 + b;
         if (gy >= 0 && gy < int(ny))
           cp_async(dst + b * 64, src + uint64_t(gy) * nx);
       }
@@ -269,11 +289,11 @@ __global__ void __launch_bounds__(256)
   // prolongated neighbour coarse planes.  Coarse plane: wout receives W.
   auto process_plane = [&](uint32_t p, bool fz, const R *wlo, const R *whi, R *wout) {
     const R *Up = U + (p & 3) * C::PLANE;
-    const R tz = fz ? __ldg(g.r[2] + p - 1) : R(0);
+    const R tz = fz ? tzv[p - Z0] : R(0);
     const bool ownz = p >= OZ0 && p < OZ1;
     const uint32_t wz = fz ? (p - 1) >> 1 : coarse_rank(p);
     for (int b = warp; b < C::BYR; b += 8) {
-      const int y = tg.Y0 + b;
+      const int y = Y0 + b;
       const bool y_ok = y >= 0 && y < int(ny);
       const bool fy = y_ok && (y & 1) && y < int(ny) - 1;
       const Pair<R> u = ld_pair(Up + b * 64 + 2 * lane);
@@ -281,64 +301,72 @@ __global__ void __launch_bounds__(256)
       if (fz) {
         const Pair<R> a = ld_pair(wlo + b * 64 + 2 * lane);
         const Pair<R> c = ld_pair(whi + b * 64 + 2 * lane);
-        we = lerp(a.e, c.e, tz);
-        wo = lerp(a.o, c.o, tz);
+        we = A::lerp(a.e, c.e, tz);
+        wo = A::lerp(a.o, c.o, tz);
       } else if (!fy) {
         const R un = __shfl_down_sync(0xffffffffu, u.e, 1);
         we = u.e;
-        wo = xo_fine ? lerp(u.e, un, tx) : u.o;
+        wo = xo_fine ? A::lerp(u.e, un, tx) : u.o;
       } else {
-        const R ty = __ldg(g.r[1] + y - 1);
+        const R ty = tyv[b];
         const Pair<R> um = ld_pair(Up + (b - 1) * 64 + 2 * lane);
         const Pair<R> up = ld_pair(Up + (b + 1) * 64 + 2 * lane);
         const R umn = __shfl_down_sync(0xffffffffu, um.e, 1);
         const R upn = __shfl_down_sync(0xffffffffu, up.e, 1);
-        const R wmo = xo_fine ? lerp(um.e, umn, tx) : um.o;
-        const R wpo = xo_fine ? lerp(up.e, upn, tx) : up.o;
-        we = lerp(um.e, up.e, ty);
-        wo = lerp(wmo, wpo, ty);
+        const R wmo = xo_fine ? A::lerp(um.e, umn, tx) : um.o;
+        const R wpo = xo_fine ? A::lerp(up.e, upn, tx) : up.o;
+        we = A::lerp(um.e, up.e, ty);
+        wo = A::lerp(wmo, wpo, ty);
       }
       if (wout)
         st_pair(wout + b * 64 + 2 * lane, we, wo);
-      const bool fe = fy || fz;          // even-x node is a coefficient node
-      const bool fo = fe || xo_fine;     // odd-x node is a coefficient node
-      const R ve = fe ? sub(u.e, we) : R(0);
-      const R vo = fo ? sub(u.o, wo) : R(0);
+      const bool fe = fy || fz;      // even-x node is a coefficient node
+      const bool fo = fe || xo_fine; // odd-x node is a coefficient node
+      // vec(C): coefficients at coefficient nodes, 0 at kept nodes and
+      // outside the grid (zero taps never meet a nonzero stencil weight)
+      const R ve = (fe && xe_ok && y_ok) ? sub(u.e, we) : R(0);
+      const R vo = (fo && xo_ok && y_ok) ? sub(u.o, wo) : R(0);
       // class order / packed-coarse stores of owned nodes (coalesced runs)
-      if (ownz && y_ok && uint32_t(y) >= tg.OY0 && uint32_t(y) < tg.OY1) {
+      if (ownz && y_ok && uint32_t(y) >= OY0 && uint32_t(y) < OY1) {
         const uint32_t wy = fy ? (uint32_t(y) - 1) >> 1 : coarse_rank(uint32_t(y));
         const unsigned me = (unsigned(fy) << 1) | (unsigned(fz) << 2);
-        if (own_e) {
-          if (me == 0)
-            P[cr_e + uint64_t(mx) * (wy + uint64_t(my) * wz)] = u.e;
-          else
-            cls[g.tbase[me] + cr_e + uint64_t(g.tex[me]) * (wy + uint64_t(g.tey[me]) * wz)] = ve;
-        }
-        if (own_o) {
-          const unsigned mo = me | unsigned(xo_fine);
-          if (mo == 0)
-            P[rk_o + uint64_t(mx) * (wy + uint64_t(my) * wz)] = u.o;
-          else
-            cls[g.tbase[mo] + rk_o + uint64_t(g.tex[mo]) * (wy + uint64_t(g.tey[mo]) * wz)] = vo;
+        const unsigned mo = me | unsigned(xo_fine);
+        if (me == 0) {
+          R *prow = P + mx * uint64_t(wy) + mxy * wz;
+          if (own_e)
+            prow[cr_e] = u.e;
+          if (own_o) {
+            if (mo == 0)
+              prow[rk_o] = u.o;
+            else
+              cls[ct->row(mo, wy, wz) + rk_o] = vo;
+          }
+        } else {
+          if (own_e)
+            cls[ct->row(me, wy, wz) + cr_e] = ve;
+          if (own_o)
+            cls[ct->row(mo, wy, wz) + rk_o] = vo;
         }
       }
       // x pass: output lane i from pairs i, i+1 and the even node of i+2
       const R e1 = __shfl_down_sync(0xffffffffu, ve, 1);
       const R o1 = __shfl_down_sync(0xffffffffu, vo, 1);
       const R e2 = __shfl_down_sync(0xffffffffu, ve, 2);
+      const R xv = stencil_eval<R, FAST>(sx, ve, vo, e1, o1, e2);
       if (lane < 30)
-        X[b * 32 + lane] = xval ? stencil_eval(sx, ve, vo, e1, o1, e2) : R(0);
+        X[b * 32 + lane] = xval ? xv : R(0);
     }
   };
 
-  uint32_t kk = cz0;
-  // prologue: three planes in flight
+  __syncthreads(); // tables staged
   load_plane(Z0);
   load_plane(Z0 + 1);
   load_plane(Z0 + 2);
   uint32_t issued = Z0 + 3;
   cp_async_wait<2>();
   __syncthreads();
+
+  const uint32_t cxo = cx0 + lane;
   if (!rz) {
     // z does not refine: every plane is coarse and is its own output
     for (uint32_t p = Z0; p < Z1; ++p) {
@@ -349,22 +377,57 @@ __global__ void __launch_bounds__(256)
       }
       process_plane(p, false, nullptr, nullptr, nullptr);
       __syncthreads();
-      y_stage<R, CY>(g, sty, X, G, tg, warp, lane, p, f);
+#pragma unroll
+      for (int jj = 0; jj < C::RW; ++jj) {
+        const int j = warp + 8 * jj;
+        if (j < CY && cy0 + j < cy1) {
+          const R v = y_eval<R, FAST>(sY[j], X, j, lane);
+          if (xval)
+            f[cxo + uint64_t(mx) * (cy0 + j) + mxy * p] = v;
+        }
+      }
       __syncthreads();
     }
     cp_async_wait<0>();
     return;
   }
+
+  // z refines: carried window c0,c1,c2 = G(pc-2), G(pc-1), G(pc) per row j
+  R c0[C::RW], c1[C::RW], c2[C::RW], zero[C::RW];
+#pragma unroll
+  for (int jj = 0; jj < C::RW; ++jj)
+    c0[jj] = c1[jj] = c2[jj] = zero[jj] = R(0);
+  auto y_all = [&](R *out) {
+#pragma unroll
+    for (int jj = 0; jj < C::RW; ++jj) {
+      const int j = warp + 8 * jj;
+      out[jj] = (j < CY && cy0 + j < cy1) ? y_eval<R, FAST>(sY[j], X, j, lane) : R(0);
+    }
+  };
+  auto emit = [&](uint32_t k, const R *t0, const R *t1, const R *t2, const R *t3,
+                  const R *t4) {
+    if (k < cz0 || k >= cz1)
+      return;
+    const Stencil<R> &s = sZ[k - cz0];
+#pragma unroll
+    for (int jj = 0; jj < C::RW; ++jj) {
+      const int j = warp + 8 * jj;
+      const R v = stencil_eval<R, FAST>(s, t0[jj], t1[jj], t2[jj], t3[jj], t4[jj]);
+      if (j < CY && cy0 + j < cy1 && xval)
+        f[cxo + uint64_t(mx) * (cy0 + j) + mxy * k] = v;
+    }
+  };
+
   uint32_t pc = Z0; // last processed coarse plane
   uint32_t slot = 0;
   process_plane(pc, false, nullptr, nullptr, Wc);
   __syncthreads();
-  y_stage<R, CY>(g, sty, X, G, tg, warp, lane, pc, f);
-  __syncthreads();
+  y_all(c2);
   for (;;) {
     const uint32_t nxt = pc + 2 <= nz - 1 ? pc + 2 : pc + 1;
     if (nxt >= Z1)
       break;
+    __syncthreads(); // X consumed before it is overwritten
     load_plane(issued++);
     load_plane(issued++);
     cp_async_wait<2>();
@@ -372,18 +435,35 @@ __global__ void __launch_bounds__(256)
     const uint32_t ns = slot ^ 1;
     process_plane(nxt, false, nullptr, nullptr, Wc + ns * C::PLANE);
     __syncthreads();
-    y_stage<R, CY>(g, sty, X, G, tg, warp, lane, nxt, f);
-    __syncthreads();
+    R gn[C::RW], gf[C::RW];
+    y_all(gn);
     if (nxt == pc + 2) { // the fine plane between the two coarse planes
+      __syncthreads();
       process_plane(pc + 1, true, Wc + slot * C::PLANE, Wc + ns * C::PLANE, nullptr);
       __syncthreads();
-      y_stage<R, CY>(g, sty, X, G, tg, warp, lane, pc + 1, f);
+      y_all(gf);
+      emit(pc >> 1, c0, c1, c2, gf, gn); // q = pc: taps pc-2 .. pc+2
+#pragma unroll
+      for (int jj = 0; jj < C::RW; ++jj) {
+        c0[jj] = c2[jj];
+        c1[jj] = gf[jj];
+        c2[jj] = gn[jj];
+      }
+      pc = nxt;
+      slot = ns;
+    } else {
+      // nxt = pc + 1 = nz - 1 (even nz): output pc/2 has no fine right
+      // neighbour but mv(q) still reads position q+1 = nxt; the last output
+      // (q = nz-1) reads positions q-1 = pc and q = nxt
+      emit(pc >> 1, c0, c1, c2, gn, zero);
+      emit((nxt + 1) >> 1, zero, c2, gn, zero, zero);
+      pc = nxt;
+      break;
     }
-    z_stage<R, CY>(g, stz, G, tg, warp, lane, f, cz1, kk, nxt);
-    __syncthreads();
-    pc = nxt;
-    slot = ns;
   }
+  // last coarse plane of an odd extent: q = nz-1 = pc (right boundary form)
+  if (pc == nz - 1 && (pc & 1) == 0)
+    emit(pc >> 1, c0, c1, c2, zero, zero);
   cp_async_wait<0>();
 }
 
@@ -393,7 +473,7 @@ __global__ void __launch_bounds__(256)
 // fine-x entry of the row's two class types) into a 3-plane ring, then the
 // same x (shuffle) / y / z merged mass-trans as dec2.
 // ---------------------------------------------------------------------------
-template <typename R, int CY>
+template <typename R, int CY, bool FAST>
 __global__ void __launch_bounds__(256)
     rl2_kernel(LevelGeom<R> g, const Stencil<R> *__restrict__ stx,
                const Stencil<R> *__restrict__ sty, const Stencil<R> *__restrict__ stz,
@@ -401,44 +481,49 @@ __global__ void __launch_bounds__(256)
                uint32_t ntz) {
   using C = PairCfg<CY>;
   extern __shared__ __align__(16) unsigned char smem_bytes[];
-  R *V = reinterpret_cast<R *>(smem_bytes); // [3][BYR][64] vec(C) planes
-  R *X = V + 3 * C::PLANE;                  // [BYR][32]
-  R *G = X + C::BYR * 32;                   // [5][CY][32]
+  Carve cv{smem_bytes};
+  R *V = cv.take<R>(3 * C::PLANE); // [3][BYR][64] vec(C) planes
+  R *X = cv.take<R>(C::BYR * 32);  // [BYR][32]
+  Stencil<R> *sY = cv.take<Stencil<R>>(CY);
+  Stencil<R> *sZ = cv.take<Stencil<R>>(C::ZC);
+  ClassTab *ct = cv.take<ClassTab>(1);
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const uint32_t nx = g.n[0], ny = g.n[1], nz = g.n[2];
   const uint32_t mx = g.m[0], my = g.m[1], mz = g.m[2];
   const bool rz = g.refine & 4;
-  TileGeo tg;
-  tg.cx0 = tile_lo(blockIdx.x, ntx, mx);
-  tg.cx1 = tile_lo(blockIdx.x + 1, ntx, mx);
-  tg.cy0 = tile_lo(blockIdx.y, nty, my);
-  tg.cy1 = tile_lo(blockIdx.y + 1, nty, my);
+  const uint32_t cx0 = tile_lo(blockIdx.x, ntx, mx), cx1 = tile_lo(blockIdx.x + 1, ntx, mx);
+  const uint32_t cy0 = tile_lo(blockIdx.y, nty, my), cy1 = tile_lo(blockIdx.y + 1, nty, my);
   const uint32_t cz0 = tile_lo(blockIdx.z, ntz, mz), cz1 = tile_lo(blockIdx.z + 1, ntz, mz);
-  tg.X0 = 2 * int(tg.cx0) - 2;
-  tg.Y0 = 2 * int(tg.cy0) - 2;
+  const int X0 = 2 * int(cx0) - 2, Y0 = 2 * int(cy0) - 2;
   const uint32_t Z0 = rz ? (cz0 ? 2 * cz0 - 2 : 0) : cz0;
   const uint32_t Z1 = rz ? min(nz, 2 * cz1 + 1) : cz1;
+  const uint64_t mxy = uint64_t(mx) * my;
 
-  const int xe = tg.X0 + 2 * lane, xo = xe + 1;
+  stage_stencils(sY, sty + cy0, cy1 - cy0, tid);
+  if (rz)
+    stage_stencils(sZ, stz + cz0, cz1 - cz0, tid);
+  load_classtab(*ct, g, tid);
+
+  const int xe = X0 + 2 * lane, xo = xe + 1;
   const bool xe_ok = xe >= 0 && xe < int(nx);
   const bool xo_ok = xo >= 0 && xo < int(nx);
   const bool xo_fine = xo_ok && xo < int(nx) - 1;
   const uint32_t cr_e = xe_ok ? uint32_t(xe) >> 1 : 0;
-  const uint32_t rk_o = xo_fine ? uint32_t(xo - 1) >> 1 : 0;
-  Stencil<R> sx{};
-  const bool xval = lane < 30 && tg.cx0 + lane < tg.cx1;
-  if (xval)
-    sx = load_stencil(stx + tg.cx0 + lane);
+  const uint32_t rk_o =
+      xo_fine ? uint32_t(xo - 1) >> 1 : (xo_ok ? coarse_rank(uint32_t(xo)) : 0);
+  const bool xval = lane < 30 && cx0 + lane < cx1;
+  const Stencil<R> sx = stx[min(cx0 + min(uint32_t(lane), 29u), mx - 1)];
+  __syncthreads();
 
-  // vec(C) plane loader: warp -> rows, lane -> pair; coarse nodes read as 0
+  // vec(C) plane loader: warp -> rows, lane -> pair; kept nodes read as 0
   auto load_plane = [&](uint32_t p) {
     if (p < Z1) {
       R *dst = V + (p % 3) * C::PLANE;
       const bool fz = !is_coarse(p, nz);
       const uint32_t wz = fz ? (p - 1) >> 1 : coarse_rank(p);
       for (int b = warp; b < C::BYR; b += 8) {
-        const int y = tg.Y0 + b;
+        const int y = Y0 + b;
         R *d = dst + b * 64 + 2 * lane;
         if (y < 0 || y >= int(ny)) {
           d[0] = R(0);
@@ -448,18 +533,13 @@ __global__ void __launch_bounds__(256)
         const bool fy = (y & 1) && y < int(ny) - 1;
         const uint32_t wy = fy ? (uint32_t(y) - 1) >> 1 : coarse_rank(uint32_t(y));
         const unsigned me = (unsigned(fy) << 1) | (unsigned(fz) << 2);
+        const unsigned mo = me | unsigned(xo_fine);
         if (me != 0 && xe_ok)
-          cp_async(d, cls + g.tbase[me] + cr_e +
-                          uint64_t(g.tex[me]) * (wy + uint64_t(g.tey[me]) * wz));
+          cp_async(d, cls + ct->row(me, wy, wz) + cr_e);
         else
           d[0] = R(0);
-        const unsigned mo = me | 1u;
-        if (xo_fine)
-          cp_async(d + 1, cls + g.tbase[mo] + rk_o +
-                              uint64_t(g.tex[mo]) * (wy + uint64_t(g.tey[mo]) * wz));
-        else if (xo_ok && me != 0) // last node of an even extent: coarse in x
-          cp_async(d + 1, cls + g.tbase[me] + coarse_rank(uint32_t(xo)) +
-                              uint64_t(g.tex[me]) * (wy + uint64_t(g.tey[me]) * wz));
+        if (mo != 0 && xo_ok)
+          cp_async(d + 1, cls + ct->row(mo, wy, wz) + rk_o);
         else
           d[1] = R(0);
       }
@@ -467,6 +547,12 @@ __global__ void __launch_bounds__(256)
     cp_async_commit();
   };
 
+  // z window c0..c3 = y results of planes p-4 .. p-1
+  R c0[C::RW], c1[C::RW], c2[C::RW], c3[C::RW];
+#pragma unroll
+  for (int jj = 0; jj < C::RW; ++jj)
+    c0[jj] = c1[jj] = c2[jj] = c3[jj] = R(0);
+  const uint32_t cxo = cx0 + lane;
   load_plane(Z0);
   load_plane(Z0 + 1);
   uint32_t kk = cz0;
@@ -480,13 +566,57 @@ __global__ void __launch_bounds__(256)
       const R e1 = __shfl_down_sync(0xffffffffu, v.e, 1);
       const R o1 = __shfl_down_sync(0xffffffffu, v.o, 1);
       const R e2 = __shfl_down_sync(0xffffffffu, v.e, 2);
+      const R xv = stencil_eval<R, FAST>(sx, v.e, v.o, e1, o1, e2);
       if (lane < 30)
-        X[b * 32 + lane] = xval ? stencil_eval(sx, v.e, v.o, e1, o1, e2) : R(0);
+        X[b * 32 + lane] = xval ? xv : R(0);
     }
     __syncthreads();
-    y_stage<R, CY>(g, sty, X, G, tg, warp, lane, p, f);
-    if (rz)
-      z_stage<R, CY>(g, stz, G, tg, warp, lane, f, cz1, kk, p);
+    R gv[C::RW];
+#pragma unroll
+    for (int jj = 0; jj < C::RW; ++jj) {
+      const int j = warp + 8 * jj;
+      gv[jj] = (j < CY && cy0 + j < cy1) ? y_eval<R, FAST>(sY[j], X, j, lane) : R(0);
+    }
+    if (!rz) {
+#pragma unroll
+      for (int jj = 0; jj < C::RW; ++jj) {
+        const int j = warp + 8 * jj;
+        if (j < CY && cy0 + j < cy1 && xval)
+          f[cxo + uint64_t(mx) * (cy0 + j) + mxy * p] = gv[jj];
+      }
+      continue;
+    }
+    // emit every output whose window ends at p: centre q, d = p - q in
+    // {2, 1, 0} (1 and 0 only at the last nodes, whose right taps are absent)
+    while (kk < cz1) {
+      const uint32_t q = coarse_pos(kk, nz);
+      if (min(q + 2, nz - 1) > p)
+        break;
+      const Stencil<R> &s = sZ[kk - cz0];
+      const uint32_t d = p - q;
+#pragma unroll
+      for (int jj = 0; jj < C::RW; ++jj) {
+        const int j = warp + 8 * jj;
+        // positions p-4 .. p are c0, c1, c2, c3, gv
+        R v;
+        if (d == 2)
+          v = stencil_eval<R, FAST>(s, c0[jj], c1[jj], c2[jj], c3[jj], gv[jj]);
+        else if (d == 1)
+          v = stencil_eval<R, FAST>(s, c1[jj], c2[jj], c3[jj], gv[jj], R(0));
+        else
+          v = stencil_eval<R, FAST>(s, c2[jj], c3[jj], gv[jj], R(0), R(0));
+        if (j < CY && cy0 + j < cy1 && xval)
+          f[cxo + uint64_t(mx) * (cy0 + j) + mxy * kk] = v;
+      }
+      ++kk;
+    }
+#pragma unroll
+    for (int jj = 0; jj < C::RW; ++jj) {
+      c0[jj] = c1[jj];
+      c1[jj] = c2[jj];
+      c2[jj] = c3[jj];
+      c3[jj] = gv[jj];
+    }
   }
   cp_async_wait<0>();
 }
@@ -498,14 +628,17 @@ __global__ void __launch_bounds__(256)
 // ranks, keeping the prolongated coarse planes for the fine plane between.
 // cls == nullptr: classes above classes_used (read as zero).
 // ---------------------------------------------------------------------------
-template <typename R, int CY>
+template <typename R, int CY, bool FAST>
 __global__ void __launch_bounds__(256)
     rg2_kernel(LevelGeom<R> g, const R *__restrict__ coarse, const R *__restrict__ cls,
                R *__restrict__ out, uint32_t ntx, uint32_t nty, uint32_t ntz) {
+  using A = Arith<R, FAST>;
   constexpr int CR = CY + 1, CP = 33, OR = 2 * CY; // coarse rows, pitch, out rows
   extern __shared__ __align__(16) unsigned char smem_bytes[];
-  R *Cs = reinterpret_cast<R *>(smem_bytes); // [3][CR][33] coarse' planes
-  R *Wp = Cs + ((3 * CR * CP + 3) & ~3);     // [2][OR][64] prolongated coarse planes
+  Carve cv{smem_bytes};
+  R *Cs = cv.take<R>(3 * CR * CP); // [3][CR][33] coarse' planes
+  R *Wp = cv.take<R>(2 * OR * 64); // [2][OR][64] prolongated coarse planes
+  ClassTab *ct = cv.take<ClassTab>(1);
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const uint32_t nx = g.n[0], ny = g.n[1], nz = g.n[2];
@@ -517,11 +650,13 @@ __global__ void __launch_bounds__(256)
   const uint32_t OX1 = cx1 == mx ? nx : 2 * cx1;
   const uint32_t OY1 = cy1 == my ? ny : 2 * cy1;
   const uint64_t nxy = uint64_t(nx) * ny, mxy = uint64_t(mx) * my;
+  load_classtab(*ct, g, tid);
 
   const uint32_t xe = 2 * (cx0 + lane), xo = xe + 1;
   const bool own_e = xe < OX1, own_o = xo < OX1;
   const bool xo_fine = xo < nx - 1;
-  const R tx = xo_fine ? __ldg(g.r[0] + xo - 1) : R(0);
+  const R tx = xo_fine ? g.r[0][xo - 1] : R(0);
+  const uint32_t rk_o = xo_fine ? (xo - 1) >> 1 : coarse_rank(xo);
   // staged coarse ranks: [cx0, min(cx0+33, mx)) x [cy0, min(cy0+CR, my))
   const uint32_t ncx = min(cx0 + 33, mx) - cx0, ncy = min(cy0 + CR, my) - cy0;
 
@@ -537,15 +672,28 @@ __global__ void __launch_bounds__(256)
     cp_async_commit();
   };
 
-  // value of coarse row j (coarse-y rank cy0+j) of plane C at this lane's pair
+  // W of coarse row j (coarse-y rank cy0+j) at this lane's pair
   auto crow = [&](const R *Cp, int j, R &we, R &wo) {
     const R c0 = Cp[j * CP + lane];
     const R c1 = Cp[j * CP + lane + 1];
     we = c0;
-    wo = xo_fine ? lerp(c0, c1, tx) : c1; // xo == nx-1 (even nx): coarse rank +1
+    wo = xo_fine ? A::lerp(c0, c1, tx) : c1; // xo == nx-1 (even nx): coarse rank +1
+  };
+  auto wrow = [&](const R *Cp, uint32_t y, bool fy, R &we, R &wo) {
+    if (!fy) {
+      crow(Cp, int(coarse_rank(y) - cy0), we, wo);
+    } else {
+      const R ty = g.r[1][y - 1];
+      R me_, mo_, pe_, po_;
+      const int j = int((y - 1) >> 1) - int(cy0);
+      crow(Cp, j, me_, mo_);
+      crow(Cp, j + 1, pe_, po_);
+      we = A::lerp(me_, pe_, ty);
+      wo = A::lerp(mo_, po_, ty);
+    }
   };
 
-  // writes one output row (fine y), with coalesced stores through shuffles
+  // one output row, coalesced stores through shuffles
   auto store_row = [&](uint32_t pz, uint32_t y, R ve, R vo) {
     R *orow = out + nxy * pz + uint64_t(y) * nx + 2 * cx0;
     const int src = lane >> 1;
@@ -563,7 +711,7 @@ __global__ void __launch_bounds__(256)
   // one output plane: coarse (W from Cp, stored to wout) or fine (lerp_z)
   auto emit_plane = [&](uint32_t pz, bool fz, const R *Cp, const R *wlo, const R *whi,
                         R *wout) {
-    const R tz = fz ? __ldg(g.r[2] + pz - 1) : R(0);
+    const R tz = fz ? g.r[2][pz - 1] : R(0);
     const uint32_t wz = fz ? (pz - 1) >> 1 : coarse_rank(pz);
     for (int r = warp; r < OR; r += 8) {
       const uint32_t y = 2 * cy0 + r;
@@ -574,39 +722,24 @@ __global__ void __launch_bounds__(256)
       if (fz) {
         const Pair<R> a = ld_pair(wlo + r * 64 + 2 * lane);
         const Pair<R> c = ld_pair(whi + r * 64 + 2 * lane);
-        we = lerp(a.e, c.e, tz);
-        wo = lerp(a.o, c.o, tz);
-      } else if (!fy) {
-        crow(Cp, int(coarse_rank(y) - cy0), we, wo);
+        we = A::lerp(a.e, c.e, tz);
+        wo = A::lerp(a.o, c.o, tz);
       } else {
-        const R ty = __ldg(g.r[1] + y - 1);
-        R me_, mo_, pe_, po_;
-        const int j = int((y - 1) >> 1) - int(cy0);
-        crow(Cp, j, me_, mo_);
-        crow(Cp, j + 1, pe_, po_);
-        we = lerp(me_, pe_, ty);
-        wo = lerp(mo_, po_, ty);
+        wrow(Cp, y, fy, we, wo);
       }
       if (wout)
         st_pair(wout + r * 64 + 2 * lane, we, wo);
       const bool fe = fy || fz, fo = fe || xo_fine;
       const uint32_t wy = fy ? (y - 1) >> 1 : coarse_rank(y);
       const unsigned me = (unsigned(fy) << 1) | (unsigned(fz) << 2);
+      const unsigned mo = me | unsigned(xo_fine);
       R ve = we, vo = wo;
       if (fe) {
-        const R c = (cls && own_e)
-                        ? __ldg(cls + g.tbase[me] + (xe >> 1) +
-                                uint64_t(g.tex[me]) * (wy + uint64_t(g.tey[me]) * wz))
-                        : R(0);
+        const R c = (cls && own_e) ? __ldg(cls + ct->row(me, wy, wz) + (xe >> 1)) : R(0);
         ve = add(we, c);
       }
       if (fo) {
-        const unsigned mo = me | unsigned(xo_fine);
-        const uint32_t rx = xo_fine ? (xo - 1) >> 1 : coarse_rank(xo);
-        const R c = (cls && own_o)
-                        ? __ldg(cls + g.tbase[mo] + rx +
-                                uint64_t(g.tex[mo]) * (wy + uint64_t(g.tey[mo]) * wz))
-                        : R(0);
+        const R c = (cls && own_o) ? __ldg(cls + ct->row(mo, wy, wz) + rk_o) : R(0);
         vo = add(wo, c);
       }
       store_row(pz, y, ve, vo);
@@ -614,6 +747,7 @@ __global__ void __launch_bounds__(256)
   };
 
   // planes of coarse ranks [kz0, kz1) plus the fine planes between k and k+1
+  __syncthreads();
   load_plane(kz0);
   load_plane(kz0 + 1);
   load_plane(kz0 + 2);
@@ -635,31 +769,17 @@ __global__ void __launch_bounds__(256)
     cp_async_wait<2>();
     __syncthreads();
     const uint32_t ns = slot ^ 1;
-    // coarse plane k+1: emitted only inside the chunk, prolongated W needed
-    // by the fine plane between k and k+1 either way
-    if (k + 1 < kz1)
-      emit_plane(p1, false, Cs + ((k + 1) % 3) * CR * CP, nullptr, nullptr,
-                 rz ? Wp + ns * OR * 64 : nullptr);
-    else if (fine_between) {
-      // W of the first plane of the next chunk (not emitted here)
-      const R *Cp = Cs + ((k + 1) % 3) * CR * CP;
+    const R *Cn = Cs + ((k + 1) % 3) * CR * CP;
+    if (k + 1 < kz1) {
+      emit_plane(p1, false, Cn, nullptr, nullptr, rz ? Wp + ns * OR * 64 : nullptr);
+    } else {
+      // W of the first plane of the next chunk (needed, not emitted here)
       for (int r = warp; r < OR; r += 8) {
         const uint32_t y = 2 * cy0 + r;
         if (y >= OY1)
           break;
-        const bool fy = (y & 1) && y < ny - 1;
         R we, wo;
-        if (!fy) {
-          crow(Cp, int(coarse_rank(y) - cy0), we, wo);
-        } else {
-          const R ty = __ldg(g.r[1] + y - 1);
-          R me_, mo_, pe_, po_;
-          const int j = int((y - 1) >> 1) - int(cy0);
-          crow(Cp, j, me_, mo_);
-          crow(Cp, j + 1, pe_, po_);
-          we = lerp(me_, pe_, ty);
-          wo = lerp(mo_, po_, ty);
-        }
+        wrow(Cn, y, (y & 1) && y < ny - 1, we, wo);
         st_pair(Wp + ns * OR * 64 + r * 64 + 2 * lane, we, wo);
       }
     }

@@ -193,6 +193,7 @@ struct mgrg_plan {
   int nrefine = 0;
   TileKind tile = TileKind::t32x8;
   bool pair_path = false; // x and y refine: pair-lane kernels (kernels2.cuh)
+  bool fast = false;      // MGRG_FLAG_FAST: FMA arithmetic policy
   uint32_t zchunk = 32;
   mgrg_status deferred = MGRG_OK;         // SingularSystem found at build time
   std::string deferred_msg;
@@ -315,7 +316,40 @@ Stencil<R> make_stencil(const std::vector<double> &hd, const std::vector<double>
     s.hp1 = h(q + 1);
     s.cr = R(R(1) - r(q));
   }
-  if (allow_shift && q != 2 * c)
+  // fast path: the merged 5-tap weights, formed in fp64 from the fp64
+  // geometry and rounded once
+  double wq[5] = {0, 0, 0, 0, 0}; // positions q-2 .. q+2
+  auto H = [&](uint64_t i) { return hd[i]; };
+  if (q == 0) {
+    wq[2] += 2 * H(0);
+    wq[3] += H(0);
+  } else if (q == n - 1) {
+    wq[1] += H(n - 2);
+    wq[2] += 2 * H(n - 2);
+  } else {
+    wq[1] += H(q - 1);
+    wq[2] += 2 * (H(q - 1) + H(q));
+    wq[3] += H(q);
+  }
+  if (fl & ST_HASL) {
+    const double cl = rd[q - 2];
+    wq[0] += cl * H(q - 2);
+    wq[1] += cl * 2 * (H(q - 2) + H(q - 1));
+    wq[2] += cl * H(q - 1);
+  }
+  if (fl & ST_HASR) {
+    const double cr = 1.0 - rd[q];
+    wq[2] += cr * H(q);
+    wq[3] += cr * 2 * (H(q) + H(q + 1));
+    wq[4] += cr * H(q + 1);
+  }
+  const bool shift = allow_shift && q != 2 * c;
+  for (int t = 0; t < 5; ++t) {
+    // taps are relative to the nominal centre 2c (x, y) or q (z)
+    const int src = shift ? t - 1 : t;
+    s.w[t] = (src >= 0 && src < 5) ? R(wq[src]) : R(0);
+  }
+  if (shift)
     fl |= ST_SHIFT;
   s.flags = fl;
   return s;
@@ -453,13 +487,17 @@ static_assert(sizeof(Stencil<double>) % sizeof(double) == 0, "stencil layout");
 constexpr uint32_t kZChunk = 32; // coarse-z planes per CTA of the pair-lane kernels
 template <typename R> constexpr int pair_cy() { return sizeof(R) == 4 ? 16 : 8; }
 
-template <typename R, int CY> void set_pair_attrs() {
-  cudaFuncSetAttribute(dec2_kernel<R, CY>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+template <typename R, int CY, bool FAST> void set_pair_attrs_t() {
+  cudaFuncSetAttribute(dec2_kernel<R, CY, FAST>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        int(dec2_smem<R, CY>()));
-  cudaFuncSetAttribute(rl2_kernel<R, CY>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  cudaFuncSetAttribute(rl2_kernel<R, CY, FAST>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        int(rl2_smem<R, CY>()));
-  cudaFuncSetAttribute(rg2_kernel<R, CY>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  cudaFuncSetAttribute(rg2_kernel<R, CY, FAST>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        int(rg2_smem<R, CY>()));
+}
+template <typename R, int CY> void set_pair_attrs() {
+  set_pair_attrs_t<R, CY, false>();
+  set_pair_attrs_t<R, CY, true>();
 }
 
 template <typename R> dim3 pair_grid(const LevelGeom<R> &g, uint32_t cx) {
@@ -469,28 +507,32 @@ template <typename R> dim3 pair_grid(const LevelGeom<R> &g, uint32_t cx) {
 }
 
 template <typename R>
-void launch_dec2(const LevelGeom<R> &g, const std::array<const Stencil<R> *, 3> &st,
-                 const R *in, R *cls, R *P, R *f, cudaStream_t s) {
+void launch_dec2(bool fast, const LevelGeom<R> &g,
+                 const std::array<const Stencil<R> *, 3> &st, const R *in, R *cls, R *P,
+                 R *f, cudaStream_t s) {
   constexpr int CY = pair_cy<R>();
   const dim3 grid = pair_grid(g, 30);
-  dec2_kernel<R, CY><<<grid, 256, dec2_smem<R, CY>(), s>>>(g, st[0], st[1], st[2], in, cls,
-                                                           P, f, grid.x, grid.y, grid.z);
+  auto k = fast ? dec2_kernel<R, CY, true> : dec2_kernel<R, CY, false>;
+  k<<<grid, 256, dec2_smem<R, CY>(), s>>>(g, st[0], st[1], st[2], in, cls, P, f, grid.x,
+                                          grid.y, grid.z);
 }
 template <typename R>
-void launch_rl2(const LevelGeom<R> &g, const std::array<const Stencil<R> *, 3> &st,
-                const R *cls, R *f, cudaStream_t s) {
+void launch_rl2(bool fast, const LevelGeom<R> &g,
+                const std::array<const Stencil<R> *, 3> &st, const R *cls, R *f,
+                cudaStream_t s) {
   constexpr int CY = pair_cy<R>();
   const dim3 grid = pair_grid(g, 30);
-  rl2_kernel<R, CY><<<grid, 256, rl2_smem<R, CY>(), s>>>(g, st[0], st[1], st[2], cls, f,
-                                                         grid.x, grid.y, grid.z);
+  auto k = fast ? rl2_kernel<R, CY, true> : rl2_kernel<R, CY, false>;
+  k<<<grid, 256, rl2_smem<R, CY>(), s>>>(g, st[0], st[1], st[2], cls, f, grid.x, grid.y,
+                                         grid.z);
 }
 template <typename R>
-void launch_rg2(const LevelGeom<R> &g, const R *coarse, const R *cls, R *out,
+void launch_rg2(bool fast, const LevelGeom<R> &g, const R *coarse, const R *cls, R *out,
                 cudaStream_t s) {
   constexpr int CY = pair_cy<R>();
   const dim3 grid = pair_grid(g, 32);
-  rg2_kernel<R, CY><<<grid, 256, rg2_smem<R, CY>(), s>>>(g, coarse, cls, out, grid.x,
-                                                         grid.y, grid.z);
+  auto k = fast ? rg2_kernel<R, CY, true> : rg2_kernel<R, CY, false>;
+  k<<<grid, 256, rg2_smem<R, CY>(), s>>>(g, coarse, cls, out, grid.x, grid.y, grid.z);
 }
 
 // Batched Thomas along kernel dim kd of the m-lattice `g.m`.
@@ -574,7 +616,7 @@ mgrg_status run_decompose(mgrg_plan *p, const R *d_in, R *d_cls, cudaStream_t s)
     if (mgrg_status st = rec.begin(MGRG_K_DEC_LEVEL, l, es * (2 * Fn + Cn)))
       return st;
     if (p->pair_path)
-      launch_dec2<R>(g, P.sten[l], a, cls, Pout, F, s);
+      launch_dec2<R>(p->fast, g, P.sten[l], a, cls, Pout, F, s);
     else if (p->tile == TileKind::t32x8)
       launch_dec_level<R, 32, 8>(g, a, cls, Pout, F, p->zchunk, s);
     else
@@ -617,7 +659,7 @@ mgrg_status run_recompose(mgrg_plan *p, const R *d_cls, int k, R *d_out,
       if (mgrg_status st = rec.begin(MGRG_K_REC_LOAD, l, es * Fn))
         return st;
       if (p->pair_path)
-        launch_rl2<R>(g, P.sten[l], cls, F, s);
+        launch_rl2<R>(p->fast, g, P.sten[l], cls, F, s);
       else if (p->tile == TileKind::t32x8)
         launch_rec_load<R, 32, 8>(g, cls, F, p->zchunk, s);
       else
@@ -638,7 +680,7 @@ mgrg_status run_recompose(mgrg_plan *p, const R *d_cls, int k, R *d_out,
       if (mgrg_status st = rec.begin(MGRG_K_REC_GPK, l, es * 2 * Fn))
         return st;
       if (p->pair_path)
-        launch_rg2<R>(g, F, cls, out, s);
+        launch_rg2<R>(p->fast, g, F, cls, out, s);
       else if (p->tile == TileKind::t32x8)
         launch_rec_gpk<R, 32, 8>(g, F, cls, out, p->zchunk, s);
       else
@@ -649,7 +691,7 @@ mgrg_status run_recompose(mgrg_plan *p, const R *d_cls, int k, R *d_out,
       if (mgrg_status st = rec.begin(MGRG_K_REC_GPK, l, es * (Fn + Cn)))
         return st;
       if (p->pair_path)
-        launch_rg2<R>(g, prev, nullptr, out, s);
+        launch_rg2<R>(p->fast, g, prev, nullptr, out, s);
       else if (p->tile == TileKind::t32x8)
         launch_rec_gpk<R, 32, 8>(g, prev, nullptr, out, p->zchunk, s);
       else
@@ -735,6 +777,9 @@ mgrg_status mgrg_plan_create(const mgrg_grid_desc *desc, mgrg_plan **out) {
     }
   p->tile = nd == 1 ? TileKind::t128x1 : TileKind::t32x8;
   p->pair_path = (p->refine & 3u) == 3u;
+  p->fast = (desc->flags & MGRG_FLAG_FAST) != 0;
+  if (const char *fe = std::getenv("MGRG_FAST"))
+    p->fast = std::atoi(fe) != 0;
   if (const char *gp = std::getenv("MGRG_GENERIC"))
     if (std::atoi(gp) != 0)
       p->pair_path = false;

@@ -42,7 +42,8 @@ def _tensor_ptr(t):
 class Plan:
     """mgrg_plan: hierarchy + geometry + device workspace for one grid."""
 
-    def __init__(self, shape, dtype="float32", coords=None, levels=None, device=0):
+    def __init__(self, shape, dtype="float32", coords=None, levels=None, device=0,
+                 fast: bool = False):
         L = _lib.lib()
         self.shape = tuple(int(s) for s in shape)
         self.dtype = _dtype_name(dtype)
@@ -68,6 +69,8 @@ class Plan:
         if levels is not None and int(levels) < 1:
             raise errors.InvalidLevel("level count must be at least 1")
         desc.device = self.device
+        desc.flags = _lib.MGRG_FLAG_FAST if fast else 0
+        self.fast = bool(fast)
         h = ctypes.c_void_p()
         _lib.check(L.mgrg_plan_create(ctypes.byref(desc), ctypes.byref(h)))
         self._h = h
