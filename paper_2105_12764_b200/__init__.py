@@ -14,6 +14,8 @@ from .refactor import (LevelPassStats, PassStats, PhaseCounters, ReconstructionR
                        RefactoredData, RefactorOptions, TensorGrid, decompose, make_grid,
                        recompose, recompose_with_report, uniform_coords, value_range,
                        weighted_l2_norm)
+from .parallel import (BlockShardedRefactor, embarrassing_decompose, embarrassing_recompose,
+                       split_blocks)
 
 __all__ = [
     "Plan", "TensorGrid", "RefactoredData", "RefactorOptions", "PassStats",
@@ -21,5 +23,6 @@ __all__ = [
     "recompose_with_report", "make_grid", "uniform_coords", "value_range",
     "weighted_l2_norm", "errors", "Error", "InvalidGrid", "InvalidLevel", "ShapeError",
     "InvalidFusion", "SingularSystem", "TooManyWorkers", "WorkerFailure", "CorruptFile",
-    "MissingClass", "InvalidBound", "IoError",
+    "MissingClass", "InvalidBound", "IoError", "embarrassing_decompose",
+    "embarrassing_recompose", "BlockShardedRefactor", "split_blocks",
 ]
