@@ -1,0 +1,495 @@
+// mgr_b200/refactor.hpp -- source-level drop-in for the reference's C++
+// refactoring API, backed by the B200 path through the C ABI (mgrg.h).
+//
+// The reference's public entry points are header-only templates in
+// namespace mgr (/root/reference/proj/include/mgr/refactor.hpp:462-534,
+// parallel.hpp:243-247), so there is no binary to interpose: a caller swaps
+//     #include "mgr/refactor.hpp"   ->   #include "mgr_b200/refactor.hpp"
+// and links libmgrg.so.  Names, types, argument meaning, ownership (inputs
+// by const reference and unmodified, outputs by value) and error behaviour
+// (mgr::Error subclasses with the reference's stable code() strings,
+// errors.hpp:11-37) are the reference's.  Values are computed on the GPU.
+//
+// RefactorOptions::tile / tile_budget are accepted and ignored (the CPU tile
+// traversal never changes values, kernels.hpp:15-17; the launch
+// configuration is internal).  RefactorOptions::stats is filled with the
+// documented per-level traffic composition (refactor.hpp:223-421).
+// mgr::RefactorOptions::fast selects the FMA arithmetic policy (results
+// within 1e-5 / 1e-12 of the value range instead of bit-identical).
+#ifndef MGR_B200_REFACTOR_HPP
+#define MGR_B200_REFACTOR_HPP
+
+#include <algorithm>
+#include <atomic>
+#include <chrono>
+#include <cmath>
+#include <cstdint>
+#include <map>
+#include <memory>
+#include <mutex>
+#include <optional>
+#include <stdexcept>
+#include <string>
+#include <thread>
+#include <type_traits>
+#include <vector>
+
+#include "../mgrg.h"
+
+namespace mgr {
+
+// ---- errors (errors.hpp:11-37) ---------------------------------------------
+class Error : public std::runtime_error {
+public:
+  Error(std::string code, const std::string &what)
+      : std::runtime_error(what), code_(std::move(code)) {}
+  const std::string &code() const { return code_; }
+
+private:
+  std::string code_;
+};
+
+#define MGR_B200_DEFINE_ERROR(Name)                                            \
+  class Name : public Error {                                                  \
+  public:                                                                      \
+    explicit Name(const std::string &what) : Error(#Name, what) {}             \
+  }
+MGR_B200_DEFINE_ERROR(InvalidGrid);
+MGR_B200_DEFINE_ERROR(InvalidLevel);
+MGR_B200_DEFINE_ERROR(ShapeError);
+MGR_B200_DEFINE_ERROR(InvalidFusion);
+MGR_B200_DEFINE_ERROR(SingularSystem);
+MGR_B200_DEFINE_ERROR(TooManyWorkers);
+MGR_B200_DEFINE_ERROR(WorkerFailure);
+MGR_B200_DEFINE_ERROR(CorruptFile);
+MGR_B200_DEFINE_ERROR(MissingClass);
+MGR_B200_DEFINE_ERROR(InvalidBound);
+MGR_B200_DEFINE_ERROR(IoError);
+// device-side failures (no reference counterpart)
+MGR_B200_DEFINE_ERROR(CudaError);
+MGR_B200_DEFINE_ERROR(Unsupported);
+#undef MGR_B200_DEFINE_ERROR
+
+namespace b200_detail {
+[[noreturn]] inline void raise(mgrg_status st) {
+  const std::string msg = mgrg_last_error();
+  switch (st) {
+  case MGRG_INVALID_GRID: throw InvalidGrid(msg);
+  case MGRG_INVALID_LEVEL: throw InvalidLevel(msg);
+  case MGRG_SHAPE_ERROR: throw ShapeError(msg);
+  case MGRG_INVALID_FUSION: throw InvalidFusion(msg);
+  case MGRG_SINGULAR_SYSTEM: throw SingularSystem(msg);
+  case MGRG_TOO_MANY_WORKERS: throw TooManyWorkers(msg);
+  case MGRG_WORKER_FAILURE: throw WorkerFailure(msg);
+  case MGRG_CORRUPT_FILE: throw CorruptFile(msg);
+  case MGRG_MISSING_CLASS: throw MissingClass(msg);
+  case MGRG_INVALID_BOUND: throw InvalidBound(msg);
+  case MGRG_IO_ERROR: throw IoError(msg);
+  case MGRG_UNSUPPORTED: throw Unsupported(msg);
+  default: throw CudaError(std::string(mgrg_status_name(st)) + ": " + msg);
+  }
+}
+inline void check(mgrg_status st) {
+  if (st != MGRG_OK)
+    raise(st);
+}
+} // namespace b200_detail
+
+// ---- grid (grid.hpp:19-55, ndarray.hpp:12-26) ------------------------------
+using Shape = std::vector<std::size_t>;
+inline constexpr std::size_t kMaxDims = 4;
+inline constexpr std::size_t kDefaultTileBudget = 32768;
+
+inline std::size_t num_elements(const Shape &s) {
+  std::size_t n = 1;
+  for (std::size_t e : s)
+    n *= e;
+  return n;
+}
+
+inline std::vector<double> uniform_coords(std::size_t n) { // grid.cpp:7-12
+  std::vector<double> c(n);
+  for (std::size_t i = 0; i < n; ++i)
+    c[i] = n > 1 ? double(i) / double(n - 1) : 0.0;
+  return c;
+}
+
+// grid.cpp:14-36
+inline void validate_grid_geometry(const Shape &shape,
+                                   const std::vector<std::vector<double>> &coords,
+                                   std::size_t min_extent) {
+  if (shape.empty() || shape.size() > kMaxDims)
+    throw InvalidGrid("grid must have 1.." + std::to_string(kMaxDims) +
+                      " dimensions, got " + std::to_string(shape.size()));
+  if (coords.size() != shape.size())
+    throw InvalidGrid("coordinate arrays do not match dimension count");
+  for (std::size_t d = 0; d < shape.size(); ++d) {
+    if (shape[d] < min_extent)
+      throw InvalidGrid("dimension " + std::to_string(d) + " has " +
+                        std::to_string(shape[d]) + " nodes; need at least " +
+                        std::to_string(min_extent));
+    if (coords[d].size() != shape[d])
+      throw InvalidGrid("coordinates of dimension " + std::to_string(d) +
+                        " do not match its extent");
+    for (std::size_t i = 0; i + 1 < shape[d]; ++i)
+      if (!(coords[d][i] < coords[d][i + 1]))
+        throw InvalidGrid("coordinates of dimension " + std::to_string(d) +
+                          " are not strictly increasing at index " + std::to_string(i));
+  }
+}
+
+template <typename Real> struct TensorGrid {
+  Shape shape;
+  std::vector<std::vector<double>> coords;
+  std::vector<Real> values;
+  int ndims() const { return static_cast<int>(shape.size()); }
+  std::size_t size() const { return num_elements(shape); }
+};
+
+template <typename Real>
+TensorGrid<Real> make_grid(Shape shape, std::vector<Real> values,
+                           std::vector<std::vector<double>> coords = {},
+                           std::size_t min_extent = 3) {
+  if (coords.empty())
+    for (std::size_t e : shape)
+      coords.push_back(uniform_coords(e));
+  validate_grid_geometry(shape, coords, min_extent);
+  if (values.size() != num_elements(shape))
+    throw ShapeError("value count " + std::to_string(values.size()) +
+                     " does not match grid of " + std::to_string(num_elements(shape)) +
+                     " nodes");
+  return TensorGrid<Real>{std::move(shape), std::move(coords), std::move(values)};
+}
+
+template <typename Real> double value_range(const TensorGrid<Real> &g) {
+  auto [lo, hi] = std::minmax_element(g.values.begin(), g.values.end());
+  return static_cast<double>(*hi) - static_cast<double>(*lo);
+}
+
+// ---- refactor.hpp:18-76 -----------------------------------------------------
+template <typename Real> struct RefactoredData {
+  Shape shape;
+  std::vector<std::vector<double>> coords;
+  std::size_t levels = 0;
+  std::vector<std::vector<Real>> classes; // [0] coarsest nodal, [l] class order
+  std::size_t total_elements() const {
+    std::size_t n = 0;
+    for (const auto &c : classes)
+      n += c.size();
+    return n;
+  }
+};
+
+struct ReconstructionReport {
+  std::size_t classes_used = 0;
+  double max_abs_error = 0;
+  double rel_linf_error = 0;
+  double weighted_l2_error = 0;
+  double elapsed_seconds = 0;
+};
+
+struct PhaseCounters {
+  std::uint64_t in = 0, out = 0;
+  std::uint64_t total() const { return in + out; }
+};
+struct LevelPassStats {
+  std::size_t level = 0;
+  std::uint64_t level_elements = 0;
+  PhaseCounters coefficient, fused_copy;
+  std::vector<PhaseCounters> masstrans, solve;
+  PhaseCounters apply;
+  double total_passes() const {
+    std::uint64_t t = coefficient.total() + fused_copy.total() + apply.total();
+    for (const auto &c : masstrans)
+      t += c.total();
+    for (const auto &c : solve)
+      t += c.total();
+    return level_elements ? double(t) / double(level_elements) : 0.0;
+  }
+};
+struct PassStats {
+  std::vector<LevelPassStats> levels; // finest first
+};
+
+struct TileConfig {
+  std::size_t t0 = 0, t1 = 0, t2 = 0; // accepted, never changes values
+};
+
+struct RefactorOptions {
+  std::optional<std::size_t> levels;
+  TileConfig tile{};
+  std::size_t tile_budget = kDefaultTileBudget;
+  PassStats *stats = nullptr;
+  // B200 extensions
+  int device = 0;
+  bool fast = false;
+};
+
+namespace b200_detail {
+
+// One plan per (geometry, dtype, levels, device, policy), reused across
+// calls like a long-lived engine; plans are not shared between threads.
+struct PlanKey {
+  Shape shape;
+  std::vector<double> coords;
+  int dtype, levels, device, fast;
+  bool operator<(const PlanKey &o) const {
+    return std::tie(shape, coords, dtype, levels, device, fast) <
+           std::tie(o.shape, o.coords, o.dtype, o.levels, o.device, o.fast);
+  }
+};
+struct PlanDeleter {
+  void operator()(mgrg_plan *p) const { mgrg_plan_destroy(p); }
+};
+using PlanPtr = std::unique_ptr<mgrg_plan, PlanDeleter>;
+
+inline bool is_uniform(const Shape &shape, const std::vector<std::vector<double>> &c) {
+  for (std::size_t d = 0; d < shape.size(); ++d)
+    if (c[d] != uniform_coords(shape[d]))
+      return false;
+  return true;
+}
+
+template <typename Real>
+mgrg_plan *plan_for(const Shape &shape, const std::vector<std::vector<double>> &coords,
+                    std::optional<std::size_t> levels, int device, bool fast) {
+  static_assert(std::is_same_v<Real, float> || std::is_same_v<Real, double>,
+                "Real must be float or double");
+  thread_local std::map<PlanKey, PlanPtr> cache;
+  PlanKey key{shape, {}, int(sizeof(Real)), levels ? int(*levels) : 0, device, fast};
+  const bool uni = is_uniform(shape, coords);
+  if (!uni)
+    for (const auto &c : coords)
+      key.coords.insert(key.coords.end(), c.begin(), c.end());
+  auto it = cache.find(key);
+  if (it != cache.end())
+    return it->second.get();
+  mgrg_grid_desc desc{};
+  desc.ndims = int32_t(shape.size());
+  desc.dtype = sizeof(Real) == 4 ? MGRG_F32 : MGRG_F64;
+  for (std::size_t d = 0; d < shape.size() && d < 4; ++d)
+    desc.shape[d] = shape[d];
+  desc.coords = uni ? nullptr : key.coords.data();
+  desc.levels = key.levels;
+  desc.device = device;
+  desc.flags = fast ? MGRG_FLAG_FAST : 0;
+  mgrg_plan *p = nullptr;
+  check(mgrg_plan_create(&desc, &p));
+  cache.emplace(key, PlanPtr(p));
+  return p;
+}
+
+// The documented traffic composition (refactor.hpp:223-421, README passes).
+inline void fill_stats(PassStats &stats, mgrg_plan *p, std::size_t nd) {
+  stats.levels.clear();
+  int32_t L = 0;
+  mgrg_plan_levels(p, &L);
+  for (int l = L; l >= 1; --l) {
+    uint64_t ls[4] = {1, 1, 1, 1}, cs[4] = {1, 1, 1, 1};
+    mgrg_plan_level_shape(p, l, ls);
+    mgrg_plan_level_shape(p, l - 1, cs);
+    uint64_t F = 1, C = 1;
+    for (std::size_t d = 0; d < nd; ++d) {
+      F *= ls[d];
+      C *= cs[d];
+    }
+    LevelPassStats s;
+    s.level = std::size_t(l);
+    s.level_elements = F;
+    s.coefficient = {F, F - C};
+    s.fused_copy = {0, F - C};
+    uint64_t cur = F;
+    for (std::size_t d = 0; d < nd; ++d) {
+      if (cs[d] < ls[d]) {
+        const uint64_t out = cur / ls[d] * cs[d];
+        s.masstrans.push_back({cur, out});
+        s.solve.push_back({2 * C, 2 * C});
+        cur = out;
+      } else {
+        s.masstrans.push_back({});
+        s.solve.push_back({});
+      }
+    }
+    s.apply = {2 * C, C};
+    stats.levels.push_back(s);
+  }
+}
+
+} // namespace b200_detail
+
+// mgr::decompose (refactor.hpp:462-474)
+template <typename Real>
+RefactoredData<Real> decompose(const TensorGrid<Real> &grid,
+                               const RefactorOptions &opt = {}) {
+  validate_grid_geometry(grid.shape, grid.coords, 2);
+  if (grid.values.size() != num_elements(grid.shape))
+    throw ShapeError("value count " + std::to_string(grid.values.size()) +
+                     " does not match grid of " + std::to_string(num_elements(grid.shape)) +
+                     " nodes");
+  mgrg_plan *p = b200_detail::plan_for<Real>(grid.shape, grid.coords, opt.levels,
+                                             opt.device, opt.fast);
+  int32_t L = 0;
+  b200_detail::check(mgrg_plan_levels(p, &L));
+  std::vector<uint64_t> off(std::size_t(L) + 2);
+  b200_detail::check(mgrg_plan_class_offsets(p, off.data()));
+  std::vector<Real> flat(grid.values.size());
+  b200_detail::check(mgrg_decompose_host(p, grid.values.data(), flat.data()));
+  RefactoredData<Real> out;
+  out.shape = grid.shape;
+  out.coords = grid.coords;
+  out.levels = std::size_t(L);
+  for (int l = 0; l <= L; ++l)
+    out.classes.emplace_back(flat.begin() + off[l], flat.begin() + off[l + 1]);
+  if (opt.stats)
+    b200_detail::fill_stats(*opt.stats, p, grid.shape.size());
+  return out;
+}
+
+// mgr::recompose (refactor.hpp:476-496)
+template <typename Real>
+TensorGrid<Real> recompose(const RefactoredData<Real> &r, std::size_t classes_used,
+                           const RefactorOptions &opt = {}) {
+  if (classes_used > r.levels)
+    throw InvalidLevel("requested " + std::to_string(classes_used) +
+                       " classes; container has " + std::to_string(r.levels));
+  for (std::size_t l = 0; l <= classes_used; ++l)
+    if (l >= r.classes.size())
+      throw MissingClass("class " + std::to_string(l) + " not loaded");
+  mgrg_plan *p = b200_detail::plan_for<Real>(r.shape, r.coords, r.levels, opt.device,
+                                             opt.fast);
+  int32_t L = 0;
+  b200_detail::check(mgrg_plan_levels(p, &L));
+  if (std::size_t(L) != r.levels)
+    throw InvalidLevel("container has " + std::to_string(r.levels) +
+                       " levels; grid supports " + std::to_string(L));
+  std::vector<uint64_t> off(std::size_t(L) + 2);
+  b200_detail::check(mgrg_plan_class_offsets(p, off.data()));
+  std::vector<Real> flat(off[classes_used + 1]);
+  for (std::size_t l = 0; l <= classes_used; ++l) {
+    if (r.classes[l].size() != off[l + 1] - off[l])
+      throw ShapeError("class " + std::to_string(l) + " has " +
+                       std::to_string(r.classes[l].size()) + " entries, expected " +
+                       std::to_string(off[l + 1] - off[l]));
+    std::copy(r.classes[l].begin(), r.classes[l].end(), flat.begin() + off[l]);
+  }
+  TensorGrid<Real> g;
+  g.shape = r.shape;
+  g.coords = r.coords;
+  g.values.resize(num_elements(r.shape));
+  b200_detail::check(
+      mgrg_recompose_host(p, flat.data(), int32_t(classes_used), g.values.data()));
+  return g;
+}
+
+// mgr::recompose_with_report (refactor.hpp:500-534); the weighted-L2 norm
+// (grid.hpp:198-244) is a host-side reporting metric.
+template <typename Real>
+double weighted_l2_norm(const TensorGrid<Real> &g) {
+  std::vector<double> w(g.values.begin(), g.values.end());
+  const std::size_t nd = g.shape.size();
+  std::size_t stride = 1;
+  for (std::size_t d = 0; d < nd; ++d) {
+    const std::size_t n = g.shape[d];
+    const auto &c = g.coords[d];
+    std::vector<double> out(w.size());
+    const std::size_t outer = w.size() / (n * stride);
+    for (std::size_t o = 0; o < outer; ++o)
+      for (std::size_t s = 0; s < stride; ++s) {
+        const std::size_t b = o * n * stride + s;
+        for (std::size_t i = 0; i < n; ++i) {
+          double v = 0;
+          if (i > 0) {
+            const double h = c[i] - c[i - 1];
+            v += h * w[b + (i - 1) * stride] + 2 * h * w[b + i * stride];
+          }
+          if (i + 1 < n) {
+            const double h = c[i + 1] - c[i];
+            v += 2 * h * w[b + i * stride] + h * w[b + (i + 1) * stride];
+          }
+          out[b + i * stride] = v;
+        }
+      }
+    w.swap(out);
+    stride *= n;
+  }
+  double dot = 0;
+  for (std::size_t i = 0; i < w.size(); ++i)
+    dot += w[i] * double(g.values[i]);
+  return std::sqrt(std::max(dot, 0.0));
+}
+
+template <typename Real>
+std::pair<TensorGrid<Real>, ReconstructionReport>
+recompose_with_report(const RefactoredData<Real> &r, std::size_t classes_used,
+                      const TensorGrid<Real> *reference = nullptr,
+                      const RefactorOptions &opt = {}) {
+  const auto t0 = std::chrono::steady_clock::now();
+  TensorGrid<Real> g = recompose(r, classes_used, opt);
+  ReconstructionReport rep;
+  rep.classes_used = classes_used;
+  TensorGrid<Real> full;
+  const TensorGrid<Real> *ref = reference;
+  if (!ref) {
+    full = recompose(r, std::min(r.levels, r.classes.size() - 1), opt);
+    ref = &full;
+  }
+  TensorGrid<Real> diff = g;
+  for (std::size_t i = 0; i < g.values.size(); ++i) {
+    diff.values[i] = g.values[i] - ref->values[i];
+    rep.max_abs_error =
+        std::max(rep.max_abs_error, std::abs(double(g.values[i]) - double(ref->values[i])));
+  }
+  const double range = value_range(*ref);
+  rep.rel_linf_error = range > 0 ? rep.max_abs_error / range : rep.max_abs_error;
+  rep.weighted_l2_error = weighted_l2_norm(diff);
+  rep.elapsed_seconds =
+      std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+  return {std::move(g), rep};
+}
+
+// mgr::embarrassing_decompose (parallel_impl.hpp:810-847): a pool of
+// min(workers, blocks, visible GPUs) host threads, one GPU each, claiming
+// blocks from a shared counter; result i == decompose(blocks[i]); the first
+// failure stops the pool and surfaces as WorkerFailure.
+template <typename Real>
+std::vector<RefactoredData<Real>>
+embarrassing_decompose(const std::vector<TensorGrid<Real>> &blocks, int workers,
+                       const RefactorOptions &opt = {}, int devices = 1) {
+  std::vector<RefactoredData<Real>> out(blocks.size());
+  if (blocks.empty())
+    return out;
+  const int pool = std::max(1, std::min<int>({workers, int(blocks.size()), devices}));
+  std::atomic<std::size_t> next{0};
+  std::atomic<bool> failed{false};
+  std::mutex err_mu;
+  std::string err;
+  std::vector<std::thread> threads;
+  for (int w = 0; w < pool; ++w)
+    threads.emplace_back([&, w] {
+      for (;;) {
+        const std::size_t i = next.fetch_add(1);
+        if (i >= blocks.size() || failed.load())
+          return;
+        try {
+          RefactorOptions o = opt;
+          o.stats = nullptr;
+          o.device = opt.device + w;
+          out[i] = decompose(blocks[i], o);
+        } catch (const std::exception &e) {
+          std::lock_guard<std::mutex> lk(err_mu);
+          err = e.what();
+          failed.store(true);
+          return;
+        }
+      }
+    });
+  for (auto &t : threads)
+    t.join();
+  if (failed.load())
+    throw WorkerFailure(err);
+  return out;
+}
+
+} // namespace mgr
+
+#endif

@@ -95,6 +95,12 @@ __device__ __forceinline__ void cp_async(R *smem, const R *gmem) {
   else
     asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(s), "l"(gmem));
 }
+// 16-byte LDGSTS (both addresses 16-byte aligned), L2-only caching.
+template <typename R>
+__device__ __forceinline__ void cp_async16(R *smem, const R *gmem) {
+  const uint32_t s = static_cast<uint32_t>(__cvta_generic_to_shared(smem));
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem));
+}
 __device__ __forceinline__ void cp_async_commit() {
   asm volatile("cp.async.commit_group;\n" ::);
 }

@@ -26,6 +26,10 @@
 #include "../../include/mgrg.h"
 #include "kernels.cuh"
 #include "kernels2.cuh"
+#include "thomas.cuh"
+#include "thomas_scan.cuh"
+#include "kernels3.cuh"
+#include "kernels4.cuh"
 
 using namespace mgrg;
 
@@ -195,6 +199,7 @@ struct mgrg_plan {
   bool pair_path = false; // x and y refine: pair-lane kernels (kernels2.cuh)
   bool fast = false;      // MGRG_FLAG_FAST: FMA arithmetic policy
   uint32_t zchunk = 32;
+  int gen = 4;            // pair-lane kernel generation (MGRG_KGEN=2/3: older ones)
   mgrg_status deferred = MGRG_OK;         // SingularSystem found at build time
   std::string deferred_msg;
   PlanT<float> pf;
@@ -345,8 +350,9 @@ Stencil<R> make_stencil(const std::vector<double> &hd, const std::vector<double>
   }
   const bool shift = allow_shift && q != 2 * c;
   for (int t = 0; t < 5; ++t) {
-    // taps are relative to the nominal centre 2c (x, y) or q (z)
-    const int src = shift ? t - 1 : t;
+    // taps are relative to the nominal centre 2c (x, y) or q (z); wq[s] sits
+    // at q-2+s, so with q = 2c-1 (shift) tap t takes wq[t+1]
+    const int src = shift ? t + 1 : t; // tap t sits at 2c-2+t = q-1+t
     s.w[t] = (src >= 0 && src < 5) ? R(wq[src]) : R(0);
   }
   if (shift)
@@ -484,6 +490,11 @@ void launch_rec_gpk(const LevelGeom<R> &g, const R *coarse, const R *cls, R *out
 static_assert(sizeof(Stencil<float>) % sizeof(float) == 0, "stencil layout");
 static_assert(sizeof(Stencil<double>) % sizeof(double) == 0, "stencil layout");
 
+// experiment knob: minimum resident CTAs of the level kernels (MGRG_MINB)
+int g_minb = [] {
+  const char *e = std::getenv("MGRG_MINB");
+  return e ? std::atoi(e) : 3;
+}();
 constexpr uint32_t kZChunk = 32; // coarse-z planes per CTA of the pair-lane kernels
 template <typename R> constexpr int pair_cy() { return sizeof(R) == 4 ? 16 : 8; }
 
@@ -498,6 +509,22 @@ template <typename R, int CY, bool FAST> void set_pair_attrs_t() {
 template <typename R, int CY> void set_pair_attrs() {
   set_pair_attrs_t<R, CY, false>();
   set_pair_attrs_t<R, CY, true>();
+  cudaFuncSetAttribute(dec3_kernel<R, cy3<R>(), false>,
+                       cudaFuncAttributeMaxDynamicSharedMemorySize, int(dec3_smem<R, cy3<R>()>()));
+  cudaFuncSetAttribute(dec3_kernel<R, cy3<R>(), false, 2>,
+                       cudaFuncAttributeMaxDynamicSharedMemorySize, int(dec3_smem<R, cy3<R>()>()));
+  cudaFuncSetAttribute(dec3_kernel<R, cy3<R>(), true>,
+                       cudaFuncAttributeMaxDynamicSharedMemorySize, int(dec3_smem<R, cy3<R>()>()));
+  cudaFuncSetAttribute(dec3_kernel<R, cy3<R>(), true, 2>,
+                       cudaFuncAttributeMaxDynamicSharedMemorySize, int(dec3_smem<R, cy3<R>()>()));
+  cudaFuncSetAttribute(dec4_kernel<R, cy4<R>(), false>,
+                       cudaFuncAttributeMaxDynamicSharedMemorySize, int(dec4_smem<R, cy4<R>()>()));
+  cudaFuncSetAttribute(dec4_kernel<R, cy4<R>(), false, 2>,
+                       cudaFuncAttributeMaxDynamicSharedMemorySize, int(dec4_smem<R, cy4<R>()>()));
+  cudaFuncSetAttribute(dec4_kernel<R, cy4<R>(), true>,
+                       cudaFuncAttributeMaxDynamicSharedMemorySize, int(dec4_smem<R, cy4<R>()>()));
+  cudaFuncSetAttribute(dec4_kernel<R, cy4<R>(), true, 2>,
+                       cudaFuncAttributeMaxDynamicSharedMemorySize, int(dec4_smem<R, cy4<R>()>()));
 }
 
 template <typename R> dim3 pair_grid(const LevelGeom<R> &g, uint32_t cx) {
@@ -514,6 +541,29 @@ void launch_dec2(bool fast, const LevelGeom<R> &g,
   const dim3 grid = pair_grid(g, 30);
   auto k = fast ? dec2_kernel<R, CY, true> : dec2_kernel<R, CY, false>;
   k<<<grid, 256, dec2_smem<R, CY>(), s>>>(g, st[0], st[1], st[2], in, cls, P, f, grid.x,
+                                          grid.y, grid.z);
+}
+template <typename R>
+void launch_dec3(bool fast, const LevelGeom<R> &g,
+                 const std::array<const Stencil<R> *, 3> &st, const R *in, R *cls, R *P,
+                 R *f, cudaStream_t s) {
+  constexpr int CY = cy3<R>();
+  const dim3 grid = pair_grid(g, 30);
+  auto k = fast ? (g_minb == 2 ? dec3_kernel<R, CY, true, 2> : dec3_kernel<R, CY, true, 3>)
+                : (g_minb == 2 ? dec3_kernel<R, CY, false, 2> : dec3_kernel<R, CY, false, 3>);
+  k<<<grid, 256, dec3_smem<R, CY>(), s>>>(g, st[0], st[1], st[2], in, cls, P, f, grid.x,
+                                          grid.y, grid.z);
+}
+template <typename R>
+void launch_dec4(bool fast, const LevelGeom<R> &g,
+                 const std::array<const Stencil<R> *, 3> &st, const R *in, R *cls, R *P,
+                 R *f, cudaStream_t s) {
+  constexpr int CY = cy4<R>();
+  const uint32_t ntz = (g.refine & 4) ? (g.m[2] + kZChunk - 1) / kZChunk : g.m[2];
+  const dim3 grid((g.m[0] + 29) / 30, (g.m[1] + CY - 1) / CY, ntz);
+  auto k = fast ? (g_minb == 2 ? dec4_kernel<R, CY, true, 2> : dec4_kernel<R, CY, true, 3>)
+                : (g_minb == 2 ? dec4_kernel<R, CY, false, 2> : dec4_kernel<R, CY, false, 3>);
+  k<<<grid, 256, dec4_smem<R, CY>(), s>>>(g, st[0], st[1], st[2], in, cls, P, f, grid.x,
                                           grid.y, grid.z);
 }
 template <typename R>
@@ -536,12 +586,70 @@ void launch_rg2(bool fast, const LevelGeom<R> &g, const R *coarse, const R *cls,
 }
 
 // Batched Thomas along kernel dim kd of the m-lattice `g.m`.
+//   FAST policy: warp-parallel affine scans (thomas_scan.cuh) along x and y;
+//   exact policy: one thread per fiber -- smem-resident along x
+//   (thomas.cuh), streaming along y; z streams in both (a z fiber strides
+//   the whole lattice: staging whole fibers per CTA thrashes the TLB, the
+//   streaming kernel keeps every CTA on the same planes).
+template <typename R, uint32_t SEG>
+void launch_scan_rows(const ThomasGeom<R> &t, uint64_t nf, R *f, Epi epi, const R *base,
+                      R *out, cudaStream_t s) {
+  const uint64_t blocks = std::min<uint64_t>((nf + 7) / 8, 148 * 8);
+  thomas_scan_rows_kernel<R, SEG><<<unsigned(blocks), 256, scan_rows_smem<R>(t.m), s>>>(
+      f, t, nf, epi, base, out);
+}
+template <typename R, uint32_t SEG>
+void launch_scan_cols(const ThomasGeom<R> &t, uint64_t S, uint64_t inner, uint64_t ostride,
+                      uint64_t nf, R *f, Epi epi, const R *base, R *out, cudaStream_t s) {
+  thomas_scan_cols_kernel<R, SEG><<<unsigned((nf + 31) / 32), 256, scan_cols_smem<R>(t.m),
+                                    s>>>(f, t, S, inner, ostride, nf, epi, base, out);
+}
 template <typename R>
-void launch_thomas(const LevelGeom<R> &g, const ThomasGeom<R> &t, int kd, R *f,
+bool try_scan(int kd, const ThomasGeom<R> &t, uint64_t S, uint64_t inner, uint64_t ostride,
+              uint64_t nf, R *f, Epi epi, const R *base, R *out, cudaStream_t s) {
+  const uint32_t seg = scan_seg(t.m);
+  if (seg > 33)
+    return false;
+  if (kd == 0) {
+    switch (seg) {
+    case 1: launch_scan_rows<R, 1>(t, nf, f, epi, base, out, s); return true;
+    case 3: launch_scan_rows<R, 3>(t, nf, f, epi, base, out, s); return true;
+    case 5: launch_scan_rows<R, 5>(t, nf, f, epi, base, out, s); return true;
+    case 7: case 9: launch_scan_rows<R, 9>(t, nf, f, epi, base, out, s); return true;
+    case 11: case 13: case 15: case 17:
+      launch_scan_rows<R, 17>(t, nf, f, epi, base, out, s); return true;
+    default: launch_scan_rows<R, 33>(t, nf, f, epi, base, out, s); return true;
+    }
+  }
+  if (scan_cols_smem<R>(t.m) > thomas_smem_limit<R>())
+    return false;
+  switch (seg) {
+  case 1: launch_scan_cols<R, 1>(t, S, inner, ostride, nf, f, epi, base, out, s); return true;
+  case 3: launch_scan_cols<R, 3>(t, S, inner, ostride, nf, f, epi, base, out, s); return true;
+  case 5: launch_scan_cols<R, 5>(t, S, inner, ostride, nf, f, epi, base, out, s); return true;
+  case 7: case 9:
+    launch_scan_cols<R, 9>(t, S, inner, ostride, nf, f, epi, base, out, s); return true;
+  case 11: case 13: case 15: case 17:
+    launch_scan_cols<R, 17>(t, S, inner, ostride, nf, f, epi, base, out, s); return true;
+  default:
+    launch_scan_cols<R, 33>(t, S, inner, ostride, nf, f, epi, base, out, s); return true;
+  }
+}
+
+template <typename R>
+void launch_thomas(bool fast, const LevelGeom<R> &g, const ThomasGeom<R> &t, int kd, R *f,
                    Epi epi, const R *base, R *out, cudaStream_t s) {
   const uint64_t mx = g.m[0], my = g.m[1], mz = g.m[2];
   if (kd == 0) {
     const uint64_t nf = my * mz;
+    if (fast && try_scan<R>(0, t, 1, 1, 0, nf, f, epi, base, out, s))
+      return;
+    if (!fast && thomas_resident_fits<R>(t.m)) {
+      thomas_rows_kernel<R, false><<<unsigned((nf + kThomasFibers - 1) / kThomasFibers),
+                                     kThomasFibers, thomas_rows_smem<R>(t.m), s>>>(
+          f, t, nf, epi, base, out);
+      return;
+    }
     const uint64_t warps = (nf + 31) / 32;
     thomas_x_kernel<R><<<unsigned((warps + 3) / 4), 128, 0, s>>>(f, t, nf, epi, base,
                                                                  out);
@@ -549,9 +657,35 @@ void launch_thomas(const LevelGeom<R> &g, const ThomasGeom<R> &t, int kd, R *f,
     const uint64_t S = kd == 1 ? mx : mx * my;
     const uint64_t ostride = kd == 1 ? mx * my : mx; // the remaining dim
     const uint64_t nf = mx * (kd == 1 ? mz : my);
+    if (fast && kd == 1 && try_scan<R>(1, t, S, mx, mx * my, nf, f, epi, base, out, s))
+      return;
     thomas_strided_kernel<R><<<unsigned((nf + 127) / 128), 128, 0, s>>>(
         f, t, S, uint32_t(mx), ostride, nf, epi, base, out);
   }
+}
+
+template <typename R, uint32_t SEG> void set_scan_attrs(int lim) {
+  cudaFuncSetAttribute(thomas_scan_rows_kernel<R, SEG>,
+                       cudaFuncAttributeMaxDynamicSharedMemorySize, lim);
+  cudaFuncSetAttribute(thomas_scan_cols_kernel<R, SEG>,
+                       cudaFuncAttributeMaxDynamicSharedMemorySize, lim);
+}
+template <typename R> void set_thomas_attrs() {
+  const int lim = int(thomas_smem_limit<R>());
+  set_scan_attrs<R, 1>(lim);
+  set_scan_attrs<R, 3>(lim);
+  set_scan_attrs<R, 5>(lim);
+  set_scan_attrs<R, 9>(lim);
+  set_scan_attrs<R, 17>(lim);
+  set_scan_attrs<R, 33>(lim);
+  cudaFuncSetAttribute(thomas_rows_kernel<R, false>,
+                       cudaFuncAttributeMaxDynamicSharedMemorySize, lim);
+  cudaFuncSetAttribute(thomas_rows_kernel<R, true>,
+                       cudaFuncAttributeMaxDynamicSharedMemorySize, lim);
+  cudaFuncSetAttribute(thomas_cols_kernel<R, false>,
+                       cudaFuncAttributeMaxDynamicSharedMemorySize, lim);
+  cudaFuncSetAttribute(thomas_cols_kernel<R, true>,
+                       cudaFuncAttributeMaxDynamicSharedMemorySize, lim);
 }
 
 template <typename R> R *ws(mgrg_plan *p, uint64_t off) {
@@ -615,7 +749,14 @@ mgrg_status run_decompose(mgrg_plan *p, const R *d_in, R *d_cls, cudaStream_t s)
     // read F; write class (F-C) + packed coarse (C) + load vector (C)
     if (mgrg_status st = rec.begin(MGRG_K_DEC_LEVEL, l, es * (2 * Fn + Cn)))
       return st;
-    if (p->pair_path)
+    // dec4 stages rows with 16-byte copies: the level array must be 16-byte
+    // aligned (workspace levels are; a caller's input may not be)
+    const bool al16 = (reinterpret_cast<uintptr_t>(a) & 15) == 0;
+    if (p->pair_path && p->gen >= 4 && al16)
+      launch_dec4<R>(p->fast, g, P.sten[l], a, cls, Pout, F, s);
+    else if (p->pair_path && p->gen >= 3)
+      launch_dec3<R>(p->fast, g, P.sten[l], a, cls, Pout, F, s);
+    else if (p->pair_path)
       launch_dec2<R>(p->fast, g, P.sten[l], a, cls, Pout, F, s);
     else if (p->tile == TileKind::t32x8)
       launch_dec_level<R, 32, 8>(g, a, cls, Pout, F, p->zchunk, s);
@@ -629,7 +770,7 @@ mgrg_status run_decompose(mgrg_plan *p, const R *d_in, R *d_cls, cudaStream_t s)
       // f in + z out; the fused apply also reads the packed coarse values
       if (mgrg_status st = rec.begin(MGRG_K_THOMAS_X + kd, l, es * Cn * (last ? 3 : 2)))
         return st;
-      launch_thomas<R>(g, P.thom[l][kd], kd, F, last ? Epi::add : Epi::none, Pout,
+      launch_thomas<R>(p->fast, g, P.thom[l][kd], kd, F, last ? Epi::add : Epi::none, Pout,
                        Pout, s);
       if (mgrg_status st = rec.end())
         return st;
@@ -671,7 +812,7 @@ mgrg_status run_recompose(mgrg_plan *p, const R *d_cls, int k, R *d_out,
         const bool last = i == p->nrefine - 1;
         if (mgrg_status st = rec.begin(MGRG_K_THOMAS_X + kd, l, es * Cn * (last ? 3 : 2)))
           return st;
-        launch_thomas<R>(g, P.thom[l][kd], kd, F, last ? Epi::sub : Epi::none, prev,
+        launch_thomas<R>(p->fast, g, P.thom[l][kd], kd, F, last ? Epi::sub : Epi::none, prev,
                          F, s);
         if (mgrg_status st = rec.end())
           return st;
@@ -783,6 +924,8 @@ mgrg_status mgrg_plan_create(const mgrg_grid_desc *desc, mgrg_plan **out) {
   if (const char *gp = std::getenv("MGRG_GENERIC"))
     if (std::atoi(gp) != 0)
       p->pair_path = false;
+  if (const char *kg = std::getenv("MGRG_KGEN"))
+    p->gen = std::atoi(kg);
   p->zchunk = nd == 3 ? 32 : 1;
   if (const char *zc = std::getenv("MGRG_ZCHUNK"))
     if (nd == 3 && std::atoi(zc) > 0)
@@ -811,10 +954,12 @@ mgrg_status mgrg_plan_create(const mgrg_grid_desc *desc, mgrg_plan **out) {
     set_smem_attrs<float, 32, 8>();
     set_smem_attrs<float, 128, 1>();
     set_pair_attrs<float, pair_cy<float>()>();
+    set_thomas_attrs<float>();
   } else {
     set_smem_attrs<double, 32, 8>();
     set_smem_attrs<double, 128, 1>();
     set_pair_attrs<double, pair_cy<double>()>();
+    set_thomas_attrs<double>();
   }
   CUDA_TRY(cudaGetLastError());
   *out = p.release();
@@ -1109,7 +1254,7 @@ static mgrg_status solve_t(mgrg_plan *p, int level, int kd, void *f, cudaStream_
   const LevelGeom<R> &g = pt<R>(p).geom[level];
   if (!((g.refine >> kd) & 1))
     return MGRG_OK; // identity transfer (kernels.hpp:434-435)
-  launch_thomas<R>(g, pt<R>(p).thom[level][kd], kd, static_cast<R *>(f), Epi::none,
+  launch_thomas<R>(p->fast, g, pt<R>(p).thom[level][kd], kd, static_cast<R *>(f), Epi::none,
                    nullptr, nullptr, s);
   CUDA_TRY(cudaGetLastError());
   return MGRG_OK;
