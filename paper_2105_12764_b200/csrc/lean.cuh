@@ -1,0 +1,685 @@
+// lean.cuh -- warp-tiled level kernels of the FAST policy for dyadic levels
+// (every extent odd, so the coarse nodes are exactly the even positions).
+//
+// Why a separate family: the ncu captures of the pair-lane kernels
+// (profiles/r01_*, r02_*) are issue-bound at 2-4 warp instructions per fine
+// element with DRAM at 17-30 % of peak; their generality (even extents,
+// per-row shifts, CTA-wide staging and barriers) costs the instructions.
+// Here every warp is an independent tile and all per-row decisions are
+// compile-time:
+//   * lane a owns the coarse x column qc = 30*tx - 1 + a, i.e. the fine pair
+//     (2qc, 2qc+1); lanes 1..30 produce outputs, lanes 0 and 31 are the
+//     reach-2 halo of the merged R*M window;
+//   * a row at fine (y, plane p) starts at p*n0*n1 + y*n0, whose parity is
+//     (p + y) & 1 for odd n0, n1: the parity of every row of the unrolled
+//     band is known at compile time, so every row is ONE 8/16-byte load per
+//     lane (LDG.64/128), misaligned rows fetch (o_{a-1}, e_a) and take o_a
+//     from the next lane;
+//   * the warp walks a band of TY coarse rows (2TY+3 fine rows) through a
+//     chunk of coarse planes, two fine planes per step (the even plane 2k,
+//     then the odd plane 2k-1 between the last two even ones): GPK as
+//     prolongation x -> y -> z with the even planes' interpolant W carried
+//     in registers, merged R*M along x on shuffles, along y over the band's
+//     rows in registers, along z as three rolling accumulators.
+// No shared memory, no barriers; the level array, class buffer and load
+// vector are touched once each (plus the band's 3 halo rows, L2-resident).
+#pragma once
+
+#include "kernels2.cuh"
+
+namespace mgrg {
+
+template <typename R> __host__ __device__ constexpr int lean_ty() { return sizeof(R) == 4 ? 4 : 2; } // coarse y rows per warp band
+constexpr int kLeanZC = 32;   // coarse z planes per warp chunk
+constexpr int kLeanWPB = 4;   // warps per CTA (independent tiles)
+constexpr int kLeanOut = 30;  // coarse x outputs per warp
+
+// Warp tiles of a lean launch: x tiles of 30 coarse columns, y bands of
+// lean_ty<R>() coarse rows, z chunks of kLeanZC coarse planes (1 in 2-D).
+struct LeanTiles {
+  uint32_t ntx, nty, ntz;
+  __host__ __device__ uint64_t warps() const { return uint64_t(ntx) * nty * ntz; }
+};
+
+template <typename R> struct Vec2;
+template <> struct Vec2<float> { using T = float2; };
+template <> struct Vec2<double> { using T = double2; };
+
+// Per coarse index c of one dimension (padded: entry c+2, zero rows at
+// c = -2, -1, m, m+1): the merged R*M weights on taps 2c-2 .. 2c+2 and the
+// lerp ratio t of the odd node 2c+1 (0 when it does not exist).  Built on
+// the host from the fp64 geometry (mgrg.cu lean_table).
+template <typename R> struct LeanW {
+  R w[5];
+  R t;
+  R pad[2];
+};
+
+template <typename R> struct W5r {
+  R w0, w1, w2, w3, w4;
+};
+template <typename R> __device__ __forceinline__ W5r<R> lean_w(const LeanW<R> *__restrict__ p) {
+  return {__ldg(p->w), __ldg(p->w + 1), __ldg(p->w + 2), __ldg(p->w + 3), __ldg(p->w + 4)};
+}
+
+// Merged R*M along x for the lane's output column: taps are the vec(C)
+// values at 2qc-2 .. 2qc+2 (lane a-1's pair, own pair, lane a+1's even).
+template <typename R>
+__device__ __forceinline__ R lean_xpass(const W5r<R> &wx, R ce, R co) {
+  const R em = __shfl_up_sync(0xffffffffu, ce, 1);
+  const R om = __shfl_up_sync(0xffffffffu, co, 1);
+  const R ep = __shfl_down_sync(0xffffffffu, ce, 1);
+  R v = wx.w0 * em;
+  v = fma(wx.w1, om, v);
+  v = fma(wx.w2, ce, v);
+  v = fma(wx.w3, co, v);
+  return fma(wx.w4, ep, v);
+}
+// Same on a row whose even nodes are kept (coarse in every other dim): the
+// even taps are zero.
+template <typename R> __device__ __forceinline__ R lean_xpass_odd(const W5r<R> &wx, R co) {
+  const R om = __shfl_up_sync(0xffffffffu, co, 1);
+  return fma(wx.w3, co, wx.w1 * om);
+}
+
+template <typename R> __device__ __forceinline__ R flerp(R a, R b, R t) {
+  return fma(t, b - a, a);
+}
+
+// Raw 8/16-byte load of one row for the lane: ALIGNED rows fetch the lane's
+// (e, o) pair, misaligned rows (o_{a-1}, e_a).  `p` points at the lane's
+// even node (column clamped into the level).  Only an aligned pair can
+// cross the end of the array (even node = last element of the row, in the
+// last row); the last column loads its even node alone.
+template <typename R, bool ALIGNED>
+__device__ __forceinline__ typename Vec2<R>::T lean_raw(const R *__restrict__ p, bool lastcol) {
+  using V = typename Vec2<R>::T;
+  if constexpr (ALIGNED) {
+    V v;
+    if (lastcol) {
+      v.x = __ldg(p);
+      v.y = R(0);
+    } else {
+      v = __ldg(reinterpret_cast<const V *>(p));
+    }
+    return v;
+  } else {
+    return __ldg(reinterpret_cast<const V *>(p - 1));
+  }
+}
+template <typename R, bool ALIGNED>
+__device__ __forceinline__ Pair<R> lean_pair(const typename Vec2<R>::T &v) {
+  if constexpr (ALIGNED)
+    return {v.x, v.y};
+  else
+    return {v.y, __shfl_down_sync(0xffffffffu, v.x, 1)};
+}
+
+// Class/packed stores of one plane: row r of the band writes its even node
+// to be[r&1] + ex_e*(r>>1) and its odd node to bo[r&1] + ex_o*(r>>1).
+template <typename R> struct PlaneOut {
+  R *be0, *bo0, *be1, *bo1; // even rows (e, o), odd rows (e, o)
+};
+
+// ---------------------------------------------------------------------------
+// One fine plane of the band: loads, GPK (interpolant W from the in-plane
+// prolongation, or from the z lerp of the two even planes around), class
+// stores, x pass and y pass.  EVEN: plane is coarse along z.
+//   PAR: parity of the plane's row 0 (aligned rows are those with
+//        (r + PAR) even, r = band row index, band row 0 even).
+template <typename R, int TY, bool EVEN>
+__device__ __forceinline__ void lean_plane(
+    const R *__restrict__ pin, const int *rowoff, bool lastcol, R txr, const R *tyr,
+    const W5r<R> &wx, const W5r<R> *wy, bool ve, bool vo, uint32_t stmask_e,
+    uint32_t stmask_o, const PlaneOut<R> &po, int ex_e, int ex_o, R *We, R *Wo,
+    const R *WLe, const R *WLo, R tz, R *Y) {
+  constexpr int NR = 2 * TY + 3;
+  using V = typename Vec2<R>::T;
+  V raw[NR];
+  // EVEN planes: aligned rows are the even ones; ODD planes: the odd ones
+#pragma unroll
+  for (int r = 0; r < NR; ++r) {
+    const R *p = pin + rowoff[r];
+    if (((r & 1) == 0) == EVEN)
+      raw[r] = lean_raw<R, true>(p, lastcol);
+    else
+      raw[r] = lean_raw<R, false>(p, lastcol);
+  }
+  Pair<R> u[NR];
+#pragma unroll
+  for (int r = 0; r < NR; ++r)
+    u[r] = (((r & 1) == 0) == EVEN) ? lean_pair<R, true>(raw[r]) : lean_pair<R, false>(raw[r]);
+  R X[NR];
+  if constexpr (EVEN) {
+#pragma unroll
+    for (int r = 0; r < NR; r += 2) {
+      const R un = __shfl_down_sync(0xffffffffu, u[r].e, 1);
+      We[r] = u[r].e;
+      Wo[r] = flerp(u[r].e, un, txr);
+    }
+#pragma unroll
+    for (int r = 1; r < NR; r += 2) {
+      We[r] = flerp(We[r - 1], We[r + 1], tyr[r >> 1]);
+      Wo[r] = flerp(Wo[r - 1], Wo[r + 1], tyr[r >> 1]);
+    }
+  }
+#pragma unroll
+  for (int r = 0; r < NR; ++r) {
+    R we, wo;
+    if constexpr (EVEN) {
+      we = We[r];
+      wo = Wo[r];
+    } else {
+      we = flerp(WLe[r], We[r], tz);
+      wo = flerp(WLo[r], Wo[r], tz);
+    }
+    const bool kept = EVEN && !(r & 1); // even node coarse in every dim
+    const R ce = (kept || !ve) ? R(0) : u[r].e - we;
+    const R co = vo ? u[r].o - wo : R(0);
+    const int rr = r >> 1;
+    if ((stmask_e >> r) & 1u)
+      ((r & 1) ? po.be1 : po.be0)[int64_t(ex_e) * rr] = kept ? u[r].e : ce;
+    if ((stmask_o >> r) & 1u)
+      ((r & 1) ? po.bo1 : po.bo0)[int64_t(ex_o) * rr] = co;
+    X[r] = kept ? lean_xpass_odd(wx, co) : lean_xpass(wx, ce, co);
+  }
+#pragma unroll
+  for (int j = 0; j < TY; ++j) {
+    R v = wy[j].w0 * X[2 * j];
+    v = fma(wy[j].w1, X[2 * j + 1], v);
+    v = fma(wy[j].w2, X[2 * j + 2], v);
+    v = fma(wy[j].w3, X[2 * j + 3], v);
+    Y[j] = fma(wy[j].w4, X[2 * j + 4], v);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Decompose level kernel: GPK forward (class stores, packed kept nodes) and
+// the load vector f = (R*M)_z (R*M)_y (R*M)_x vec(C) on the coarse lattice.
+// Z3 = false: 2-D level (n2 == 1), one plane.
+template <typename R, bool Z3>
+__global__ void __launch_bounds__(32 * kLeanWPB, 3)
+    lean_dec_kernel(LevelGeom<R> g, const LeanW<R> *__restrict__ lx,
+                    const LeanW<R> *__restrict__ ly, const LeanW<R> *__restrict__ lz,
+                    const R *__restrict__ in, R *__restrict__ cls, R *__restrict__ P,
+                    R *__restrict__ f, LeanTiles tl) {
+  constexpr int TY = lean_ty<R>(), NR = 2 * TY + 3;
+  const int lane = threadIdx.x & 31;
+  const uint64_t wid = uint64_t(blockIdx.x) * kLeanWPB + (threadIdx.x >> 5);
+  if (wid >= tl.warps())
+    return;
+  const uint32_t tx = uint32_t(wid % tl.ntx);
+  const uint64_t rest = wid / tl.ntx;
+  const uint32_t tyb = uint32_t(rest % tl.nty), tzc = uint32_t(rest / tl.nty);
+
+  const int n0 = int(g.n[0]), n1 = int(g.n[1]), n2 = int(g.n[2]);
+  const int m0 = int(g.m[0]), m1 = int(g.m[1]), m2 = int(g.m[2]);
+  const int64_t nxy = int64_t(n0) * n1;
+
+  // ---- lane x geometry
+  const int qc = int(kLeanOut * tx) - 1 + lane;
+  const bool ve = qc >= 0 && qc < m0;     // even node 2qc exists
+  const bool vo = qc >= 0 && qc + 1 < m0; // odd node 2qc+1 exists
+  const bool outl = lane >= 1 && lane <= kLeanOut && ve;
+  const LeanW<R> *lxq = lx + (min(max(qc, -2), m0 + 1) + 2);
+  const R txr = __ldg(&lxq->t);
+  W5r<R> wx = lean_w(lxq);
+  if (!outl)
+    wx = {R(0), R(0), R(0), R(0), R(0)};
+  const int qs = min(max(qc, 0), m0 - 1); // load column (clamped)
+  const bool lastcol = qs == m0 - 1;
+
+  // ---- y band: rows Y0 + r, r = 0 .. NR-1
+  const int cy0 = int(tyb) * TY, cy1 = min(cy0 + TY, m1);
+  const int Y0 = 2 * cy0 - 2;
+  int rowoff[NR];
+  uint32_t ownrows = 0;
+#pragma unroll
+  for (int r = 0; r < NR; ++r) {
+    const int y = Y0 + r;
+    const bool rv = y >= 0 && y < n1;
+    // invalid rows read a row of the same parity (values unused: weights 0)
+    rowoff[r] = (rv ? y : (r & 1)) * n0 + 2 * qs;
+    if (rv && r >= 2 && r < 2 + 2 * (cy1 - cy0))
+      ownrows |= 1u << r;
+  }
+  R tyr[TY + 1];
+#pragma unroll
+  for (int i = 0; i <= TY; ++i)
+    tyr[i] = __ldg(&ly[min(cy0 - 1 + i, m1 + 1) + 2].t); // odd row 2(cy0 - 1 + i) + 1
+  W5r<R> wy[TY];
+#pragma unroll
+  for (int j = 0; j < TY; ++j)
+    wy[j] = lean_w(ly + min(cy0 + j, m1 + 1) + 2);
+  const uint32_t st_e = outl ? ownrows : 0u, st_o = (outl && vo) ? ownrows : 0u;
+
+  // ---- z chunk
+  const int cz0 = Z3 ? int(tzc) * kLeanZC : 0;
+  const int cz1 = Z3 ? min(cz0 + kLeanZC, m2) : 1;
+
+  R WLe[NR], WLo[NR];
+#pragma unroll
+  for (int r = 0; r < NR; ++r)
+    WLe[r] = WLo[r] = R(0);
+  R accM[TY], acc0[TY]; // partial f of outputs k-1 and k at step k
+#pragma unroll
+  for (int j = 0; j < TY; ++j)
+    accM[j] = acc0[j] = R(0);
+  const int64_t m01 = int64_t(m0) * m1;
+  R *fq = f + qc + int64_t(m0) * cy0;
+
+  for (int k = Z3 ? cz0 - 1 : 0; k <= (Z3 ? cz1 : 0); ++k) {
+    R YE[TY], YO[TY];
+    R We[NR], Wo[NR];
+    // ================= even plane 2k =================
+    const int pe = 2 * k;
+    if (pe >= 0 && pe < n2) {
+      const bool own = pe >= 2 * cz0 && pe < 2 * cz1;
+      // zr = k; rows start at yr = cy0 - 1
+      const int64_t yb = int64_t(cy0) - 1;
+      PlaneOut<R> po;
+      po.be0 = P + qc + int64_t(m0) * (yb + int64_t(m1) * k);
+      po.bo0 = cls + g.tbase[1] + qc + int64_t(m0 - 1) * (yb + int64_t(m1) * k);
+      po.be1 = cls + g.tbase[2] + qc + int64_t(m0) * (yb + int64_t(m1 - 1) * k);
+      po.bo1 = cls + g.tbase[3] + qc + int64_t(m0 - 1) * (yb + int64_t(m1 - 1) * k);
+      lean_plane<R, TY, true>(in + int64_t(pe) * nxy, rowoff, lastcol, txr, tyr, wx, wy, ve,
+                              vo, own ? st_e : 0u, own ? st_o : 0u, po, m0, m0 - 1, We, Wo,
+                              nullptr, nullptr, R(0), YE);
+    } else {
+#pragma unroll
+      for (int r = 0; r < NR; ++r)
+        We[r] = Wo[r] = R(0);
+#pragma unroll
+      for (int j = 0; j < TY; ++j)
+        YE[j] = R(0);
+    }
+    if constexpr (!Z3) {
+#pragma unroll
+      for (int j = 0; j < TY; ++j)
+        if (outl && cy0 + j < cy1)
+          fq[int64_t(m0) * j] = YE[j];
+      break;
+    }
+    // ================= odd plane 2k - 1 =================
+    const int pz = pe - 1;
+    const LeanW<R> *lzk = lz + k + 1; // coarse c = k - 1 (padded index c + 2)
+    if (k >= cz0 && pz >= 1 && pz < n2) {
+      const bool own = pz >= 2 * cz0 && pz < 2 * cz1;
+      const int64_t yb = int64_t(cy0) - 1;
+      const int64_t zr = k - 1;
+      PlaneOut<R> po;
+      po.be0 = cls + g.tbase[4] + qc + int64_t(m0) * (yb + int64_t(m1) * zr);
+      po.bo0 = cls + g.tbase[5] + qc + int64_t(m0 - 1) * (yb + int64_t(m1) * zr);
+      po.be1 = cls + g.tbase[6] + qc + int64_t(m0) * (yb + int64_t(m1 - 1) * zr);
+      po.bo1 = cls + g.tbase[7] + qc + int64_t(m0 - 1) * (yb + int64_t(m1 - 1) * zr);
+      lean_plane<R, TY, false>(in + int64_t(pz) * nxy, rowoff, lastcol, txr, tyr, wx, wy, ve,
+                               vo, own ? st_e : 0u, own ? st_o : 0u, po, m0, m0 - 1, We, Wo,
+                               WLe, WLo, __ldg(&lzk->t), YO);
+    } else {
+#pragma unroll
+      for (int j = 0; j < TY; ++j)
+        YO[j] = R(0);
+    }
+#pragma unroll
+    for (int r = 0; r < NR; ++r) {
+      WLe[r] = We[r];
+      WLo[r] = Wo[r];
+    }
+    // ================= z pass (rolling accumulators) =================
+    {
+      const R a3 = __ldg(lzk->w + 3), a4 = __ldg(lzk->w + 4);       // output k-1
+      const R b1 = __ldg(lzk[1].w + 1), b2 = __ldg(lzk[1].w + 2);   // output k
+      const R c0 = __ldg(lzk[2].w);                                 // output k+1
+      const bool emit = outl && k - 1 >= cz0 && k - 1 < cz1;
+#pragma unroll
+      for (int j = 0; j < TY; ++j) {
+        const R out = fma(a3, YO[j], fma(a4, YE[j], accM[j]));
+        if (emit && cy0 + j < cy1)
+          fq[int64_t(m0) * j + m01 * (k - 1)] = out;
+        accM[j] = fma(b1, YO[j], fma(b2, YE[j], acc0[j]));
+        acc0[j] = c0 * YE[j];
+      }
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Recompose load vector: f = (R*M)_z (R*M)_y (R*M)_x vec(C) read from the
+// class buffer of level l (coarse-in-every-dim nodes are zero).  Same warp
+// tiling and band walk as lean_dec_kernel; the class rows are coalesced
+// 4/8-byte loads (lane qc of a type row is element qc).
+template <typename R, bool Z3>
+__global__ void __launch_bounds__(32 * kLeanWPB, 4)
+    lean_rload_kernel(LevelGeom<R> g, const LeanW<R> *__restrict__ lx,
+                      const LeanW<R> *__restrict__ ly, const LeanW<R> *__restrict__ lz,
+                      const R *__restrict__ cls, R *__restrict__ f, LeanTiles tl) {
+  constexpr int TY = lean_ty<R>(), NR = 2 * TY + 3;
+  const int lane = threadIdx.x & 31;
+  const uint64_t wid = uint64_t(blockIdx.x) * kLeanWPB + (threadIdx.x >> 5);
+  if (wid >= tl.warps())
+    return;
+  const uint32_t tx = uint32_t(wid % tl.ntx);
+  const uint64_t rest = wid / tl.ntx;
+  const uint32_t tyb = uint32_t(rest % tl.nty), tzc = uint32_t(rest / tl.nty);
+  const int n1 = int(g.n[1]), n2 = int(g.n[2]);
+  const int m0 = int(g.m[0]), m1 = int(g.m[1]), m2 = int(g.m[2]);
+
+  const int qc = int(kLeanOut * tx) - 1 + lane;
+  const bool ve = qc >= 0 && qc < m0;
+  const bool vo = qc >= 0 && qc + 1 < m0;
+  const bool outl = lane >= 1 && lane <= kLeanOut && ve;
+  W5r<R> wx = lean_w(lx + (min(max(qc, -2), m0 + 1) + 2));
+  if (!outl)
+    wx = {R(0), R(0), R(0), R(0), R(0)};
+  const int qe = min(max(qc, 0), m0 - 1), qo = min(max(qc, 0), max(m0 - 2, 0));
+
+  const int cy0 = int(tyb) * TY, cy1 = min(cy0 + TY, m1);
+  const int Y0 = 2 * cy0 - 2;
+  uint32_t rowvalid = 0;
+#pragma unroll
+  for (int r = 0; r < NR; ++r)
+    if (Y0 + r >= 0 && Y0 + r < n1)
+      rowvalid |= 1u << r;
+  W5r<R> wy[TY];
+#pragma unroll
+  for (int j = 0; j < TY; ++j)
+    wy[j] = lean_w(ly + min(cy0 + j, m1 + 1) + 2);
+  // class row rank of band row r is cy0 - 1 + (r >> 1); ranks outside the
+  // type's y range belong to invalid rows (masked) and read a valid row
+  const int yrmax_e = m1 - 1, yrmax_o = m1 - 2;
+
+  const int cz0 = Z3 ? int(tzc) * kLeanZC : 0;
+  const int cz1 = Z3 ? min(cz0 + kLeanZC, m2) : 1;
+  R accM[TY], acc0[TY];
+#pragma unroll
+  for (int j = 0; j < TY; ++j)
+    accM[j] = acc0[j] = R(0);
+  const int64_t m01 = int64_t(m0) * m1;
+  R *fq = f + qc + int64_t(m0) * cy0;
+
+  for (int k = Z3 ? cz0 - 1 : 0; k <= (Z3 ? cz1 : 0); ++k) {
+    R YE[TY], YO[TY];
+    const int pe = 2 * k;
+    if (pe >= 0 && pe < n2) {
+      const R *b1 = cls + g.tbase[1] + qo + int64_t(m0 - 1) * (int64_t(m1) * k);
+      const R *b2 = cls + g.tbase[2] + qe + int64_t(m0) * (int64_t(m1 - 1) * k);
+      const R *b3 = cls + g.tbase[3] + qo + int64_t(m0 - 1) * (int64_t(m1 - 1) * k);
+      int re[NR];
+#pragma unroll
+      for (int r = 0; r < NR; ++r)
+        re[r] = min(max(cy0 - 1 + (r >> 1), 0), (r & 1) ? max(yrmax_o, 0) : yrmax_e);
+      R ue[NR], uo[NR];
+#pragma unroll
+      for (int r = 0; r < NR; ++r) {
+        ue[r] = (r & 1) ? __ldg(b2 + int64_t(m0) * re[r]) : R(0); // even rows: kept
+        uo[r] = __ldg(((r & 1) ? b3 : b1) + int64_t(m0 - 1) * re[r]);
+      }
+      R X[NR];
+#pragma unroll
+      for (int r = 0; r < NR; ++r) {
+        const bool rv = (rowvalid >> r) & 1u;
+        const R co = (vo && rv) ? uo[r] : R(0);
+        if (!(r & 1)) {
+          X[r] = lean_xpass_odd(wx, co);
+        } else {
+          const R ce = (ve && rv) ? ue[r] : R(0);
+          X[r] = lean_xpass(wx, ce, co);
+        }
+      }
+#pragma unroll
+      for (int j = 0; j < TY; ++j) {
+        R v = wy[j].w0 * X[2 * j];
+        v = fma(wy[j].w1, X[2 * j + 1], v);
+        v = fma(wy[j].w2, X[2 * j + 2], v);
+        v = fma(wy[j].w3, X[2 * j + 3], v);
+        YE[j] = fma(wy[j].w4, X[2 * j + 4], v);
+      }
+    } else {
+#pragma unroll
+      for (int j = 0; j < TY; ++j)
+        YE[j] = R(0);
+    }
+    if constexpr (!Z3) {
+#pragma unroll
+      for (int j = 0; j < TY; ++j)
+        if (outl && cy0 + j < cy1)
+          fq[int64_t(m0) * j] = YE[j];
+      break;
+    }
+    const int pz = pe - 1;
+    const LeanW<R> *lzk = lz + k + 1;
+    if (k >= cz0 && pz >= 1 && pz < n2) {
+      const int64_t zr = k - 1;
+      int re[NR];
+#pragma unroll
+      for (int r = 0; r < NR; ++r)
+        re[r] = min(max(cy0 - 1 + (r >> 1), 0), (r & 1) ? max(yrmax_o, 0) : yrmax_e);
+      const R *b4 = cls + g.tbase[4] + qe + int64_t(m0) * (int64_t(m1) * zr);
+      const R *b5 = cls + g.tbase[5] + qo + int64_t(m0 - 1) * (int64_t(m1) * zr);
+      const R *b6 = cls + g.tbase[6] + qe + int64_t(m0) * (int64_t(m1 - 1) * zr);
+      const R *b7 = cls + g.tbase[7] + qo + int64_t(m0 - 1) * (int64_t(m1 - 1) * zr);
+      R ue[NR], uo[NR];
+#pragma unroll
+      for (int r = 0; r < NR; ++r) {
+        ue[r] = __ldg(((r & 1) ? b6 : b4) + int64_t(m0) * re[r]);
+        uo[r] = __ldg(((r & 1) ? b7 : b5) + int64_t(m0 - 1) * re[r]);
+      }
+      R X[NR];
+#pragma unroll
+      for (int r = 0; r < NR; ++r) {
+        const bool rv = (rowvalid >> r) & 1u;
+        const R ce = (ve && rv) ? ue[r] : R(0);
+        const R co = (vo && rv) ? uo[r] : R(0);
+        X[r] = lean_xpass(wx, ce, co);
+      }
+#pragma unroll
+      for (int j = 0; j < TY; ++j) {
+        R v = wy[j].w0 * X[2 * j];
+        v = fma(wy[j].w1, X[2 * j + 1], v);
+        v = fma(wy[j].w2, X[2 * j + 2], v);
+        v = fma(wy[j].w3, X[2 * j + 3], v);
+        YO[j] = fma(wy[j].w4, X[2 * j + 4], v);
+      }
+    } else {
+#pragma unroll
+      for (int j = 0; j < TY; ++j)
+        YO[j] = R(0);
+    }
+    {
+      const R a3 = __ldg(lzk->w + 3), a4 = __ldg(lzk->w + 4);
+      const R b1 = __ldg(lzk[1].w + 1), b2 = __ldg(lzk[1].w + 2);
+      const R c0 = __ldg(lzk[2].w);
+      const bool emit = outl && k - 1 >= cz0 && k - 1 < cz1;
+#pragma unroll
+      for (int j = 0; j < TY; ++j) {
+        const R out = fma(a3, YO[j], fma(a4, YE[j], accM[j]));
+        if (emit && cy0 + j < cy1)
+          fq[int64_t(m0) * j + m01 * (k - 1)] = out;
+        accM[j] = fma(b1, YO[j], fma(b2, YE[j], acc0[j]));
+        acc0[j] = c0 * YE[j];
+      }
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Recompose GPK inverse: level array = prolongation of the corrected coarse
+// lattice (x -> y -> z lerps) + the class values at fine nodes.  Lane a of
+// a warp owns coarse column qc = 31*tx + a (lane 31 is the x-lerp halo),
+// the warp a band of TG coarse rows (fine rows 2cy0 .. 2cy1-1, plus the
+// coarse row cy1 for the last odd row) through a chunk of coarse planes;
+// the interpolant of the previous even plane is carried in registers.
+// CLS = false: classes above classes_used (all zero): pure prolongation.
+template <typename R> __host__ __device__ constexpr int lean_tg() { return sizeof(R) == 4 ? 4 : 2; }
+constexpr int kLeanGOut = 31;
+
+template <typename R, bool ALIGNED>
+__device__ __forceinline__ void lean_store_pair(R *p, R e, R o, bool we, bool wo) {
+  // p points at the lane's even node
+  if constexpr (ALIGNED) {
+    if (we && wo) {
+      using V = typename Vec2<R>::T;
+      V v;
+      v.x = e;
+      v.y = o;
+      *reinterpret_cast<V *>(p) = v;
+      return;
+    }
+  }
+  if (we)
+    p[0] = e;
+  if (wo)
+    p[1] = o;
+}
+
+template <typename R, bool Z3, bool CLS>
+__global__ void __launch_bounds__(32 * kLeanWPB, 4)
+    lean_rgpk_kernel(LevelGeom<R> g, const LeanW<R> *__restrict__ lx,
+                     const LeanW<R> *__restrict__ ly, const LeanW<R> *__restrict__ lz,
+                     const R *__restrict__ coarse, const R *__restrict__ cls,
+                     R *__restrict__ out, LeanTiles tl) {
+  constexpr int TG = lean_tg<R>(), NF = 2 * TG + 1; // fine rows incl. halo row 2cy1
+  const int lane = threadIdx.x & 31;
+  const uint64_t wid = uint64_t(blockIdx.x) * kLeanWPB + (threadIdx.x >> 5);
+  if (wid >= tl.warps())
+    return;
+  const uint32_t tx = uint32_t(wid % tl.ntx);
+  const uint64_t rest = wid / tl.ntx;
+  const uint32_t tyb = uint32_t(rest % tl.nty), tzc = uint32_t(rest / tl.nty);
+  const int n0 = int(g.n[0]), n1 = int(g.n[1]), n2 = int(g.n[2]);
+  const int m0 = int(g.m[0]), m1 = int(g.m[1]), m2 = int(g.m[2]);
+  const int64_t nxy = int64_t(n0) * n1;
+  const int64_t m01 = int64_t(m0) * m1;
+
+  const int qc = int(kLeanGOut * tx) + lane;
+  const bool own = lane < kLeanGOut && qc < m0; // writes e (and o if it exists)
+  const bool ownO = own && qc + 1 < m0;
+  const int qe = min(qc, m0 - 1), qo = min(qc, max(m0 - 2, 0));
+  const R txr = __ldg(&lx[min(qc, m0 + 1) + 2].t);
+
+  const int cy0 = int(tyb) * TG, cy1 = min(cy0 + TG, m1);
+  // fine rows 2cy0 + i, i = 0 .. 2TG (i = 2TG: halo, never written)
+  uint32_t wrow = 0;
+#pragma unroll
+  for (int i = 0; i < 2 * TG; ++i)
+    if (2 * cy0 + i < n1 && i < 2 * (cy1 - cy0))
+      wrow |= 1u << i;
+  R tyr[TG];
+#pragma unroll
+  for (int i = 0; i < TG; ++i)
+    tyr[i] = __ldg(&ly[min(cy0 + i, m1 + 1) + 2].t); // odd row 2(cy0+i)+1
+  int crow[TG + 1]; // clamped coarse rows
+#pragma unroll
+  for (int i = 0; i <= TG; ++i)
+    crow[i] = min(cy0 + i, m1 - 1);
+  int rfo[TG]; // clamped class rank of odd rows
+#pragma unroll
+  for (int i = 0; i < TG; ++i)
+    rfo[i] = min(cy0 + i, max(m1 - 2, 0));
+
+  const int cz0 = Z3 ? int(tzc) * kLeanZC : 0;
+  const int cz1 = Z3 ? min(cz0 + kLeanZC, m2) : 1;
+  R WLe[NF], WLo[NF];
+  // step k: even plane 2k (coarse plane k) and, for k > cz0, the odd plane
+  // 2k-1 between coarse planes k-1 and k
+  const int kend = Z3 ? min(cz1, m2 - 1) : 0;
+  for (int k = cz0; k <= kend; ++k) {
+    R We[NF], Wo[NF];
+    {
+      R c[TG + 1];
+      const R *cp = coarse + m01 * k + qe;
+#pragma unroll
+      for (int i = 0; i <= TG; ++i)
+        c[i] = __ldg(cp + int64_t(m0) * crow[i]);
+#pragma unroll
+      for (int i = 0; i <= TG; ++i) {
+        const R cn = __shfl_down_sync(0xffffffffu, c[i], 1);
+        We[2 * i] = c[i];
+        Wo[2 * i] = flerp(c[i], cn, txr);
+      }
+#pragma unroll
+      for (int i = 0; i < TG; ++i) {
+        We[2 * i + 1] = flerp(We[2 * i], We[2 * i + 2], tyr[i]);
+        Wo[2 * i + 1] = flerp(Wo[2 * i], Wo[2 * i + 2], tyr[i]);
+      }
+    }
+    // ---- even plane 2k (written when k < cz1)
+    if (k < cz1) {
+      const R *c1 = cls + g.tbase[1] + qo + int64_t(m0 - 1) * (int64_t(m1) * k);
+      const R *c2 = cls + g.tbase[2] + qe + int64_t(m0) * (int64_t(m1 - 1) * k);
+      const R *c3 = cls + g.tbase[3] + qo + int64_t(m0 - 1) * (int64_t(m1 - 1) * k);
+      R v1[TG], v2[TG], v3[TG];
+#pragma unroll
+      for (int i = 0; i < TG; ++i) {
+        v1[i] = CLS ? __ldg(c1 + int64_t(m0 - 1) * crow[i]) : R(0);
+        v2[i] = CLS ? __ldg(c2 + int64_t(m0) * rfo[i]) : R(0);
+        v3[i] = CLS ? __ldg(c3 + int64_t(m0 - 1) * rfo[i]) : R(0);
+      }
+      R *op = out + int64_t(2 * k) * nxy + int64_t(2 * cy0) * n0 + 2 * qc;
+#pragma unroll
+      for (int i = 0; i < TG; ++i) {
+        // even row 2(cy0+i): parity of (2k + 2(cy0+i)) is even -> aligned
+        if ((wrow >> (2 * i)) & 1u)
+          lean_store_pair<R, true>(op + int64_t(2 * i) * n0, We[2 * i], Wo[2 * i] + v1[i], own,
+                                   ownO);
+        if ((wrow >> (2 * i + 1)) & 1u)
+          lean_store_pair<R, false>(op + int64_t(2 * i + 1) * n0, We[2 * i + 1] + v2[i],
+                                    Wo[2 * i + 1] + v3[i], own, ownO);
+      }
+    }
+    // ---- odd plane 2k-1
+    if (Z3 && k > cz0) {
+      const R tz = __ldg(&lz[k - 1 + 2].t);
+      const int64_t zr = k - 1;
+      const R *c4 = cls + g.tbase[4] + qe + int64_t(m0) * (int64_t(m1) * zr);
+      const R *c5 = cls + g.tbase[5] + qo + int64_t(m0 - 1) * (int64_t(m1) * zr);
+      const R *c6 = cls + g.tbase[6] + qe + int64_t(m0) * (int64_t(m1 - 1) * zr);
+      const R *c7 = cls + g.tbase[7] + qo + int64_t(m0 - 1) * (int64_t(m1 - 1) * zr);
+      R v4[TG], v5[TG], v6[TG], v7[TG];
+#pragma unroll
+      for (int i = 0; i < TG; ++i) {
+        v4[i] = CLS ? __ldg(c4 + int64_t(m0) * crow[i]) : R(0);
+        v5[i] = CLS ? __ldg(c5 + int64_t(m0 - 1) * crow[i]) : R(0);
+        v6[i] = CLS ? __ldg(c6 + int64_t(m0) * rfo[i]) : R(0);
+        v7[i] = CLS ? __ldg(c7 + int64_t(m0 - 1) * rfo[i]) : R(0);
+      }
+      R *op = out + int64_t(2 * k - 1) * nxy + int64_t(2 * cy0) * n0 + 2 * qc;
+#pragma unroll
+      for (int i = 0; i < TG; ++i) {
+        // odd plane: even rows misaligned, odd rows aligned
+        if ((wrow >> (2 * i)) & 1u)
+          lean_store_pair<R, false>(op + int64_t(2 * i) * n0,
+                                    flerp(WLe[2 * i], We[2 * i], tz) + v4[i],
+                                    flerp(WLo[2 * i], Wo[2 * i], tz) + v5[i], own, ownO);
+        if ((wrow >> (2 * i + 1)) & 1u)
+          lean_store_pair<R, true>(op + int64_t(2 * i + 1) * n0,
+                                   flerp(WLe[2 * i + 1], We[2 * i + 1], tz) + v6[i],
+                                   flerp(WLo[2 * i + 1], Wo[2 * i + 1], tz) + v7[i], own,
+                                   ownO);
+      }
+    }
+#pragma unroll
+    for (int r = 0; r < NF; ++r) {
+      WLe[r] = We[r];
+      WLo[r] = Wo[r];
+    }
+  }
+}
+
+template <typename R> LeanTiles lean_gtiles(uint32_t m0, uint32_t m1, uint32_t m2, bool z3) {
+  LeanTiles t;
+  t.ntx = (m0 + kLeanGOut - 1) / kLeanGOut;
+  t.nty = (m1 + lean_tg<R>() - 1) / lean_tg<R>();
+  t.ntz = z3 ? (m2 + kLeanZC - 1) / kLeanZC : 1;
+  return t;
+}
+
+template <typename R> LeanTiles lean_tiles(uint32_t m0, uint32_t m1, uint32_t m2, bool z3) {
+  LeanTiles t;
+  t.ntx = (m0 + kLeanOut - 1) / kLeanOut;
+  t.nty = (m1 + lean_ty<R>() - 1) / lean_ty<R>();
+  t.ntz = z3 ? (m2 + kLeanZC - 1) / kLeanZC : 1;
+  return t;
+}
+
+} // namespace mgrg

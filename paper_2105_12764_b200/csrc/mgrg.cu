@@ -30,6 +30,7 @@
 #include "thomas_scan.cuh"
 #include "kernels3.cuh"
 #include "kernels4.cuh"
+#include "lean.cuh"
 
 using namespace mgrg;
 
@@ -179,6 +180,7 @@ template <typename R> struct PlanT {
   std::vector<LevelGeom<R>> geom;                 // [l], l = 1..L
   std::vector<std::array<ThomasGeom<R>, 3>> thom; // [l][kd] (level-(l-1) factors)
   std::vector<std::array<const Stencil<R> *, 3>> sten; // [l][kd] merged R*M tables
+  std::vector<std::array<const LeanW<R> *, 3>> lean;   // [l][kd] lean tables (padded)
   R *d_geom = nullptr;
 };
 
@@ -200,6 +202,7 @@ struct mgrg_plan {
   bool fast = false;      // MGRG_FLAG_FAST: FMA arithmetic policy
   uint32_t zchunk = 32;
   int gen = 4;            // pair-lane kernel generation (MGRG_KGEN=2/3: older ones)
+  bool lean = false;      // dyadic x/y(/z) refinement: lean warp-tiled kernels (lean.cuh)
   mgrg_status deferred = MGRG_OK;         // SingularSystem found at build time
   std::string deferred_msg;
   PlanT<float> pf;
@@ -367,7 +370,7 @@ template <typename R> mgrg_status upload_geometry(mgrg_plan *p) {
   // host staging of every per-level array in R, then one upload
   std::vector<R> buf;
   struct Ref {
-    size_t h[3], r[3], th[3], tf[3], ti[3], st[3];
+    size_t h[3], r[3], th[3], tf[3], ti[3], st[3], lw[3];
   };
   std::vector<Ref> refs(L + 1);
   auto push = [&](const std::vector<R> &v) {
@@ -380,7 +383,7 @@ template <typename R> mgrg_status upload_geometry(mgrg_plan *p) {
   for (int l = 1; l <= L; ++l) {
     for (int kd = 0; kd < 3; ++kd) {
       refs[l].h[kd] = refs[l].r[kd] = refs[l].th[kd] = refs[l].tf[kd] =
-          refs[l].ti[kd] = refs[l].st[kd] = size_t(-1);
+          refs[l].ti[kd] = refs[l].st[kd] = refs[l].lw[kd] = size_t(-1);
       const int ud = p->kmap[kd];
       if (ud < 0)
         continue;
@@ -409,6 +412,18 @@ template <typename R> mgrg_status upload_geometry(mgrg_plan *p) {
           std::memcpy(raw.data() + c * (sizeof(Stencil<R>) / sizeof(R)), &st, sizeof(st));
         }
         refs[l].st[kd] = push(raw);
+        // lean table: entry c+2 for c in [-2, m+1]; FAST weights + odd-node ratio
+        constexpr size_t LW = sizeof(LeanW<R>) / sizeof(R);
+        std::vector<R> lw((m + 4) * LW, R(0));
+        for (uint64_t c = 0; c < m; ++c) {
+          const Stencil<R> st = make_stencil<R>(H.h[ud][l], H.r[ud][l], n, c, kd < 2);
+          LeanW<R> e{};
+          for (int t = 0; t < 5; ++t)
+            e.w[t] = st.w[t];
+          e.t = 2 * c + 1 < n - 1 ? R(H.r[ud][l][2 * c]) : R(0);
+          std::memcpy(lw.data() + (c + 2) * LW, &e, sizeof(e));
+        }
+        refs[l].lw[kd] = push(lw);
       }
     }
   }
@@ -422,6 +437,7 @@ template <typename R> mgrg_status upload_geometry(mgrg_plan *p) {
   P.geom.assign(L + 1, LevelGeom<R>{});
   P.thom.assign(L + 1, {});
   P.sten.assign(L + 1, {nullptr, nullptr, nullptr});
+  P.lean.assign(L + 1, {nullptr, nullptr, nullptr});
   for (int l = 1; l <= L; ++l) {
     LevelGeom<R> &g = P.geom[l];
     g.refine = 0;
@@ -440,6 +456,9 @@ template <typename R> mgrg_status upload_geometry(mgrg_plan *p) {
       P.sten[l][kd] = refs[l].st[kd] == size_t(-1)
                           ? nullptr
                           : reinterpret_cast<const Stencil<R> *>(base + refs[l].st[kd]);
+      P.lean[l][kd] = refs[l].lw[kd] == size_t(-1)
+                          ? nullptr
+                          : reinterpret_cast<const LeanW<R> *>(base + refs[l].lw[kd]);
     }
     fill_layout(g);
   }
@@ -565,6 +584,48 @@ void launch_dec4(bool fast, const LevelGeom<R> &g,
                 : (g_minb == 2 ? dec4_kernel<R, CY, false, 2> : dec4_kernel<R, CY, false, 3>);
   k<<<grid, 256, dec4_smem<R, CY>(), s>>>(g, st[0], st[1], st[2], in, cls, P, f, grid.x,
                                           grid.y, grid.z);
+}
+template <typename R> bool lean_out_ok(const R *out) {
+  return (reinterpret_cast<uintptr_t>(out) & (2 * sizeof(R) - 1)) == 0;
+}
+template <typename R> bool lean_level(const LevelGeom<R> &g) {
+  return (g.n[0] & 1u) && (g.n[1] & 1u) && (g.n[2] & 1u);
+}
+template <typename R>
+void launch_lean_dec(const LevelGeom<R> &g, const std::array<const LeanW<R> *, 3> &st,
+                     const R *in, R *cls, R *P, R *f, cudaStream_t s) {
+  const bool z3 = g.n[2] > 1;
+  const LeanTiles t = lean_tiles<R>(g.m[0], g.m[1], g.m[2], z3);
+  const unsigned blocks = unsigned((t.warps() + kLeanWPB - 1) / kLeanWPB);
+  if (z3)
+    lean_dec_kernel<R, true><<<blocks, 32 * kLeanWPB, 0, s>>>(g, st[0], st[1], st[2], in, cls,
+                                                              P, f, t);
+  else
+    lean_dec_kernel<R, false><<<blocks, 32 * kLeanWPB, 0, s>>>(g, st[0], st[1], st[2], in,
+                                                               cls, P, f, t);
+}
+template <typename R>
+void launch_lean_rload(const LevelGeom<R> &g, const std::array<const LeanW<R> *, 3> &st,
+                       const R *cls, R *f, cudaStream_t s) {
+  const bool z3 = g.n[2] > 1;
+  const LeanTiles t = lean_tiles<R>(g.m[0], g.m[1], g.m[2], z3);
+  const unsigned blocks = unsigned((t.warps() + kLeanWPB - 1) / kLeanWPB);
+  if (z3)
+    lean_rload_kernel<R, true><<<blocks, 32 * kLeanWPB, 0, s>>>(g, st[0], st[1], st[2], cls, f,
+                                                                t);
+  else
+    lean_rload_kernel<R, false><<<blocks, 32 * kLeanWPB, 0, s>>>(g, st[0], st[1], st[2], cls,
+                                                                 f, t);
+}
+template <typename R>
+void launch_lean_rgpk(const LevelGeom<R> &g, const std::array<const LeanW<R> *, 3> &st,
+                      const R *coarse, const R *cls, R *out, cudaStream_t s) {
+  const bool z3 = g.n[2] > 1;
+  const LeanTiles t = lean_gtiles<R>(g.m[0], g.m[1], g.m[2], z3);
+  const unsigned blocks = unsigned((t.warps() + kLeanWPB - 1) / kLeanWPB);
+  auto k = z3 ? (cls ? lean_rgpk_kernel<R, true, true> : lean_rgpk_kernel<R, true, false>)
+              : (cls ? lean_rgpk_kernel<R, false, true> : lean_rgpk_kernel<R, false, false>);
+  k<<<blocks, 32 * kLeanWPB, 0, s>>>(g, st[0], st[1], st[2], coarse, cls, out, t);
 }
 template <typename R>
 void launch_rl2(bool fast, const LevelGeom<R> &g,
@@ -752,7 +813,10 @@ mgrg_status run_decompose(mgrg_plan *p, const R *d_in, R *d_cls, cudaStream_t s)
     // dec4 stages rows with 16-byte copies: the level array must be 16-byte
     // aligned (workspace levels are; a caller's input may not be)
     const bool al16 = (reinterpret_cast<uintptr_t>(a) & 15) == 0;
-    if (p->pair_path && p->gen >= 4 && al16)
+    const bool alv = (reinterpret_cast<uintptr_t>(a) & (2 * sizeof(R) - 1)) == 0;
+    if (p->fast && p->lean && alv && lean_level(g))
+      launch_lean_dec<R>(g, P.lean[l], a, cls, Pout, F, s);
+    else if (p->pair_path && p->gen >= 4 && al16)
       launch_dec4<R>(p->fast, g, P.sten[l], a, cls, Pout, F, s);
     else if (p->pair_path && p->gen >= 3)
       launch_dec3<R>(p->fast, g, P.sten[l], a, cls, Pout, F, s);
@@ -799,7 +863,9 @@ mgrg_status run_recompose(mgrg_plan *p, const R *d_cls, int k, R *d_out,
       // read class (F-C); write load vector (C)
       if (mgrg_status st = rec.begin(MGRG_K_REC_LOAD, l, es * Fn))
         return st;
-      if (p->pair_path)
+      if (p->fast && p->lean && lean_level(g))
+        launch_lean_rload<R>(g, P.lean[l], cls, F, s);
+      else if (p->pair_path)
         launch_rl2<R>(p->fast, g, P.sten[l], cls, F, s);
       else if (p->tile == TileKind::t32x8)
         launch_rec_load<R, 32, 8>(g, cls, F, p->zchunk, s);
@@ -820,7 +886,9 @@ mgrg_status run_recompose(mgrg_plan *p, const R *d_cls, int k, R *d_out,
       // read coarse' (C) + class (F-C); write the level array (F)
       if (mgrg_status st = rec.begin(MGRG_K_REC_GPK, l, es * 2 * Fn))
         return st;
-      if (p->pair_path)
+      if (p->fast && p->lean && lean_level(g) && lean_out_ok<R>(out))
+        launch_lean_rgpk<R>(g, P.lean[l], F, cls, out, s);
+      else if (p->pair_path)
         launch_rg2<R>(p->fast, g, F, cls, out, s);
       else if (p->tile == TileKind::t32x8)
         launch_rec_gpk<R, 32, 8>(g, F, cls, out, p->zchunk, s);
@@ -831,7 +899,9 @@ mgrg_status run_recompose(mgrg_plan *p, const R *d_cls, int k, R *d_out,
       // coarse values are a_{l-1} unchanged and the fine ones interp + 0.
       if (mgrg_status st = rec.begin(MGRG_K_REC_GPK, l, es * (Fn + Cn)))
         return st;
-      if (p->pair_path)
+      if (p->fast && p->lean && lean_level(g) && lean_out_ok<R>(out))
+        launch_lean_rgpk<R>(g, P.lean[l], prev, nullptr, out, s);
+      else if (p->pair_path)
         launch_rg2<R>(p->fast, g, prev, nullptr, out, s);
       else if (p->tile == TileKind::t32x8)
         launch_rec_gpk<R, 32, 8>(g, prev, nullptr, out, p->zchunk, s);
@@ -926,6 +996,13 @@ mgrg_status mgrg_plan_create(const mgrg_grid_desc *desc, mgrg_plan **out) {
       p->pair_path = false;
   if (const char *kg = std::getenv("MGRG_KGEN"))
     p->gen = std::atoi(kg);
+  {
+    // lean family: x, y (and z) refine; used on every level whose extents
+    // are all odd (coarse = even positions), see lean_level()
+    p->lean = p->refine == 7u || (p->refine == 3u && p->kext[L][2] == 1);
+    if (const char *le = std::getenv("MGRG_LEAN"))
+      p->lean = p->lean && std::atoi(le) != 0;
+  }
   p->zchunk = nd == 3 ? 32 : 1;
   if (const char *zc = std::getenv("MGRG_ZCHUNK"))
     if (nd == 3 && std::atoi(zc) > 0)
