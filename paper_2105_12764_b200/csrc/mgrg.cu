@@ -31,6 +31,7 @@
 #include "kernels3.cuh"
 #include "kernels4.cuh"
 #include "lean.cuh"
+#include "thomas_fiber.cuh"
 
 using namespace mgrg;
 
@@ -181,6 +182,7 @@ template <typename R> struct PlanT {
   std::vector<std::array<ThomasGeom<R>, 3>> thom; // [l][kd] (level-(l-1) factors)
   std::vector<std::array<const Stencil<R> *, 3>> sten; // [l][kd] merged R*M tables
   std::vector<std::array<const LeanW<R> *, 3>> lean;   // [l][kd] lean tables (padded)
+  std::vector<std::array<ThomasLean<R>, 3>> tlean;     // [l][kd] chunked Thomas tables
   R *d_geom = nullptr;
 };
 
@@ -370,7 +372,7 @@ template <typename R> mgrg_status upload_geometry(mgrg_plan *p) {
   // host staging of every per-level array in R, then one upload
   std::vector<R> buf;
   struct Ref {
-    size_t h[3], r[3], th[3], tf[3], ti[3], st[3], lw[3];
+    size_t h[3], r[3], th[3], tf[3], ti[3], st[3], lw[3], tl[3];
   };
   std::vector<Ref> refs(L + 1);
   auto push = [&](const std::vector<R> &v) {
@@ -383,7 +385,7 @@ template <typename R> mgrg_status upload_geometry(mgrg_plan *p) {
   for (int l = 1; l <= L; ++l) {
     for (int kd = 0; kd < 3; ++kd) {
       refs[l].h[kd] = refs[l].r[kd] = refs[l].th[kd] = refs[l].tf[kd] =
-          refs[l].ti[kd] = refs[l].st[kd] = refs[l].lw[kd] = size_t(-1);
+          refs[l].ti[kd] = refs[l].st[kd] = refs[l].lw[kd] = refs[l].tl[kd] = size_t(-1);
       const int ud = p->kmap[kd];
       if (ud < 0)
         continue;
@@ -404,6 +406,35 @@ template <typename R> mgrg_status upload_geometry(mgrg_plan *p) {
         refs[l].th[kd] = push(th);
         refs[l].tf[kd] = push(tf);
         refs[l].ti[kd] = push(ti);
+        {
+          // chunked-Thomas tables (thomas_fiber.cuh): {fwd, ip, g, PF, PB}
+          // per position (8-padded), PFend, PBstart [kTfChunks]; products in
+          // fp64 from the working-precision factors, rounded once
+          const uint32_t mm = uint32_t(tf.size());
+          std::vector<R> tl(tf_tab_elems<R>(mm), R(0));
+          R *Q = tl.data(), *Tpe = Q + 8 * size_t(mm), *Tps = Tpe + kTfChunks;
+          for (uint32_t i = 0; i < mm; ++i) {
+            Q[8 * i] = tf[i];
+            Q[8 * i + 1] = ti[i];
+            Q[8 * i + 2] = i + 1 < mm ? R(-double(ti[i]) * double(th[i])) : R(0);
+          }
+          for (int w = 0; w < kTfChunks; ++w) {
+            const uint32_t a = tf_chunk_lo(w, mm), b = tf_chunk_lo(w + 1, mm);
+            double pr = 1.0;
+            for (uint32_t i = a; i < b; ++i) {
+              pr *= double(tf[i]);
+              Q[8 * i + 3] = R(pr);
+            }
+            Tpe[w] = R(pr);
+            pr = 1.0;
+            for (uint32_t i = b; i > a; --i) {
+              pr *= double(Q[8 * (i - 1) + 2]);
+              Q[8 * (i - 1) + 4] = R(pr);
+            }
+            Tps[w] = R(pr);
+          }
+          refs[l].tl[kd] = push(tl);
+        }
         // stencil table (raw bytes of Stencil<R>, a whole number of R's)
         const uint64_t n = H.ext[l][ud], m = H.ext[l - 1][ud];
         std::vector<R> raw(m * (sizeof(Stencil<R>) / sizeof(R)));
@@ -438,6 +469,7 @@ template <typename R> mgrg_status upload_geometry(mgrg_plan *p) {
   P.thom.assign(L + 1, {});
   P.sten.assign(L + 1, {nullptr, nullptr, nullptr});
   P.lean.assign(L + 1, {nullptr, nullptr, nullptr});
+  P.tlean.assign(L + 1, {});
   for (int l = 1; l <= L; ++l) {
     LevelGeom<R> &g = P.geom[l];
     g.refine = 0;
@@ -456,6 +488,13 @@ template <typename R> mgrg_status upload_geometry(mgrg_plan *p) {
       P.sten[l][kd] = refs[l].st[kd] == size_t(-1)
                           ? nullptr
                           : reinterpret_cast<const Stencil<R> *>(base + refs[l].st[kd]);
+      if (refs[l].tl[kd] != size_t(-1)) {
+        ThomasLean<R> &q = P.tlean[l][kd];
+        const uint32_t mm = g.m[kd];
+        const R *b0 = base + refs[l].tl[kd];
+        q.m = mm;
+        q.tab = b0;
+      }
       P.lean[l][kd] = refs[l].lw[kd] == size_t(-1)
                           ? nullptr
                           : reinterpret_cast<const LeanW<R> *>(base + refs[l].lw[kd]);
@@ -509,6 +548,11 @@ void launch_rec_gpk(const LevelGeom<R> &g, const R *coarse, const R *cls, R *out
 static_assert(sizeof(Stencil<float>) % sizeof(float) == 0, "stencil layout");
 static_assert(sizeof(Stencil<double>) % sizeof(double) == 0, "stencil layout");
 
+// experiment knob: chunked fiber-resident Thomas (MGRG_TFIBER=0 disables)
+int g_thomas_fiber = [] {
+  const char *e = std::getenv("MGRG_TFIBER");
+  return e ? std::atoi(e) : 1;
+}();
 // experiment knob: minimum resident CTAs of the level kernels (MGRG_MINB)
 int g_minb = [] {
   const char *e = std::getenv("MGRG_MINB");
@@ -697,10 +741,52 @@ bool try_scan(int kd, const ThomasGeom<R> &t, uint64_t S, uint64_t inner, uint64
   }
 }
 
+template <typename R> constexpr size_t tf_limit() { return 200 * 1024; }
+
+template <typename R, int DIM, int CH> auto tf_kernel() {
+  return thomas_fiber_kernel<R, DIM, CH>;
+}
+template <typename R, int DIM>
+void (*tf_pick(int ch))(R *, ThomasLean<R>, uint64_t, uint32_t, uint32_t, Epi, const R *, R *) {
+  switch (ch) {
+  case 1: return tf_kernel<R, DIM, 1>();
+  case 2: return tf_kernel<R, DIM, 2>();
+  case 3: return tf_kernel<R, DIM, 3>();
+  case 5: return tf_kernel<R, DIM, 5>();
+  case 9: return tf_kernel<R, DIM, 9>();
+  case 17: return tf_kernel<R, DIM, 17>();
+  default: return tf_kernel<R, DIM, 33>();
+  }
+}
 template <typename R>
-void launch_thomas(bool fast, const LevelGeom<R> &g, const ThomasGeom<R> &t, int kd, R *f,
-                   Epi epi, const R *base, R *out, cudaStream_t s) {
+void launch_tf(int kd, int ch, unsigned blocks, size_t sm, cudaStream_t s, R *f,
+               const ThomasLean<R> &tl, uint64_t nfib, uint32_t mx, uint32_t my, Epi epi,
+               const R *base, R *out) {
+  auto k = kd == 0 ? tf_pick<R, 0>(ch) : (kd == 1 ? tf_pick<R, 1>(ch) : tf_pick<R, 2>(ch));
+  k<<<blocks, 32 * kTfChunks, sm, s>>>(f, tl, nfib, mx, my, epi, base, out);
+}
+template <typename R> void set_tf_attrs() {
+  const int lim = int(tf_limit<R>());
+  for (int ch : {1, 2, 3, 5, 9, 17, 33}) {
+    cudaFuncSetAttribute(tf_pick<R, 0>(ch), cudaFuncAttributeMaxDynamicSharedMemorySize, lim);
+    cudaFuncSetAttribute(tf_pick<R, 1>(ch), cudaFuncAttributeMaxDynamicSharedMemorySize, lim);
+    cudaFuncSetAttribute(tf_pick<R, 2>(ch), cudaFuncAttributeMaxDynamicSharedMemorySize, lim);
+  }
+}
+
+template <typename R>
+void launch_thomas(bool fast, const LevelGeom<R> &g, const ThomasGeom<R> &t,
+                   const ThomasLean<R> &tl, int kd, R *f, Epi epi, const R *base, R *out,
+                   cudaStream_t s) {
   const uint64_t mx = g.m[0], my = g.m[1], mz = g.m[2];
+  if (fast && tl.tab && tf_ch(tl.m) && tf_smem<R>(kd, tl.m) <= tf_limit<R>() &&
+      g_thomas_fiber) {
+    const uint64_t nfib = kd == 0 ? my * mz : (kd == 1 ? mx * mz : mx * my);
+    const unsigned blocks = unsigned((nfib + kTfFibers - 1) / kTfFibers);
+    launch_tf<R>(kd, tf_ch(tl.m), blocks, tf_smem<R>(kd, tl.m), s, f, tl, nfib, uint32_t(mx),
+                 uint32_t(my), epi, base, out);
+    return;
+  }
   if (kd == 0) {
     const uint64_t nf = my * mz;
     if (fast && try_scan<R>(0, t, 1, 1, 0, nf, f, epi, base, out, s))
@@ -747,6 +833,7 @@ template <typename R> void set_thomas_attrs() {
                        cudaFuncAttributeMaxDynamicSharedMemorySize, lim);
   cudaFuncSetAttribute(thomas_cols_kernel<R, true>,
                        cudaFuncAttributeMaxDynamicSharedMemorySize, lim);
+  set_tf_attrs<R>();
 }
 
 template <typename R> R *ws(mgrg_plan *p, uint64_t off) {
@@ -834,8 +921,8 @@ mgrg_status run_decompose(mgrg_plan *p, const R *d_in, R *d_cls, cudaStream_t s)
       // f in + z out; the fused apply also reads the packed coarse values
       if (mgrg_status st = rec.begin(MGRG_K_THOMAS_X + kd, l, es * Cn * (last ? 3 : 2)))
         return st;
-      launch_thomas<R>(p->fast, g, P.thom[l][kd], kd, F, last ? Epi::add : Epi::none, Pout,
-                       Pout, s);
+      launch_thomas<R>(p->fast, g, P.thom[l][kd], P.tlean[l][kd], kd, F,
+                       last ? Epi::add : Epi::none, Pout, Pout, s);
       if (mgrg_status st = rec.end())
         return st;
     }
@@ -878,8 +965,8 @@ mgrg_status run_recompose(mgrg_plan *p, const R *d_cls, int k, R *d_out,
         const bool last = i == p->nrefine - 1;
         if (mgrg_status st = rec.begin(MGRG_K_THOMAS_X + kd, l, es * Cn * (last ? 3 : 2)))
           return st;
-        launch_thomas<R>(p->fast, g, P.thom[l][kd], kd, F, last ? Epi::sub : Epi::none, prev,
-                         F, s);
+        launch_thomas<R>(p->fast, g, P.thom[l][kd], P.tlean[l][kd], kd, F,
+                         last ? Epi::sub : Epi::none, prev, F, s);
         if (mgrg_status st = rec.end())
           return st;
       }
@@ -1331,7 +1418,8 @@ static mgrg_status solve_t(mgrg_plan *p, int level, int kd, void *f, cudaStream_
   const LevelGeom<R> &g = pt<R>(p).geom[level];
   if (!((g.refine >> kd) & 1))
     return MGRG_OK; // identity transfer (kernels.hpp:434-435)
-  launch_thomas<R>(p->fast, g, pt<R>(p).thom[level][kd], kd, static_cast<R *>(f), Epi::none,
+  launch_thomas<R>(p->fast, g, pt<R>(p).thom[level][kd], pt<R>(p).tlean[level][kd], kd,
+                   static_cast<R *>(f), Epi::none,
                    nullptr, nullptr, s);
   CUDA_TRY(cudaGetLastError());
   return MGRG_OK;

@@ -1,0 +1,226 @@
+// thomas_fiber.cuh -- FAST-policy batched Thomas solve with whole fibers
+// resident on chip: one HBM read and one HBM write per element.
+//
+// The level-(l-1) mass matrix along a dimension is the same for every fiber
+// (TridiagonalOperator::build, kernels.hpp:98-136), so the recurrences
+//   forward : v_i = f_i + fwd_i * v_{i-1}
+//   backward: x_i = ip_i * v_i + g_i * x_{i+1},   g_i = -ip_i * h_i
+// (thomas_fiber, kernels.hpp:143-151, rearranged: same operator) split into
+// chunks with fiber-independent carry maps: a chunk [a, b) solved with a
+// zero carry-in is corrected by PF_i * c (forward, PF_i = prod_{a..i} fwd)
+// and PB_i * d (backward, PB_i = prod_{i..b-1} g), where the carries c, d
+// follow from the neighbouring chunks' end values by a short sequential
+// pass over the 16 chunks of the CTA (host-precomputed chunk multipliers).
+//
+// CTA = 32 fibers x 16 chunks: warp w owns chunk w of every fiber, lane =
+// fiber, and keeps the chunk (<= CH values) in registers through all three
+// passes.  The tile is staged through shared memory with asynchronous
+// copies (no registers held by loads in flight): y/z fibers as [position]
+// [fiber] rows (position i of the 32 fibers is a row of 32 consecutive x
+// nodes, coalesced), x fibers as the contiguous region of 32 rows with
+// 16-byte copies (pitch m, odd on dyadic levels: conflict-free per-fiber
+// reads).  y/z results go straight to HBM per position; x results back
+// through the tile with 16-byte stores.  The last solve of a
+// level fuses the epilogue (a_{l-1} = P + z on decompose, coarse' =
+// a_{l-1} - z on recompose).
+#pragma once
+
+#include <type_traits>
+
+#include "common.cuh"
+#include "level.cuh"
+
+namespace mgrg {
+
+constexpr int kTfChunks = 16; // warps per CTA = chunks per fiber
+constexpr int kTfFibers = 32;
+
+// Tables: q8[i] = {fwd_i, ip_i, g_i, PF_i, PB_i, 0, 0, 0}, then the chunk
+// multipliers pfend[w] (PF at the chunk end), pbstart[w] (PB at its start).
+template <typename R> struct ThomasLean {
+  const R *tab; // [8m] q8, [kTfChunks] pfend, [kTfChunks] pbstart
+  uint32_t m;
+};
+template <typename R> __host__ __device__ inline size_t tf_tab_elems(uint32_t m) {
+  return 8 * size_t(m) + 2 * kTfChunks;
+}
+// shared memory: [x tile (DIM 0)][carries][tables], 16-byte aligned parts
+template <typename R> __host__ __device__ inline size_t tf_tile_elems(int dim, uint32_t m) {
+  (void)dim;
+  return (size_t(kTfFibers) * m + 3) & ~size_t(3);
+}
+template <typename R> __host__ __device__ inline size_t tf_smem(int dim, uint32_t m) {
+  return (tf_tile_elems<R>(dim, m) + size_t(kTfChunks) * kTfFibers + tf_tab_elems<R>(m)) *
+         sizeof(R);
+}
+__host__ __device__ inline uint32_t tf_chunk_lo(int w, uint32_t m) {
+  return uint32_t((uint64_t(w) * m) / kTfChunks);
+}
+// chunk-length class of a fiber length: the kernel instantiation
+__host__ inline int tf_ch(uint32_t m) {
+  const uint32_t c = (m + kTfChunks - 1) / kTfChunks;
+  for (int ch : {1, 2, 3, 5, 9, 17, 33})
+    if (c <= uint32_t(ch))
+      return ch;
+  return 0; // too long: not handled here
+}
+
+// 16-byte async copy of n elements (src, dst 16-byte aligned) by the CTA.
+template <typename R>
+__device__ __forceinline__ void tf_copy_in(R *dst, const R *src, size_t n, int tid) {
+  constexpr int V = 16 / sizeof(R);
+  const size_t nv = n / V;
+  for (size_t e = tid; e < nv; e += 32 * kTfChunks)
+    cp_async16(dst + e * V, src + e * V);
+  for (size_t e = nv * V + tid; e < n; e += 32 * kTfChunks)
+    cp_async(dst + e, src + e);
+}
+
+// DIM 0: fibers are rows along x (fiber id = row id, positions contiguous);
+// DIM 1: fiber id F = x + m0 * z, position i at x + m0 * (i + m1 * z);
+// DIM 2: fiber id F = x + m0 * y, position i at F + m0 * m1 * i.
+template <typename R, int DIM, int CH>
+__global__ void __launch_bounds__(32 * kTfChunks, sizeof(R) == 4 ? 2 : 1)
+    thomas_fiber_kernel(R *__restrict__ f, ThomasLean<R> t, uint64_t nfib, uint32_t m0,
+                        uint32_t m1, Epi epi, const R *base, R *out) {
+  extern __shared__ __align__(16) unsigned char tf_raw[];
+  R *sm = reinterpret_cast<R *>(tf_raw);
+  const uint32_t m = t.m;
+  R *tile = sm;
+  R *carry = sm + tf_tile_elems<R>(DIM, m);
+  R *tab = carry + kTfChunks * kTfFibers;
+  const R *pfend = tab + 8 * size_t(m), *pbstart = pfend + kTfChunks;
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  const uint64_t F0 = uint64_t(blockIdx.x) * kTfFibers;
+  const int nf = int(nfib - F0 < uint64_t(kTfFibers) ? nfib - F0 : uint64_t(kTfFibers));
+  const uint64_t m01 = uint64_t(m0) * m1;
+  const uint32_t a = tf_chunk_lo(w, m), len = tf_chunk_lo(w + 1, m) - a;
+
+  // fiber address of the lane (DIM 1, 2; lanes past the end repeat the last)
+  uint64_t fa = 0;
+  if (DIM == 1) {
+    const uint64_t F = F0 + min(lane, nf - 1);
+    fa = (F % m0) + m01 * (F / m0);
+  } else if (DIM == 2) {
+    fa = F0 + min(lane, nf - 1);
+  }
+  const uint64_t ps = DIM == 1 ? m0 : m01; // position stride (DIM 1, 2)
+
+  tf_copy_in(tab, t.tab, tf_tab_elems<R>(m), tid);
+  R v[CH];
+  if (DIM == 0) {
+    tf_copy_in(tile, f + F0 * m, size_t(nf) * m, tid);
+    cp_async_commit();
+    cp_async_wait<0>();
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < CH; ++k)
+      v[k] = (uint32_t(k) < len && lane < nf) ? tile[size_t(lane) * m + a + k] : R(0);
+  } else {
+    // position-major tile [i][fiber]: each position is one coalesced row
+    for (uint32_t i = w; i < m; i += kTfChunks)
+      cp_async(tile + size_t(i) * kTfFibers + lane, f + fa + ps * i);
+    cp_async_commit();
+    cp_async_wait<0>();
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < CH; ++k)
+      v[k] = uint32_t(k) < len ? tile[size_t(a + k) * kTfFibers + lane] : R(0);
+  }
+
+  // ---- forward, zero carry-in
+  R acc = R(0);
+#pragma unroll
+  for (int k = 0; k < CH; ++k)
+    if (uint32_t(k) < len) {
+      acc = fma(tab[8 * (a + k)], acc, v[k]);
+      v[k] = acc;
+    }
+  carry[w * 32 + lane] = acc;
+  __syncthreads();
+  R c = R(0);
+  for (int k = 0; k < w; ++k)
+    c = fma(pfend[k], c, carry[k * 32 + lane]);
+  // ---- forward fix-up + backward, zero carry-in (descending)
+  R x = R(0);
+#pragma unroll
+  for (int k = CH - 1; k >= 0; --k)
+    if (uint32_t(k) < len) {
+      const R *q = tab + 8 * (a + k);
+      const R vj = fma(q[3], c, v[k]);
+      x = fma(q[2], x, q[1] * vj);
+      v[k] = x;
+    }
+  __syncthreads(); // every warp has read the forward carries
+  carry[w * 32 + lane] = x;
+  __syncthreads();
+  R d = R(0);
+  for (int k = kTfChunks - 1; k > w; --k)
+    d = fma(pbstart[k], d, carry[k * 32 + lane]);
+  // ---- backward fix-up, epilogue, store
+#pragma unroll
+  for (int k = 0; k < CH; ++k)
+    if (uint32_t(k) < len)
+      v[k] = fma(tab[8 * (a + k) + 4], d, v[k]);
+  if (DIM == 0) {
+    if (lane < nf)
+#pragma unroll
+      for (int k = 0; k < CH; ++k)
+        if (uint32_t(k) < len)
+          tile[size_t(lane) * m + a + k] = v[k];
+    __syncthreads();
+    constexpr int V = 16 / sizeof(R);
+    using VT = typename std::conditional<sizeof(R) == 4, float4, double2>::type;
+    const size_t n = size_t(nf) * m, nv = n / V;
+    R *dst = epi == Epi::none ? f + F0 * m : out + F0 * m;
+    const R *bs = base + F0 * m;
+    const bool vec = ((reinterpret_cast<uintptr_t>(dst) |
+                       (epi == Epi::none ? 0 : reinterpret_cast<uintptr_t>(bs))) & 15) == 0;
+    for (size_t e = vec ? tid : nv; e < nv; e += 32 * kTfChunks) {
+      VT z = *reinterpret_cast<const VT *>(tile + e * V);
+      if (epi != Epi::none) {
+        const VT b = *reinterpret_cast<const VT *>(bs + e * V);
+        R *zz = reinterpret_cast<R *>(&z);
+        const R *bb = reinterpret_cast<const R *>(&b);
+#pragma unroll
+        for (int q = 0; q < V; ++q)
+          zz[q] = epi == Epi::add ? bb[q] + zz[q] : bb[q] - zz[q];
+      }
+      *reinterpret_cast<VT *>(dst + e * V) = z;
+    }
+    for (size_t e = (vec ? nv * V : 0) + tid; e < n; e += 32 * kTfChunks) {
+      const R z = tile[e];
+      dst[e] = epi == Epi::none ? z : (epi == Epi::add ? bs[e] + z : bs[e] - z);
+    }
+  } else if (lane < nf) {
+    R *p = (epi == Epi::none ? f : out) + fa + ps * a;
+    const R *q = base + fa + ps * a;
+    if (epi == Epi::none) {
+#pragma unroll
+      for (int k = 0; k < CH; ++k) {
+        if (uint32_t(k) < len)
+          *p = v[k];
+        p += ps;
+      }
+    } else {
+      // base values in batches of 8 (bounded registers, 8 loads in flight)
+#pragma unroll
+      for (int k0 = 0; k0 < CH; k0 += 8) {
+        R bv[8];
+#pragma unroll
+        for (int k = k0; k < k0 + 8 && k < CH; ++k) {
+          bv[k - k0] = uint32_t(k) < len ? *q : R(0);
+          q += ps;
+        }
+#pragma unroll
+        for (int k = k0; k < k0 + 8 && k < CH; ++k) {
+          if (uint32_t(k) < len)
+            *p = epi == Epi::add ? bv[k - k0] + v[k] : bv[k - k0] - v[k];
+          p += ps;
+        }
+      }
+    }
+  }
+}
+
+} // namespace mgrg
