@@ -38,6 +38,7 @@ constexpr int kLeanOut = 30;  // coarse x outputs per warp
 // lean_ty<R>() coarse rows, z chunks of kLeanZC coarse planes (1 in 2-D).
 struct LeanTiles {
   uint32_t ntx, nty, ntz;
+  int zc; // coarse z planes per chunk (host-chosen per level: enough warps)
   __host__ __device__ uint64_t warps() const { return uint64_t(ntx) * nty * ntz; }
 };
 
@@ -86,33 +87,68 @@ template <typename R> __device__ __forceinline__ R flerp(R a, R b, R t) {
   return fma(t, b - a, a);
 }
 
-// Raw 8/16-byte load of one row for the lane: ALIGNED rows fetch the lane's
-// (e, o) pair, misaligned rows (o_{a-1}, e_a).  `p` points at the lane's
-// even node (column clamped into the level).  Only an aligned pair can
-// cross the end of the array (even node = last element of the row, in the
-// last row); the last column loads its even node alone.
-template <typename R, bool ALIGNED>
-__device__ __forceinline__ typename Vec2<R>::T lean_raw(const R *__restrict__ p, bool lastcol) {
-  using V = typename Vec2<R>::T;
-  if constexpr (ALIGNED) {
-    V v;
-    if (lastcol) {
-      v.x = __ldg(p);
-      v.y = R(0);
-    } else {
-      v = __ldg(reinterpret_cast<const V *>(p));
-    }
-    return v;
-  } else {
-    return __ldg(reinterpret_cast<const V *>(p - 1));
-  }
-}
 template <typename R, bool ALIGNED>
 __device__ __forceinline__ Pair<R> lean_pair(const typename Vec2<R>::T &v) {
   if constexpr (ALIGNED)
     return {v.x, v.y};
   else
     return {v.y, __shfl_down_sync(0xffffffffu, v.x, 1)};
+}
+
+// Per-warp staging ring of the decompose kernel: 3 plane slots of NR rows;
+// a staged row is the 16-byte aligned superset of the lane pairs' 64
+// elements (RP elements, NCH 16-byte chunks), fetched with LDGSTS.128 so
+// that two planes of loads are in flight while one is processed, without
+// holding registers.
+template <typename R> struct LeanStage {
+  static constexpr int V = 16 / int(sizeof(R));
+  static constexpr int NCH = (64 + 2 * V - 2) / V; // ceil((64 + V - 1) / V)
+  static constexpr int RP = NCH * V;
+};
+
+// Issue the copies of one plane into `slot`.  `pb` points at the plane's
+// element 0, q = (element index of pb) mod V, row r starts at element
+// rowoff[r] of the plane.  Interior planes (every chunk inside the array)
+// take the unchecked path; near the array ends chunks before element 0 are
+// skipped (invalid columns) and chunks crossing the end go element-wise.
+template <typename R, int NR>
+__device__ __forceinline__ void lean_stage_plane(R *slot, const R *__restrict__ pb, int q,
+                                                 const int *rowoff, bool interior,
+                                                 int64_t pbase, int64_t ntot, int lane) {
+  constexpr int V = LeanStage<R>::V, NCH = LeanStage<R>::NCH, RP = LeanStage<R>::RP;
+  // lane c copies chunk c (and c + 32 when NCH > 32) of every row
+  const R *gl = pb - q + lane * V; // 16-byte aligned element of the plane
+  R *sl = slot + lane * V;
+  if (interior) {
+    if (lane < NCH) {
+#pragma unroll
+      for (int r = 0; r < NR; ++r)
+        cp_async16(sl + r * RP, gl + ((q + rowoff[r]) & ~(V - 1)));
+    }
+    if (NCH > 32 && lane + 32 < NCH) {
+#pragma unroll
+      for (int r = 0; r < NR; ++r)
+        cp_async16(sl + r * RP + 32 * V, gl + ((q + rowoff[r]) & ~(V - 1)) + 32 * V);
+    }
+    return;
+  }
+#pragma unroll
+  for (int r = 0; r < NR; ++r) {
+    const int s0 = ((q + rowoff[r]) & ~(V - 1)) - q;
+#pragma unroll
+    for (int c = lane; c < NCH; c += 32) {
+      const int64_t g = pbase + s0 + int64_t(c) * V;
+      R *d = slot + r * RP + c * V;
+      if (g >= 0 && g + V <= ntot) {
+        cp_async16(d, pb + s0 + c * V);
+      } else if (g >= 0) {
+#pragma unroll
+        for (int v = 0; v < V; ++v)
+          if (g + v < ntot)
+            cp_async(d + v, pb + s0 + c * V + v);
+      }
+    }
+  }
 }
 
 // Class/packed stores of one plane: row r of the band writes its even node
@@ -129,21 +165,27 @@ template <typename R> struct PlaneOut {
 //        (r + PAR) even, r = band row index, band row 0 even).
 template <typename R, int TY, bool EVEN>
 __device__ __forceinline__ void lean_plane(
-    const R *__restrict__ pin, const int *rowoff, bool lastcol, R txr, const R *tyr,
+    const R *__restrict__ slot, int q, const int *rowoff, R txr, const R *tyr,
     const W5r<R> &wx, const W5r<R> *wy, bool ve, bool vo, uint32_t stmask_e,
     uint32_t stmask_o, const PlaneOut<R> &po, int ex_e, int ex_o, R *We, R *Wo,
     const R *WLe, const R *WLo, R tz, R *Y) {
   constexpr int NR = 2 * TY + 3;
+  constexpr int RP = LeanStage<R>::RP;
   using V = typename Vec2<R>::T;
+  const int lane = threadIdx.x & 31;
   V raw[NR];
-  // EVEN planes: aligned rows are the even ones; ODD planes: the odd ones
+  // staged row r holds the band row from its 16-byte aligned start; the
+  // lane's even node sits at shift_r + 2*lane, shift_r = (q + rowoff[r]) mod
+  // V.  EVEN planes: aligned rows (even shift) are the even ones; odd
+  // planes: the odd ones.
+  const R *sl = slot + 2 * lane;
 #pragma unroll
   for (int r = 0; r < NR; ++r) {
-    const R *p = pin + rowoff[r];
+    const R *p = sl + r * RP + ((q + rowoff[r]) & (LeanStage<R>::V - 1));
     if (((r & 1) == 0) == EVEN)
-      raw[r] = lean_raw<R, true>(p, lastcol);
+      raw[r] = *reinterpret_cast<const V *>(p);
     else
-      raw[r] = lean_raw<R, false>(p, lastcol);
+      raw[r] = *reinterpret_cast<const V *>(p - 1);
   }
   Pair<R> u[NR];
 #pragma unroll
@@ -178,9 +220,9 @@ __device__ __forceinline__ void lean_plane(
     const R co = vo ? u[r].o - wo : R(0);
     const int rr = r >> 1;
     if ((stmask_e >> r) & 1u)
-      ((r & 1) ? po.be1 : po.be0)[int64_t(ex_e) * rr] = kept ? u[r].e : ce;
+      ((r & 1) ? po.be1 : po.be0)[uint32_t(ex_e * rr)] = kept ? u[r].e : ce;
     if ((stmask_o >> r) & 1u)
-      ((r & 1) ? po.bo1 : po.bo0)[int64_t(ex_o) * rr] = co;
+      ((r & 1) ? po.bo1 : po.bo0)[uint32_t(ex_o * rr)] = co;
     X[r] = kept ? lean_xpass_odd(wx, co) : lean_xpass(wx, ce, co);
   }
 #pragma unroll
@@ -197,6 +239,10 @@ __device__ __forceinline__ void lean_plane(
 // Decompose level kernel: GPK forward (class stores, packed kept nodes) and
 // the load vector f = (R*M)_z (R*M)_y (R*M)_x vec(C) on the coarse lattice.
 // Z3 = false: 2-D level (n2 == 1), one plane.
+template <typename R> __host__ __device__ constexpr size_t lean_dec_smem() {
+  return size_t(kLeanWPB) * 3 * (2 * lean_ty<R>() + 3) * LeanStage<R>::RP * sizeof(R);
+}
+
 template <typename R, bool Z3>
 __global__ void __launch_bounds__(32 * kLeanWPB, 3)
     lean_dec_kernel(LevelGeom<R> g, const LeanW<R> *__restrict__ lx,
@@ -204,7 +250,10 @@ __global__ void __launch_bounds__(32 * kLeanWPB, 3)
                     const R *__restrict__ in, R *__restrict__ cls, R *__restrict__ P,
                     R *__restrict__ f, LeanTiles tl) {
   constexpr int TY = lean_ty<R>(), NR = 2 * TY + 3;
+  constexpr int V = LeanStage<R>::V, SLOT = NR * LeanStage<R>::RP;
+  extern __shared__ __align__(16) unsigned char lean_raw_sm[];
   const int lane = threadIdx.x & 31;
+  R *ring = reinterpret_cast<R *>(lean_raw_sm) + size_t(threadIdx.x >> 5) * 3 * SLOT;
   const uint64_t wid = uint64_t(blockIdx.x) * kLeanWPB + (threadIdx.x >> 5);
   if (wid >= tl.warps())
     return;
@@ -214,7 +263,7 @@ __global__ void __launch_bounds__(32 * kLeanWPB, 3)
 
   const int n0 = int(g.n[0]), n1 = int(g.n[1]), n2 = int(g.n[2]);
   const int m0 = int(g.m[0]), m1 = int(g.m[1]), m2 = int(g.m[2]);
-  const int64_t nxy = int64_t(n0) * n1;
+  const int64_t nxy = int64_t(n0) * n1, ntot = nxy * n2;
 
   // ---- lane x geometry
   const int qc = int(kLeanOut * tx) - 1 + lane;
@@ -226,20 +275,19 @@ __global__ void __launch_bounds__(32 * kLeanWPB, 3)
   W5r<R> wx = lean_w(lxq);
   if (!outl)
     wx = {R(0), R(0), R(0), R(0), R(0)};
-  const int qs = min(max(qc, 0), m0 - 1); // load column (clamped)
-  const bool lastcol = qs == m0 - 1;
+  const int X0 = 2 * (int(kLeanOut * tx) - 1); // lane 0's even node
 
   // ---- y band: rows Y0 + r, r = 0 .. NR-1
   const int cy0 = int(tyb) * TY, cy1 = min(cy0 + TY, m1);
   const int Y0 = 2 * cy0 - 2;
-  int rowoff[NR];
+  int rowoff[NR]; // within-plane element offset of band row r (n0 * n1 < 2^31)
   uint32_t ownrows = 0;
 #pragma unroll
   for (int r = 0; r < NR; ++r) {
     const int y = Y0 + r;
     const bool rv = y >= 0 && y < n1;
-    // invalid rows read a row of the same parity (values unused: weights 0)
-    rowoff[r] = (rv ? y : (r & 1)) * n0 + 2 * qs;
+    // invalid rows stage a row of the same parity (values unused: weights 0)
+    rowoff[r] = (rv ? y : (r & 1)) * n0 + X0;
     if (rv && r >= 2 && r < 2 + 2 * (cy1 - cy0))
       ownrows |= 1u << r;
   }
@@ -253,9 +301,41 @@ __global__ void __launch_bounds__(32 * kLeanWPB, 3)
     wy[j] = lean_w(ly + min(cy0 + j, m1 + 1) + 2);
   const uint32_t st_e = outl ? ownrows : 0u, st_o = (outl && vo) ? ownrows : 0u;
 
-  // ---- z chunk
-  const int cz0 = Z3 ? int(tzc) * kLeanZC : 0;
-  const int cz1 = Z3 ? min(cz0 + kLeanZC, m2) : 1;
+  // ---- z chunk and the plane sequence: j = 0: even plane 2(cz0-1); then
+  // per step k = cz0 .. cz1: even plane 2k (j odd), odd plane 2k-1 (j even)
+  const int cz0 = Z3 ? int(tzc) * tl.zc : 0;
+  const int cz1 = Z3 ? min(cz0 + tl.zc, m2) : 1;
+  const int kbeg = Z3 ? cz0 - 1 : 0, kend = Z3 ? cz1 : 0;
+  const int J = Z3 ? 2 * (cz1 - cz0 + 1) + 1 : 1;
+  auto plane_of = [&](int j) -> int { // fine plane index, or -1 when skipped
+    if (!Z3)
+      return 0;
+    const int k = j == 0 ? cz0 - 1 : cz0 + (j - 1) / 2;
+    const int p = (j == 0 || (j & 1)) ? 2 * k : 2 * k - 1;
+    const bool ok = (j & 1) || j == 0 ? (p >= 0 && p < n2) : (p >= 1 && p < n2);
+    return ok ? p : -1;
+  };
+  // rows of the band lie in [rowoff[0], rowoff[NR-1] + 64 + V) of a plane
+  int rlo = rowoff[0], rhi = rowoff[0];
+#pragma unroll
+  for (int r = 1; r < NR; ++r) {
+    rlo = min(rlo, rowoff[r]);
+    rhi = max(rhi, rowoff[r]);
+  }
+  rlo -= V;
+  rhi += LeanStage<R>::RP + V;
+  auto issue = [&](int j) {
+    const int p = j < J ? plane_of(j) : -1;
+    if (p >= 0) {
+      const int64_t pbase = int64_t(p) * nxy;
+      const bool interior = pbase + rlo >= 0 && pbase + rhi <= ntot;
+      const int slot = j % 3;
+      lean_stage_plane<R, NR>(ring + slot * SLOT, in + pbase, int(pbase & (V - 1)), rowoff,
+                              interior, pbase, ntot, lane);
+    }
+    cp_async_commit();
+  };
+  auto q_of = [&](int p) -> int { return int((int64_t(p) * nxy) & (V - 1)); };
 
   R WLe[NR], WLo[NR];
 #pragma unroll
@@ -268,57 +348,79 @@ __global__ void __launch_bounds__(32 * kLeanWPB, 3)
   const int64_t m01 = int64_t(m0) * m1;
   R *fq = f + qc + int64_t(m0) * cy0;
 
-  for (int k = Z3 ? cz0 - 1 : 0; k <= (Z3 ? cz1 : 0); ++k) {
+  issue(0);
+  issue(1);
+  int j = 0, js = 0; // plane counter and its ring slot (j % 3)
+  for (int k = kbeg; k <= kend; ++k) {
     R YE[TY], YO[TY];
     R We[NR], Wo[NR];
     // ================= even plane 2k =================
-    const int pe = 2 * k;
-    if (pe >= 0 && pe < n2) {
-      const bool own = pe >= 2 * cz0 && pe < 2 * cz1;
-      // zr = k; rows start at yr = cy0 - 1
-      const int64_t yb = int64_t(cy0) - 1;
-      PlaneOut<R> po;
-      po.be0 = P + qc + int64_t(m0) * (yb + int64_t(m1) * k);
-      po.bo0 = cls + g.tbase[1] + qc + int64_t(m0 - 1) * (yb + int64_t(m1) * k);
-      po.be1 = cls + g.tbase[2] + qc + int64_t(m0) * (yb + int64_t(m1 - 1) * k);
-      po.bo1 = cls + g.tbase[3] + qc + int64_t(m0 - 1) * (yb + int64_t(m1 - 1) * k);
-      lean_plane<R, TY, true>(in + int64_t(pe) * nxy, rowoff, lastcol, txr, tyr, wx, wy, ve,
-                              vo, own ? st_e : 0u, own ? st_o : 0u, po, m0, m0 - 1, We, Wo,
-                              nullptr, nullptr, R(0), YE);
-    } else {
+    {
+      const int pe = 2 * k;
+      issue(j + 2);
+      cp_async_wait<2>();
+      __syncwarp();
+      if (pe >= 0 && pe < n2) {
+        const bool own = pe >= 2 * cz0 && pe < 2 * cz1;
+        const int64_t yb = int64_t(cy0) - 1; // rank of band row 0
+        PlaneOut<R> po;
+        po.be0 = P + qc + int64_t(m0) * (yb + int64_t(m1) * k);
+        po.bo0 = cls + g.tbase[1] + qc + int64_t(m0 - 1) * (yb + int64_t(m1) * k);
+        po.be1 = cls + g.tbase[2] + qc + int64_t(m0) * (yb + int64_t(m1 - 1) * k);
+        po.bo1 = cls + g.tbase[3] + qc + int64_t(m0 - 1) * (yb + int64_t(m1 - 1) * k);
+        lean_plane<R, TY, true>(ring + js * SLOT, q_of(pe), rowoff, txr, tyr, wx, wy, ve,
+                                vo, own ? st_e : 0u, own ? st_o : 0u, po, m0, m0 - 1, We, Wo,
+                                nullptr, nullptr, R(0), YE);
+      } else {
 #pragma unroll
-      for (int r = 0; r < NR; ++r)
-        We[r] = Wo[r] = R(0);
+        for (int r = 0; r < NR; ++r)
+          We[r] = Wo[r] = R(0);
 #pragma unroll
-      for (int j = 0; j < TY; ++j)
-        YE[j] = R(0);
+        for (int i = 0; i < TY; ++i)
+          YE[i] = R(0);
+      }
+      __syncwarp(); // slot j % 3 is refilled by issue(j + 3)
+      ++j;
+      js = js == 2 ? 0 : js + 1;
     }
     if constexpr (!Z3) {
 #pragma unroll
-      for (int j = 0; j < TY; ++j)
-        if (outl && cy0 + j < cy1)
-          fq[int64_t(m0) * j] = YE[j];
+      for (int i = 0; i < TY; ++i)
+        if (outl && cy0 + i < cy1)
+          fq[int64_t(m0) * i] = YE[i];
       break;
     }
     // ================= odd plane 2k - 1 =================
-    const int pz = pe - 1;
+    const int pz = 2 * k - 1;
     const LeanW<R> *lzk = lz + k + 1; // coarse c = k - 1 (padded index c + 2)
-    if (k >= cz0 && pz >= 1 && pz < n2) {
-      const bool own = pz >= 2 * cz0 && pz < 2 * cz1;
-      const int64_t yb = int64_t(cy0) - 1;
-      const int64_t zr = k - 1;
-      PlaneOut<R> po;
-      po.be0 = cls + g.tbase[4] + qc + int64_t(m0) * (yb + int64_t(m1) * zr);
-      po.bo0 = cls + g.tbase[5] + qc + int64_t(m0 - 1) * (yb + int64_t(m1) * zr);
-      po.be1 = cls + g.tbase[6] + qc + int64_t(m0) * (yb + int64_t(m1 - 1) * zr);
-      po.bo1 = cls + g.tbase[7] + qc + int64_t(m0 - 1) * (yb + int64_t(m1 - 1) * zr);
-      lean_plane<R, TY, false>(in + int64_t(pz) * nxy, rowoff, lastcol, txr, tyr, wx, wy, ve,
-                               vo, own ? st_e : 0u, own ? st_o : 0u, po, m0, m0 - 1, We, Wo,
-                               WLe, WLo, __ldg(&lzk->t), YO);
+    if (k >= cz0) {
+      issue(j + 2);
+      cp_async_wait<2>();
+      __syncwarp();
+      if (pz >= 1 && pz < n2) {
+        const bool own = pz >= 2 * cz0 && pz < 2 * cz1;
+        const int64_t yb = int64_t(cy0) - 1;
+        const int64_t zr = k - 1;
+        PlaneOut<R> po;
+        po.be0 = cls + g.tbase[4] + qc + int64_t(m0) * (yb + int64_t(m1) * zr);
+        po.bo0 = cls + g.tbase[5] + qc + int64_t(m0 - 1) * (yb + int64_t(m1) * zr);
+        po.be1 = cls + g.tbase[6] + qc + int64_t(m0) * (yb + int64_t(m1 - 1) * zr);
+        po.bo1 = cls + g.tbase[7] + qc + int64_t(m0 - 1) * (yb + int64_t(m1 - 1) * zr);
+        lean_plane<R, TY, false>(ring + js * SLOT, q_of(pz), rowoff, txr, tyr, wx, wy, ve,
+                                 vo, own ? st_e : 0u, own ? st_o : 0u, po, m0, m0 - 1, We,
+                                 Wo, WLe, WLo, __ldg(&lzk->t), YO);
+      } else {
+#pragma unroll
+        for (int i = 0; i < TY; ++i)
+          YO[i] = R(0);
+      }
+      __syncwarp();
+      ++j;
+      js = js == 2 ? 0 : js + 1;
     } else {
 #pragma unroll
-      for (int j = 0; j < TY; ++j)
-        YO[j] = R(0);
+      for (int i = 0; i < TY; ++i)
+        YO[i] = R(0);
     }
 #pragma unroll
     for (int r = 0; r < NR; ++r) {
@@ -327,20 +429,21 @@ __global__ void __launch_bounds__(32 * kLeanWPB, 3)
     }
     // ================= z pass (rolling accumulators) =================
     {
-      const R a3 = __ldg(lzk->w + 3), a4 = __ldg(lzk->w + 4);       // output k-1
-      const R b1 = __ldg(lzk[1].w + 1), b2 = __ldg(lzk[1].w + 2);   // output k
-      const R c0 = __ldg(lzk[2].w);                                 // output k+1
+      const R a3 = __ldg(lzk->w + 3), a4 = __ldg(lzk->w + 4);     // output k-1
+      const R b1 = __ldg(lzk[1].w + 1), b2 = __ldg(lzk[1].w + 2); // output k
+      const R c0 = __ldg(lzk[2].w);                               // output k+1
       const bool emit = outl && k - 1 >= cz0 && k - 1 < cz1;
 #pragma unroll
-      for (int j = 0; j < TY; ++j) {
-        const R out = fma(a3, YO[j], fma(a4, YE[j], accM[j]));
-        if (emit && cy0 + j < cy1)
-          fq[int64_t(m0) * j + m01 * (k - 1)] = out;
-        accM[j] = fma(b1, YO[j], fma(b2, YE[j], acc0[j]));
-        acc0[j] = c0 * YE[j];
+      for (int i = 0; i < TY; ++i) {
+        const R out = fma(a3, YO[i], fma(a4, YE[i], accM[i]));
+        if (emit && cy0 + i < cy1)
+          fq[int64_t(m0) * i + m01 * (k - 1)] = out;
+        accM[i] = fma(b1, YO[i], fma(b2, YE[i], acc0[i]));
+        acc0[i] = c0 * YE[i];
       }
     }
   }
+  cp_async_wait<0>();
 }
 
 // ---------------------------------------------------------------------------
@@ -388,8 +491,8 @@ __global__ void __launch_bounds__(32 * kLeanWPB, 4)
   // type's y range belong to invalid rows (masked) and read a valid row
   const int yrmax_e = m1 - 1, yrmax_o = m1 - 2;
 
-  const int cz0 = Z3 ? int(tzc) * kLeanZC : 0;
-  const int cz1 = Z3 ? min(cz0 + kLeanZC, m2) : 1;
+  const int cz0 = Z3 ? int(tzc) * tl.zc : 0;
+  const int cz1 = Z3 ? min(cz0 + tl.zc, m2) : 1;
   R accM[TY], acc0[TY];
 #pragma unroll
   for (int j = 0; j < TY; ++j)
@@ -577,8 +680,8 @@ __global__ void __launch_bounds__(32 * kLeanWPB, 4)
   for (int i = 0; i < TG; ++i)
     rfo[i] = min(cy0 + i, max(m1 - 2, 0));
 
-  const int cz0 = Z3 ? int(tzc) * kLeanZC : 0;
-  const int cz1 = Z3 ? min(cz0 + kLeanZC, m2) : 1;
+  const int cz0 = Z3 ? int(tzc) * tl.zc : 0;
+  const int cz1 = Z3 ? min(cz0 + tl.zc, m2) : 1;
   R WLe[NF], WLo[NF];
   // step k: even plane 2k (coarse plane k) and, for k > cz0, the odd plane
   // 2k-1 between coarse planes k-1 and k
@@ -666,19 +769,34 @@ __global__ void __launch_bounds__(32 * kLeanWPB, 4)
   }
 }
 
-template <typename R> LeanTiles lean_gtiles(uint32_t m0, uint32_t m1, uint32_t m2, bool z3) {
-  LeanTiles t;
-  t.ntx = (m0 + kLeanGOut - 1) / kLeanGOut;
-  t.nty = (m1 + lean_tg<R>() - 1) / lean_tg<R>();
-  t.ntz = z3 ? (m2 + kLeanZC - 1) / kLeanZC : 1;
-  return t;
+// z chunk length: the longest (fewest halo planes, kLeanZC) that still
+// gives about two full waves of warps; small levels get short chunks so the
+// per-warp plane walk (a serial chain of dependent steps) stays short.
+inline int lean_zc(uint64_t xy_tiles, uint32_t m2, bool z3) {
+  if (!z3)
+    return 1;
+  const uint64_t want = 148ull * 32; // warps
+  int zc = kLeanZC;
+  while (zc > 2 && xy_tiles * ((m2 + zc - 1) / zc) < want)
+    zc /= 2;
+  return zc;
 }
 
 template <typename R> LeanTiles lean_tiles(uint32_t m0, uint32_t m1, uint32_t m2, bool z3) {
   LeanTiles t;
   t.ntx = (m0 + kLeanOut - 1) / kLeanOut;
   t.nty = (m1 + lean_ty<R>() - 1) / lean_ty<R>();
-  t.ntz = z3 ? (m2 + kLeanZC - 1) / kLeanZC : 1;
+  t.zc = lean_zc(uint64_t(t.ntx) * t.nty, m2, z3);
+  t.ntz = z3 ? (m2 + t.zc - 1) / t.zc : 1;
+  return t;
+}
+
+template <typename R> LeanTiles lean_gtiles(uint32_t m0, uint32_t m1, uint32_t m2, bool z3) {
+  LeanTiles t;
+  t.ntx = (m0 + kLeanGOut - 1) / kLeanGOut;
+  t.nty = (m1 + lean_tg<R>() - 1) / lean_tg<R>();
+  t.zc = lean_zc(uint64_t(t.ntx) * t.nty, m2, z3);
+  t.ntz = z3 ? (m2 + t.zc - 1) / t.zc : 1;
   return t;
 }
 

@@ -642,11 +642,11 @@ void launch_lean_dec(const LevelGeom<R> &g, const std::array<const LeanW<R> *, 3
   const LeanTiles t = lean_tiles<R>(g.m[0], g.m[1], g.m[2], z3);
   const unsigned blocks = unsigned((t.warps() + kLeanWPB - 1) / kLeanWPB);
   if (z3)
-    lean_dec_kernel<R, true><<<blocks, 32 * kLeanWPB, 0, s>>>(g, st[0], st[1], st[2], in, cls,
-                                                              P, f, t);
+    lean_dec_kernel<R, true><<<blocks, 32 * kLeanWPB, lean_dec_smem<R>(), s>>>(
+        g, st[0], st[1], st[2], in, cls, P, f, t);
   else
-    lean_dec_kernel<R, false><<<blocks, 32 * kLeanWPB, 0, s>>>(g, st[0], st[1], st[2], in,
-                                                               cls, P, f, t);
+    lean_dec_kernel<R, false><<<blocks, 32 * kLeanWPB, lean_dec_smem<R>(), s>>>(
+        g, st[0], st[1], st[2], in, cls, P, f, t);
 }
 template <typename R>
 void launch_lean_rload(const LevelGeom<R> &g, const std::array<const LeanW<R> *, 3> &st,

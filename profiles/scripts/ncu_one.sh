@@ -8,5 +8,6 @@ timeout 900 ncu --set full --clock-control none --import-source on -k regex:$K -
 ncu -i gpurun_out/$TAG.ncu-rep --page raw --csv > gpurun_out/$TAG.raw.csv 2>/dev/null
 ncu -i gpurun_out/$TAG.ncu-rep --page details --csv > gpurun_out/$TAG.details.csv 2>/dev/null
 ncu -i gpurun_out/$TAG.ncu-rep --page source --csv --print-source sass > gpurun_out/$TAG.sass.csv 2>/dev/null
-gzip -f gpurun_out/$TAG.sass.csv
+ncu -i gpurun_out/$TAG.ncu-rep --page source --csv --print-source cuda > gpurun_out/$TAG.cuda.csv 2>/dev/null
+gzip -f gpurun_out/$TAG.sass.csv gpurun_out/$TAG.cuda.csv
 mkdir -p /tmp/reps && mv gpurun_out/$TAG.ncu-rep /tmp/reps/
