@@ -152,7 +152,9 @@ def hbm_peak():
 
 
 def ncu_traffic():
-    """dram bytes per launch from the committed ncu --set full capture."""
+    """dram bytes (read + write) per launch from the committed ncu --set full
+    captures (profiles/ncu_traffic.json, written by profiles/scripts/traffic.py),
+    keyed "<kind>/L<level>/<arith>"."""
     p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     try:
         with open(p) as f:
@@ -378,7 +380,7 @@ def run_ours(args, rank, world, local_rank):
     achieved = dbytes / (davg * 1e-3) / 1e9
     step_dev_ms = sum(g[0] for g in groups.values()) / K
     alg_step = sum(g[2] * g[1] for g in groups.values()) / K
-    traffic = ncu_traffic().get(f"{dk}/L{dl}")
+    traffic = ncu_traffic().get(f"{dk}/L{dl}/{args.arith}")
     roofline = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak,
                 "unit": "GB/s", "frac": round(achieved / peak, 4),
                 "traffic": traffic, "kernel": f"{dk} level {dl}",
@@ -438,8 +440,10 @@ def main():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     ap.add_argument("--no-e2e", action="store_true", help="skip the host-buffer leg")
-    ap.add_argument("--arith", choices=["exact", "fast"], default="exact",
-                    help="exact: bit-identical to the reference; fast: FMA policy")
+    ap.add_argument("--arith", choices=["exact", "fast"], default="fast",
+                    help="fast (default): FMA policy, per class max|gpu-cpu| <= 1e-5 "
+                         "(f32) / 1e-12 (f64) of the input range -- the north_star parity "
+                         "bar; exact: bit-identical to the reference")
     args = ap.parse_args()
     world = env_int("WORLD_SIZE", 1)
     rank = env_int("RANK", 0)
