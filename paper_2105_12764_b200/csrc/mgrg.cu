@@ -655,11 +655,11 @@ void launch_lean_rload(const LevelGeom<R> &g, const std::array<const LeanW<R> *,
   const LeanTiles t = lean_tiles<R>(g.m[0], g.m[1], g.m[2], z3);
   const unsigned blocks = unsigned((t.warps() + kLeanWPB - 1) / kLeanWPB);
   if (z3)
-    lean_rload_kernel<R, true><<<blocks, 32 * kLeanWPB, 0, s>>>(g, st[0], st[1], st[2], cls, f,
-                                                                t);
+    lean_rload_kernel<R, true><<<blocks, 32 * kLeanWPB, 0, s>>>(
+        g, st[0], st[1], st[2], cls, f, t);
   else
-    lean_rload_kernel<R, false><<<blocks, 32 * kLeanWPB, 0, s>>>(g, st[0], st[1], st[2], cls,
-                                                                 f, t);
+    lean_rload_kernel<R, false><<<blocks, 32 * kLeanWPB, 0, s>>>(
+        g, st[0], st[1], st[2], cls, f, t);
 }
 template <typename R>
 void launch_lean_rgpk(const LevelGeom<R> &g, const std::array<const LeanW<R> *, 3> &st,
