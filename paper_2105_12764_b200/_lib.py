@@ -10,7 +10,8 @@ import os
 from . import errors
 
 PKG_DIR = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(PKG_DIR, "libmgrg.so")
+# MGRG_LIB: an alternative in-tree build (kernel-variant experiments)
+LIB_PATH = os.environ.get("MGRG_LIB") or os.path.join(PKG_DIR, "libmgrg.so")
 HEADER = os.path.join(os.path.dirname(PKG_DIR), "include", "mgrg.h")
 
 MGRG_F32 = 4

@@ -33,6 +33,12 @@ template <typename R> __host__ __device__ constexpr int lean_ty() { return sizeo
 constexpr int kLeanZC = 32;   // coarse z planes per warp chunk
 constexpr int kLeanWPB = 4;   // warps per CTA (independent tiles)
 constexpr int kLeanOut = 30;  // coarse x outputs per warp
+#ifndef LEAN_RL_TY
+#define LEAN_RL_TY 6
+#endif
+#ifndef LEAN_RL_MINB
+#define LEAN_RL_MINB 3
+#endif
 
 // Warp tiles of a lean launch: x tiles of 30 coarse columns, y bands of
 // lean_ty<R>() coarse rows, z chunks of kLeanZC coarse planes (1 in 2-D).
@@ -451,12 +457,16 @@ __global__ void __launch_bounds__(32 * kLeanWPB, 3)
 // class buffer of level l (coarse-in-every-dim nodes are zero).  Same warp
 // tiling and band walk as lean_dec_kernel; the class rows are coalesced
 // 4/8-byte loads (lane qc of a type row is element qc).
+template <typename R> __host__ __device__ constexpr int lean_ty_rl() {
+  return sizeof(R) == 4 ? LEAN_RL_TY : 4; // taller band: fewer halo rows (no W registers here)
+}
+
 template <typename R, bool Z3>
-__global__ void __launch_bounds__(32 * kLeanWPB, 4)
+__global__ void __launch_bounds__(32 * kLeanWPB, LEAN_RL_MINB)
     lean_rload_kernel(LevelGeom<R> g, const LeanW<R> *__restrict__ lx,
                       const LeanW<R> *__restrict__ ly, const LeanW<R> *__restrict__ lz,
                       const R *__restrict__ cls, R *__restrict__ f, LeanTiles tl) {
-  constexpr int TY = lean_ty<R>(), NR = 2 * TY + 3;
+  constexpr int TY = lean_ty_rl<R>(), NR = 2 * TY + 3;
   const int lane = threadIdx.x & 31;
   const uint64_t wid = uint64_t(blockIdx.x) * kLeanWPB + (threadIdx.x >> 5);
   if (wid >= tl.warps())
@@ -500,32 +510,57 @@ __global__ void __launch_bounds__(32 * kLeanWPB, 4)
   const int64_t m01 = int64_t(m0) * m1;
   R *fq = f + qc + int64_t(m0) * cy0;
 
+  // class row offsets of band row r (rank cy0 - 1 + (r >> 1) clamped into
+  // the type's y range; invalid rows are masked), loop invariant
+  uint32_t oe[NR], oo[NR];
+#pragma unroll
+  for (int r = 0; r < NR; ++r) {
+    const uint32_t rk =
+        uint32_t(min(max(cy0 - 1 + (r >> 1), 0), (r & 1) ? max(yrmax_o, 0) : yrmax_e));
+    oe[r] = uint32_t(m0) * rk;
+    oo[r] = uint32_t(m0 - 1) * rk;
+  }
+  const R *cbe = cls + qe, *cbo = cls + qo;
+
   for (int k = Z3 ? cz0 - 1 : 0; k <= (Z3 ? cz1 : 0); ++k) {
     R YE[TY], YO[TY];
-    const int pe = 2 * k;
-    if (pe >= 0 && pe < n2) {
-      const R *b1 = cls + g.tbase[1] + qo + int64_t(m0 - 1) * (int64_t(m1) * k);
-      const R *b2 = cls + g.tbase[2] + qe + int64_t(m0) * (int64_t(m1 - 1) * k);
-      const R *b3 = cls + g.tbase[3] + qo + int64_t(m0 - 1) * (int64_t(m1 - 1) * k);
-      int re[NR];
+    const int pe = 2 * k, pz = pe - 1;
+    const bool ev = pe >= 0 && pe < n2;
+    const bool ov = Z3 && k >= cz0 && pz >= 1 && pz < n2;
+    // ---- both planes' loads first (one batch of independent loads per
+    // step); invalid planes read a valid one and are zeroed below
+    const int64_t ke = ev ? k : 0, ko = ov ? k - 1 : 0;
+    const R *b1 = cbo + g.tbase[1] + int64_t(m0 - 1) * (int64_t(m1) * ke);
+    const R *b2 = cbe + g.tbase[2] + int64_t(m0) * (int64_t(m1 - 1) * ke);
+    const R *b3 = cbo + g.tbase[3] + int64_t(m0 - 1) * (int64_t(m1 - 1) * ke);
+    R ueE[NR], uoE[NR], ueO[NR], uoO[NR];
 #pragma unroll
-      for (int r = 0; r < NR; ++r)
-        re[r] = min(max(cy0 - 1 + (r >> 1), 0), (r & 1) ? max(yrmax_o, 0) : yrmax_e);
-      R ue[NR], uo[NR];
+    for (int r = 0; r < NR; ++r) {
+      ueE[r] = (r & 1) ? __ldg(b2 + oe[r]) : R(0); // even rows: kept nodes
+      uoE[r] = __ldg(((r & 1) ? b3 : b1) + oo[r]);
+    }
+    if constexpr (Z3) {
+      const R *b4 = cbe + g.tbase[4] + int64_t(m0) * (int64_t(m1) * ko);
+      const R *b5 = cbo + g.tbase[5] + int64_t(m0 - 1) * (int64_t(m1) * ko);
+      const R *b6 = cbe + g.tbase[6] + int64_t(m0) * (int64_t(m1 - 1) * ko);
+      const R *b7 = cbo + g.tbase[7] + int64_t(m0 - 1) * (int64_t(m1 - 1) * ko);
 #pragma unroll
       for (int r = 0; r < NR; ++r) {
-        ue[r] = (r & 1) ? __ldg(b2 + int64_t(m0) * re[r]) : R(0); // even rows: kept
-        uo[r] = __ldg(((r & 1) ? b3 : b1) + int64_t(m0 - 1) * re[r]);
+        ueO[r] = __ldg(((r & 1) ? b6 : b4) + oe[r]);
+        uoO[r] = __ldg(((r & 1) ? b7 : b5) + oo[r]);
       }
+    }
+    // ---- even plane
+    {
       R X[NR];
 #pragma unroll
       for (int r = 0; r < NR; ++r) {
-        const bool rv = (rowvalid >> r) & 1u;
-        const R co = (vo && rv) ? uo[r] : R(0);
+        const bool rv = ev && ((rowvalid >> r) & 1u);
+        const R co = (vo && rv) ? uoE[r] : R(0);
         if (!(r & 1)) {
           X[r] = lean_xpass_odd(wx, co);
         } else {
-          const R ce = (ve && rv) ? ue[r] : R(0);
+          const R ce = (ve && rv) ? ueE[r] : R(0);
           X[r] = lean_xpass(wx, ce, co);
         }
       }
@@ -537,10 +572,6 @@ __global__ void __launch_bounds__(32 * kLeanWPB, 4)
         v = fma(wy[j].w3, X[2 * j + 3], v);
         YE[j] = fma(wy[j].w4, X[2 * j + 4], v);
       }
-    } else {
-#pragma unroll
-      for (int j = 0; j < TY; ++j)
-        YE[j] = R(0);
     }
     if constexpr (!Z3) {
 #pragma unroll
@@ -549,30 +580,15 @@ __global__ void __launch_bounds__(32 * kLeanWPB, 4)
           fq[int64_t(m0) * j] = YE[j];
       break;
     }
-    const int pz = pe - 1;
     const LeanW<R> *lzk = lz + k + 1;
-    if (k >= cz0 && pz >= 1 && pz < n2) {
-      const int64_t zr = k - 1;
-      int re[NR];
-#pragma unroll
-      for (int r = 0; r < NR; ++r)
-        re[r] = min(max(cy0 - 1 + (r >> 1), 0), (r & 1) ? max(yrmax_o, 0) : yrmax_e);
-      const R *b4 = cls + g.tbase[4] + qe + int64_t(m0) * (int64_t(m1) * zr);
-      const R *b5 = cls + g.tbase[5] + qo + int64_t(m0 - 1) * (int64_t(m1) * zr);
-      const R *b6 = cls + g.tbase[6] + qe + int64_t(m0) * (int64_t(m1 - 1) * zr);
-      const R *b7 = cls + g.tbase[7] + qo + int64_t(m0 - 1) * (int64_t(m1 - 1) * zr);
-      R ue[NR], uo[NR];
-#pragma unroll
-      for (int r = 0; r < NR; ++r) {
-        ue[r] = __ldg(((r & 1) ? b6 : b4) + int64_t(m0) * re[r]);
-        uo[r] = __ldg(((r & 1) ? b7 : b5) + int64_t(m0 - 1) * re[r]);
-      }
+    // ---- odd plane
+    {
       R X[NR];
 #pragma unroll
       for (int r = 0; r < NR; ++r) {
-        const bool rv = (rowvalid >> r) & 1u;
-        const R ce = (ve && rv) ? ue[r] : R(0);
-        const R co = (vo && rv) ? uo[r] : R(0);
+        const bool rv = ov && ((rowvalid >> r) & 1u);
+        const R ce = (ve && rv) ? ueO[r] : R(0);
+        const R co = (vo && rv) ? uoO[r] : R(0);
         X[r] = lean_xpass(wx, ce, co);
       }
 #pragma unroll
@@ -583,10 +599,6 @@ __global__ void __launch_bounds__(32 * kLeanWPB, 4)
         v = fma(wy[j].w3, X[2 * j + 3], v);
         YO[j] = fma(wy[j].w4, X[2 * j + 4], v);
       }
-    } else {
-#pragma unroll
-      for (int j = 0; j < TY; ++j)
-        YO[j] = R(0);
     }
     {
       const R a3 = __ldg(lzk->w + 3), a4 = __ldg(lzk->w + 4);
@@ -786,6 +798,15 @@ template <typename R> LeanTiles lean_tiles(uint32_t m0, uint32_t m1, uint32_t m2
   LeanTiles t;
   t.ntx = (m0 + kLeanOut - 1) / kLeanOut;
   t.nty = (m1 + lean_ty<R>() - 1) / lean_ty<R>();
+  t.zc = lean_zc(uint64_t(t.ntx) * t.nty, m2, z3);
+  t.ntz = z3 ? (m2 + t.zc - 1) / t.zc : 1;
+  return t;
+}
+
+template <typename R> LeanTiles lean_rtiles(uint32_t m0, uint32_t m1, uint32_t m2, bool z3) {
+  LeanTiles t;
+  t.ntx = (m0 + kLeanOut - 1) / kLeanOut;
+  t.nty = (m1 + lean_ty_rl<R>() - 1) / lean_ty_rl<R>();
   t.zc = lean_zc(uint64_t(t.ntx) * t.nty, m2, z3);
   t.ntz = z3 ? (m2 + t.zc - 1) / t.zc : 1;
   return t;

@@ -652,7 +652,7 @@ template <typename R>
 void launch_lean_rload(const LevelGeom<R> &g, const std::array<const LeanW<R> *, 3> &st,
                        const R *cls, R *f, cudaStream_t s) {
   const bool z3 = g.n[2] > 1;
-  const LeanTiles t = lean_tiles<R>(g.m[0], g.m[1], g.m[2], z3);
+  const LeanTiles t = lean_rtiles<R>(g.m[0], g.m[1], g.m[2], z3);
   const unsigned blocks = unsigned((t.warps() + kLeanWPB - 1) / kLeanWPB);
   if (z3)
     lean_rload_kernel<R, true><<<blocks, 32 * kLeanWPB, 0, s>>>(
