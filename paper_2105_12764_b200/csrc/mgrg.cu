@@ -553,6 +553,11 @@ int g_thomas_fiber = [] {
   const char *e = std::getenv("MGRG_TFIBER");
   return e ? std::atoi(e) : 1;
 }();
+// experiment knob: one-launch Thomas for small lattices (MGRG_TSMALL=0 disables)
+int g_thomas_small = [] {
+  const char *e = std::getenv("MGRG_TSMALL");
+  return e ? std::atoi(e) : 1;
+}();
 // experiment knob: minimum resident CTAs of the level kernels (MGRG_MINB)
 int g_minb = [] {
   const char *e = std::getenv("MGRG_MINB");
@@ -743,6 +748,17 @@ bool try_scan(int kd, const ThomasGeom<R> &t, uint64_t S, uint64_t inner, uint64
 
 template <typename R> constexpr size_t tf_limit() { return 200 * 1024; }
 
+// small coarse lattices: one CTA solves every dimension (thomas_small_kernel)
+template <typename R> bool ts_fits(const LevelGeom<R> &g) {
+  return g_thomas_small && ts_smem<R>(g.coarse_nodes()) <= 96 * 1024;
+}
+template <typename R>
+void launch_thomas_small(const LevelGeom<R> &g, const std::array<ThomasGeom<R>, 3> &t, R *f,
+                         Epi epi, const R *base, R *out, cudaStream_t s) {
+  thomas_small_kernel<R><<<1, kTsThreads, ts_smem<R>(g.coarse_nodes()), s>>>(
+      f, t[0], t[1], t[2], g.m[0], g.m[1], g.m[2], g.refine, epi, base, out);
+}
+
 template <typename R, int DIM, int CH> auto tf_kernel() {
   return thomas_fiber_kernel<R, DIM, CH>;
 }
@@ -834,6 +850,8 @@ template <typename R> void set_thomas_attrs() {
   cudaFuncSetAttribute(thomas_cols_kernel<R, true>,
                        cudaFuncAttributeMaxDynamicSharedMemorySize, lim);
   set_tf_attrs<R>();
+  cudaFuncSetAttribute(thomas_small_kernel<R>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       96 * 1024);
 }
 
 template <typename R> R *ws(mgrg_plan *p, uint64_t off) {
@@ -915,6 +933,15 @@ mgrg_status run_decompose(mgrg_plan *p, const R *d_in, R *d_cls, cudaStream_t s)
       launch_dec_level<R, 128, 1>(g, a, cls, Pout, F, p->zchunk, s);
     if (mgrg_status st = rec.end())
       return st;
+    if (p->fast && ts_fits<R>(g)) {
+      // all solves + apply in one launch (small coarse lattice)
+      if (mgrg_status st = rec.begin(MGRG_K_THOMAS_X, l, es * Cn * 3))
+        return st;
+      launch_thomas_small<R>(g, P.thom[l], F, Epi::add, Pout, Pout, s);
+      if (mgrg_status st = rec.end())
+        return st;
+      continue;
+    }
     for (int i = 0; i < p->nrefine; ++i) {
       const int kd = p->refine_dims[i];
       const bool last = i == p->nrefine - 1;
@@ -960,7 +987,15 @@ mgrg_status run_recompose(mgrg_plan *p, const R *d_cls, int k, R *d_out,
         launch_rec_load<R, 128, 1>(g, cls, F, p->zchunk, s);
       if (mgrg_status st = rec.end())
         return st;
-      for (int i = 0; i < p->nrefine; ++i) {
+      const bool small = p->fast && ts_fits<R>(g);
+      if (small) {
+        if (mgrg_status st = rec.begin(MGRG_K_THOMAS_X, l, es * Cn * 3))
+          return st;
+        launch_thomas_small<R>(g, P.thom[l], F, Epi::sub, prev, F, s);
+        if (mgrg_status st = rec.end())
+          return st;
+      }
+      for (int i = 0; i < (small ? 0 : p->nrefine); ++i) {
         const int kd = p->refine_dims[i];
         const bool last = i == p->nrefine - 1;
         if (mgrg_status st = rec.begin(MGRG_K_THOMAS_X + kd, l, es * Cn * (last ? 3 : 2)))

@@ -224,3 +224,67 @@ __global__ void __launch_bounds__(32 * kTfChunks, sizeof(R) == 4 ? 2 : 1)
 }
 
 } // namespace mgrg
+
+namespace mgrg {
+
+// Small coarse lattices (the bottom levels of the hierarchy): all three
+// solves of a level and the epilogue in ONE launch of one CTA, the lattice
+// resident in shared memory.  Saves two launches per level on levels whose
+// kernels are launch/latency bound (a few microseconds of work each).
+// FAST policy; sequential Thomas per fiber (thomas_fiber, kernels.hpp:143-151)
+// with the working-precision factors of TridiagonalOperator::build.
+constexpr int kTsThreads = 512;
+template <typename R> __host__ __device__ inline size_t ts_smem(uint64_t n) {
+  return size_t(n) * sizeof(R);
+}
+
+template <typename R>
+__global__ void __launch_bounds__(kTsThreads)
+    thomas_small_kernel(R *__restrict__ f, ThomasGeom<R> tx, ThomasGeom<R> ty,
+                        ThomasGeom<R> tz, uint32_t m0, uint32_t m1, uint32_t m2,
+                        uint32_t refine, Epi epi, const R *base, R *out) {
+  extern __shared__ __align__(16) unsigned char ts_raw[];
+  R *s = reinterpret_cast<R *>(ts_raw);
+  const uint32_t n = m0 * m1 * m2;
+  for (uint32_t i = threadIdx.x; i < n; i += kTsThreads)
+    s[i] = f[i];
+  __syncthreads();
+  const uint32_t ext[3] = {m0, m1, m2};
+  const uint32_t str[3] = {1, m0, m0 * m1};
+  const ThomasGeom<R> *tg[3] = {&tx, &ty, &tz};
+#pragma unroll
+  for (int d = 0; d < 3; ++d) {
+    if (!((refine >> d) & 1u))
+      continue;
+    const ThomasGeom<R> &t = *tg[d];
+    const uint32_t m = ext[d], st = str[d], nf = n / m;
+    for (uint32_t fb = threadIdx.x; fb < nf; fb += kTsThreads) {
+      // fiber fb: position 0 at (fb % st) + (fb / st) * st * m
+      R *p = s + (fb % st) + (fb / st) * st * m;
+      R v = p[0];
+      for (uint32_t i = 1; i < m; ++i) {
+        v = fma(__ldg(t.fwd + i), v, p[i * st]);
+        p[i * st] = v;
+      }
+      R x = v * __ldg(t.ip + m - 1);
+      p[(m - 1) * st] = x;
+      for (uint32_t i = m - 1; i > 0; --i) {
+        const uint32_t j = i - 1;
+        x = (p[j * st] - __ldg(t.h + j) * x) * __ldg(t.ip + j);
+        p[j * st] = x;
+      }
+    }
+    __syncthreads();
+  }
+  for (uint32_t i = threadIdx.x; i < n; i += kTsThreads) {
+    const R z = s[i];
+    if (epi == Epi::none)
+      f[i] = z;
+    else if (epi == Epi::add)
+      out[i] = base[i] + z;
+    else
+      out[i] = base[i] - z;
+  }
+}
+
+} // namespace mgrg
