@@ -44,7 +44,8 @@ constexpr int kLeanOut = 30;  // coarse x outputs per warp
 // lean_ty<R>() coarse rows, z chunks of kLeanZC coarse planes (1 in 2-D).
 struct LeanTiles {
   uint32_t ntx, nty, ntz;
-  int zc; // coarse z planes per chunk (host-chosen per level: enough warps)
+  int zc;           // coarse z planes per chunk (host-chosen per level: enough warps)
+  uint32_t tz0 = 0; // first z chunk of this launch (pipelined host path: slab groups)
   __host__ __device__ uint64_t warps() const { return uint64_t(ntx) * nty * ntz; }
 };
 
@@ -265,7 +266,7 @@ __global__ void __launch_bounds__(32 * kLeanWPB, 3)
     return;
   const uint32_t tx = uint32_t(wid % tl.ntx);
   const uint64_t rest = wid / tl.ntx;
-  const uint32_t tyb = uint32_t(rest % tl.nty), tzc = uint32_t(rest / tl.nty);
+  const uint32_t tyb = uint32_t(rest % tl.nty), tzc = uint32_t(rest / tl.nty) + tl.tz0;
 
   const int n0 = int(g.n[0]), n1 = int(g.n[1]), n2 = int(g.n[2]);
   const int m0 = int(g.m[0]), m1 = int(g.m[1]), m2 = int(g.m[2]);
@@ -473,7 +474,7 @@ __global__ void __launch_bounds__(32 * kLeanWPB, LEAN_RL_MINB)
     return;
   const uint32_t tx = uint32_t(wid % tl.ntx);
   const uint64_t rest = wid / tl.ntx;
-  const uint32_t tyb = uint32_t(rest % tl.nty), tzc = uint32_t(rest / tl.nty);
+  const uint32_t tyb = uint32_t(rest % tl.nty), tzc = uint32_t(rest / tl.nty) + tl.tz0;
   const int n1 = int(g.n[1]), n2 = int(g.n[2]);
   const int m0 = int(g.m[0]), m1 = int(g.m[1]), m2 = int(g.m[2]);
 
@@ -660,7 +661,7 @@ __global__ void __launch_bounds__(32 * kLeanWPB, 4)
     return;
   const uint32_t tx = uint32_t(wid % tl.ntx);
   const uint64_t rest = wid / tl.ntx;
-  const uint32_t tyb = uint32_t(rest % tl.nty), tzc = uint32_t(rest / tl.nty);
+  const uint32_t tyb = uint32_t(rest % tl.nty), tzc = uint32_t(rest / tl.nty) + tl.tz0;
   const int n0 = int(g.n[0]), n1 = int(g.n[1]), n2 = int(g.n[2]);
   const int m0 = int(g.m[0]), m1 = int(g.m[1]), m2 = int(g.m[2]);
   const int64_t nxy = int64_t(n0) * n1;

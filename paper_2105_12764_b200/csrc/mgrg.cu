@@ -216,6 +216,8 @@ struct mgrg_plan {
   uint64_t offA = 0, offB = 0, offF = 0; // element offsets inside d_ws
   void *d_stage = nullptr;               // host-API staging (2N elements), lazy
   cudaStream_t own_stream = nullptr;
+  cudaStream_t s_in = nullptr, s_out = nullptr; // host-API copy streams (pipelined path)
+  cudaEvent_t ev_in[16] = {}, ev_dec[16] = {}, ev_done = nullptr;
   uint64_t last_launches = 0;
   // per-launch profiling (mgrg_plan_set_profiling)
   bool profiling = false;
@@ -551,6 +553,11 @@ static_assert(sizeof(Stencil<double>) % sizeof(double) == 0, "stencil layout");
 // experiment knob: chunked fiber-resident Thomas (MGRG_TFIBER=0 disables)
 int g_thomas_fiber = [] {
   const char *e = std::getenv("MGRG_TFIBER");
+  return e ? std::atoi(e) : 1;
+}();
+// pipelined host-buffer decompose (MGRG_PIPELINE=0 disables)
+int g_pipelined_host = [] {
+  const char *e = std::getenv("MGRG_PIPELINE");
   return e ? std::atoi(e) : 1;
 }();
 // experiment knob: one-launch Thomas for small lattices (MGRG_TSMALL=0 disables)
@@ -900,7 +907,8 @@ mgrg_status Recorder::end() {
 }
 
 template <typename R>
-mgrg_status run_decompose(mgrg_plan *p, const R *d_in, R *d_cls, cudaStream_t s) {
+mgrg_status run_decompose(mgrg_plan *p, const R *d_in, R *d_cls, cudaStream_t s,
+                          bool top_done = false) {
   PlanT<R> &P = pt<R>(p);
   const int L = p->H.L;
   R *F = ws<R>(p, p->offF);
@@ -913,6 +921,7 @@ mgrg_status run_decompose(mgrg_plan *p, const R *d_in, R *d_cls, cudaStream_t s)
     R *Pout = l == 1 ? d_cls : level_buf<R>(p, l - 1);
     R *cls = d_cls + p->nodes[l - 1];
     // read F; write class (F-C) + packed coarse (C) + load vector (C)
+    if (!(top_done && l == L)) {
     if (mgrg_status st = rec.begin(MGRG_K_DEC_LEVEL, l, es * (2 * Fn + Cn)))
       return st;
     // dec4 stages rows with 16-byte copies: the level array must be 16-byte
@@ -933,6 +942,7 @@ mgrg_status run_decompose(mgrg_plan *p, const R *d_in, R *d_cls, cudaStream_t s)
       launch_dec_level<R, 128, 1>(g, a, cls, Pout, F, p->zchunk, s);
     if (mgrg_status st = rec.end())
       return st;
+    }
     if (p->fast && ts_fits<R>(g)) {
       // all solves + apply in one launch (small coarse lattice)
       if (mgrg_status st = rec.begin(MGRG_K_THOMAS_X, l, es * Cn * 3))
@@ -1177,6 +1187,17 @@ mgrg_status mgrg_plan_destroy(mgrg_plan *p) {
     cudaFree(p->d_stage);
     if (p->own_stream)
       cudaStreamDestroy(p->own_stream);
+    for (cudaStream_t q : {p->s_in, p->s_out})
+      if (q)
+        cudaStreamDestroy(q);
+    for (int i = 0; i < 16; ++i) {
+      if (p->ev_in[i])
+        cudaEventDestroy(p->ev_in[i]);
+      if (p->ev_dec[i])
+        cudaEventDestroy(p->ev_dec[i]);
+    }
+    if (p->ev_done)
+      cudaEventDestroy(p->ev_done);
   }
   delete p;
   return MGRG_OK;
@@ -1322,8 +1343,96 @@ static mgrg_status ensure_stage(mgrg_plan *p) {
     return fail(e == cudaErrorMemoryAllocation ? MGRG_OUT_OF_MEMORY : MGRG_CUDA_ERROR,
                 std::string("staging allocation: ") + cudaGetErrorString(e));
   CUDA_TRY(cudaStreamCreateWithFlags(&p->own_stream, cudaStreamNonBlocking));
+  CUDA_TRY(cudaStreamCreateWithFlags(&p->s_in, cudaStreamNonBlocking));
+  CUDA_TRY(cudaStreamCreateWithFlags(&p->s_out, cudaStreamNonBlocking));
+  for (int i = 0; i < 16; ++i) {
+    CUDA_TRY(cudaEventCreateWithFlags(&p->ev_in[i], cudaEventDisableTiming));
+    CUDA_TRY(cudaEventCreateWithFlags(&p->ev_dec[i], cudaEventDisableTiming));
+  }
+  CUDA_TRY(cudaEventCreateWithFlags(&p->ev_done, cudaEventDisableTiming));
   return MGRG_OK;
 }
+
+extern "C++" {
+// Pipelined host-buffer decompose (FAST, dyadic 3-D finest level): the input
+// goes up in z slabs on one copy stream, the finest-level kernel runs per
+// slab group as soon as its planes (plus one halo plane) are resident, and
+// each group's finished class-L pieces (z-major within every class type) go
+// down on the other copy stream while later slabs are still uploading --
+// PCIe carries both directions at once.  The finest level's Thomas solves
+// and the coarser levels follow; classes 0..L-1 (1/8 of the data) last.
+template <typename R>
+mgrg_status decompose_host_pipelined(mgrg_plan *p, const R *h_in, R *h_cls) {
+  PlanT<R> &P = pt<R>(p);
+  const int L = p->H.L;
+  const LevelGeom<R> &g = P.geom[L];
+  const uint64_t N = p->nodes[L], nxy = uint64_t(g.n[0]) * g.n[1];
+  R *din = static_cast<R *>(p->d_stage), *dcls = din + N;
+  R *clsL = dcls + p->nodes[L - 1];
+  R *Pout = L == 1 ? dcls : level_buf<R>(p, L - 1);
+  R *F = ws<R>(p, p->offF);
+  const LeanTiles t = lean_tiles<R>(g.m[0], g.m[1], g.m[2], true);
+  const int G = int(std::min<uint32_t>(t.ntz, 8));
+  const uint32_t n2 = g.n[2], m2 = g.m[2];
+  auto chunk0 = [&](int q) { return uint32_t((uint64_t(q) * t.ntz) / G); };
+  auto fplane = [&](uint32_t c) { return std::min<uint32_t>(2 * c * t.zc, n2); };
+  cudaStream_t sc = p->own_stream;
+  // uploads
+  for (int q = 0; q < G; ++q) {
+    const uint32_t z0 = fplane(chunk0(q)), z1 = q == G - 1 ? n2 : fplane(chunk0(q + 1));
+    CUDA_TRY(cudaMemcpyAsync(din + z0 * nxy, h_in + z0 * nxy, (z1 - z0) * nxy * sizeof(R),
+                             cudaMemcpyHostToDevice, p->s_in));
+    CUDA_TRY(cudaEventRecord(p->ev_in[q], p->s_in));
+  }
+  for (int q = 0; q < G; ++q) {
+    const uint32_t c0 = chunk0(q), c1 = chunk0(q + 1);
+    // the group reads fine planes up to 2*c1*zc: the next slab's first plane
+    CUDA_TRY(cudaStreamWaitEvent(sc, p->ev_in[std::min(q + 1, G - 1)], 0));
+    LeanTiles tg = t;
+    tg.tz0 = c0;
+    tg.ntz = c1 - c0;
+    const unsigned blocks = unsigned((tg.warps() + kLeanWPB - 1) / kLeanWPB);
+    lean_dec_kernel<R, true><<<blocks, 32 * kLeanWPB, lean_dec_smem<R>(), sc>>>(
+        g, P.lean[L][0], P.lean[L][1], P.lean[L][2], din, clsL, Pout, F, tg);
+    CUDA_TRY(cudaGetLastError());
+    CUDA_TRY(cudaEventRecord(p->ev_dec[q], sc));
+    CUDA_TRY(cudaStreamWaitEvent(p->s_out, p->ev_dec[q], 0));
+    // class-L pieces of coarse z planes [c0*zc, c1*zc): even-z types (1..3)
+    // have m2 z ranks, odd-z types (4..7) m2 - 1
+    const uint32_t zr0 = c0 * t.zc;
+    for (unsigned ty = 1; ty < 8; ++ty) {
+      const uint32_t nz = (ty & 4) ? m2 - 1 : m2;
+      const uint32_t a = std::min(zr0, nz), b = std::min<uint32_t>(c1 * t.zc, nz);
+      if (q == G - 1 && b < nz)
+        return fail(MGRG_CUDA_ERROR, "pipelined decompose: slab groups do not cover z");
+      if (b <= a)
+        continue;
+      const uint64_t S = uint64_t(g.tex[ty]) * g.tey[ty];
+      const uint64_t off = p->nodes[L - 1] + g.tbase[ty] + S * a;
+      CUDA_TRY(cudaMemcpyAsync(h_cls + off, dcls + off, S * (b - a) * sizeof(R),
+                               cudaMemcpyDeviceToHost, p->s_out));
+    }
+  }
+  // finest level's solves + coarser levels, then classes 0..L-1
+  if (mgrg_status st = run_decompose<R>(p, din, dcls, sc, /*top_done=*/true))
+    return st;
+  CUDA_TRY(cudaEventRecord(p->ev_done, sc));
+  CUDA_TRY(cudaStreamWaitEvent(p->s_out, p->ev_done, 0));
+  CUDA_TRY(cudaMemcpyAsync(h_cls, dcls, p->nodes[L - 1] * sizeof(R), cudaMemcpyDeviceToHost,
+                           p->s_out));
+  CUDA_TRY(cudaStreamSynchronize(p->s_out));
+  CUDA_TRY(cudaStreamSynchronize(sc));
+  return MGRG_OK;
+}
+
+template <typename R> bool pipelined_ok(mgrg_plan *p) {
+  const int L = p->H.L;
+  const LevelGeom<R> &g = pt<R>(p).geom[L];
+  return p->fast && p->lean && p->refine == 7u && lean_level(g) && g.n[2] > 1 &&
+         p->nodes[L] >= (uint64_t(1) << 22) && g_pipelined_host;
+}
+} // extern "C++"
+
 
 mgrg_status mgrg_decompose_host(mgrg_plan *p, const void *h_values, void *h_classes) {
   g_last_error.clear();
@@ -1334,6 +1443,14 @@ mgrg_status mgrg_decompose_host(mgrg_plan *p, const void *h_values, void *h_clas
   DeviceGuard guard(p->device);
   if (mgrg_status st = ensure_stage(p))
     return st;
+  if (p->deferred)
+    return fail(p->deferred, p->deferred_msg);
+  if (p->dtype == MGRG_F32 ? pipelined_ok<float>(p) : pipelined_ok<double>(p))
+    return p->dtype == MGRG_F32
+               ? decompose_host_pipelined<float>(p, static_cast<const float *>(h_values),
+                                                 static_cast<float *>(h_classes))
+               : decompose_host_pipelined<double>(p, static_cast<const double *>(h_values),
+                                                  static_cast<double *>(h_classes));
   const uint64_t bytes = p->nodes[p->H.L] * p->esize;
   char *din = static_cast<char *>(p->d_stage), *dout = din + bytes;
   CUDA_TRY(cudaMemcpyAsync(din, h_values, bytes, cudaMemcpyHostToDevice, p->own_stream));
