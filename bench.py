@@ -322,6 +322,12 @@ def run_ours(args, rank, world, local_rank):
     for _ in range(max(3, args.warmup)):
         step()
     torch.cuda.synchronize()
+    # kernel launches of one step (decompose + recompose), counted by the plan
+    plan.decompose(d_in, d_cls, stream)
+    launches_per_step = plan.last_launches
+    plan.recompose(d_cls, L, d_out, stream)
+    launches_per_step += plan.last_launches
+    torch.cuda.synchronize()
     # size-independent correctness of what is being timed: lossless round trip
     diff = (d_out - d_in).abs().max().item()
     rng = (d_in.max() - d_in.min()).item()
@@ -332,7 +338,9 @@ def run_ours(args, rank, world, local_rank):
            for _ in range(K)]
     e_start = torch.cuda.Event(enable_timing=True)
     e_end = torch.cuda.Event(enable_timing=True)
-    plan.set_profiling(True)
+    # per-launch events on the top two levels only (every launch of the
+    # small levels bracketed by events would add ~0.7 ms to a 9 ms step)
+    plan.set_profiling(True, top_levels=2)
     sampler = ClockSampler(local_rank)
     sampler.start()
     time.sleep(0.2)
@@ -356,7 +364,6 @@ def run_ours(args, rank, world, local_rank):
         prev = evs[i][1]
     prof = plan.profile(reset=True)
     plan.set_profiling(False)
-    launches_per_step = len(prof) // K if K else 0
 
     t = torch.tensor([total_ms, statistics.median(dec_ms), statistics.median(rec_ms)],
                      dtype=torch.float64, device=device)
@@ -378,14 +385,20 @@ def run_ours(args, rank, world, local_rank):
     (dk, dl), (dtot, dcnt, dbytes) = max(groups.items(), key=lambda kv: kv[1][0])
     davg = dtot / dcnt
     achieved = dbytes / (davg * 1e-3) / 1e9
-    step_dev_ms = sum(g[0] for g in groups.values()) / K
-    alg_step = sum(g[2] * g[1] for g in groups.values()) / K
+    # algorithmic bytes of one step from the hierarchy:
+    # decompose s*[2F + (2D+2)C], recompose s*[3F + (2D+1)C] per level
+    offs = plan.class_offsets
+    D = sum(1 for n in SHAPE if n >= 3)
+    alg_step = 0
+    for lv in range(1, L + 1):
+        Fn, Cn = offs[lv + 1], offs[lv]
+        alg_step += esize * ((2 * Fn + (2 * D + 2) * Cn) + (3 * Fn + (2 * D + 1) * Cn))
     traffic = ncu_traffic().get(f"{dk}/L{dl}/{args.arith}")
     roofline = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak,
                 "unit": "GB/s", "frac": round(achieved / peak, 4),
                 "traffic": traffic, "kernel": f"{dk} level {dl}",
                 "algorithmic_bytes_per_launch": dbytes,
-                "avg_launch_ms": round(davg, 4), "share_of_step": round(dtot / K / step_dev_ms, 3),
+                "avg_launch_ms": round(davg, 4), "share_of_step": round(dtot / K / ms_step, 3),
                 "peak_source": f"{peak_kind} (MEASURED_PEAKS.json hbm_gbs)"
                 if peak_kind == "measured" else "fallback 6.65 TB/s (B200_PROFILING.md)"}
     step_roofline = {"algorithmic_bytes_per_step": alg_step,

@@ -160,7 +160,10 @@ mgrg_status mgrg_plan_last_launches(const mgrg_plan *plan, uint64_t *launches);
  * across calls until reset).  mgrg_plan_profile_read waits for the recorded
  * work, then fills up to `cap` entries: kernel kind (mgrg_kernel_kind),
  * level, device milliseconds and the algorithmic HBM bytes of that launch
- * (SURVEY.md §8(d) accounting); *count receives the number recorded. */
+ * (SURVEY.md §8(d) accounting); *count receives the number recorded.
+ * enable > 0 profiles every launch; enable < 0 only the launches of the top
+ * -enable levels (L, L-1, ...), keeping the event overhead out of a timed
+ * loop's small levels; 0 turns profiling off. */
 typedef enum mgrg_kernel_kind {
   MGRG_K_DEC_LEVEL = 0, /* GPK + class store + R*M (decompose)      */
   MGRG_K_THOMAS_X = 1,  /* Thomas along dim 0 (+1, +2: dims 1, 2)   */

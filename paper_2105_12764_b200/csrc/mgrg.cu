@@ -221,6 +221,7 @@ struct mgrg_plan {
   uint64_t last_launches = 0;
   // per-launch profiling (mgrg_plan_set_profiling)
   bool profiling = false;
+  int prof_min_level = 0; // profile launches of levels >= this one only
   struct Prof {
     int kind, level;
     uint64_t bytes;
@@ -876,13 +877,15 @@ struct Recorder {
   mgrg_plan *p;
   cudaStream_t s;
   uint64_t launches = 0;
+  bool active = false; // the current launch is bracketed by events
   mgrg_status begin(int kind, int level, uint64_t bytes);
   mgrg_status end();
 };
 
 mgrg_status Recorder::begin(int kind, int level, uint64_t bytes) {
   ++launches;
-  if (!p->profiling)
+  active = p->profiling && level >= p->prof_min_level;
+  if (!active)
     return MGRG_OK;
   if (p->prof_used + 2 > p->event_pool.size()) {
     for (int i = 0; i < 64; ++i) {
@@ -900,7 +903,7 @@ mgrg_status Recorder::begin(int kind, int level, uint64_t bytes) {
 }
 
 mgrg_status Recorder::end() {
-  if (!p->profiling)
+  if (!active)
     return MGRG_OK;
   CUDA_TRY(cudaEventRecord(p->prof.back().e1, s));
   return MGRG_OK;
@@ -1256,6 +1259,8 @@ mgrg_status mgrg_plan_set_profiling(mgrg_plan *p, int32_t enable) {
   if (mgrg_status st = check_plan(p))
     return st;
   p->profiling = enable != 0;
+  // enable < 0: only the top -enable levels (fewer events in a timed loop)
+  p->prof_min_level = enable < 0 ? p->H.L + 1 + enable : 0;
   return MGRG_OK;
 }
 

@@ -120,8 +120,11 @@ class Plan:
         return n.value
 
     # -- per-launch profiling ------------------------------------------------------
-    def set_profiling(self, enable: bool = True):
-        _lib.check(_lib.lib().mgrg_plan_set_profiling(self._h, int(enable)))
+    def set_profiling(self, enable=True, top_levels=None):
+        """Per-launch CUDA-event timing; top_levels=k profiles only the
+        launches of levels L .. L-k+1."""
+        mode = 0 if not enable else (-int(top_levels) if top_levels else 1)
+        _lib.check(_lib.lib().mgrg_plan_set_profiling(self._h, mode))
         _lib.check(_lib.lib().mgrg_plan_profile_reset(self._h))
 
     def profile(self, reset: bool = True):
