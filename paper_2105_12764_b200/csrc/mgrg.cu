@@ -411,18 +411,19 @@ template <typename R> mgrg_status upload_geometry(mgrg_plan *p) {
         refs[l].ti[kd] = push(ti);
         {
           // chunked-Thomas tables (thomas_fiber.cuh): {fwd, ip, g, PF, PB}
-          // per position (8-padded), PFend, PBstart [kTfChunks]; products in
+          // per position (8-padded), PFend, PBstart [tf_nch]; products in
           // fp64 from the working-precision factors, rounded once
           const uint32_t mm = uint32_t(tf.size());
           std::vector<R> tl(tf_tab_elems<R>(mm), R(0));
-          R *Q = tl.data(), *Tpe = Q + 8 * size_t(mm), *Tps = Tpe + kTfChunks;
+          const int nch = std::max(tf_nch(mm), 1);
+          R *Q = tl.data(), *Tpe = Q + 8 * size_t(mm), *Tps = Tpe + nch;
           for (uint32_t i = 0; i < mm; ++i) {
             Q[8 * i] = tf[i];
             Q[8 * i + 1] = ti[i];
             Q[8 * i + 2] = i + 1 < mm ? R(-double(ti[i]) * double(th[i])) : R(0);
           }
-          for (int w = 0; w < kTfChunks; ++w) {
-            const uint32_t a = tf_chunk_lo(w, mm), b = tf_chunk_lo(w + 1, mm);
+          for (int w = 0; w < tf_nch(mm); ++w) {
+            const uint32_t a = tf_chunk_lo(w, mm, nch), b = tf_chunk_lo(w + 1, mm, nch);
             double pr = 1.0;
             for (uint32_t i = a; i < b; ++i) {
               pr *= double(tf[i]);
@@ -767,35 +768,50 @@ void launch_thomas_small(const LevelGeom<R> &g, const std::array<ThomasGeom<R>, 
       f, t[0], t[1], t[2], g.m[0], g.m[1], g.m[2], g.refine, epi, base, out);
 }
 
-template <typename R, int DIM, int CH> auto tf_kernel() {
-  return thomas_fiber_kernel<R, DIM, CH>;
+template <typename R, int DIM, int CH, int NF> auto tf_kernel() {
+  return thomas_fiber_kernel<R, DIM, CH, NF>;
 }
 template <typename R, int DIM>
-void (*tf_pick(int ch))(R *, ThomasLean<R>, uint64_t, uint32_t, uint32_t, Epi, const R *, R *) {
+void (*tf_pick(int ch, int nf))(R *, ThomasLean<R>, uint64_t, uint32_t, uint32_t, Epi,
+                                const R *, R *) {
+  if (nf == 4) {
+    switch (ch) {
+    case 5: return tf_kernel<R, DIM, 5, 4>();
+    case 9: return tf_kernel<R, DIM, 9, 4>();
+    case 17: return tf_kernel<R, DIM, 17, 4>();
+    default: return tf_kernel<R, DIM, 33, 4>();
+    }
+  }
   switch (ch) {
-  case 1: return tf_kernel<R, DIM, 1>();
-  case 2: return tf_kernel<R, DIM, 2>();
-  case 3: return tf_kernel<R, DIM, 3>();
-  case 5: return tf_kernel<R, DIM, 5>();
-  case 9: return tf_kernel<R, DIM, 9>();
-  case 17: return tf_kernel<R, DIM, 17>();
-  default: return tf_kernel<R, DIM, 33>();
+  case 1: return tf_kernel<R, DIM, 1, 32>();
+  case 2: return tf_kernel<R, DIM, 2, 32>();
+  case 3: return tf_kernel<R, DIM, 3, 32>();
+  case 5: return tf_kernel<R, DIM, 5, 32>();
+  case 9: return tf_kernel<R, DIM, 9, 32>();
+  case 17: return tf_kernel<R, DIM, 17, 32>();
+  default: return tf_kernel<R, DIM, 33, 32>();
   }
 }
 template <typename R>
-void launch_tf(int kd, int ch, unsigned blocks, size_t sm, cudaStream_t s, R *f,
-               const ThomasLean<R> &tl, uint64_t nfib, uint32_t mx, uint32_t my, Epi epi,
-               const R *base, R *out) {
-  auto k = kd == 0 ? tf_pick<R, 0>(ch) : (kd == 1 ? tf_pick<R, 1>(ch) : tf_pick<R, 2>(ch));
-  k<<<blocks, 32 * kTfChunks, sm, s>>>(f, tl, nfib, mx, my, epi, base, out);
+void launch_tf(int kd, const ThomasLean<R> &tl, uint64_t nfib, uint32_t mx, uint32_t my,
+               Epi epi, const R *base, R *out, R *f, cudaStream_t s) {
+  const int nf = tf_nf(tl.m), ch = std::max(tf_ch(tl.m), nf == 4 ? 5 : 1);
+  const unsigned blocks = unsigned((nfib + nf - 1) / nf);
+  auto k = kd == 0 ? tf_pick<R, 0>(ch, nf) : (kd == 1 ? tf_pick<R, 1>(ch, nf)
+                                                      : tf_pick<R, 2>(ch, nf));
+  k<<<blocks, kTfThreads, tf_smem<R>(kd, tl.m), s>>>(f, tl, nfib, mx, my, epi, base, out);
 }
 template <typename R> void set_tf_attrs() {
   const int lim = int(tf_limit<R>());
-  for (int ch : {1, 2, 3, 5, 9, 17, 33}) {
-    cudaFuncSetAttribute(tf_pick<R, 0>(ch), cudaFuncAttributeMaxDynamicSharedMemorySize, lim);
-    cudaFuncSetAttribute(tf_pick<R, 1>(ch), cudaFuncAttributeMaxDynamicSharedMemorySize, lim);
-    cudaFuncSetAttribute(tf_pick<R, 2>(ch), cudaFuncAttributeMaxDynamicSharedMemorySize, lim);
-  }
+  for (int nf : {32, 4})
+    for (int ch : {1, 2, 3, 5, 9, 17, 33}) {
+      cudaFuncSetAttribute(tf_pick<R, 0>(ch, nf), cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           lim);
+      cudaFuncSetAttribute(tf_pick<R, 1>(ch, nf), cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           lim);
+      cudaFuncSetAttribute(tf_pick<R, 2>(ch, nf), cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           lim);
+    }
 }
 
 template <typename R>
@@ -806,9 +822,7 @@ void launch_thomas(bool fast, const LevelGeom<R> &g, const ThomasGeom<R> &t,
   if (fast && tl.tab && tf_ch(tl.m) && tf_smem<R>(kd, tl.m) <= tf_limit<R>() &&
       g_thomas_fiber) {
     const uint64_t nfib = kd == 0 ? my * mz : (kd == 1 ? mx * mz : mx * my);
-    const unsigned blocks = unsigned((nfib + kTfFibers - 1) / kTfFibers);
-    launch_tf<R>(kd, tf_ch(tl.m), blocks, tf_smem<R>(kd, tl.m), s, f, tl, nfib, uint32_t(mx),
-                 uint32_t(my), epi, base, out);
+    launch_tf<R>(kd, tl, nfib, uint32_t(mx), uint32_t(my), epi, base, out, f, s);
     return;
   }
   if (kd == 0) {

@@ -32,37 +32,59 @@
 
 namespace mgrg {
 
-constexpr int kTfChunks = 16; // warps per CTA = chunks per fiber
-constexpr int kTfFibers = 32;
+constexpr int kTfThreads = 512; // threads per CTA = fibers x chunks
+
+// Fiber-group shape for a fiber length m: NF fibers x NCH = 512/NF chunks
+// per CTA with chunks of at most 33 positions.  Short fibers (m <= 528,
+// every 3-D level here) use 32 fibers per CTA (a warp = one chunk of 32
+// fibers: coalesced position rows); long 2-D fibers (m <= 4224) 4 fibers
+// x 128 chunks.  0 = not handled (the streaming kernels take over).
+__host__ __device__ inline int tf_nf(uint32_t m) {
+  return m <= 16u * 33u ? 32 : (m <= 128u * 33u ? 4 : 0);
+}
+__host__ __device__ inline int tf_nch(uint32_t m) {
+  const int nf = tf_nf(m);
+  return nf ? kTfThreads / nf : 0;
+}
 
 // Tables: q8[i] = {fwd_i, ip_i, g_i, PF_i, PB_i, 0, 0, 0}, then the chunk
-// multipliers pfend[w] (PF at the chunk end), pbstart[w] (PB at its start).
+// multipliers pfend[w] (PF at the chunk end), pbstart[w] (PB at its start),
+// w < tf_nch(m).
 template <typename R> struct ThomasLean {
-  const R *tab; // [8m] q8, [kTfChunks] pfend, [kTfChunks] pbstart
+  const R *tab; // [8m] q8, [nch] pfend, [nch] pbstart
   uint32_t m;
 };
 template <typename R> __host__ __device__ inline size_t tf_tab_elems(uint32_t m) {
-  return 8 * size_t(m) + 2 * kTfChunks;
+  return 8 * size_t(m) + 2 * size_t(tf_nch(m));
 }
-// shared memory: [x tile (DIM 0)][carries][tables], 16-byte aligned parts
-template <typename R> __host__ __device__ inline size_t tf_tile_elems(int dim, uint32_t m) {
-  (void)dim;
-  return (size_t(kTfFibers) * m + 3) & ~size_t(3);
+// the coefficient table is staged in shared memory when it fits beside the
+// tile (every 3-D level); long 2-D fibers read it through L1
+template <typename R> __host__ __device__ inline bool tf_tab_smem(uint32_t m) {
+  return tf_nf(m) == 32;
+}
+// shared memory: [tile NF x m][carries NCH x NF][tables], 16-byte aligned parts
+template <typename R> __host__ __device__ inline size_t tf_tile_elems(uint32_t m) {
+  return (size_t(tf_nf(m)) * m + 3) & ~size_t(3);
 }
 template <typename R> __host__ __device__ inline size_t tf_smem(int dim, uint32_t m) {
-  return (tf_tile_elems<R>(dim, m) + size_t(kTfChunks) * kTfFibers + tf_tab_elems<R>(m)) *
+  (void)dim;
+  return (tf_tile_elems<R>(m) + size_t(kTfThreads) +
+          (tf_tab_smem<R>(m) ? tf_tab_elems<R>(m) : 0)) *
          sizeof(R);
 }
-__host__ __device__ inline uint32_t tf_chunk_lo(int w, uint32_t m) {
-  return uint32_t((uint64_t(w) * m) / kTfChunks);
+__host__ __device__ inline uint32_t tf_chunk_lo(int w, uint32_t m, int nch) {
+  return uint32_t((uint64_t(w) * m) / nch);
 }
 // chunk-length class of a fiber length: the kernel instantiation
 __host__ inline int tf_ch(uint32_t m) {
-  const uint32_t c = (m + kTfChunks - 1) / kTfChunks;
+  const int nch = tf_nch(m);
+  if (!nch)
+    return 0;
+  const uint32_t c = (m + nch - 1) / nch;
   for (int ch : {1, 2, 3, 5, 9, 17, 33})
     if (c <= uint32_t(ch))
       return ch;
-  return 0; // too long: not handled here
+  return 0;
 }
 
 // 16-byte async copy of n elements (src, dst 16-byte aligned) by the CTA.
@@ -70,43 +92,48 @@ template <typename R>
 __device__ __forceinline__ void tf_copy_in(R *dst, const R *src, size_t n, int tid) {
   constexpr int V = 16 / sizeof(R);
   const size_t nv = n / V;
-  for (size_t e = tid; e < nv; e += 32 * kTfChunks)
+  for (size_t e = tid; e < nv; e += kTfThreads)
     cp_async16(dst + e * V, src + e * V);
-  for (size_t e = nv * V + tid; e < n; e += 32 * kTfChunks)
+  for (size_t e = nv * V + tid; e < n; e += kTfThreads)
     cp_async(dst + e, src + e);
 }
 
 // DIM 0: fibers are rows along x (fiber id = row id, positions contiguous);
 // DIM 1: fiber id F = x + m0 * z, position i at x + m0 * (i + m1 * z);
 // DIM 2: fiber id F = x + m0 * y, position i at F + m0 * m1 * i.
-template <typename R, int DIM, int CH>
-__global__ void __launch_bounds__(32 * kTfChunks, sizeof(R) == 4 ? 2 : 1)
+// Thread t: fiber t % NF, chunk t / NF.
+template <typename R, int DIM, int CH, int NF>
+__global__ void __launch_bounds__(kTfThreads, sizeof(R) == 4 ? 2 : 1)
     thomas_fiber_kernel(R *__restrict__ f, ThomasLean<R> t, uint64_t nfib, uint32_t m0,
                         uint32_t m1, Epi epi, const R *base, R *out) {
+  constexpr int NCH = kTfThreads / NF;
+  constexpr bool TSM = NF == 32; // coefficient table in shared memory
   extern __shared__ __align__(16) unsigned char tf_raw[];
   R *sm = reinterpret_cast<R *>(tf_raw);
   const uint32_t m = t.m;
   R *tile = sm;
-  R *carry = sm + tf_tile_elems<R>(DIM, m);
-  R *tab = carry + kTfChunks * kTfFibers;
-  const R *pfend = tab + 8 * size_t(m), *pbstart = pfend + kTfChunks;
-  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
-  const uint64_t F0 = uint64_t(blockIdx.x) * kTfFibers;
-  const int nf = int(nfib - F0 < uint64_t(kTfFibers) ? nfib - F0 : uint64_t(kTfFibers));
+  R *carry = sm + tf_tile_elems<R>(m);
+  R *stab = carry + kTfThreads;
+  const R *tab = TSM ? stab : t.tab;
+  const R *pfend = tab + 8 * size_t(m), *pbstart = pfend + NCH;
+  const int tid = threadIdx.x, fi = tid % NF, w = tid / NF;
+  const uint64_t F0 = uint64_t(blockIdx.x) * NF;
+  const int nf = int(nfib - F0 < uint64_t(NF) ? nfib - F0 : uint64_t(NF));
   const uint64_t m01 = uint64_t(m0) * m1;
-  const uint32_t a = tf_chunk_lo(w, m), len = tf_chunk_lo(w + 1, m) - a;
+  const uint32_t a = tf_chunk_lo(w, m, NCH), len = tf_chunk_lo(w + 1, m, NCH) - a;
 
-  // fiber address of the lane (DIM 1, 2; lanes past the end repeat the last)
+  // fiber address of the thread (DIM 1, 2; fibers past the end repeat the last)
   uint64_t fa = 0;
   if (DIM == 1) {
-    const uint64_t F = F0 + min(lane, nf - 1);
+    const uint64_t F = F0 + min(fi, nf - 1);
     fa = (F % m0) + m01 * (F / m0);
   } else if (DIM == 2) {
-    fa = F0 + min(lane, nf - 1);
+    fa = F0 + min(fi, nf - 1);
   }
   const uint64_t ps = DIM == 1 ? m0 : m01; // position stride (DIM 1, 2)
 
-  tf_copy_in(tab, t.tab, tf_tab_elems<R>(m), tid);
+  if (TSM)
+    tf_copy_in(stab, t.tab, tf_tab_elems<R>(m), tid);
   R v[CH];
   if (DIM == 0) {
     tf_copy_in(tile, f + F0 * m, size_t(nf) * m, tid);
@@ -115,17 +142,17 @@ __global__ void __launch_bounds__(32 * kTfChunks, sizeof(R) == 4 ? 2 : 1)
     __syncthreads();
 #pragma unroll
     for (int k = 0; k < CH; ++k)
-      v[k] = (uint32_t(k) < len && lane < nf) ? tile[size_t(lane) * m + a + k] : R(0);
+      v[k] = (uint32_t(k) < len && fi < nf) ? tile[size_t(fi) * m + a + k] : R(0);
   } else {
     // position-major tile [i][fiber]: each position is one coalesced row
-    for (uint32_t i = w; i < m; i += kTfChunks)
-      cp_async(tile + size_t(i) * kTfFibers + lane, f + fa + ps * i);
+    for (uint32_t i = w; i < m; i += NCH)
+      cp_async(tile + size_t(i) * NF + fi, f + fa + ps * i);
     cp_async_commit();
     cp_async_wait<0>();
     __syncthreads();
 #pragma unroll
     for (int k = 0; k < CH; ++k)
-      v[k] = uint32_t(k) < len ? tile[size_t(a + k) * kTfFibers + lane] : R(0);
+      v[k] = uint32_t(k) < len ? tile[size_t(a + k) * NF + fi] : R(0);
   }
 
   // ---- forward, zero carry-in
@@ -136,11 +163,11 @@ __global__ void __launch_bounds__(32 * kTfChunks, sizeof(R) == 4 ? 2 : 1)
       acc = fma(tab[8 * (a + k)], acc, v[k]);
       v[k] = acc;
     }
-  carry[w * 32 + lane] = acc;
+  carry[w * NF + fi] = acc;
   __syncthreads();
   R c = R(0);
   for (int k = 0; k < w; ++k)
-    c = fma(pfend[k], c, carry[k * 32 + lane]);
+    c = fma(pfend[k], c, carry[k * NF + fi]);
   // ---- forward fix-up + backward, zero carry-in (descending)
   R x = R(0);
 #pragma unroll
@@ -151,23 +178,23 @@ __global__ void __launch_bounds__(32 * kTfChunks, sizeof(R) == 4 ? 2 : 1)
       x = fma(q[2], x, q[1] * vj);
       v[k] = x;
     }
-  __syncthreads(); // every warp has read the forward carries
-  carry[w * 32 + lane] = x;
+  __syncthreads(); // every thread has read the forward carries
+  carry[w * NF + fi] = x;
   __syncthreads();
   R d = R(0);
-  for (int k = kTfChunks - 1; k > w; --k)
-    d = fma(pbstart[k], d, carry[k * 32 + lane]);
+  for (int k = NCH - 1; k > w; --k)
+    d = fma(pbstart[k], d, carry[k * NF + fi]);
   // ---- backward fix-up, epilogue, store
 #pragma unroll
   for (int k = 0; k < CH; ++k)
     if (uint32_t(k) < len)
       v[k] = fma(tab[8 * (a + k) + 4], d, v[k]);
   if (DIM == 0) {
-    if (lane < nf)
+    if (fi < nf)
 #pragma unroll
       for (int k = 0; k < CH; ++k)
         if (uint32_t(k) < len)
-          tile[size_t(lane) * m + a + k] = v[k];
+          tile[size_t(fi) * m + a + k] = v[k];
     __syncthreads();
     constexpr int V = 16 / sizeof(R);
     using VT = typename std::conditional<sizeof(R) == 4, float4, double2>::type;
@@ -176,7 +203,7 @@ __global__ void __launch_bounds__(32 * kTfChunks, sizeof(R) == 4 ? 2 : 1)
     const R *bs = base + F0 * m;
     const bool vec = ((reinterpret_cast<uintptr_t>(dst) |
                        (epi == Epi::none ? 0 : reinterpret_cast<uintptr_t>(bs))) & 15) == 0;
-    for (size_t e = vec ? tid : nv; e < nv; e += 32 * kTfChunks) {
+    for (size_t e = vec ? tid : nv; e < nv; e += kTfThreads) {
       VT z = *reinterpret_cast<const VT *>(tile + e * V);
       if (epi != Epi::none) {
         const VT b = *reinterpret_cast<const VT *>(bs + e * V);
@@ -188,11 +215,11 @@ __global__ void __launch_bounds__(32 * kTfChunks, sizeof(R) == 4 ? 2 : 1)
       }
       *reinterpret_cast<VT *>(dst + e * V) = z;
     }
-    for (size_t e = (vec ? nv * V : 0) + tid; e < n; e += 32 * kTfChunks) {
+    for (size_t e = (vec ? nv * V : 0) + tid; e < n; e += kTfThreads) {
       const R z = tile[e];
       dst[e] = epi == Epi::none ? z : (epi == Epi::add ? bs[e] + z : bs[e] - z);
     }
-  } else if (lane < nf) {
+  } else if (fi < nf) {
     R *p = (epi == Epi::none ? f : out) + fa + ps * a;
     const R *q = base + fa + ps * a;
     if (epi == Epi::none) {
