@@ -181,6 +181,29 @@ mgrg_status mgrg_plan_profile_read(mgrg_plan *plan, uint64_t cap, int32_t *kinds
 /* Library version string. */
 const char *mgrg_version(void);
 
+/* ---- MGRF container --------------------------------
+ * CRC-32 of device bytes (mgr::crc32, pipeline.cpp:13-28: reflected
+ * 0xEDB88320, init / final xor 0xFFFFFFFF -- zlib's crc32), computed on the
+ * GPU; synchronous on `stream`. */
+mgrg_status mgrg_crc32(const void *d_bytes, uint64_t nbytes, uint32_t *crc, void *stream);
+/* Per-class CRC-32 of a device class buffer, classes 0..upto -> crcs[0..upto]
+ * (the MGRF class records, pipeline.cpp:188-191). */
+mgrg_status mgrg_class_crc32(mgrg_plan *plan, const void *d_classes, int32_t upto,
+                             uint32_t *crcs, void *stream);
+/* mgr::write_refactored (pipeline.cpp:180-206, layout pipeline.hpp:27-39)
+ * straight from the device class buffer: byte-identical file; CRCs on the
+ * GPU, payload streamed through pinned chunks.  IoError on file failures. */
+mgrg_status mgrg_write_refactored(mgrg_plan *plan, const void *d_classes, const char *path,
+                                  uint64_t *bytes_written);
+/* mgr::read_refactored (pipeline.cpp:233-300) into a device class buffer:
+ * classes 0..classes (classes < 0: all) are read -- bytes past that prefix
+ * are never touched -- and CRC-checked on the GPU (MGRG_CORRUPT_FILE "crc
+ * mismatch in class c"; a short payload gives MGRG_MISSING_CLASS).  The
+ * container must describe this plan's grid, dtype and depth. */
+mgrg_status mgrg_read_refactored(mgrg_plan *plan, const char *path, int32_t classes,
+                                 void *d_classes, int32_t *classes_loaded,
+                                 uint64_t *bytes_consumed);
+
 #ifdef __cplusplus
 }
 #endif

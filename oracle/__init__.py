@@ -285,3 +285,43 @@ def ref_random_increasing_coords(n: int, seed: int):
                                                     ctypes.c_void_p]
     lib.mgrref_random_increasing_coords(n, seed, _ptr(out))
     return out
+
+
+# ---- MGRF container (reference pipeline.cpp:180-300), impl="ref" only -------
+def ref_write_refactored(classes, shape, levels, path, coords=None) -> int:
+    """The reference's mgr::write_refactored on the RefactoredData given by
+    its flat class buffer; returns the bytes written."""
+    lib = _lib("ref")
+    classes = np.ascontiguousarray(classes)
+    fn = getattr(lib, f"mgrref_write_refactored_{_sfx(classes.dtype)}")
+    fn.restype = ctypes.c_int64
+    keep, cptr = _coords_arr(shape, coords)
+    n = fn(ctypes.c_int(len(shape)), _shape_arr(shape), cptr,
+           ctypes.c_int(levels), classes.ctypes.data_as(ctypes.c_void_p),
+           os.fsencode(path))
+    del keep
+    if n < 0:
+        raise OracleError(int(-n), "mgrref_write_refactored")
+    return int(n)
+
+
+def ref_read_refactored(path, n_elements, dtype, classes=-1):
+    """The reference's mgr::read_refactored: (flat classes 0..k, k loaded,
+    bytes consumed); raises OracleError(code) like the reference throws."""
+    lib = _lib("ref")
+    out = np.zeros(n_elements, dtype=dtype)
+    loaded = ctypes.c_int(0)
+    lib.mgrref_read_refactored.restype = ctypes.c_int64
+    n = lib.mgrref_read_refactored(os.fsencode(path), ctypes.c_int(classes),
+                                   out.ctypes.data_as(ctypes.c_void_p), ctypes.byref(loaded))
+    if n < 0:
+        raise OracleError(int(-n), "mgrref_read_refactored")
+    return out, loaded.value, int(n)
+
+
+def ref_crc32(data: bytes) -> int:
+    """mgr::crc32 (pipeline.cpp:13-28)."""
+    lib = _lib("ref")
+    lib.mgrref_crc32.restype = ctypes.c_uint32
+    buf = np.frombuffer(bytes(data), dtype=np.uint8)
+    return int(lib.mgrref_crc32(buf.ctypes.data_as(ctypes.c_void_p), ctypes.c_uint64(buf.size)))

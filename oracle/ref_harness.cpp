@@ -14,6 +14,7 @@
 #include <vector>
 
 #include "mgr/parallel.hpp"
+#include "mgr/pipeline.hpp"
 #include "mgr/refactor.hpp"
 #include "oracle.hpp" // reference tests/oracle.hpp: deterministic data helpers
 
@@ -179,6 +180,35 @@ int solve_impl(int nd, const uint64_t *shape, const double *coords, int cap,
 
 } // namespace
 
+namespace {
+// MGRF container (pipeline.cpp:180-300): write the RefactoredData given by
+// its flat class buffer (class l at N_{l-1}) with the reference writer.
+template <typename Real>
+int64_t write_impl(int nd, const uint64_t *shape, const double *coords, int levels,
+                   const Real *classes, const char *path) {
+  try {
+    mgr::RefactoredData<Real> r;
+    r.shape = to_shape(nd, shape);
+    r.coords = to_coords(nd, shape, coords);
+    r.levels = std::size_t(levels);
+    const auto hier = mgr::build_hierarchy(r.shape, r.coords,
+                                           std::optional<std::size_t>(levels), 2);
+    std::size_t off = 0;
+    for (std::size_t l = 0; l <= r.levels; ++l) {
+      const std::size_t sz =
+          l == 0 ? hier.num_nodes(0) : hier.num_nodes(l) - hier.num_nodes(l - 1);
+      r.classes.emplace_back(classes + off, classes + off + sz);
+      off += sz;
+    }
+    return int64_t(mgr::write_refactored(r, path));
+  } catch (const mgr::Error &e) {
+    return -int64_t(code_of(e));
+  } catch (...) {
+    return -15;
+  }
+}
+} // namespace
+
 extern "C" {
 
 int mgrref_decompose_f64(int nd, const uint64_t *shape, const double *coords,
@@ -288,6 +318,45 @@ void mgrref_random_vector(uint64_t n, unsigned seed, double lo, double hi,
 void mgrref_random_increasing_coords(uint64_t n, unsigned seed, double *out) {
   const auto v = oracle::random_increasing_coords(n, seed);
   std::memcpy(out, v.data(), n * sizeof(double));
+}
+
+int64_t mgrref_write_refactored_f32(int nd, const uint64_t *shape, const double *coords,
+                                    int levels, const float *classes, const char *path) {
+  return write_impl<float>(nd, shape, coords, levels, classes, path);
+}
+int64_t mgrref_write_refactored_f64(int nd, const uint64_t *shape, const double *coords,
+                                    int levels, const double *classes, const char *path) {
+  return write_impl<double>(nd, shape, coords, levels, classes, path);
+}
+// read_refactored (pipeline.cpp:233-300): classes 0..k (k < 0: all) into a
+// flat buffer; returns bytes consumed, or -(status code).
+int64_t mgrref_read_refactored(const char *path, int k, void *classes, int *loaded) {
+  try {
+    std::optional<std::size_t> want;
+    if (k >= 0)
+      want = std::size_t(k);
+    const auto rr = mgr::read_refactored(path, want);
+    std::size_t off = 0;
+    std::visit(
+        [&](const auto &r) {
+          using Real = typename std::decay_t<decltype(r.classes[0])>::value_type;
+          for (const auto &c : r.classes) {
+            std::memcpy(static_cast<Real *>(classes) + off, c.data(), c.size() * sizeof(Real));
+            off += c.size();
+          }
+        },
+        rr.data);
+    if (loaded)
+      *loaded = int(rr.classes_loaded);
+    return int64_t(rr.bytes_consumed);
+  } catch (const mgr::Error &e) {
+    return -int64_t(code_of(e));
+  } catch (...) {
+    return -15;
+  }
+}
+uint32_t mgrref_crc32(const uint8_t *data, uint64_t n) {
+  return mgr::crc32(std::span<const uint8_t>(data, n));
 }
 
 } // extern "C"

@@ -10,6 +10,8 @@ from .errors import (CorruptFile, Error, InvalidBound, InvalidFusion, InvalidGri
                      InvalidLevel, IoError, MissingClass, ShapeError, SingularSystem,
                      TooManyWorkers, WorkerFailure)
 from .plan import Plan
+from .container import (ReadResult, RefactorFileHeader, crc32, read_refactored,
+                        read_refactored_header, write_refactored)
 from .refactor import (LevelPassStats, PassStats, PhaseCounters, ReconstructionReport,
                        RefactoredData, RefactorOptions, TensorGrid, decompose, make_grid,
                        recompose, recompose_with_report, uniform_coords, value_range,
@@ -24,5 +26,7 @@ __all__ = [
     "weighted_l2_norm", "errors", "Error", "InvalidGrid", "InvalidLevel", "ShapeError",
     "InvalidFusion", "SingularSystem", "TooManyWorkers", "WorkerFailure", "CorruptFile",
     "MissingClass", "InvalidBound", "IoError", "embarrassing_decompose",
-    "embarrassing_recompose", "BlockShardedRefactor", "split_blocks",
+    "embarrassing_recompose", "BlockShardedRefactor", "split_blocks", "crc32",
+    "write_refactored", "read_refactored", "read_refactored_header", "ReadResult",
+    "RefactorFileHeader",
 ]

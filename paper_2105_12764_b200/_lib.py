@@ -26,6 +26,7 @@ EXPORTS = (
     "mgrg_apply_correction", "mgrg_reorder", "mgrg_last_error",
     "mgrg_status_name", "mgrg_plan_last_launches", "mgrg_version",
     "mgrg_plan_set_profiling", "mgrg_plan_profile_reset", "mgrg_plan_profile_read",
+    "mgrg_crc32", "mgrg_class_crc32", "mgrg_write_refactored", "mgrg_read_refactored",
 )
 
 KERNEL_KINDS = {0: "dec_level", 1: "thomas_x", 2: "thomas_y", 3: "thomas_z",
@@ -83,6 +84,11 @@ def lib() -> ctypes.CDLL:
             "mgrg_plan_set_profiling": [vp, i32],
             "mgrg_plan_profile_reset": [vp],
             "mgrg_plan_profile_read": [vp, u64, vp, vp, vp, vp, ctypes.POINTER(u64)],
+            "mgrg_crc32": [vp, u64, ctypes.POINTER(ctypes.c_uint32), vp],
+            "mgrg_class_crc32": [vp, vp, i32, vp, vp],
+            "mgrg_write_refactored": [vp, vp, ctypes.c_char_p, ctypes.POINTER(u64)],
+            "mgrg_read_refactored": [vp, ctypes.c_char_p, i32, vp, ctypes.POINTER(i32),
+                                     ctypes.POINTER(u64)],
         }
         for name, args in sig.items():
             fn = getattr(L, name)

@@ -81,6 +81,7 @@ struct Hierarchy {
   uint64_t shape[4] = {1, 1, 1, 1};
   std::vector<std::vector<uint64_t>> ext;             // [l][d]
   std::vector<std::vector<std::vector<double>>> h, r; // [d][l][i]
+  std::vector<std::vector<double>> coords;            // [d][i], finest level (MGRF header)
 };
 
 mgrg_status build_hierarchy(const mgrg_grid_desc &desc, Hierarchy &H) {
@@ -115,6 +116,7 @@ mgrg_status build_hierarchy(const mgrg_grid_desc &desc, Hierarchy &H) {
                                            " are not strictly increasing at index " +
                                            std::to_string(i));
   }
+  H.coords = coords;
   int levels = 0;
   bool any = false;
   for (int d = 0; d < nd; ++d) {
@@ -1663,3 +1665,5 @@ mgrg_status mgrg_reorder(mgrg_plan *p, int32_t level, int32_t dir, const void *d
 }
 
 } // extern "C"
+
+#include "container.cuh"

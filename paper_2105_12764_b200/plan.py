@@ -4,6 +4,7 @@ arrays (host entry points); torch is only the allocator/stream provider."""
 from __future__ import annotations
 
 import ctypes
+import os
 
 import numpy as np
 
@@ -211,6 +212,42 @@ class Plan:
             out = np.empty(self.num_elements, dtype=self.np_dtype)
         _lib.check(_lib.lib().mgrg_recompose_host(self._h, c.ctypes.data, k, out.ctypes.data))
         return out
+
+    # -- MGRF container straight from / into device class buffers ---------------
+    def class_crc32(self, classes, upto=None, stream=None):
+        """Per-class CRC-32 (the MGRF class records) of a device class buffer."""
+        k = self.levels if upto is None else int(upto)
+        self._check_tensor(classes, self.class_offsets[k + 1], "classes")
+        out = (ctypes.c_uint32 * (k + 1))()
+        _lib.check(_lib.lib().mgrg_class_crc32(self._h, _tensor_ptr(classes), k, out,
+                                               _stream_ptr(stream)))
+        return [int(x) for x in out]
+
+    def write_refactored(self, classes, path) -> int:
+        """mgr::write_refactored (pipeline.cpp:180-206) from the device class
+        buffer; returns the bytes written (header + payloads)."""
+        self._check_tensor(classes, self.num_elements, "classes")
+        n = ctypes.c_uint64(0)
+        _lib.check(_lib.lib().mgrg_write_refactored(self._h, _tensor_ptr(classes),
+                                                    os.fsencode(str(path)), ctypes.byref(n)))
+        return int(n.value)
+
+    def read_refactored(self, path, classes=None, out=None):
+        """mgr::read_refactored (pipeline.cpp:233-300) into a device class
+        buffer: (tensor, classes_loaded, bytes_consumed); only the header and
+        classes 0..classes are read, each CRC-checked on the GPU."""
+        import torch
+
+        if out is None:
+            out = torch.zeros(self.num_elements, dtype=getattr(torch, self.dtype),
+                              device=torch.device("cuda", self.device))
+        self._check_tensor(out, self.num_elements, "classes")
+        loaded = ctypes.c_int32(0)
+        used = ctypes.c_uint64(0)
+        _lib.check(_lib.lib().mgrg_read_refactored(
+            self._h, os.fsencode(str(path)), -1 if classes is None else int(classes),
+            _tensor_ptr(out), ctypes.byref(loaded), ctypes.byref(used)))
+        return out, int(loaded.value), int(used.value)
 
     # -- unit-level kernels (kernels.hpp API), device tensors, in order on the
     #    current stream ------------------------------------------------------------
