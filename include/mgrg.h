@@ -204,6 +204,25 @@ mgrg_status mgrg_read_refactored(mgrg_plan *plan, const char *path, int32_t clas
                                  void *d_classes, int32_t *classes_loaded,
                                  uint64_t *bytes_consumed);
 
+/* ---- compression pipeline ------------------------
+ * mgr::compress (pipeline.hpp:149-183) of a device field: decompose, the
+ * error-bound search (uniform quantizer starting at 2*eb/(L+1), halved until
+ * the full recompose meets eb; at most 25 attempts) and the zigzag-varint
+ * coding on the GPU, codec 0 (store) / 1 (zlib) on the host.  *out is a
+ * malloc'd "MGRC" container (free with mgrg_free); bytes equal the
+ * reference's under the exact arithmetic policy.  MGRG_INVALID_BOUND for
+ * eb <= 0, an unknown codec or a bound the quantizer cannot reach. */
+mgrg_status mgrg_compress(mgrg_plan *plan, const void *d_values, double error_bound,
+                          int32_t codec, uint8_t **out, uint64_t *out_size, double *bin,
+                          double *measured);
+void mgrg_free(void *ptr);
+/* mgr::decompress (pipeline.cpp:517-547) into a device field: container
+ * parse + codec on the host, varint decode / dequantize / recompose on the
+ * GPU; MGRG_CORRUPT_FILE with the reference's messages. */
+mgrg_status mgrg_decompress(mgrg_plan *plan, const uint8_t *bytes, uint64_t size,
+                            void *d_values, double *error_bound, double *bin,
+                            double *measured, int32_t *codec);
+
 #ifdef __cplusplus
 }
 #endif

@@ -325,3 +325,35 @@ def ref_crc32(data: bytes) -> int:
     lib.mgrref_crc32.restype = ctypes.c_uint32
     buf = np.frombuffer(bytes(data), dtype=np.uint8)
     return int(lib.mgrref_crc32(buf.ctypes.data_as(ctypes.c_void_p), ctypes.c_uint64(buf.size)))
+
+
+def ref_compress(values, shape, error_bound, codec=1, coords=None):
+    """The reference's mgr::compress: (container bytes, bin, measured)."""
+    lib = _lib("ref")
+    values = np.ascontiguousarray(values)
+    fn = getattr(lib, f"mgrref_compress_{_sfx(values.dtype)}")
+    fn.restype = ctypes.c_int64
+    cap = values.nbytes * 3 + (1 << 20)
+    out = np.empty(cap, dtype=np.uint8)
+    b, m = ctypes.c_double(0), ctypes.c_double(0)
+    keep, cptr = _coords_arr(shape, coords)
+    n = fn(ctypes.c_int(len(shape)), _shape_arr(shape), cptr, _ptr(values),
+           ctypes.c_double(error_bound), ctypes.c_int(codec), _ptr(out), ctypes.c_uint64(cap),
+           ctypes.byref(b), ctypes.byref(m))
+    del keep
+    if n < 0:
+        raise OracleError(int(-n), "mgrref_compress")
+    return out[:n].tobytes(), b.value, m.value
+
+
+def ref_decompress(data: bytes, n_elements, dtype):
+    """The reference's mgr::decompress -> flat values."""
+    lib = _lib("ref")
+    lib.mgrref_decompress.restype = ctypes.c_int64
+    buf = np.frombuffer(bytes(data), dtype=np.uint8)
+    out = np.zeros(n_elements, dtype=dtype)
+    rc = lib.mgrref_decompress(_ptr(buf), ctypes.c_uint64(buf.size), _ptr(out),
+                               ctypes.c_uint64(n_elements))
+    if rc < 0:
+        raise OracleError(int(-rc), "mgrref_decompress")
+    return out

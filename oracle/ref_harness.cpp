@@ -207,6 +207,30 @@ int64_t write_impl(int nd, const uint64_t *shape, const double *coords, int leve
     return -15;
   }
 }
+
+// compress / decompress (pipeline.hpp:149-198, pipeline.cpp:517-547)
+template <typename Real>
+int64_t compress_impl(int nd, const uint64_t *shape, const double *coords, const Real *values,
+                      double eb, int codec, uint8_t *out, uint64_t cap, double *bin,
+                      double *measured) {
+  try {
+    mgr::TensorGrid<Real> g;
+    g.shape = to_shape(nd, shape);
+    g.coords = to_coords(nd, shape, coords);
+    g.values.assign(values, values + mgr::num_elements(g.shape));
+    const auto r = mgr::compress(g, eb, mgr::codec_by_id(uint8_t(codec)));
+    if (r.bytes.size() > cap)
+      return -16;
+    std::memcpy(out, r.bytes.data(), r.bytes.size());
+    *bin = r.report.bin_width;
+    *measured = r.report.measured_max_abs_error;
+    return int64_t(r.bytes.size());
+  } catch (const mgr::Error &e) {
+    return -int64_t(code_of(e));
+  } catch (...) {
+    return -15;
+  }
+}
 } // namespace
 
 extern "C" {
@@ -349,6 +373,38 @@ int64_t mgrref_read_refactored(const char *path, int k, void *classes, int *load
     if (loaded)
       *loaded = int(rr.classes_loaded);
     return int64_t(rr.bytes_consumed);
+  } catch (const mgr::Error &e) {
+    return -int64_t(code_of(e));
+  } catch (...) {
+    return -15;
+  }
+}
+int64_t mgrref_compress_f32(int nd, const uint64_t *shape, const double *coords,
+                            const float *values, double eb, int codec, uint8_t *out,
+                            uint64_t cap, double *bin, double *measured) {
+  return compress_impl<float>(nd, shape, coords, values, eb, codec, out, cap, bin, measured);
+}
+int64_t mgrref_compress_f64(int nd, const uint64_t *shape, const double *coords,
+                            const double *values, double eb, int codec, uint8_t *out,
+                            uint64_t cap, double *bin, double *measured) {
+  return compress_impl<double>(nd, shape, coords, values, eb, codec, out, cap, bin, measured);
+}
+// decompress into a flat value buffer; returns 0 or -(status code)
+int64_t mgrref_decompress(const uint8_t *bytes, uint64_t n, void *values, uint64_t cap_elems) {
+  try {
+    const auto d = mgr::decompress(std::span<const uint8_t>(bytes, n));
+    int64_t rc = 0;
+    std::visit(
+        [&](const auto &g) {
+          using Real = typename std::decay_t<decltype(g.values)>::value_type;
+          if (g.values.size() > cap_elems) {
+            rc = -16;
+            return;
+          }
+          std::memcpy(values, g.values.data(), g.values.size() * sizeof(Real));
+        },
+        d.grid);
+    return rc;
   } catch (const mgr::Error &e) {
     return -int64_t(code_of(e));
   } catch (...) {

@@ -10,7 +10,8 @@ from .errors import (CorruptFile, Error, InvalidBound, InvalidFusion, InvalidGri
                      InvalidLevel, IoError, MissingClass, ShapeError, SingularSystem,
                      TooManyWorkers, WorkerFailure)
 from .plan import Plan
-from .container import (ReadResult, RefactorFileHeader, crc32, read_refactored,
+from .container import (CompressionReport, CompressResult, DecompressResult, ReadResult,
+                        RefactorFileHeader, compress, crc32, decompress, read_refactored,
                         read_refactored_header, write_refactored)
 from .refactor import (LevelPassStats, PassStats, PhaseCounters, ReconstructionReport,
                        RefactoredData, RefactorOptions, TensorGrid, decompose, make_grid,
@@ -28,5 +29,6 @@ __all__ = [
     "MissingClass", "InvalidBound", "IoError", "embarrassing_decompose",
     "embarrassing_recompose", "BlockShardedRefactor", "split_blocks", "crc32",
     "write_refactored", "read_refactored", "read_refactored_header", "ReadResult",
-    "RefactorFileHeader",
+    "RefactorFileHeader", "compress", "decompress", "CompressResult", "DecompressResult",
+    "CompressionReport",
 ]

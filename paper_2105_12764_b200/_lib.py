@@ -27,6 +27,7 @@ EXPORTS = (
     "mgrg_status_name", "mgrg_plan_last_launches", "mgrg_version",
     "mgrg_plan_set_profiling", "mgrg_plan_profile_reset", "mgrg_plan_profile_read",
     "mgrg_crc32", "mgrg_class_crc32", "mgrg_write_refactored", "mgrg_read_refactored",
+    "mgrg_compress", "mgrg_free", "mgrg_decompress",
 )
 
 KERNEL_KINDS = {0: "dec_level", 1: "thomas_x", 2: "thomas_y", 3: "thomas_z",
@@ -89,11 +90,19 @@ def lib() -> ctypes.CDLL:
             "mgrg_write_refactored": [vp, vp, ctypes.c_char_p, ctypes.POINTER(u64)],
             "mgrg_read_refactored": [vp, ctypes.c_char_p, i32, vp, ctypes.POINTER(i32),
                                      ctypes.POINTER(u64)],
+            "mgrg_compress": [vp, vp, ctypes.c_double, i32, ctypes.POINTER(vp),
+                              ctypes.POINTER(u64), ctypes.POINTER(ctypes.c_double),
+                              ctypes.POINTER(ctypes.c_double)],
+            "mgrg_decompress": [vp, vp, u64, vp, ctypes.POINTER(ctypes.c_double),
+                                ctypes.POINTER(ctypes.c_double),
+                                ctypes.POINTER(ctypes.c_double), ctypes.POINTER(i32)],
         }
         for name, args in sig.items():
             fn = getattr(L, name)
             fn.argtypes = args
             fn.restype = ctypes.c_int
+        L.mgrg_free.argtypes = [vp]
+        L.mgrg_free.restype = None
         L.mgrg_last_error.restype = ctypes.c_char_p
         L.mgrg_last_error.argtypes = []
         L.mgrg_status_name.restype = ctypes.c_char_p

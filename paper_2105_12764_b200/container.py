@@ -9,7 +9,13 @@ include/mgr/pipeline.hpp:15-63 / src/pipeline.cpp:13-300:
   path (classes streamed from / into the device class buffer, per-class CRCs
   on the GPU): files are byte-identical to the reference writer's.
 
-Plan.write_refactored / Plan.read_refactored are the device-buffer forms."""
+Plan.write_refactored / Plan.read_refactored are the device-buffer forms.
+
+Compression pipeline (pipeline.hpp:149-198):
+``compress(grid, error_bound, codec="zlib")`` / ``decompress(bytes)`` with the
+decompose, the quantizer's error-bound search and the zigzag-varint coding on
+the GPU and the codec (store / zlib) on the host; Plan.compress /
+Plan.decompress are the device-field forms."""
 from __future__ import annotations
 
 import ctypes
@@ -163,3 +169,99 @@ def read_refactored(path, classes=None, device: int = 0) -> ReadResult:
     data = RefactoredData(tuple(h.shape), [c.copy() for c in h.coords], int(h.levels),
                           [flat[s] for s in sl], None)
     return ReadResult(data, h, used, loaded)
+
+
+# ---- compression pipeline ----------------------------------------------------
+_CODECS = {"store": 0, "zlib": 1}
+_CODEC_NAMES = {v: k for k, v in _CODECS.items()}
+
+
+@dataclass
+class CompressionReport:
+    """pipeline.hpp:90-96."""
+    error_bound: float = 0.0
+    bin_width: float = 0.0
+    measured_max_abs_error: float = 0.0
+    compression_ratio: float = 0.0
+    codec: str = ""
+
+
+@dataclass
+class CompressResult:
+    bytes: bytes
+    report: CompressionReport
+
+
+@dataclass
+class DecompressResult:
+    grid: object
+    report: CompressionReport
+
+
+def compress(grid, error_bound: float, codec: str = "zlib", opt=None) -> CompressResult:
+    """mgr::compress (pipeline.hpp:149-183) of a TensorGrid."""
+    import torch
+
+    from .refactor import RefactorOptions, _all_uniform, _plan_for, _validate_geometry
+
+    opt = opt or RefactorOptions()
+    if not error_bound > 0:
+        raise errors.InvalidBound("error bound must be positive")
+    if codec not in _CODECS:
+        raise errors.InvalidBound(f"unknown codec: {codec}")
+    _validate_geometry(grid.shape, grid.coords, 2)
+    vals = grid.values
+    plan = _plan_for(grid.shape, grid.coords if not _all_uniform(grid) else None,
+                     vals.dtype, opt.levels, opt.device)
+    d = vals.reshape(-1) if hasattr(vals, "is_cuda") else \
+        torch.from_numpy(np.ascontiguousarray(vals).reshape(-1)).to(f"cuda:{opt.device}")
+    data, b, m = plan.compress(d, error_bound, _CODECS[codec])
+    raw = plan.num_elements * np.dtype(plan.dtype).itemsize
+    return CompressResult(data, CompressionReport(error_bound, b, m, raw / len(data), codec))
+
+
+def _compressed_header(data: bytes):
+    """parse_compressed_container's header fields (pipeline.cpp:476-503)."""
+    at = 0
+
+    def take(n):
+        nonlocal at
+        if at + n > len(data):
+            raise errors.CorruptFile("unexpected end of data")
+        s = data[at:at + n]
+        at += n
+        return s
+
+    if take(4) != b"MGRC":
+        raise errors.CorruptFile("bad magic")
+    if take(1)[0] != _VERSION:
+        raise errors.CorruptFile("unsupported version")
+    codec = take(1)[0]
+    dt = take(1)[0]
+    if dt not in (4, 8):
+        raise errors.CorruptFile("unsupported dtype")
+    nd = take(1)[0]
+    if nd < 1 or nd > 4:
+        raise errors.CorruptFile("bad dimension count")
+    shape = tuple(struct.unpack("<Q", take(8))[0] for _ in range(nd))
+    coords = [np.frombuffer(take(8 * n), dtype="<f8").copy() for n in shape]
+    levels = struct.unpack("<Q", take(8))[0]
+    if levels > 64:
+        raise errors.CorruptFile("implausible level count")
+    if codec not in _CODEC_NAMES:
+        raise errors.CorruptFile(f"unknown codec id {codec}")
+    return codec, dt, shape, coords, levels
+
+
+def decompress(data: bytes, device: int = 0) -> DecompressResult:
+    """mgr::decompress (pipeline.cpp:517-547) -> TensorGrid on the device."""
+    from .refactor import TensorGrid, _plan_for, uniform_coords
+
+    codec, dt, shape, coords, levels = _compressed_header(data)
+    uni = all(np.array_equal(c, uniform_coords(n)) for c, n in zip(coords, shape))
+    plan = _plan_for(shape, None if uni else coords, "float32" if dt == 4 else "float64",
+                     int(levels), device)
+    out, e, b, m, c = plan.decompress(data)
+    grid = TensorGrid(tuple(shape), [c_.copy() for c_ in coords], out)
+    raw = plan.num_elements * dt
+    return DecompressResult(grid, CompressionReport(e, b, m, raw / len(data), _CODEC_NAMES[c]))

@@ -1667,3 +1667,4 @@ mgrg_status mgrg_reorder(mgrg_plan *p, int32_t level, int32_t dir, const void *d
 } // extern "C"
 
 #include "container.cuh"
+#include "compress.cuh"

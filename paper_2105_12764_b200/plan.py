@@ -249,6 +249,41 @@ class Plan:
             _tensor_ptr(out), ctypes.byref(loaded), ctypes.byref(used)))
         return out, int(loaded.value), int(used.value)
 
+    # -- compression pipeline (pipeline.hpp:149-198) on device fields ---------
+    def compress(self, values, error_bound: float, codec: int = 1):
+        """mgr::compress of a device field: (container bytes, bin, measured
+        max abs error); codec 0 = store, 1 = zlib."""
+        self._check_tensor(values, self.num_elements, "values")
+        out = ctypes.c_void_p()
+        n = ctypes.c_uint64(0)
+        b, m = ctypes.c_double(0), ctypes.c_double(0)
+        L = _lib.lib()
+        _lib.check(L.mgrg_compress(self._h, _tensor_ptr(values), float(error_bound),
+                                   int(codec), ctypes.byref(out), ctypes.byref(n),
+                                   ctypes.byref(b), ctypes.byref(m)))
+        try:
+            data = ctypes.string_at(out.value, n.value)
+        finally:
+            L.mgrg_free(out)
+        return data, b.value, m.value
+
+    def decompress(self, data: bytes, out=None):
+        """mgr::decompress into a device field: (tensor, error_bound, bin,
+        measured, codec id)."""
+        import torch
+
+        if out is None:
+            out = torch.empty(self.num_elements, dtype=getattr(torch, self.dtype),
+                              device=torch.device("cuda", self.device))
+        self._check_tensor(out, self.num_elements, "values")
+        buf = ctypes.create_string_buffer(bytes(data), len(data))
+        e, b, m = ctypes.c_double(0), ctypes.c_double(0), ctypes.c_double(0)
+        c = ctypes.c_int32(0)
+        _lib.check(_lib.lib().mgrg_decompress(self._h, buf, len(data), _tensor_ptr(out),
+                                              ctypes.byref(e), ctypes.byref(b),
+                                              ctypes.byref(m), ctypes.byref(c)))
+        return out, e.value, b.value, m.value, int(c.value)
+
     # -- unit-level kernels (kernels.hpp API), device tensors, in order on the
     #    current stream ------------------------------------------------------------
     def gpk(self, level: int, values, inverse: bool = False, stream=None):
