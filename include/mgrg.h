@@ -223,6 +223,22 @@ mgrg_status mgrg_decompress(mgrg_plan *plan, const uint8_t *bytes, uint64_t size
                             void *d_values, double *error_bound, double *bin,
                             double *measured, int32_t *codec);
 
+/* Host-buffer forms of the container / compression entry points (the
+ * reference's pipeline callers hold host vectors; include/mgr_b200/pipeline.hpp
+ * uses these).  Same semantics; staged through the plan's device buffers. */
+mgrg_status mgrg_crc32_host(const void *h_bytes, uint64_t nbytes, uint32_t *crc);
+mgrg_status mgrg_write_refactored_host(mgrg_plan *plan, const void *h_classes,
+                                       const char *path, uint64_t *bytes_written);
+mgrg_status mgrg_read_refactored_host(mgrg_plan *plan, const char *path, int32_t classes,
+                                      void *h_classes, int32_t *classes_loaded,
+                                      uint64_t *bytes_consumed);
+mgrg_status mgrg_compress_host(mgrg_plan *plan, const void *h_values, double error_bound,
+                               int32_t codec, uint8_t **out, uint64_t *out_size, double *bin,
+                               double *measured);
+mgrg_status mgrg_decompress_host(mgrg_plan *plan, const uint8_t *bytes, uint64_t size,
+                                 void *h_values, double *error_bound, double *bin,
+                                 double *measured, int32_t *codec);
+
 #ifdef __cplusplus
 }
 #endif

@@ -27,7 +27,9 @@ EXPORTS = (
     "mgrg_status_name", "mgrg_plan_last_launches", "mgrg_version",
     "mgrg_plan_set_profiling", "mgrg_plan_profile_reset", "mgrg_plan_profile_read",
     "mgrg_crc32", "mgrg_class_crc32", "mgrg_write_refactored", "mgrg_read_refactored",
-    "mgrg_compress", "mgrg_free", "mgrg_decompress",
+    "mgrg_compress", "mgrg_free", "mgrg_decompress", "mgrg_crc32_host",
+    "mgrg_write_refactored_host", "mgrg_read_refactored_host", "mgrg_compress_host",
+    "mgrg_decompress_host",
 )
 
 KERNEL_KINDS = {0: "dec_level", 1: "thomas_x", 2: "thomas_y", 3: "thomas_z",

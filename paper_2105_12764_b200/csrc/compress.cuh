@@ -361,3 +361,99 @@ mgrg_status mgrg_decompress(mgrg_plan *p, const uint8_t *bytes, uint64_t size, v
 }
 
 } // extern "C"
+
+// ---- host-buffer forms (what the reference's pipeline callers hold) -------
+extern "C" {
+
+mgrg_status mgrg_crc32_host(const void *h_bytes, uint64_t nbytes, uint32_t *crc) {
+  g_last_error.clear();
+  if ((!h_bytes && nbytes) || !crc)
+    return fail(MGRG_INVALID_ARGUMENT, "null argument");
+  void *d = nullptr;
+  CUDA_TRY(cudaMalloc(&d, nbytes ? nbytes : 1));
+  mgrg_status st = MGRG_OK;
+  if (cudaMemcpy(d, h_bytes, nbytes, cudaMemcpyHostToDevice) != cudaSuccess)
+    st = fail(MGRG_CUDA_ERROR, "crc32 upload");
+  if (!st)
+    st = mgrg_crc32(d, nbytes, crc, nullptr);
+  cudaFree(d);
+  return st;
+}
+
+mgrg_status mgrg_write_refactored_host(mgrg_plan *p, const void *h_classes, const char *path,
+                                       uint64_t *bytes_written) {
+  g_last_error.clear();
+  if (mgrg_status st = check_plan(p))
+    return st;
+  if (!h_classes)
+    return fail(MGRG_INVALID_ARGUMENT, "null host buffer");
+  DeviceGuard guard(p->device);
+  if (mgrg_status st = ensure_stage(p))
+    return st;
+  const uint64_t bytes = p->nodes[p->H.L] * p->esize;
+  CUDA_TRY(cudaMemcpyAsync(p->d_stage, h_classes, bytes, cudaMemcpyHostToDevice, p->own_stream));
+  CUDA_TRY(cudaStreamSynchronize(p->own_stream));
+  return mgrg_write_refactored(p, p->d_stage, path, bytes_written);
+}
+
+mgrg_status mgrg_read_refactored_host(mgrg_plan *p, const char *path, int32_t classes,
+                                      void *h_classes, int32_t *classes_loaded,
+                                      uint64_t *bytes_consumed) {
+  g_last_error.clear();
+  if (mgrg_status st = check_plan(p))
+    return st;
+  if (!h_classes)
+    return fail(MGRG_INVALID_ARGUMENT, "null host buffer");
+  DeviceGuard guard(p->device);
+  if (mgrg_status st = ensure_stage(p))
+    return st;
+  int32_t loaded = 0;
+  if (mgrg_status st = mgrg_read_refactored(p, path, classes, p->d_stage, &loaded,
+                                            bytes_consumed))
+    return st;
+  const uint64_t bytes = p->nodes[loaded] * p->esize; // classes 0..loaded
+  CUDA_TRY(cudaMemcpyAsync(h_classes, p->d_stage, bytes, cudaMemcpyDeviceToHost, p->own_stream));
+  CUDA_TRY(cudaStreamSynchronize(p->own_stream));
+  if (classes_loaded)
+    *classes_loaded = loaded;
+  return MGRG_OK;
+}
+
+mgrg_status mgrg_compress_host(mgrg_plan *p, const void *h_values, double error_bound,
+                               int32_t codec, uint8_t **out, uint64_t *out_size, double *bin,
+                               double *measured) {
+  g_last_error.clear();
+  if (mgrg_status st = check_plan(p))
+    return st;
+  if (!h_values)
+    return fail(MGRG_INVALID_ARGUMENT, "null host buffer");
+  DeviceGuard guard(p->device);
+  if (mgrg_status st = ensure_stage(p))
+    return st;
+  const uint64_t bytes = p->nodes[p->H.L] * p->esize;
+  CUDA_TRY(cudaMemcpyAsync(p->d_stage, h_values, bytes, cudaMemcpyHostToDevice, p->own_stream));
+  CUDA_TRY(cudaStreamSynchronize(p->own_stream));
+  return mgrg_compress(p, p->d_stage, error_bound, codec, out, out_size, bin, measured);
+}
+
+mgrg_status mgrg_decompress_host(mgrg_plan *p, const uint8_t *bytes, uint64_t size,
+                                 void *h_values, double *error_bound, double *bin,
+                                 double *measured, int32_t *codec) {
+  g_last_error.clear();
+  if (mgrg_status st = check_plan(p))
+    return st;
+  if (!h_values)
+    return fail(MGRG_INVALID_ARGUMENT, "null host buffer");
+  DeviceGuard guard(p->device);
+  if (mgrg_status st = ensure_stage(p))
+    return st;
+  if (mgrg_status st = mgrg_decompress(p, bytes, size, p->d_stage, error_bound, bin, measured,
+                                       codec))
+    return st;
+  const uint64_t n = p->nodes[p->H.L] * p->esize;
+  CUDA_TRY(cudaMemcpyAsync(h_values, p->d_stage, n, cudaMemcpyDeviceToHost, p->own_stream));
+  CUDA_TRY(cudaStreamSynchronize(p->own_stream));
+  return MGRG_OK;
+}
+
+} // extern "C"

@@ -28,3 +28,24 @@ def test_cpp_shim_matches_reference(tmp_path, oracle_mod):
     out = subprocess.run([exe], capture_output=True, text=True, timeout=300)
     assert out.returncode == 0, out.stderr
     assert "shim ok" in out.stdout
+
+
+PSRC = os.path.join(ROOT, "tests", "cpp", "test_pipeline_shim.cpp")
+
+
+def test_pipeline_header_compiles_standalone():
+    subprocess.run(["g++", "-std=c++20", "-fsyntax-only", "-Wall", "-Wextra",
+                    "-I", os.path.join(ROOT, "include"), PSRC], check=True)
+
+
+@pytest.mark.gpu
+def test_cpp_pipeline_shim_matches_reference(tmp_path, oracle_mod):
+    if not oracle_mod.available("ref"):
+        pytest.skip("oracle/_ref not built")
+    exe = str(tmp_path / "test_pipeline_shim")
+    subprocess.run(["g++", "-std=c++20", "-O2", "-I", os.path.join(ROOT, "include"), PSRC,
+                    "-L", PKG, "-lmgrg", "-L", REF, "-lmgr_ref", "-lz", "-pthread",
+                    f"-Wl,-rpath,{PKG}:{REF}", "-o", exe], check=True)
+    out = subprocess.run([exe, str(tmp_path)], capture_output=True, text=True, timeout=300)
+    assert out.returncode == 0, out.stderr
+    assert "pipeline ok" in out.stdout
