@@ -63,12 +63,16 @@ template <typename R> __host__ __device__ inline bool tf_tab_smem(uint32_t m) {
   return tf_nf(m) == 32;
 }
 // shared memory: [tile NF x m][carries NCH x NF][tables], 16-byte aligned parts
-template <typename R> __host__ __device__ inline size_t tf_tile_elems(uint32_t m) {
-  return (size_t(tf_nf(m)) * m + 3) & ~size_t(3);
+template <typename R> __host__ __device__ inline size_t tf_tile_elems(int dim, uint32_t m) {
+  // NF fibers per position; z fibers in 32-fiber groups are staged with
+  // 16-byte chunks of a superset (pitch (32 + 2V - 2) / V * V, V = 16/sizeof(R))
+  const int nf = tf_nf(m), v = 16 / int(sizeof(R));
+  const size_t pitch =
+      (nf == 32 && dim == 2) ? size_t((32 + 2 * v - 2) / v * v) : size_t(nf);
+  return (pitch * m + 3) & ~size_t(3);
 }
 template <typename R> __host__ __device__ inline size_t tf_smem(int dim, uint32_t m) {
-  (void)dim;
-  return (tf_tile_elems<R>(m) + size_t(kTfThreads) +
+  return (tf_tile_elems<R>(dim, m) + size_t(kTfThreads) +
           (tf_tab_smem<R>(m) ? tf_tab_elems<R>(m) : 0)) *
          sizeof(R);
 }
@@ -112,7 +116,7 @@ __global__ void __launch_bounds__(kTfThreads, sizeof(R) == 4 ? 2 : 1)
   R *sm = reinterpret_cast<R *>(tf_raw);
   const uint32_t m = t.m;
   R *tile = sm;
-  R *carry = sm + tf_tile_elems<R>(m);
+  R *carry = sm + tf_tile_elems<R>(DIM, m);
   R *stab = carry + kTfThreads;
   const R *tab = TSM ? stab : t.tab;
   const R *pfend = tab + 8 * size_t(m), *pbstart = pfend + NCH;
@@ -131,6 +135,15 @@ __global__ void __launch_bounds__(kTfThreads, sizeof(R) == 4 ? 2 : 1)
     fa = F0 + min(fi, nf - 1);
   }
   const uint64_t ps = DIM == 1 ? m0 : m01; // position stride (DIM 1, 2)
+  // 16-byte staging of whole position rows (DIM 1, 2 with 32 fibers): the
+  // CTA's fibers must be one contiguous run of x nodes (DIM 1: not across a
+  // z plane; DIM 2: always)
+  constexpr int V = 16 / int(sizeof(R));
+  constexpr int NCK = (NF + 2 * V - 2) / V; // chunks of a row superset
+  constexpr int RW = NCK * V;               // staged row pitch (elements)
+  const uint64_t F0row = DIM == 1 ? (F0 % m0) + m01 * (F0 / m0) : F0;
+  const bool contiguous = DIM == 2 || (F0 % m0) + uint64_t(nf) <= m0;
+  const uint64_t ntot = nfib * m;
 
   if (TSM)
     tf_copy_in(stab, t.tab, tf_tab_elems<R>(m), tid);
@@ -143,6 +156,39 @@ __global__ void __launch_bounds__(kTfThreads, sizeof(R) == 4 ? 2 : 1)
 #pragma unroll
     for (int k = 0; k < CH; ++k)
       v[k] = (uint32_t(k) < len && fi < nf) ? tile[size_t(fi) * m + a + k] : R(0);
+  } else if (NF == 32 && DIM == 2 && contiguous) {
+    // position-major tile [i][RW]: position i's 32 fibers are one contiguous
+    // run; it is fetched as the 16-byte aligned superset (NCK chunks, one
+    // LDGSTS.128 each: ~4x fewer copy operations than element copies) and
+    // read back at the row's shift
+    constexpr int RPR = 32 / NCK; // rows per warp copy instruction
+    const int lane = tid & 31;
+    for (uint32_t i0 = w; i0 < m; i0 += NCH * RPR) {
+      const uint32_t i = i0 + uint32_t(lane / NCK) * NCH;
+      const int c = lane % NCK;
+      if (lane < RPR * NCK && i < m) {
+        const uint64_t s0 = (F0row + ps * i) & ~uint64_t(V - 1);
+        const uint64_t g = s0 + uint64_t(c) * V;
+        R *d = tile + size_t(i) * RW + c * V;
+        if (g + V <= ntot) {
+          cp_async16(d, f + g);
+        } else {
+#pragma unroll
+          for (int e = 0; e < V; ++e)
+            if (g + e < ntot)
+              cp_async(d + e, f + g + e);
+        }
+      }
+    }
+    cp_async_commit();
+    cp_async_wait<0>();
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < CH; ++k) {
+      const uint32_t i = a + k;
+      const int sh = int((F0row + ps * i) & uint64_t(V - 1));
+      v[k] = uint32_t(k) < len ? tile[size_t(i) * RW + sh + fi] : R(0);
+    }
   } else {
     // position-major tile [i][fiber]: each position is one coalesced row
     for (uint32_t i = w; i < m; i += NCH)
