@@ -761,12 +761,15 @@ template <typename R> constexpr size_t tf_limit() { return 200 * 1024; }
 
 // small coarse lattices: one CTA solves every dimension (thomas_small_kernel)
 template <typename R> bool ts_fits(const LevelGeom<R> &g) {
-  return g_thomas_small && ts_smem<R>(g.coarse_nodes()) <= 96 * 1024;
+  return g_thomas_small &&
+         ts_smem<R>(g.coarse_nodes(), uint64_t(g.m[0]) + g.m[1] + g.m[2]) <= 96 * 1024;
 }
 template <typename R>
 void launch_thomas_small(const LevelGeom<R> &g, const std::array<ThomasGeom<R>, 3> &t, R *f,
                          Epi epi, const R *base, R *out, cudaStream_t s) {
-  thomas_small_kernel<R><<<1, kTsThreads, ts_smem<R>(g.coarse_nodes()), s>>>(
+  thomas_small_kernel<R><<<1, kTsThreads,
+                           ts_smem<R>(g.coarse_nodes(), uint64_t(g.m[0]) + g.m[1] + g.m[2]),
+                           s>>>(
       f, t[0], t[1], t[2], g.m[0], g.m[1], g.m[2], g.refine, epi, base, out);
 }
 

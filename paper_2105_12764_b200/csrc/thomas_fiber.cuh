@@ -307,8 +307,8 @@ namespace mgrg {
 // FAST policy; sequential Thomas per fiber (thomas_fiber, kernels.hpp:143-151)
 // with the working-precision factors of TridiagonalOperator::build.
 constexpr int kTsThreads = 512;
-template <typename R> __host__ __device__ inline size_t ts_smem(uint64_t n) {
-  return size_t(n) * sizeof(R);
+template <typename R> __host__ __device__ inline size_t ts_smem(uint64_t n, uint64_t ext_sum) {
+  return size_t(n + 3 * ext_sum) * sizeof(R); // lattice + factors of every dim
 }
 
 template <typename R>
@@ -319,31 +319,50 @@ __global__ void __launch_bounds__(kTsThreads)
   extern __shared__ __align__(16) unsigned char ts_raw[];
   R *s = reinterpret_cast<R *>(ts_raw);
   const uint32_t n = m0 * m1 * m2;
-  for (uint32_t i = threadIdx.x; i < n; i += kTsThreads)
-    s[i] = f[i];
-  __syncthreads();
+  // the factors of every dimension go to shared memory with the lattice:
+  // the recurrences below then never wait on a global load
+  R *fac = s + n; // [d][fwd | ip | h] x m_d
   const uint32_t ext[3] = {m0, m1, m2};
   const uint32_t str[3] = {1, m0, m0 * m1};
   const ThomasGeom<R> *tg[3] = {&tx, &ty, &tz};
+  uint32_t fo[3], acc = 0;
+  for (int d = 0; d < 3; ++d) {
+    fo[d] = acc;
+    if ((refine >> d) & 1u)
+      acc += 3 * ext[d];
+  }
+  for (uint32_t i = threadIdx.x; i < n; i += kTsThreads)
+    s[i] = f[i];
+  for (int d = 0; d < 3; ++d) {
+    if (!((refine >> d) & 1u))
+      continue;
+    const uint32_t m = ext[d];
+    for (uint32_t i = threadIdx.x; i < m; i += kTsThreads) {
+      fac[fo[d] + i] = tg[d]->fwd[i];
+      fac[fo[d] + m + i] = tg[d]->ip[i];
+      fac[fo[d] + 2 * m + i] = i + 1 < m ? tg[d]->h[i] : R(0);
+    }
+  }
+  __syncthreads();
 #pragma unroll
   for (int d = 0; d < 3; ++d) {
     if (!((refine >> d) & 1u))
       continue;
-    const ThomasGeom<R> &t = *tg[d];
     const uint32_t m = ext[d], st = str[d], nf = n / m;
+    const R *fw = fac + fo[d], *ip = fw + m, *hh = ip + m;
     for (uint32_t fb = threadIdx.x; fb < nf; fb += kTsThreads) {
       // fiber fb: position 0 at (fb % st) + (fb / st) * st * m
       R *p = s + (fb % st) + (fb / st) * st * m;
       R v = p[0];
       for (uint32_t i = 1; i < m; ++i) {
-        v = fma(__ldg(t.fwd + i), v, p[i * st]);
+        v = fma(fw[i], v, p[i * st]);
         p[i * st] = v;
       }
-      R x = v * __ldg(t.ip + m - 1);
+      R x = v * ip[m - 1];
       p[(m - 1) * st] = x;
       for (uint32_t i = m - 1; i > 0; --i) {
         const uint32_t j = i - 1;
-        x = (p[j * st] - __ldg(t.h + j) * x) * __ldg(t.ip + j);
+        x = (p[j * st] - hh[j] * x) * ip[j];
         p[j * st] = x;
       }
     }
