@@ -417,18 +417,20 @@ template <typename R> mgrg_status upload_geometry(mgrg_plan *p) {
           // fp64 from the working-precision factors, rounded once
           const uint32_t mm = uint32_t(tf.size());
           std::vector<R> tl(tf_tab_elems<R>(mm), R(0));
-          const int nch = std::max(tf_nch(mm), 1);
-          R *Q = tl.data(), *Tpe = Q + 8 * size_t(mm), *Tps = Tpe + nch;
-          for (uint32_t i = 0; i < mm; ++i) {
-            Q[8 * i] = tf[i];
-            Q[8 * i + 1] = ti[i];
-            Q[8 * i + 2] = i + 1 < mm ? R(-double(ti[i]) * double(th[i])) : R(0);
+          const int nch = std::max(tf_nch(mm), 1), ch = std::max(tf_ch(mm), 1);
+          const uint32_t mp = std::max<uint32_t>(uint32_t(nch) * uint32_t(ch), mm);
+          R *Q = tl.data(), *Tpe = Q + 8 * size_t(mp), *Tps = Tpe + nch;
+          for (uint32_t i = 0; i < mp; ++i) { // padding: fwd = g = 0, ip = 1
+            const bool real = i < mm;
+            Q[8 * i] = real ? tf[i] : R(0);
+            Q[8 * i + 1] = real ? ti[i] : R(1);
+            Q[8 * i + 2] = (i + 1 < mm) ? R(-double(ti[i]) * double(th[i])) : R(0);
           }
           for (int w = 0; w < tf_nch(mm); ++w) {
-            const uint32_t a = tf_chunk_lo(w, mm, nch), b = tf_chunk_lo(w + 1, mm, nch);
+            const uint32_t a = uint32_t(w) * uint32_t(ch), b = a + uint32_t(ch);
             double pr = 1.0;
             for (uint32_t i = a; i < b; ++i) {
-              pr *= double(tf[i]);
+              pr *= double(Q[8 * i]);
               Q[8 * i + 3] = R(pr);
             }
             Tpe[w] = R(pr);

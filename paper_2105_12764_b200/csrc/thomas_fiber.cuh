@@ -54,8 +54,25 @@ template <typename R> struct ThomasLean {
   const R *tab; // [8m] q8, [nch] pfend, [nch] pbstart
   uint32_t m;
 };
+// chunk length of a fiber length (the kernel instantiation), 0 = not handled
+__host__ __device__ inline int tf_ch(uint32_t m) {
+  const int nch = tf_nch(m);
+  if (!nch)
+    return 0;
+  const uint32_t c = (m + nch - 1) / nch;
+  const int cls[7] = {1, 2, 3, 5, 9, 17, 33};
+  for (int i = 0; i < 7; ++i)
+    if (c <= uint32_t(cls[i]))
+      return cls[i];
+  return 0;
+}
+// positions covered by the chunks (every chunk exactly CH long; positions
+// m .. mp-1 are padding: fwd = g = 0, so they decouple and solve to 0)
+__host__ __device__ inline uint32_t tf_padded(uint32_t m) {
+  return uint32_t(tf_nch(m)) * uint32_t(tf_ch(m));
+}
 template <typename R> __host__ __device__ inline size_t tf_tab_elems(uint32_t m) {
-  return 8 * size_t(m) + 2 * size_t(tf_nch(m));
+  return 8 * size_t(tf_padded(m) > m ? tf_padded(m) : m) + 2 * size_t(tf_nch(m));
 }
 // the coefficient table is staged in shared memory when it fits beside the
 // tile (every 3-D level); long 2-D fibers read it through L1
@@ -76,29 +93,15 @@ template <typename R> __host__ __device__ inline size_t tf_smem(int dim, uint32_
           (tf_tab_smem<R>(m) ? tf_tab_elems<R>(m) : 0)) *
          sizeof(R);
 }
-__host__ __device__ inline uint32_t tf_chunk_lo(int w, uint32_t m, int nch) {
-  return uint32_t((uint64_t(w) * m) / nch);
-}
-// chunk-length class of a fiber length: the kernel instantiation
-__host__ inline int tf_ch(uint32_t m) {
-  const int nch = tf_nch(m);
-  if (!nch)
-    return 0;
-  const uint32_t c = (m + nch - 1) / nch;
-  for (int ch : {1, 2, 3, 5, 9, 17, 33})
-    if (c <= uint32_t(ch))
-      return ch;
-  return 0;
-}
 
 // 16-byte async copy of n elements (src, dst 16-byte aligned) by the CTA.
 template <typename R>
-__device__ __forceinline__ void tf_copy_in(R *dst, const R *src, size_t n, int tid) {
+__device__ __forceinline__ void tf_copy_in(R *dst, const R *src, uint32_t n, int tid) {
   constexpr int V = 16 / sizeof(R);
-  const size_t nv = n / V;
-  for (size_t e = tid; e < nv; e += kTfThreads)
+  const uint32_t nv = n / V;
+  for (uint32_t e = tid; e < nv; e += kTfThreads)
     cp_async16(dst + e * V, src + e * V);
-  for (size_t e = nv * V + tid; e < n; e += kTfThreads)
+  for (uint32_t e = nv * V + tid; e < n; e += kTfThreads)
     cp_async(dst + e, src + e);
 }
 
@@ -119,12 +122,15 @@ __global__ void __launch_bounds__(kTfThreads, sizeof(R) == 4 ? 2 : 1)
   R *carry = sm + tf_tile_elems<R>(DIM, m);
   R *stab = carry + kTfThreads;
   const R *tab = TSM ? stab : t.tab;
-  const R *pfend = tab + 8 * size_t(m), *pbstart = pfend + NCH;
+  const uint32_t mp = uint32_t(NCH) * CH; // padded positions (>= m)
+  const R *pfend = tab + 8 * size_t(mp > m ? mp : m), *pbstart = pfend + NCH;
   const int tid = threadIdx.x, fi = tid % NF, w = tid / NF;
   const uint64_t F0 = uint64_t(blockIdx.x) * NF;
   const int nf = int(nfib - F0 < uint64_t(NF) ? nfib - F0 : uint64_t(NF));
   const uint64_t m01 = uint64_t(m0) * m1;
-  const uint32_t a = tf_chunk_lo(w, m, NCH), len = tf_chunk_lo(w + 1, m, NCH) - a;
+  // chunk w = [a, a + CH); real positions a .. a + len - 1 (len <= CH)
+  const uint32_t a = uint32_t(w) * CH;
+  const uint32_t len = a >= m ? 0u : (m - a < uint32_t(CH) ? m - a : uint32_t(CH));
 
   // fiber address of the thread (DIM 1, 2; fibers past the end repeat the last)
   uint64_t fa = 0;
@@ -149,13 +155,15 @@ __global__ void __launch_bounds__(kTfThreads, sizeof(R) == 4 ? 2 : 1)
     tf_copy_in(stab, t.tab, tf_tab_elems<R>(m), tid);
   R v[CH];
   if (DIM == 0) {
-    tf_copy_in(tile, f + F0 * m, size_t(nf) * m, tid);
+    tf_copy_in(tile, f + F0 * m, uint32_t(nf) * m, tid);
     cp_async_commit();
     cp_async_wait<0>();
     __syncthreads();
+    const uint32_t ln = fi < nf ? len : 0u;
+    const R *tp = tile + uint32_t(fi) * m + a;
 #pragma unroll
     for (int k = 0; k < CH; ++k)
-      v[k] = (uint32_t(k) < len && fi < nf) ? tile[size_t(fi) * m + a + k] : R(0);
+      v[k] = uint32_t(k) < ln ? tp[k] : R(0);
   } else if (NF == 32 && DIM == 2 && contiguous) {
     // position-major tile [i][RW]: position i's 32 fibers are one contiguous
     // run; it is fetched as the 16-byte aligned superset (NCK chunks, one
@@ -203,12 +211,12 @@ __global__ void __launch_bounds__(kTfThreads, sizeof(R) == 4 ? 2 : 1)
 
   // ---- forward, zero carry-in
   R acc = R(0);
+  const R *qa = tab + 8 * size_t(a);
 #pragma unroll
-  for (int k = 0; k < CH; ++k)
-    if (uint32_t(k) < len) {
-      acc = fma(tab[8 * (a + k)], acc, v[k]);
-      v[k] = acc;
-    }
+  for (int k = 0; k < CH; ++k) { // padded positions: fwd = 0, v = 0
+    acc = fma(qa[8 * k], acc, v[k]);
+    v[k] = acc;
+  }
   carry[w * NF + fi] = acc;
   __syncthreads();
   R c = R(0);
@@ -217,13 +225,12 @@ __global__ void __launch_bounds__(kTfThreads, sizeof(R) == 4 ? 2 : 1)
   // ---- forward fix-up + backward, zero carry-in (descending)
   R x = R(0);
 #pragma unroll
-  for (int k = CH - 1; k >= 0; --k)
-    if (uint32_t(k) < len) {
-      const R *q = tab + 8 * (a + k);
-      const R vj = fma(q[3], c, v[k]);
-      x = fma(q[2], x, q[1] * vj);
-      v[k] = x;
-    }
+  for (int k = CH - 1; k >= 0; --k) { // padded positions: g = 0, x = ip * v
+    const R *q = qa + 8 * k;
+    const R vj = fma(q[3], c, v[k]);
+    x = fma(q[2], x, q[1] * vj);
+    v[k] = x;
+  }
   __syncthreads(); // every thread has read the forward carries
   carry[w * NF + fi] = x;
   __syncthreads();
@@ -233,23 +240,24 @@ __global__ void __launch_bounds__(kTfThreads, sizeof(R) == 4 ? 2 : 1)
   // ---- backward fix-up, epilogue, store
 #pragma unroll
   for (int k = 0; k < CH; ++k)
-    if (uint32_t(k) < len)
-      v[k] = fma(tab[8 * (a + k) + 4], d, v[k]);
+    v[k] = fma(qa[8 * k + 4], d, v[k]);
   if (DIM == 0) {
-    if (fi < nf)
+    if (fi < nf) {
+      R *tq = tile + uint32_t(fi) * m + a;
 #pragma unroll
       for (int k = 0; k < CH; ++k)
         if (uint32_t(k) < len)
-          tile[size_t(fi) * m + a + k] = v[k];
+          tq[k] = v[k];
+    }
     __syncthreads();
     constexpr int V = 16 / sizeof(R);
     using VT = typename std::conditional<sizeof(R) == 4, float4, double2>::type;
-    const size_t n = size_t(nf) * m, nv = n / V;
+    const uint32_t n = uint32_t(nf) * m, nv = n / V;
     R *dst = epi == Epi::none ? f + F0 * m : out + F0 * m;
     const R *bs = base + F0 * m;
     const bool vec = ((reinterpret_cast<uintptr_t>(dst) |
                        (epi == Epi::none ? 0 : reinterpret_cast<uintptr_t>(bs))) & 15) == 0;
-    for (size_t e = vec ? tid : nv; e < nv; e += kTfThreads) {
+    for (uint32_t e = vec ? uint32_t(tid) : nv; e < nv; e += kTfThreads) {
       VT z = *reinterpret_cast<const VT *>(tile + e * V);
       if (epi != Epi::none) {
         const VT b = *reinterpret_cast<const VT *>(bs + e * V);
@@ -261,7 +269,7 @@ __global__ void __launch_bounds__(kTfThreads, sizeof(R) == 4 ? 2 : 1)
       }
       *reinterpret_cast<VT *>(dst + e * V) = z;
     }
-    for (size_t e = (vec ? nv * V : 0) + tid; e < n; e += kTfThreads) {
+    for (uint32_t e = (vec ? nv * V : 0u) + tid; e < n; e += kTfThreads) {
       const R z = tile[e];
       dst[e] = epi == Epi::none ? z : (epi == Epi::add ? bs[e] + z : bs[e] - z);
     }
