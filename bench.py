@@ -411,7 +411,10 @@ def run_ours(args, rank, world, local_rank):
 
     e2e = None
     if not args.no_e2e:
-        e2e = run_e2e(plan, d_in, d_out, N, nbytes, L, K, dist, device, world)
+        try:
+            e2e = run_e2e(plan, d_in, d_out, N, nbytes, L, K, dist, device, world)
+        except (RuntimeError, MemoryError) as ex:  # e.g. pinned host memory exhausted
+            e2e = {"value": None, "unit": "GB/s", "error": str(ex)[:200]}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
