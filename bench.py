@@ -249,10 +249,20 @@ def run_e2e(plan, d_in, d_out, N, nbytes, L, K, dist, device, world):
     step."""
     import torch
 
-    h_in = torch.empty(N, dtype=torch.float32, pin_memory=True)
-    h_in.copy_(d_in)
-    h_cls = torch.empty(N, dtype=torch.float32, pin_memory=True)
-    h_out = torch.empty(N, dtype=torch.float32, pin_memory=True)
+    ok = 1
+    try:
+        h_in = torch.empty(N, dtype=torch.float32, pin_memory=True)
+        h_in.copy_(d_in)
+        h_cls = torch.empty(N, dtype=torch.float32, pin_memory=True)
+        h_out = torch.empty(N, dtype=torch.float32, pin_memory=True)
+    except (RuntimeError, MemoryError):
+        ok = 0
+    if dist is not None:  # every rank takes the same branch (no stranded barrier)
+        t = torch.tensor([ok], dtype=torch.int32, device=device)
+        dist.all_reduce(t, op=dist.ReduceOp.MIN)
+        ok = int(t.item())
+    if not ok:
+        raise RuntimeError("pinned host buffers for the e2e leg could not be allocated")
     hin, hcls, hout = h_in.numpy(), h_cls.numpy(), h_out.numpy()
     plan.decompose_host(hin, hcls)  # warm (allocates the staging buffers)
     plan.recompose_host(hcls, L, hout)
