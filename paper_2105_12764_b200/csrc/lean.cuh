@@ -70,24 +70,72 @@ template <typename R> __device__ __forceinline__ W5r<R> lean_w(const LeanW<R> *_
   return {__ldg(p->w), __ldg(p->w + 1), __ldg(p->w + 2), __ldg(p->w + 3), __ldg(p->w + 4)};
 }
 
+// Arithmetic policy (template FAST): FMA lerps and host-precomputed 5-tap
+// FMA stencils, or the exact policy -- the reference's expressions with
+// round-to-nearest intrinsics and its merged mass-trans evaluation order
+// (stencil_eval<R, false>, kernels2.cuh), bit-identical to the CPU path.
+template <typename R, bool FAST> __device__ __forceinline__ R plerp(R a, R b, R t) {
+  if constexpr (FAST)
+    return fma(t, b - a, a);
+  else
+    return mgrg::lerp(a, b, t); // a + t * (b - a), kernels.hpp:219
+}
+template <typename R, bool FAST> __device__ __forceinline__ R psub(R a, R b) {
+  if constexpr (FAST)
+    return a - b;
+  else
+    return mgrg::sub(a, b);
+}
+template <typename R, bool FAST> __device__ __forceinline__ R padd(R a, R b) {
+  if constexpr (FAST)
+    return a + b;
+  else
+    return mgrg::add(a, b);
+}
+template <typename R, bool FAST>
+__device__ __forceinline__ R pstencil(const W5r<R> &w, const Stencil<R> &s, R t0, R t1, R t2,
+                                      R t3, R t4) {
+  if constexpr (FAST) {
+    R v = w.w0 * t0;
+    v = fma(w.w1, t1, v);
+    v = fma(w.w2, t2, v);
+    v = fma(w.w3, t3, v);
+    return fma(w.w4, t4, v);
+  } else {
+    return stencil_eval<R, false>(s, t0, t1, t2, t3, t4);
+  }
+}
+
 // Merged R*M along x for the lane's output column: taps are the vec(C)
 // values at 2qc-2 .. 2qc+2 (lane a-1's pair, own pair, lane a+1's even).
-template <typename R>
-__device__ __forceinline__ R lean_xpass(const W5r<R> &wx, R ce, R co) {
+template <typename R, bool FAST>
+__device__ __forceinline__ R lean_xpass(const W5r<R> &wx, const Stencil<R> &sx, R ce, R co) {
   const R em = __shfl_up_sync(0xffffffffu, ce, 1);
   const R om = __shfl_up_sync(0xffffffffu, co, 1);
   const R ep = __shfl_down_sync(0xffffffffu, ce, 1);
-  R v = wx.w0 * em;
-  v = fma(wx.w1, om, v);
-  v = fma(wx.w2, ce, v);
-  v = fma(wx.w3, co, v);
-  return fma(wx.w4, ep, v);
+  return pstencil<R, FAST>(wx, sx, em, om, ce, co, ep);
 }
 // Same on a row whose even nodes are kept (coarse in every other dim): the
 // even taps are zero.
-template <typename R> __device__ __forceinline__ R lean_xpass_odd(const W5r<R> &wx, R co) {
+template <typename R, bool FAST>
+__device__ __forceinline__ R lean_xpass_odd(const W5r<R> &wx, const Stencil<R> &sx, R co) {
   const R om = __shfl_up_sync(0xffffffffu, co, 1);
-  return fma(wx.w3, co, wx.w1 * om);
+  if constexpr (FAST)
+    return fma(wx.w3, co, wx.w1 * om);
+  else
+    return stencil_eval<R, false>(sx, R(0), om, R(0), co, R(0));
+}
+
+// Merged R*M along y of the band's x results, output row j (y stencil row
+// cy0 + j; rows past the level are clamped -- their outputs are not stored)
+template <typename R, bool FAST>
+__device__ __forceinline__ R lean_ypass(const W5r<R> *wy, const Stencil<R> *__restrict__ sy,
+                                        int row, const R *X, int j) {
+  Stencil<R> s;
+  if constexpr (!FAST)
+    s = sy[row];
+  return pstencil<R, FAST>(FAST ? wy[j] : W5r<R>{}, s, X[2 * j], X[2 * j + 1], X[2 * j + 2],
+                           X[2 * j + 3], X[2 * j + 4]);
 }
 
 template <typename R> __device__ __forceinline__ R flerp(R a, R b, R t) {
@@ -170,10 +218,11 @@ template <typename R> struct PlaneOut {
 // stores, x pass and y pass.  EVEN: plane is coarse along z.
 //   PAR: parity of the plane's row 0 (aligned rows are those with
 //        (r + PAR) even, r = band row index, band row 0 even).
-template <typename R, int TY, bool EVEN>
+template <typename R, int TY, bool EVEN, bool FAST>
 __device__ __forceinline__ void lean_plane(
     const R *__restrict__ slot, int q, const int *rowoff, R txr, const R *tyr,
-    const W5r<R> &wx, const W5r<R> *wy, bool ve, bool vo, uint32_t stmask_e,
+    const W5r<R> &wx, const W5r<R> *wy, const Stencil<R> &sx,
+    const Stencil<R> *__restrict__ sy, int cy0, int m1, bool ve, bool vo, uint32_t stmask_e,
     uint32_t stmask_o, const PlaneOut<R> &po, int ex_e, int ex_o, R *We, R *Wo,
     const R *WLe, const R *WLo, R tz, R *Y) {
   constexpr int NR = 2 * TY + 3;
@@ -204,12 +253,12 @@ __device__ __forceinline__ void lean_plane(
     for (int r = 0; r < NR; r += 2) {
       const R un = __shfl_down_sync(0xffffffffu, u[r].e, 1);
       We[r] = u[r].e;
-      Wo[r] = flerp(u[r].e, un, txr);
+      Wo[r] = plerp<R, FAST>(u[r].e, un, txr);
     }
 #pragma unroll
     for (int r = 1; r < NR; r += 2) {
-      We[r] = flerp(We[r - 1], We[r + 1], tyr[r >> 1]);
-      Wo[r] = flerp(Wo[r - 1], Wo[r + 1], tyr[r >> 1]);
+      We[r] = plerp<R, FAST>(We[r - 1], We[r + 1], tyr[r >> 1]);
+      Wo[r] = plerp<R, FAST>(Wo[r - 1], Wo[r + 1], tyr[r >> 1]);
     }
   }
 #pragma unroll
@@ -219,27 +268,22 @@ __device__ __forceinline__ void lean_plane(
       we = We[r];
       wo = Wo[r];
     } else {
-      we = flerp(WLe[r], We[r], tz);
-      wo = flerp(WLo[r], Wo[r], tz);
+      we = plerp<R, FAST>(WLe[r], We[r], tz);
+      wo = plerp<R, FAST>(WLo[r], Wo[r], tz);
     }
     const bool kept = EVEN && !(r & 1); // even node coarse in every dim
-    const R ce = (kept || !ve) ? R(0) : u[r].e - we;
-    const R co = vo ? u[r].o - wo : R(0);
+    const R ce = (kept || !ve) ? R(0) : psub<R, FAST>(u[r].e, we);
+    const R co = vo ? psub<R, FAST>(u[r].o, wo) : R(0);
     const int rr = r >> 1;
     if ((stmask_e >> r) & 1u)
       ((r & 1) ? po.be1 : po.be0)[uint32_t(ex_e * rr)] = kept ? u[r].e : ce;
     if ((stmask_o >> r) & 1u)
       ((r & 1) ? po.bo1 : po.bo0)[uint32_t(ex_o * rr)] = co;
-    X[r] = kept ? lean_xpass_odd(wx, co) : lean_xpass(wx, ce, co);
+    X[r] = kept ? lean_xpass_odd<R, FAST>(wx, sx, co) : lean_xpass<R, FAST>(wx, sx, ce, co);
   }
 #pragma unroll
-  for (int j = 0; j < TY; ++j) {
-    R v = wy[j].w0 * X[2 * j];
-    v = fma(wy[j].w1, X[2 * j + 1], v);
-    v = fma(wy[j].w2, X[2 * j + 2], v);
-    v = fma(wy[j].w3, X[2 * j + 3], v);
-    Y[j] = fma(wy[j].w4, X[2 * j + 4], v);
-  }
+  for (int j = 0; j < TY; ++j)
+    Y[j] = lean_ypass<R, FAST>(wy, sy, min(cy0 + j, m1 - 1), X, j);
 }
 
 // ---------------------------------------------------------------------------
@@ -250,12 +294,13 @@ template <typename R> __host__ __device__ constexpr size_t lean_dec_smem() {
   return size_t(kLeanWPB) * 3 * (2 * lean_ty<R>() + 3) * LeanStage<R>::RP * sizeof(R);
 }
 
-template <typename R, bool Z3>
+template <typename R, bool Z3, bool FAST>
 __global__ void __launch_bounds__(32 * kLeanWPB, 3)
     lean_dec_kernel(LevelGeom<R> g, const LeanW<R> *__restrict__ lx,
                     const LeanW<R> *__restrict__ ly, const LeanW<R> *__restrict__ lz,
-                    const R *__restrict__ in, R *__restrict__ cls, R *__restrict__ P,
-                    R *__restrict__ f, LeanTiles tl) {
+                    const Stencil<R> *__restrict__ sxt, const Stencil<R> *__restrict__ syt,
+                    const Stencil<R> *__restrict__ szt, const R *__restrict__ in,
+                    R *__restrict__ cls, R *__restrict__ P, R *__restrict__ f, LeanTiles tl) {
   constexpr int TY = lean_ty<R>(), NR = 2 * TY + 3;
   constexpr int V = LeanStage<R>::V, SLOT = NR * LeanStage<R>::RP;
   extern __shared__ __align__(16) unsigned char lean_raw_sm[];
@@ -282,6 +327,9 @@ __global__ void __launch_bounds__(32 * kLeanWPB, 3)
   W5r<R> wx = lean_w(lxq);
   if (!outl)
     wx = {R(0), R(0), R(0), R(0), R(0)};
+  Stencil<R> sx{}; // exact policy: the lane's x stencil (non-output lanes: unused)
+  if constexpr (!FAST)
+    sx = sxt[min(max(qc, 0), m0 - 1)];
   const int X0 = 2 * (int(kLeanOut * tx) - 1); // lane 0's even node
 
   // ---- y band: rows Y0 + r, r = 0 .. NR-1
@@ -348,10 +396,11 @@ __global__ void __launch_bounds__(32 * kLeanWPB, 3)
 #pragma unroll
   for (int r = 0; r < NR; ++r)
     WLe[r] = WLo[r] = R(0);
-  R accM[TY], acc0[TY]; // partial f of outputs k-1 and k at step k
+  R accM[TY], acc0[TY]; // FAST: partial f of outputs k-1 and k at step k
+  R YEm2[TY], YOm1[TY], YEm1[TY]; // exact: y results of planes 2k-4, 2k-3, 2k-2
 #pragma unroll
   for (int j = 0; j < TY; ++j)
-    accM[j] = acc0[j] = R(0);
+    accM[j] = acc0[j] = YEm2[j] = YOm1[j] = YEm1[j] = R(0);
   const int64_t m01 = int64_t(m0) * m1;
   R *fq = f + qc + int64_t(m0) * cy0;
 
@@ -375,7 +424,8 @@ __global__ void __launch_bounds__(32 * kLeanWPB, 3)
         po.bo0 = cls + g.tbase[1] + qc + int64_t(m0 - 1) * (yb + int64_t(m1) * k);
         po.be1 = cls + g.tbase[2] + qc + int64_t(m0) * (yb + int64_t(m1 - 1) * k);
         po.bo1 = cls + g.tbase[3] + qc + int64_t(m0 - 1) * (yb + int64_t(m1 - 1) * k);
-        lean_plane<R, TY, true>(ring + js * SLOT, q_of(pe), rowoff, txr, tyr, wx, wy, ve,
+        lean_plane<R, TY, true, FAST>(ring + js * SLOT, q_of(pe), rowoff, txr, tyr, wx, wy, sx,
+                                      syt, cy0, m1, ve,
                                 vo, own ? st_e : 0u, own ? st_o : 0u, po, m0, m0 - 1, We, Wo,
                                 nullptr, nullptr, R(0), YE);
       } else {
@@ -413,7 +463,8 @@ __global__ void __launch_bounds__(32 * kLeanWPB, 3)
         po.bo0 = cls + g.tbase[5] + qc + int64_t(m0 - 1) * (yb + int64_t(m1) * zr);
         po.be1 = cls + g.tbase[6] + qc + int64_t(m0) * (yb + int64_t(m1 - 1) * zr);
         po.bo1 = cls + g.tbase[7] + qc + int64_t(m0 - 1) * (yb + int64_t(m1 - 1) * zr);
-        lean_plane<R, TY, false>(ring + js * SLOT, q_of(pz), rowoff, txr, tyr, wx, wy, ve,
+        lean_plane<R, TY, false, FAST>(ring + js * SLOT, q_of(pz), rowoff, txr, tyr, wx, wy, sx,
+                                       syt, cy0, m1, ve,
                                  vo, own ? st_e : 0u, own ? st_o : 0u, po, m0, m0 - 1, We,
                                  Wo, WLe, WLo, __ldg(&lzk->t), YO);
       } else {
@@ -434,12 +485,12 @@ __global__ void __launch_bounds__(32 * kLeanWPB, 3)
       WLe[r] = We[r];
       WLo[r] = Wo[r];
     }
-    // ================= z pass (rolling accumulators) =================
-    {
+    // ================= z pass =================
+    const bool emit = outl && k - 1 >= cz0 && k - 1 < cz1;
+    if constexpr (FAST) { // rolling accumulators
       const R a3 = __ldg(lzk->w + 3), a4 = __ldg(lzk->w + 4);     // output k-1
       const R b1 = __ldg(lzk[1].w + 1), b2 = __ldg(lzk[1].w + 2); // output k
       const R c0 = __ldg(lzk[2].w);                               // output k+1
-      const bool emit = outl && k - 1 >= cz0 && k - 1 < cz1;
 #pragma unroll
       for (int i = 0; i < TY; ++i) {
         const R out = fma(a3, YO[i], fma(a4, YE[i], accM[i]));
@@ -447,6 +498,19 @@ __global__ void __launch_bounds__(32 * kLeanWPB, 3)
           fq[int64_t(m0) * i + m01 * (k - 1)] = out;
         accM[i] = fma(b1, YO[i], fma(b2, YE[i], acc0[i]));
         acc0[i] = c0 * YE[i];
+      }
+    } else { // exact: output k-1 from the five planes 2k-4 .. 2k
+      Stencil<R> sk{};
+      if (emit)
+        sk = szt[k - 1];
+#pragma unroll
+      for (int i = 0; i < TY; ++i) {
+        if (emit && cy0 + i < cy1)
+          fq[int64_t(m0) * i + m01 * (k - 1)] =
+              stencil_eval<R, false>(sk, YEm2[i], YOm1[i], YEm1[i], YO[i], YE[i]);
+        YEm2[i] = YEm1[i];
+        YOm1[i] = YO[i];
+        YEm1[i] = YE[i];
       }
     }
   }
@@ -462,11 +526,13 @@ template <typename R> __host__ __device__ constexpr int lean_ty_rl() {
   return sizeof(R) == 4 ? LEAN_RL_TY : 4; // taller band: fewer halo rows (no W registers here)
 }
 
-template <typename R, bool Z3>
+template <typename R, bool Z3, bool FAST>
 __global__ void __launch_bounds__(32 * kLeanWPB, LEAN_RL_MINB)
     lean_rload_kernel(LevelGeom<R> g, const LeanW<R> *__restrict__ lx,
                       const LeanW<R> *__restrict__ ly, const LeanW<R> *__restrict__ lz,
-                      const R *__restrict__ cls, R *__restrict__ f, LeanTiles tl) {
+                      const Stencil<R> *__restrict__ sxt, const Stencil<R> *__restrict__ syt,
+                      const Stencil<R> *__restrict__ szt, const R *__restrict__ cls,
+                      R *__restrict__ f, LeanTiles tl) {
   constexpr int TY = lean_ty_rl<R>(), NR = 2 * TY + 3;
   const int lane = threadIdx.x & 31;
   const uint64_t wid = uint64_t(blockIdx.x) * kLeanWPB + (threadIdx.x >> 5);
@@ -485,6 +551,9 @@ __global__ void __launch_bounds__(32 * kLeanWPB, LEAN_RL_MINB)
   W5r<R> wx = lean_w(lx + (min(max(qc, -2), m0 + 1) + 2));
   if (!outl)
     wx = {R(0), R(0), R(0), R(0), R(0)};
+  Stencil<R> sx{}; // exact policy: the lane's x stencil
+  if constexpr (!FAST)
+    sx = sxt[min(max(qc, 0), m0 - 1)];
   const int qe = min(max(qc, 0), m0 - 1), qo = min(max(qc, 0), max(m0 - 2, 0));
 
   const int cy0 = int(tyb) * TY, cy1 = min(cy0 + TY, m1);
@@ -504,10 +573,11 @@ __global__ void __launch_bounds__(32 * kLeanWPB, LEAN_RL_MINB)
 
   const int cz0 = Z3 ? int(tzc) * tl.zc : 0;
   const int cz1 = Z3 ? min(cz0 + tl.zc, m2) : 1;
-  R accM[TY], acc0[TY];
+  R accM[TY], acc0[TY];          // FAST: partial f of outputs k-1 and k
+  R YEm2[TY], YOm1[TY], YEm1[TY]; // exact: y results of planes 2k-4, 2k-3, 2k-2
 #pragma unroll
   for (int j = 0; j < TY; ++j)
-    accM[j] = acc0[j] = R(0);
+    accM[j] = acc0[j] = YEm2[j] = YOm1[j] = YEm1[j] = R(0);
   const int64_t m01 = int64_t(m0) * m1;
   R *fq = f + qc + int64_t(m0) * cy0;
 
@@ -559,20 +629,15 @@ __global__ void __launch_bounds__(32 * kLeanWPB, LEAN_RL_MINB)
         const bool rv = ev && ((rowvalid >> r) & 1u);
         const R co = (vo && rv) ? uoE[r] : R(0);
         if (!(r & 1)) {
-          X[r] = lean_xpass_odd(wx, co);
+          X[r] = lean_xpass_odd<R, FAST>(wx, sx, co);
         } else {
           const R ce = (ve && rv) ? ueE[r] : R(0);
-          X[r] = lean_xpass(wx, ce, co);
+          X[r] = lean_xpass<R, FAST>(wx, sx, ce, co);
         }
       }
 #pragma unroll
-      for (int j = 0; j < TY; ++j) {
-        R v = wy[j].w0 * X[2 * j];
-        v = fma(wy[j].w1, X[2 * j + 1], v);
-        v = fma(wy[j].w2, X[2 * j + 2], v);
-        v = fma(wy[j].w3, X[2 * j + 3], v);
-        YE[j] = fma(wy[j].w4, X[2 * j + 4], v);
-      }
+      for (int j = 0; j < TY; ++j)
+        YE[j] = lean_ypass<R, FAST>(wy, syt, min(cy0 + j, m1 - 1), X, j);
     }
     if constexpr (!Z3) {
 #pragma unroll
@@ -590,22 +655,17 @@ __global__ void __launch_bounds__(32 * kLeanWPB, LEAN_RL_MINB)
         const bool rv = ov && ((rowvalid >> r) & 1u);
         const R ce = (ve && rv) ? ueO[r] : R(0);
         const R co = (vo && rv) ? uoO[r] : R(0);
-        X[r] = lean_xpass(wx, ce, co);
+        X[r] = lean_xpass<R, FAST>(wx, sx, ce, co);
       }
 #pragma unroll
-      for (int j = 0; j < TY; ++j) {
-        R v = wy[j].w0 * X[2 * j];
-        v = fma(wy[j].w1, X[2 * j + 1], v);
-        v = fma(wy[j].w2, X[2 * j + 2], v);
-        v = fma(wy[j].w3, X[2 * j + 3], v);
-        YO[j] = fma(wy[j].w4, X[2 * j + 4], v);
-      }
+      for (int j = 0; j < TY; ++j)
+        YO[j] = lean_ypass<R, FAST>(wy, syt, min(cy0 + j, m1 - 1), X, j);
     }
-    {
+    const bool emit = outl && k - 1 >= cz0 && k - 1 < cz1;
+    if constexpr (FAST) {
       const R a3 = __ldg(lzk->w + 3), a4 = __ldg(lzk->w + 4);
       const R b1 = __ldg(lzk[1].w + 1), b2 = __ldg(lzk[1].w + 2);
       const R c0 = __ldg(lzk[2].w);
-      const bool emit = outl && k - 1 >= cz0 && k - 1 < cz1;
 #pragma unroll
       for (int j = 0; j < TY; ++j) {
         const R out = fma(a3, YO[j], fma(a4, YE[j], accM[j]));
@@ -613,6 +673,19 @@ __global__ void __launch_bounds__(32 * kLeanWPB, LEAN_RL_MINB)
           fq[int64_t(m0) * j + m01 * (k - 1)] = out;
         accM[j] = fma(b1, YO[j], fma(b2, YE[j], acc0[j]));
         acc0[j] = c0 * YE[j];
+      }
+    } else { // exact: output k-1 from the five planes 2k-4 .. 2k
+      Stencil<R> sk{};
+      if (emit)
+        sk = szt[k - 1];
+#pragma unroll
+      for (int j = 0; j < TY; ++j) {
+        if (emit && cy0 + j < cy1)
+          fq[int64_t(m0) * j + m01 * (k - 1)] =
+              stencil_eval<R, false>(sk, YEm2[j], YOm1[j], YEm1[j], YO[j], YE[j]);
+        YEm2[j] = YEm1[j];
+        YOm1[j] = YO[j];
+        YEm1[j] = YE[j];
       }
     }
   }
@@ -648,7 +721,7 @@ __device__ __forceinline__ void lean_store_pair(R *p, R e, R o, bool we, bool wo
     p[1] = o;
 }
 
-template <typename R, bool Z3, bool CLS>
+template <typename R, bool Z3, bool CLS, bool FAST>
 __global__ void __launch_bounds__(32 * kLeanWPB, 4)
     lean_rgpk_kernel(LevelGeom<R> g, const LeanW<R> *__restrict__ lx,
                      const LeanW<R> *__restrict__ ly, const LeanW<R> *__restrict__ lz,
@@ -711,12 +784,12 @@ __global__ void __launch_bounds__(32 * kLeanWPB, 4)
       for (int i = 0; i <= TG; ++i) {
         const R cn = __shfl_down_sync(0xffffffffu, c[i], 1);
         We[2 * i] = c[i];
-        Wo[2 * i] = flerp(c[i], cn, txr);
+        Wo[2 * i] = plerp<R, FAST>(c[i], cn, txr);
       }
 #pragma unroll
       for (int i = 0; i < TG; ++i) {
-        We[2 * i + 1] = flerp(We[2 * i], We[2 * i + 2], tyr[i]);
-        Wo[2 * i + 1] = flerp(Wo[2 * i], Wo[2 * i + 2], tyr[i]);
+        We[2 * i + 1] = plerp<R, FAST>(We[2 * i], We[2 * i + 2], tyr[i]);
+        Wo[2 * i + 1] = plerp<R, FAST>(Wo[2 * i], Wo[2 * i + 2], tyr[i]);
       }
     }
     // ---- even plane 2k (written when k < cz1)
@@ -736,11 +809,11 @@ __global__ void __launch_bounds__(32 * kLeanWPB, 4)
       for (int i = 0; i < TG; ++i) {
         // even row 2(cy0+i): parity of (2k + 2(cy0+i)) is even -> aligned
         if ((wrow >> (2 * i)) & 1u)
-          lean_store_pair<R, true>(op + int64_t(2 * i) * n0, We[2 * i], Wo[2 * i] + v1[i], own,
+          lean_store_pair<R, true>(op + int64_t(2 * i) * n0, We[2 * i], padd<R, FAST>(Wo[2 * i], v1[i]), own,
                                    ownO);
         if ((wrow >> (2 * i + 1)) & 1u)
-          lean_store_pair<R, false>(op + int64_t(2 * i + 1) * n0, We[2 * i + 1] + v2[i],
-                                    Wo[2 * i + 1] + v3[i], own, ownO);
+          lean_store_pair<R, false>(op + int64_t(2 * i + 1) * n0, padd<R, FAST>(We[2 * i + 1], v2[i]),
+                                    padd<R, FAST>(Wo[2 * i + 1], v3[i]), own, ownO);
       }
     }
     // ---- odd plane 2k-1
@@ -765,12 +838,12 @@ __global__ void __launch_bounds__(32 * kLeanWPB, 4)
         // odd plane: even rows misaligned, odd rows aligned
         if ((wrow >> (2 * i)) & 1u)
           lean_store_pair<R, false>(op + int64_t(2 * i) * n0,
-                                    flerp(WLe[2 * i], We[2 * i], tz) + v4[i],
-                                    flerp(WLo[2 * i], Wo[2 * i], tz) + v5[i], own, ownO);
+                                    padd<R, FAST>(plerp<R, FAST>(WLe[2 * i], We[2 * i], tz), v4[i]),
+                                    padd<R, FAST>(plerp<R, FAST>(WLo[2 * i], Wo[2 * i], tz), v5[i]), own, ownO);
         if ((wrow >> (2 * i + 1)) & 1u)
           lean_store_pair<R, true>(op + int64_t(2 * i + 1) * n0,
-                                   flerp(WLe[2 * i + 1], We[2 * i + 1], tz) + v6[i],
-                                   flerp(WLo[2 * i + 1], Wo[2 * i + 1], tz) + v7[i], own,
+                                   padd<R, FAST>(plerp<R, FAST>(WLe[2 * i + 1], We[2 * i + 1], tz), v6[i]),
+                                   padd<R, FAST>(plerp<R, FAST>(WLo[2 * i + 1], Wo[2 * i + 1], tz), v7[i]), own,
                                    ownO);
       }
     }

@@ -654,39 +654,48 @@ template <typename R> bool lean_level(const LevelGeom<R> &g) {
   return (g.n[0] & 1u) && (g.n[1] & 1u) && (g.n[2] & 1u);
 }
 template <typename R>
-void launch_lean_dec(const LevelGeom<R> &g, const std::array<const LeanW<R> *, 3> &st,
-                     const R *in, R *cls, R *P, R *f, cudaStream_t s) {
+void launch_lean_dec(bool fast, const LevelGeom<R> &g, const std::array<const LeanW<R> *, 3> &st,
+                     const std::array<const Stencil<R> *, 3> &sc, const R *in, R *cls, R *P,
+                     R *f, cudaStream_t s) {
   const bool z3 = g.n[2] > 1;
   const LeanTiles t = lean_tiles<R>(g.m[0], g.m[1], g.m[2], z3);
   const unsigned blocks = unsigned((t.warps() + kLeanWPB - 1) / kLeanWPB);
-  if (z3)
-    lean_dec_kernel<R, true><<<blocks, 32 * kLeanWPB, lean_dec_smem<R>(), s>>>(
-        g, st[0], st[1], st[2], in, cls, P, f, t);
-  else
-    lean_dec_kernel<R, false><<<blocks, 32 * kLeanWPB, lean_dec_smem<R>(), s>>>(
-        g, st[0], st[1], st[2], in, cls, P, f, t);
+  auto k = z3 ? (fast ? lean_dec_kernel<R, true, true> : lean_dec_kernel<R, true, false>)
+              : (fast ? lean_dec_kernel<R, false, true> : lean_dec_kernel<R, false, false>);
+  k<<<blocks, 32 * kLeanWPB, lean_dec_smem<R>(), s>>>(g, st[0], st[1], st[2], sc[0], sc[1],
+                                                      sc[2], in, cls, P, f, t);
 }
 template <typename R>
-void launch_lean_rload(const LevelGeom<R> &g, const std::array<const LeanW<R> *, 3> &st,
-                       const R *cls, R *f, cudaStream_t s) {
+void launch_lean_rload(bool fast, const LevelGeom<R> &g,
+                       const std::array<const LeanW<R> *, 3> &st,
+                       const std::array<const Stencil<R> *, 3> &sc, const R *cls, R *f,
+                       cudaStream_t s) {
   const bool z3 = g.n[2] > 1;
   const LeanTiles t = lean_rtiles<R>(g.m[0], g.m[1], g.m[2], z3);
   const unsigned blocks = unsigned((t.warps() + kLeanWPB - 1) / kLeanWPB);
-  if (z3)
-    lean_rload_kernel<R, true><<<blocks, 32 * kLeanWPB, 0, s>>>(
-        g, st[0], st[1], st[2], cls, f, t);
-  else
-    lean_rload_kernel<R, false><<<blocks, 32 * kLeanWPB, 0, s>>>(
-        g, st[0], st[1], st[2], cls, f, t);
+  auto k = z3 ? (fast ? lean_rload_kernel<R, true, true> : lean_rload_kernel<R, true, false>)
+              : (fast ? lean_rload_kernel<R, false, true> : lean_rload_kernel<R, false, false>);
+  k<<<blocks, 32 * kLeanWPB, 0, s>>>(g, st[0], st[1], st[2], sc[0], sc[1], sc[2], cls, f, t);
 }
 template <typename R>
-void launch_lean_rgpk(const LevelGeom<R> &g, const std::array<const LeanW<R> *, 3> &st,
-                      const R *coarse, const R *cls, R *out, cudaStream_t s) {
+void launch_lean_rgpk(bool fast, const LevelGeom<R> &g,
+                      const std::array<const LeanW<R> *, 3> &st, const R *coarse,
+                      const R *cls, R *out, cudaStream_t s) {
   const bool z3 = g.n[2] > 1;
   const LeanTiles t = lean_gtiles<R>(g.m[0], g.m[1], g.m[2], z3);
   const unsigned blocks = unsigned((t.warps() + kLeanWPB - 1) / kLeanWPB);
-  auto k = z3 ? (cls ? lean_rgpk_kernel<R, true, true> : lean_rgpk_kernel<R, true, false>)
-              : (cls ? lean_rgpk_kernel<R, false, true> : lean_rgpk_kernel<R, false, false>);
+  using K = void (*)(LevelGeom<R>, const LeanW<R> *, const LeanW<R> *, const LeanW<R> *,
+                     const R *, const R *, R *, LeanTiles);
+  K k;
+  if (z3)
+    k = cls ? (fast ? lean_rgpk_kernel<R, true, true, true> : lean_rgpk_kernel<R, true, true, false>)
+            : (fast ? lean_rgpk_kernel<R, true, false, true>
+                    : lean_rgpk_kernel<R, true, false, false>);
+  else
+    k = cls ? (fast ? lean_rgpk_kernel<R, false, true, true>
+                    : lean_rgpk_kernel<R, false, true, false>)
+            : (fast ? lean_rgpk_kernel<R, false, false, true>
+                    : lean_rgpk_kernel<R, false, false, false>);
   k<<<blocks, 32 * kLeanWPB, 0, s>>>(g, st[0], st[1], st[2], coarse, cls, out, t);
 }
 template <typename R>
@@ -952,8 +961,8 @@ mgrg_status run_decompose(mgrg_plan *p, const R *d_in, R *d_cls, cudaStream_t s,
     // aligned (workspace levels are; a caller's input may not be)
     const bool al16 = (reinterpret_cast<uintptr_t>(a) & 15) == 0;
     const bool alv = (reinterpret_cast<uintptr_t>(a) & (2 * sizeof(R) - 1)) == 0;
-    if (p->fast && p->lean && alv && lean_level(g))
-      launch_lean_dec<R>(g, P.lean[l], a, cls, Pout, F, s);
+    if (p->lean && alv && lean_level(g))
+      launch_lean_dec<R>(p->fast, g, P.lean[l], P.sten[l], a, cls, Pout, F, s);
     else if (p->pair_path && p->gen >= 4 && al16)
       launch_dec4<R>(p->fast, g, P.sten[l], a, cls, Pout, F, s);
     else if (p->pair_path && p->gen >= 3)
@@ -1011,8 +1020,8 @@ mgrg_status run_recompose(mgrg_plan *p, const R *d_cls, int k, R *d_out,
       // read class (F-C); write load vector (C)
       if (mgrg_status st = rec.begin(MGRG_K_REC_LOAD, l, es * Fn))
         return st;
-      if (p->fast && p->lean && lean_level(g))
-        launch_lean_rload<R>(g, P.lean[l], cls, F, s);
+      if (p->lean && lean_level(g))
+        launch_lean_rload<R>(p->fast, g, P.lean[l], P.sten[l], cls, F, s);
       else if (p->pair_path)
         launch_rl2<R>(p->fast, g, P.sten[l], cls, F, s);
       else if (p->tile == TileKind::t32x8)
@@ -1042,8 +1051,8 @@ mgrg_status run_recompose(mgrg_plan *p, const R *d_cls, int k, R *d_out,
       // read coarse' (C) + class (F-C); write the level array (F)
       if (mgrg_status st = rec.begin(MGRG_K_REC_GPK, l, es * 2 * Fn))
         return st;
-      if (p->fast && p->lean && lean_level(g) && lean_out_ok<R>(out))
-        launch_lean_rgpk<R>(g, P.lean[l], F, cls, out, s);
+      if (p->lean && lean_level(g) && lean_out_ok<R>(out))
+        launch_lean_rgpk<R>(p->fast, g, P.lean[l], F, cls, out, s);
       else if (p->pair_path)
         launch_rg2<R>(p->fast, g, F, cls, out, s);
       else if (p->tile == TileKind::t32x8)
@@ -1055,8 +1064,8 @@ mgrg_status run_recompose(mgrg_plan *p, const R *d_cls, int k, R *d_out,
       // coarse values are a_{l-1} unchanged and the fine ones interp + 0.
       if (mgrg_status st = rec.begin(MGRG_K_REC_GPK, l, es * (Fn + Cn)))
         return st;
-      if (p->fast && p->lean && lean_level(g) && lean_out_ok<R>(out))
-        launch_lean_rgpk<R>(g, P.lean[l], prev, nullptr, out, s);
+      if (p->lean && lean_level(g) && lean_out_ok<R>(out))
+        launch_lean_rgpk<R>(p->fast, g, P.lean[l], prev, nullptr, out, s);
       else if (p->pair_path)
         launch_rg2<R>(p->fast, g, prev, nullptr, out, s);
       else if (p->tile == TileKind::t32x8)
@@ -1418,8 +1427,9 @@ mgrg_status decompose_host_pipelined(mgrg_plan *p, const R *h_in, R *h_cls) {
     tg.tz0 = c0;
     tg.ntz = c1 - c0;
     const unsigned blocks = unsigned((tg.warps() + kLeanWPB - 1) / kLeanWPB);
-    lean_dec_kernel<R, true><<<blocks, 32 * kLeanWPB, lean_dec_smem<R>(), sc>>>(
-        g, P.lean[L][0], P.lean[L][1], P.lean[L][2], din, clsL, Pout, F, tg);
+    lean_dec_kernel<R, true, true><<<blocks, 32 * kLeanWPB, lean_dec_smem<R>(), sc>>>(
+        g, P.lean[L][0], P.lean[L][1], P.lean[L][2], P.sten[L][0], P.sten[L][1], P.sten[L][2],
+        din, clsL, Pout, F, tg);
     CUDA_TRY(cudaGetLastError());
     CUDA_TRY(cudaEventRecord(p->ev_dec[q], sc));
     CUDA_TRY(cudaStreamWaitEvent(p->s_out, p->ev_dec[q], 0));
