@@ -124,7 +124,8 @@ mgrg_status crc32_launch(const uint8_t *d, uint64_t n, uint32_t *d_out, uint32_t
   const uint64_t tail = n - head - nblk * 512;
   const uint64_t nseg = (nblk + mgrg::kCrcSegBlocks - 1) / mgrg::kCrcSegBlocks;
   if (nblk)
-    mgrg::crc_blocks_kernel<<<unsigned((nseg + mgrg::kCrcWarps - 1) / mgrg::kCrcWarps),
+    mgrg::crc_blocks_kernel<<<unsigned(std::min<uint64_t>(
+                                  (nseg + mgrg::kCrcWarps - 1) / mgrg::kCrcWarps, 148 * 6)),
                               32 * mgrg::kCrcWarps, 0, s>>>(
         reinterpret_cast<const uint4 *>(d + head), nblk, T, d_seg);
   mgrg::crc_combine_kernel<<<1, mgrg::kCrcRuns, 0, s>>>(
