@@ -164,13 +164,6 @@ struct Carve {
 };
 __host__ __device__ constexpr size_t al16(size_t b) { return (b + 15) & ~size_t(15); }
 
-template <typename R, int CY> constexpr size_t dec2_smem() {
-  using C = PairCfg<CY>;
-  return al16(sizeof(R) * 6 * C::PLANE) + al16(sizeof(R) * C::BYR * 32) +
-         al16(sizeof(Stencil<R>) * CY) + al16(sizeof(Stencil<R>) * C::ZC) +
-         al16(sizeof(ClassTab)) + al16(sizeof(R) * C::BYR) +
-         al16(sizeof(R) * (2 * C::ZC + 4));
-}
 template <typename R, int CY> constexpr size_t rl2_smem() {
   using C = PairCfg<CY>;
   return al16(sizeof(R) * 3 * C::PLANE) + al16(sizeof(R) * C::BYR * 32) +
@@ -202,276 +195,9 @@ __device__ __forceinline__ R y_eval(const Stencil<R> &s, const R *X, int j, int 
 }
 
 // ---------------------------------------------------------------------------
-// Decompose, one level (fast path; x and y refine).  Same contract as
-// dec_level_kernel (kernels.cuh): GPK forward on `in`, class-order store
-// into `cls`, packed kept-node values into P, merged R*M of vec(C) into f.
-// ---------------------------------------------------------------------------
-template <typename R, int CY, bool FAST>
-__global__ void __launch_bounds__(256)
-    dec2_kernel(LevelGeom<R> g, const Stencil<R> *__restrict__ stx,
-                const Stencil<R> *__restrict__ sty, const Stencil<R> *__restrict__ stz,
-                const R *__restrict__ in, R *__restrict__ cls, R *__restrict__ P,
-                R *__restrict__ f, uint32_t ntx, uint32_t nty, uint32_t ntz) {
-  using C = PairCfg<CY>;
-  using A = Arith<R, FAST>;
-  extern __shared__ __align__(16) unsigned char smem_bytes[];
-  Carve cv{smem_bytes};
-  R *U = cv.take<R>(6 * C::PLANE); // [4][BYR][64] raw planes + [2][BYR][64] W planes
-  R *Wc = U + 4 * C::PLANE;
-  R *X = cv.take<R>(C::BYR * 32); // [BYR][32] x-pass results
-  Stencil<R> *sY = cv.take<Stencil<R>>(CY);
-  Stencil<R> *sZ = cv.take<Stencil<R>>(C::ZC);
-  ClassTab *ct = cv.take<ClassTab>(1);
-  R *tyv = cv.take<R>(C::BYR);        // r_y of each box row (fine rows)
-  R *tzv = cv.take<R>(2 * C::ZC + 4); // r_z of each box plane (fine planes)
-
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const uint32_t nx = g.n[0], ny = g.n[1], nz = g.n[2];
-  const uint32_t mx = g.m[0], my = g.m[1], mz = g.m[2];
-  const bool rz = g.refine & 4;
-  const uint32_t cx0 = tile_lo(blockIdx.x, ntx, mx), cx1 = tile_lo(blockIdx.x + 1, ntx, mx);
-  const uint32_t cy0 = tile_lo(blockIdx.y, nty, my), cy1 = tile_lo(blockIdx.y + 1, nty, my);
-  const uint32_t cz0 = tile_lo(blockIdx.z, ntz, mz), cz1 = tile_lo(blockIdx.z + 1, ntz, mz);
-  const int X0 = 2 * int(cx0) - 2, Y0 = 2 * int(cy0) - 2;
-  const uint32_t OX1 = cx1 == mx ? nx : 2 * cx1;
-  const uint32_t OY0 = 2 * cy0, OY1 = cy1 == my ? ny : 2 * cy1;
-  const uint32_t Z0 = rz ? (cz0 ? 2 * cz0 - 2 : 0) : cz0;
-  const uint32_t Z1 = rz ? min(nz, 2 * cz1 + 1) : cz1;
-  const uint32_t OZ0 = rz ? 2 * cz0 : cz0, OZ1 = rz ? (cz1 == mz ? nz : 2 * cz1) : cz1;
-  const uint64_t nxy = uint64_t(nx) * ny;
-  const uint64_t mxy = uint64_t(mx) * my;
-
-  // ---- stage per-CTA tables
-  stage_stencils(sY, sty + cy0, cy1 - cy0, tid);
-  if (rz)
-    stage_stencils(sZ, stz + cz0, cz1 - cz0, tid);
-  load_classtab(*ct, g, tid);
-  for (int b = tid; b < C::BYR; b += 256) {
-    const int y = Y0 + b;
-    tyv[b] = (y > 0 && y < int(ny) - 1 && (y & 1)) ? g.r[1][y - 1] : R(0);
-  }
-  if (rz)
-    for (uint32_t p = Z0 + tid; p < Z1; p += 256)
-      tzv[p - Z0] = ((p & 1) && p < nz - 1) ? g.r[2][p - 1] : R(0);
-
-  // ---- per-lane x geometry (registers for the whole kernel)
-  const int xe = X0 + 2 * lane, xo = xe + 1;
-  const bool xe_ok = xe >= 0 && xe < int(nx);
-  const bool xo_ok = xo >= 0 && xo < int(nx);
-  const bool xo_fine = xo_ok && xo < int(nx) - 1;
-  const R tx = xo_fine ? g.r[0][xo - 1] : R(0);
-  const bool own_e = lane >= 1 && xe < int(OX1);
-  const bool own_o = lane >= 1 && xo < int(OX1) && xo_ok;
-  const uint32_t cr_e = uint32_t(xe) >> 1;
-  const uint32_t rk_o = xo_fine ? uint32_t(xo - 1) >> 1 : coarse_rank(uint32_t(xo));
-  const bool xval = lane < 30 && cx0 + lane < cx1;
-  const Stencil<R> sx = stx[min(cx0 + min(uint32_t(lane), 29u), mx - 1)];
-
-  // ---- LDGSTS plane loader: thread -> column tid&63, rows (tid>>6) + 4m
-  const int lc = tid & 63, lr0 = tid >> 6;
-  const int gx = X0 + lc;
-  const bool col_ok = gx >= 0 && gx < int(nx);
-  auto load_plane = [&](uint32_t p) {
-    if (p < Z1 && col_ok) {
-      R *dst = U + (p & 3) * C::PLANE + lc;
-      const R *src = in + nxy * p + gx;
-#pragma unroll 3
-      for (int b = lr0; b < C::BYR; b += 4) {
-        const int gy = Y0 + b;
-        if (gy >= 0 && gy < int(ny))
-          cp_async(dst + b * 64, src + uint64_t(gy) * nx);
-      }
-    }
-    cp_async_commit();
-  };
-
-  // ---- GPK + stores + x pass for one plane.  Fine plane: wlo/whi are the
-  // prolongated neighbour coarse planes.  Coarse plane: wout receives W.
-  auto process_plane = [&](uint32_t p, bool fz, const R *wlo, const R *whi, R *wout) {
-    const R *Up = U + (p & 3) * C::PLANE;
-    const R tz = fz ? tzv[p - Z0] : R(0);
-    const bool ownz = p >= OZ0 && p < OZ1;
-    const uint32_t wz = fz ? (p - 1) >> 1 : coarse_rank(p);
-    for (int b = warp; b < C::BYR; b += 8) {
-      const int y = Y0 + b;
-      const bool y_ok = y >= 0 && y < int(ny);
-      const bool fy = y_ok && (y & 1) && y < int(ny) - 1;
-      const Pair<R> u = ld_pair(Up + b * 64 + 2 * lane);
-      R we, wo;
-      if (fz) {
-        const Pair<R> a = ld_pair(wlo + b * 64 + 2 * lane);
-        const Pair<R> c = ld_pair(whi + b * 64 + 2 * lane);
-        we = A::lerp(a.e, c.e, tz);
-        wo = A::lerp(a.o, c.o, tz);
-      } else if (!fy) {
-        const R un = __shfl_down_sync(0xffffffffu, u.e, 1);
-        we = u.e;
-        wo = xo_fine ? A::lerp(u.e, un, tx) : u.o;
-      } else {
-        const R ty = tyv[b];
-        const Pair<R> um = ld_pair(Up + (b - 1) * 64 + 2 * lane);
-        const Pair<R> up = ld_pair(Up + (b + 1) * 64 + 2 * lane);
-        const R umn = __shfl_down_sync(0xffffffffu, um.e, 1);
-        const R upn = __shfl_down_sync(0xffffffffu, up.e, 1);
-        const R wmo = xo_fine ? A::lerp(um.e, umn, tx) : um.o;
-        const R wpo = xo_fine ? A::lerp(up.e, upn, tx) : up.o;
-        we = A::lerp(um.e, up.e, ty);
-        wo = A::lerp(wmo, wpo, ty);
-      }
-      if (wout)
-        st_pair(wout + b * 64 + 2 * lane, we, wo);
-      const bool fe = fy || fz;      // even-x node is a coefficient node
-      const bool fo = fe || xo_fine; // odd-x node is a coefficient node
-      // vec(C): coefficients at coefficient nodes, 0 at kept nodes and
-      // outside the grid (zero taps never meet a nonzero stencil weight)
-      const R ve = (fe && xe_ok && y_ok) ? sub(u.e, we) : R(0);
-      const R vo = (fo && xo_ok && y_ok) ? sub(u.o, wo) : R(0);
-      // class order / packed-coarse stores of owned nodes (coalesced runs)
-      if (ownz && y_ok && uint32_t(y) >= OY0 && uint32_t(y) < OY1) {
-        const uint32_t wy = fy ? (uint32_t(y) - 1) >> 1 : coarse_rank(uint32_t(y));
-        const unsigned me = (unsigned(fy) << 1) | (unsigned(fz) << 2);
-        const unsigned mo = me | unsigned(xo_fine);
-        if (me == 0) {
-          R *prow = P + mx * uint64_t(wy) + mxy * wz;
-          if (own_e)
-            prow[cr_e] = u.e;
-          if (own_o) {
-            if (mo == 0)
-              prow[rk_o] = u.o;
-            else
-              cls[ct->row(mo, wy, wz) + rk_o] = vo;
-          }
-        } else {
-          if (own_e)
-            cls[ct->row(me, wy, wz) + cr_e] = ve;
-          if (own_o)
-            cls[ct->row(mo, wy, wz) + rk_o] = vo;
-        }
-      }
-      // x pass: output lane i from pairs i, i+1 and the even node of i+2
-      const R e1 = __shfl_down_sync(0xffffffffu, ve, 1);
-      const R o1 = __shfl_down_sync(0xffffffffu, vo, 1);
-      const R e2 = __shfl_down_sync(0xffffffffu, ve, 2);
-      const R xv = stencil_eval<R, FAST>(sx, ve, vo, e1, o1, e2);
-      if (lane < 30)
-        X[b * 32 + lane] = xval ? xv : R(0);
-    }
-  };
-
-  __syncthreads(); // tables staged
-  load_plane(Z0);
-  load_plane(Z0 + 1);
-  load_plane(Z0 + 2);
-  uint32_t issued = Z0 + 3;
-  cp_async_wait<2>();
-  __syncthreads();
-
-  const uint32_t cxo = cx0 + lane;
-  if (!rz) {
-    // z does not refine: every plane is coarse and is its own output
-    for (uint32_t p = Z0; p < Z1; ++p) {
-      if (p > Z0) {
-        load_plane(issued++);
-        cp_async_wait<2>();
-        __syncthreads();
-      }
-      process_plane(p, false, nullptr, nullptr, nullptr);
-      __syncthreads();
-#pragma unroll
-      for (int jj = 0; jj < C::RW; ++jj) {
-        const int j = warp + 8 * jj;
-        if (j < CY && cy0 + j < cy1) {
-          const R v = y_eval<R, FAST>(sY[j], X, j, lane);
-          if (xval)
-            f[cxo + uint64_t(mx) * (cy0 + j) + mxy * p] = v;
-        }
-      }
-      __syncthreads();
-    }
-    cp_async_wait<0>();
-    return;
-  }
-
-  // z refines: carried window c0,c1,c2 = G(pc-2), G(pc-1), G(pc) per row j
-  R c0[C::RW], c1[C::RW], c2[C::RW], zero[C::RW];
-#pragma unroll
-  for (int jj = 0; jj < C::RW; ++jj)
-    c0[jj] = c1[jj] = c2[jj] = zero[jj] = R(0);
-  auto y_all = [&](R *out) {
-#pragma unroll
-    for (int jj = 0; jj < C::RW; ++jj) {
-      const int j = warp + 8 * jj;
-      out[jj] = (j < CY && cy0 + j < cy1) ? y_eval<R, FAST>(sY[j], X, j, lane) : R(0);
-    }
-  };
-  auto emit = [&](uint32_t k, const R *t0, const R *t1, const R *t2, const R *t3,
-                  const R *t4) {
-    if (k < cz0 || k >= cz1)
-      return;
-    const Stencil<R> &s = sZ[k - cz0];
-#pragma unroll
-    for (int jj = 0; jj < C::RW; ++jj) {
-      const int j = warp + 8 * jj;
-      const R v = stencil_eval<R, FAST>(s, t0[jj], t1[jj], t2[jj], t3[jj], t4[jj]);
-      if (j < CY && cy0 + j < cy1 && xval)
-        f[cxo + uint64_t(mx) * (cy0 + j) + mxy * k] = v;
-    }
-  };
-
-  uint32_t pc = Z0; // last processed coarse plane
-  uint32_t slot = 0;
-  process_plane(pc, false, nullptr, nullptr, Wc);
-  __syncthreads();
-  y_all(c2);
-  for (;;) {
-    const uint32_t nxt = pc + 2 <= nz - 1 ? pc + 2 : pc + 1;
-    if (nxt >= Z1)
-      break;
-    __syncthreads(); // X consumed before it is overwritten
-    load_plane(issued++);
-    load_plane(issued++);
-    cp_async_wait<2>();
-    __syncthreads();
-    const uint32_t ns = slot ^ 1;
-    process_plane(nxt, false, nullptr, nullptr, Wc + ns * C::PLANE);
-    __syncthreads();
-    R gn[C::RW], gf[C::RW];
-    y_all(gn);
-    if (nxt == pc + 2) { // the fine plane between the two coarse planes
-      __syncthreads();
-      process_plane(pc + 1, true, Wc + slot * C::PLANE, Wc + ns * C::PLANE, nullptr);
-      __syncthreads();
-      y_all(gf);
-      emit(pc >> 1, c0, c1, c2, gf, gn); // q = pc: taps pc-2 .. pc+2
-#pragma unroll
-      for (int jj = 0; jj < C::RW; ++jj) {
-        c0[jj] = c2[jj];
-        c1[jj] = gf[jj];
-        c2[jj] = gn[jj];
-      }
-      pc = nxt;
-      slot = ns;
-    } else {
-      // nxt = pc + 1 = nz - 1 (even nz): output pc/2 has no fine right
-      // neighbour but mv(q) still reads position q+1 = nxt; the last output
-      // (q = nz-1) reads positions q-1 = pc and q = nxt
-      emit(pc >> 1, c0, c1, c2, gn, zero);
-      emit((nxt + 1) >> 1, zero, c2, gn, zero, zero);
-      pc = nxt;
-      break;
-    }
-  }
-  // last coarse plane of an odd extent: q = nz-1 = pc (right boundary form)
-  if (pc == nz - 1 && (pc & 1) == 0)
-    emit(pc >> 1, c0, c1, c2, zero, zero);
-  cp_async_wait<0>();
-}
-
-// ---------------------------------------------------------------------------
-// Recompose load vector, one level (fast path): vec(C) gathered from class l
-// in coalesced per-row runs (lane a reads the a-th coarse-x and the a-th
-// fine-x entry of the row's two class types) into a 3-plane ring, then the
-// same x (shuffle) / y / z merged mass-trans as dec2.
+// Recompose load vector, one level (pair-lane path for levels with an even
+// extent; x and y refine): vec(C) gathered from the class buffer, merged R*M
+// along x, y, z into f.  Same contract as rec_load_kernel (kernels.cuh).
 // ---------------------------------------------------------------------------
 template <typename R, int CY, bool FAST>
 __global__ void __launch_bounds__(256)

@@ -205,7 +205,6 @@ struct mgrg_plan {
   bool pair_path = false; // x and y refine: pair-lane kernels (kernels2.cuh)
   bool fast = false;      // MGRG_FLAG_FAST: FMA arithmetic policy
   uint32_t zchunk = 32;
-  int gen = 4;            // pair-lane kernel generation (MGRG_KGEN=2/3: older ones)
   bool lean = false;      // dyadic x/y(/z) refinement: lean warp-tiled kernels (lean.cuh)
   mgrg_status deferred = MGRG_OK;         // SingularSystem found at build time
   std::string deferred_msg;
@@ -571,17 +570,10 @@ int g_thomas_small = [] {
   const char *e = std::getenv("MGRG_TSMALL");
   return e ? std::atoi(e) : 1;
 }();
-// experiment knob: minimum resident CTAs of the level kernels (MGRG_MINB)
-int g_minb = [] {
-  const char *e = std::getenv("MGRG_MINB");
-  return e ? std::atoi(e) : 3;
-}();
 constexpr uint32_t kZChunk = 32; // coarse-z planes per CTA of the pair-lane kernels
 template <typename R> constexpr int pair_cy() { return sizeof(R) == 4 ? 16 : 8; }
 
 template <typename R, int CY, bool FAST> void set_pair_attrs_t() {
-  cudaFuncSetAttribute(dec2_kernel<R, CY, FAST>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                       int(dec2_smem<R, CY>()));
   cudaFuncSetAttribute(rl2_kernel<R, CY, FAST>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        int(rl2_smem<R, CY>()));
   cudaFuncSetAttribute(rg2_kernel<R, CY, FAST>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -590,21 +582,9 @@ template <typename R, int CY, bool FAST> void set_pair_attrs_t() {
 template <typename R, int CY> void set_pair_attrs() {
   set_pair_attrs_t<R, CY, false>();
   set_pair_attrs_t<R, CY, true>();
-  cudaFuncSetAttribute(dec3_kernel<R, cy3<R>(), false>,
-                       cudaFuncAttributeMaxDynamicSharedMemorySize, int(dec3_smem<R, cy3<R>()>()));
-  cudaFuncSetAttribute(dec3_kernel<R, cy3<R>(), false, 2>,
-                       cudaFuncAttributeMaxDynamicSharedMemorySize, int(dec3_smem<R, cy3<R>()>()));
-  cudaFuncSetAttribute(dec3_kernel<R, cy3<R>(), true>,
-                       cudaFuncAttributeMaxDynamicSharedMemorySize, int(dec3_smem<R, cy3<R>()>()));
-  cudaFuncSetAttribute(dec3_kernel<R, cy3<R>(), true, 2>,
-                       cudaFuncAttributeMaxDynamicSharedMemorySize, int(dec3_smem<R, cy3<R>()>()));
   cudaFuncSetAttribute(dec4_kernel<R, cy4<R>(), false>,
                        cudaFuncAttributeMaxDynamicSharedMemorySize, int(dec4_smem<R, cy4<R>()>()));
-  cudaFuncSetAttribute(dec4_kernel<R, cy4<R>(), false, 2>,
-                       cudaFuncAttributeMaxDynamicSharedMemorySize, int(dec4_smem<R, cy4<R>()>()));
   cudaFuncSetAttribute(dec4_kernel<R, cy4<R>(), true>,
-                       cudaFuncAttributeMaxDynamicSharedMemorySize, int(dec4_smem<R, cy4<R>()>()));
-  cudaFuncSetAttribute(dec4_kernel<R, cy4<R>(), true, 2>,
                        cudaFuncAttributeMaxDynamicSharedMemorySize, int(dec4_smem<R, cy4<R>()>()));
 }
 
@@ -615,35 +595,13 @@ template <typename R> dim3 pair_grid(const LevelGeom<R> &g, uint32_t cx) {
 }
 
 template <typename R>
-void launch_dec2(bool fast, const LevelGeom<R> &g,
-                 const std::array<const Stencil<R> *, 3> &st, const R *in, R *cls, R *P,
-                 R *f, cudaStream_t s) {
-  constexpr int CY = pair_cy<R>();
-  const dim3 grid = pair_grid(g, 30);
-  auto k = fast ? dec2_kernel<R, CY, true> : dec2_kernel<R, CY, false>;
-  k<<<grid, 256, dec2_smem<R, CY>(), s>>>(g, st[0], st[1], st[2], in, cls, P, f, grid.x,
-                                          grid.y, grid.z);
-}
-template <typename R>
-void launch_dec3(bool fast, const LevelGeom<R> &g,
-                 const std::array<const Stencil<R> *, 3> &st, const R *in, R *cls, R *P,
-                 R *f, cudaStream_t s) {
-  constexpr int CY = cy3<R>();
-  const dim3 grid = pair_grid(g, 30);
-  auto k = fast ? (g_minb == 2 ? dec3_kernel<R, CY, true, 2> : dec3_kernel<R, CY, true, 3>)
-                : (g_minb == 2 ? dec3_kernel<R, CY, false, 2> : dec3_kernel<R, CY, false, 3>);
-  k<<<grid, 256, dec3_smem<R, CY>(), s>>>(g, st[0], st[1], st[2], in, cls, P, f, grid.x,
-                                          grid.y, grid.z);
-}
-template <typename R>
 void launch_dec4(bool fast, const LevelGeom<R> &g,
                  const std::array<const Stencil<R> *, 3> &st, const R *in, R *cls, R *P,
                  R *f, cudaStream_t s) {
   constexpr int CY = cy4<R>();
   const uint32_t ntz = (g.refine & 4) ? (g.m[2] + kZChunk - 1) / kZChunk : g.m[2];
   const dim3 grid((g.m[0] + 29) / 30, (g.m[1] + CY - 1) / CY, ntz);
-  auto k = fast ? (g_minb == 2 ? dec4_kernel<R, CY, true, 2> : dec4_kernel<R, CY, true, 3>)
-                : (g_minb == 2 ? dec4_kernel<R, CY, false, 2> : dec4_kernel<R, CY, false, 3>);
+  auto k = fast ? dec4_kernel<R, CY, true> : dec4_kernel<R, CY, false>;
   k<<<grid, 256, dec4_smem<R, CY>(), s>>>(g, st[0], st[1], st[2], in, cls, P, f, grid.x,
                                           grid.y, grid.z);
 }
@@ -963,12 +921,8 @@ mgrg_status run_decompose(mgrg_plan *p, const R *d_in, R *d_cls, cudaStream_t s,
     const bool alv = (reinterpret_cast<uintptr_t>(a) & (2 * sizeof(R) - 1)) == 0;
     if (p->lean && alv && lean_level(g))
       launch_lean_dec<R>(p->fast, g, P.lean[l], P.sten[l], a, cls, Pout, F, s);
-    else if (p->pair_path && p->gen >= 4 && al16)
+    else if (p->pair_path && al16)
       launch_dec4<R>(p->fast, g, P.sten[l], a, cls, Pout, F, s);
-    else if (p->pair_path && p->gen >= 3)
-      launch_dec3<R>(p->fast, g, P.sten[l], a, cls, Pout, F, s);
-    else if (p->pair_path)
-      launch_dec2<R>(p->fast, g, P.sten[l], a, cls, Pout, F, s);
     else if (p->tile == TileKind::t32x8)
       launch_dec_level<R, 32, 8>(g, a, cls, Pout, F, p->zchunk, s);
     else
@@ -1159,8 +1113,6 @@ mgrg_status mgrg_plan_create(const mgrg_grid_desc *desc, mgrg_plan **out) {
   if (const char *gp = std::getenv("MGRG_GENERIC"))
     if (std::atoi(gp) != 0)
       p->pair_path = false;
-  if (const char *kg = std::getenv("MGRG_KGEN"))
-    p->gen = std::atoi(kg);
   {
     // lean family: x, y (and z) refine; used on every level whose extents
     // are all odd (coarse = even positions), see lean_level()
