@@ -918,8 +918,8 @@ mgrg_status run_decompose(mgrg_plan *p, const R *d_in, R *d_cls, cudaStream_t s,
     // dec4 stages rows with 16-byte copies: the level array must be 16-byte
     // aligned (workspace levels are; a caller's input may not be)
     const bool al16 = (reinterpret_cast<uintptr_t>(a) & 15) == 0;
-    const bool alv = (reinterpret_cast<uintptr_t>(a) & (2 * sizeof(R) - 1)) == 0;
-    if (p->lean && alv && lean_level(g))
+    // the lean kernel stages 16-byte aligned row supersets of the level array
+    if (p->lean && al16 && lean_level(g))
       launch_lean_dec<R>(p->fast, g, P.lean[l], P.sten[l], a, cls, Pout, F, s);
     else if (p->pair_path && al16)
       launch_dec4<R>(p->fast, g, P.sten[l], a, cls, Pout, F, s);
