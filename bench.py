@@ -285,6 +285,68 @@ def run_e2e(plan, d_in, d_out, N, nbytes, L, K, dist, device, world):
            "matches_device_path": e2e_ok}
     return e2e
 
+
+def other_configs(args, device):
+    """Device dec + rec throughput of BASELINE configs 1, 2, 3 and the config-5
+    block (secondary lines of the report; parity for them is in
+    tests/test_gpu_parity.py).  Same timing discipline: warm-up, CUDA events on
+    the launch stream, inputs resident in HBM."""
+    import torch
+
+    from paper_2105_12764_b200 import Plan
+
+    cases = [
+        ("config1 65^3 f64 uniform", (65, 65, 65), "float64", False),
+        ("config2 8193^2 f64 uniform", (8193, 8193), "float64", False),
+        ("config3 513^3 f32 non-uniform", (513, 513, 513), "float32", True),
+        ("config5 block 1025x1025x513 f64", (1025, 1025, 513), "float64", False),
+    ]
+    out = {}
+    for name, shape, dt, nonuni in cases:
+        coords = None
+        if nonuni:
+            coords = []
+            for d, n in enumerate(shape):
+                c = np.cumsum(np.random.default_rng(2105 + d).uniform(0.1, 1.0, n))
+                coords.append(c / c[-1])
+        if len(shape) == 3:
+            v = make_field_device(shape, 0, device, dt)
+        else:
+            g = torch.Generator(device=device).manual_seed(2)
+            v = torch.rand(int(np.prod(shape)), dtype=getattr(torch, dt), device=device,
+                           generator=g)
+        plan = Plan(shape, dt, coords=coords, device=device.index, fast=args.arith == "fast")
+        c = torch.empty_like(v)
+        r = torch.empty_like(v)
+        s = torch.cuda.current_stream(device)
+        for _ in range(3):
+            plan.decompose(v, c, s)
+            plan.recompose(c, plan.levels, r, s)
+        reps = 5
+        e0, e1, e2 = (torch.cuda.Event(enable_timing=True) for _ in range(3))
+        dms = rms = 0.0
+        for _ in range(reps):
+            e0.record(s)
+            plan.decompose(v, c, s)
+            e1.record(s)
+            plan.recompose(c, plan.levels, r, s)
+            e2.record(s)
+            torch.cuda.synchronize()
+            dms += e0.elapsed_time(e1)
+            rms += e1.elapsed_time(e2)
+        nb = v.numel() * v.element_size()
+        err = ((r - v).abs().max() / (v.max() - v.min())).item()
+        out[name] = {"levels": plan.levels, "decompose_ms": round(dms / reps, 4),
+                     "recompose_ms": round(rms / reps, 4),
+                     "decompose_GBps": round(nb / (dms / reps * 1e-3) / 1e9, 1),
+                     "recompose_GBps": round(nb / (rms / reps * 1e-3) / 1e9, 1),
+                     "roundtrip_rel_err": err}
+        plan.close()
+        del v, c, r
+        torch.cuda.empty_cache()
+    return out
+
+
 def run_ours(args, rank, world, local_rank):
     import torch
 
@@ -426,6 +488,13 @@ def run_ours(args, rank, world, local_rank):
         except (RuntimeError, MemoryError) as ex:  # e.g. pinned host memory exhausted
             e2e = {"value": None, "unit": "GB/s", "error": str(ex)[:200]}
 
+    others = None
+    if rank == 0 and world == 1 and not args.no_others:
+        plan.close()
+        del d_cls
+        torch.cuda.empty_cache()
+        others = other_configs(args, device)
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
         threads = cpu_threads()
@@ -453,6 +522,7 @@ def run_ours(args, rank, world, local_rank):
             "cpu_baseline": cpu, "e2e": e2e,
             "gpu_launches": launches_per_step * K,
             "clocks": clocks,
+            "other_configs": others,
         }
         print(json.dumps(out), flush=True)
     plan.close()
@@ -466,6 +536,8 @@ def main():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     ap.add_argument("--no-e2e", action="store_true", help="skip the host-buffer leg")
+    ap.add_argument("--no-others", action="store_true",
+                    help="skip the secondary BASELINE-config lines (configs 1, 2, 3, 5 block)")
     ap.add_argument("--arith", choices=["exact", "fast"], default="fast",
                     help="fast (default): FMA policy, per class max|gpu-cpu| <= 1e-5 "
                          "(f32) / 1e-12 (f64) of the input range -- the north_star parity "
