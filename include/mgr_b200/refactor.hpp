@@ -447,6 +447,36 @@ recompose_with_report(const RefactoredData<Real> &r, std::size_t classes_used,
   return {std::move(g), rep};
 }
 
+// mgr::decompose_spatiotemporal (refactor.hpp:536-567): the snapshots are
+// stacked along a trailing time dimension (time coordinates given) and the
+// stacked grid is decomposed; a 3-D series runs on the 4-D device path.
+template <typename Real>
+RefactoredData<Real>
+decompose_spatiotemporal(const std::vector<TensorGrid<Real>> &snapshots,
+                         const std::vector<double> &time_coords,
+                         const RefactorOptions &opt = {}) {
+  const std::size_t T = snapshots.size();
+  if (T < 2)
+    throw ShapeError("need at least 2 snapshots");
+  if (time_coords.size() != T)
+    throw ShapeError("time coordinate count does not match snapshots");
+  const TensorGrid<Real> &s0 = snapshots[0];
+  if (s0.shape.size() >= kMaxDims)
+    throw InvalidGrid("too many dimensions after stacking time");
+  for (const TensorGrid<Real> &s : snapshots)
+    if (s.shape != s0.shape || s.coords != s0.coords)
+      throw ShapeError("snapshots must share shape and coordinates");
+  Shape shape = s0.shape;
+  shape.push_back(T);
+  auto coords = s0.coords;
+  coords.push_back(time_coords);
+  std::vector<Real> values;
+  values.reserve(s0.values.size() * T);
+  for (const TensorGrid<Real> &s : snapshots)
+    values.insert(values.end(), s.values.begin(), s.values.end());
+  return decompose(make_grid(std::move(shape), std::move(values), std::move(coords), 2), opt);
+}
+
 // mgr::embarrassing_decompose (parallel_impl.hpp:810-847): a pool of
 // min(workers, blocks, visible GPUs) host threads, one GPU each, claiming
 // blocks from a shared counter; result i == decompose(blocks[i]); the first

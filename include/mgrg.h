@@ -53,7 +53,7 @@ typedef enum mgrg_status {
   MGRG_IO_ERROR = 11,         /* mgr::IoError                                */
   MGRG_CUDA_ERROR = 12,       /* device failure (no reference equivalent)   */
   MGRG_NCCL_ERROR = 13,       /* collective failure                          */
-  MGRG_UNSUPPORTED = 14,      /* e.g. 4-D grids (spatiotemporal, out of scope)*/
+  MGRG_UNSUPPORTED = 14,      /* a limit of this implementation (extent > 2^31) */
   MGRG_INVALID_ARGUMENT = 15, /* null pointer, bad dtype, ...                */
   MGRG_OUT_OF_MEMORY = 16
 } mgrg_status;
@@ -63,7 +63,7 @@ typedef enum mgrg_dtype { MGRG_F32 = 4, MGRG_F64 = 8 } mgrg_dtype;
 /* Grid description: TensorGrid minus the values (grid.hpp:19-26) plus
  * RefactorOptions::levels (refactor.hpp:71-76). */
 typedef struct mgrg_grid_desc {
-  int32_t ndims;         /* 1..3 (the reference allows 4; see MGRG_UNSUPPORTED) */
+  int32_t ndims;         /* 1..4 (ndarray.hpp:12 kMaxDims)                  */
   int32_t dtype;         /* mgrg_dtype */
   uint64_t shape[4];     /* finest-level extents, dim 0 fastest */
   const double *coords;  /* NULL = uniform; else sum(shape) doubles */

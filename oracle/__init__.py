@@ -152,6 +152,25 @@ def decompose(values: np.ndarray, shape, coords=None, levels_cap: int = 0,
     return out, lv.value
 
 
+def ref_spatiotemporal(values: np.ndarray, shape, time_coords, coords=None):
+    """mgr::decompose_spatiotemporal (refactor.hpp:536-567) of the reference
+    itself: values snapshot-major (len(time_coords) snapshots of `shape`).
+    Returns (classes, L)."""
+    lib = _lib("ref")
+    values = np.ascontiguousarray(values)
+    out = np.empty(values.size, dtype=values.dtype)
+    fn = getattr(lib, "mgrref_spatiotemporal_" + _sfx(values.dtype))
+    fn.argtypes = [ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int,
+                   ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
+                   ctypes.POINTER(ctypes.c_int)]
+    keep, cp = _coords_arr(shape, coords)
+    tc = np.ascontiguousarray(time_coords, dtype=np.float64)
+    lv = ctypes.c_int()
+    _check(fn(len(shape), _shape_arr(shape), cp, len(tc), _ptr(tc), _ptr(values), _ptr(out),
+              ctypes.byref(lv)), "decompose_spatiotemporal")
+    return out, lv.value
+
+
 def recompose(classes: np.ndarray, shape, levels: int, classes_used: int,
               coords=None, impl: str = "oracle") -> np.ndarray:
     """mgr::recompose (refactor.hpp:476-496) from the flat class buffer."""

@@ -77,6 +77,37 @@ int decompose_impl(int nd, const uint64_t *shape, const double *coords,
   }
 }
 
+// decompose_spatiotemporal (refactor.hpp:536-567): nsnap snapshots of one
+// nd-D grid, values snapshot-major
+template <typename Real>
+int spatiotemporal_impl(int nd, const uint64_t *shape, const double *coords, int nsnap,
+                        const double *time_coords, const Real *values, Real *classes,
+                        int *levels_out) {
+  try {
+    std::vector<mgr::TensorGrid<Real>> snaps(nsnap);
+    const std::size_t n = mgr::num_elements(to_shape(nd, shape));
+    for (int t = 0; t < nsnap; ++t) {
+      snaps[t].shape = to_shape(nd, shape);
+      snaps[t].coords = to_coords(nd, shape, coords);
+      snaps[t].values.assign(values + t * n, values + (t + 1) * n);
+    }
+    const std::vector<double> tc(time_coords, time_coords + nsnap);
+    const auto r = mgr::decompose_spatiotemporal(snaps, tc);
+    std::size_t off = 0;
+    for (const auto &c : r.classes) {
+      std::memcpy(classes + off, c.data(), c.size() * sizeof(Real));
+      off += c.size();
+    }
+    if (levels_out)
+      *levels_out = int(r.levels);
+    return 0;
+  } catch (const mgr::Error &e) {
+    return code_of(e);
+  } catch (...) {
+    return 15;
+  }
+}
+
 template <typename Real>
 int recompose_impl(int nd, const uint64_t *shape, const double *coords,
                    int levels, const Real *classes, int k, Real *values) {
@@ -242,6 +273,14 @@ int mgrref_decompose_f64(int nd, const uint64_t *shape, const double *coords,
 int mgrref_decompose_f32(int nd, const uint64_t *shape, const double *coords,
                          int cap, const float *v, float *c, int *lo) {
   return decompose_impl<float>(nd, shape, coords, cap, v, c, lo);
+}
+int mgrref_spatiotemporal_f64(int nd, const uint64_t *shape, const double *coords, int nsnap,
+                              const double *tc, const double *v, double *c, int *lo) {
+  return spatiotemporal_impl<double>(nd, shape, coords, nsnap, tc, v, c, lo);
+}
+int mgrref_spatiotemporal_f32(int nd, const uint64_t *shape, const double *coords, int nsnap,
+                              const double *tc, const float *v, float *c, int *lo) {
+  return spatiotemporal_impl<float>(nd, shape, coords, nsnap, tc, v, c, lo);
 }
 int mgrref_recompose_f64(int nd, const uint64_t *shape, const double *coords,
                          int levels, const double *c, int k, double *v) {

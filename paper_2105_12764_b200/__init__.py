@@ -14,7 +14,8 @@ from .container import (CompressionReport, CompressResult, DecompressResult, Rea
                         RefactorFileHeader, compress, crc32, decompress, read_refactored,
                         read_refactored_header, write_refactored)
 from .refactor import (LevelPassStats, PassStats, PhaseCounters, ReconstructionReport,
-                       RefactoredData, RefactorOptions, TensorGrid, decompose, make_grid,
+                       RefactoredData, RefactorOptions, TensorGrid, decompose,
+                       decompose_spatiotemporal, make_grid,
                        recompose, recompose_with_report, uniform_coords, value_range,
                        weighted_l2_norm)
 from .parallel import (BlockShardedRefactor, embarrassing_decompose, embarrassing_recompose,
@@ -23,6 +24,7 @@ from .parallel import (BlockShardedRefactor, embarrassing_decompose, embarrassin
 __all__ = [
     "Plan", "TensorGrid", "RefactoredData", "RefactorOptions", "PassStats",
     "LevelPassStats", "PhaseCounters", "ReconstructionReport", "decompose", "recompose",
+    "decompose_spatiotemporal",
     "recompose_with_report", "make_grid", "uniform_coords", "value_range",
     "weighted_l2_norm", "errors", "Error", "InvalidGrid", "InvalidLevel", "ShapeError",
     "InvalidFusion", "SingularSystem", "TooManyWorkers", "WorkerFailure", "CorruptFile",

@@ -1,0 +1,328 @@
+// gen4.cuh -- 4-D levels (spatiotemporal grids).
+//
+// The 3-D family (lean.cuh, kernels*.cuh) is tiled for three dimensions;
+// a fourth (the stacked time axis of decompose_spatiotemporal,
+// refactor.hpp:536-567) goes through this generic path instead.  Every
+// step of a level is one element-parallel pass over a compact lattice:
+//
+//   decompose  coef   : W = u - interp(u) at nodes fine in any dim, 0 at
+//                       all-coarse nodes (gpk_sweep + the vec(C) mask of
+//                       masstrans_dim0, refactor.hpp:251-307), fused with
+//                       the class store (class_slot, grid.hpp:149-164)
+//              mass d : W (dims < d coarse, dims >= d fine) -> R*M along d
+//                       (masstrans_window, kernels.hpp:158-185); one pass per
+//                       dimension that refines, ping-pong between buffers
+//              solve d: Thomas along d on the coarse lattice
+//                       (thomas_fiber, kernels.hpp:143-151), in place
+//              apply  : a_{l-1}[i] = a_l[off(i)] + z[i]  (refactor.hpp:380-399)
+//   recompose  load   : W = class value at fine nodes, 0 elsewhere
+//              mass/solve as above, then a' = a_{l-1} - z  (refactor.hpp:404-422)
+//              rgpk   : out = a' at coarse nodes, interp(a') + class at fine
+//                       nodes (scatter_class + inverse gpk_sweep)
+//
+// All arithmetic is the reference expression through the _rn intrinsics, so
+// both policies are bit-identical to the reference on 4-D grids (the FAST
+// tolerance is met trivially).  The lattices are compact and dim-0-fastest,
+// so each pass reads and writes unit-stride along dim 0; the Thomas pass for
+// d > 0 has consecutive threads on consecutive fibers (coalesced).
+#pragma once
+
+#include <cstdint>
+
+#include "common.cuh"
+
+namespace mgrg {
+
+constexpr int kGenDims = 4;
+
+template <typename R> struct Gen4Geom {
+  uint32_t n[kGenDims];            // level-l extents
+  uint32_t m[kGenDims];            // level-(l-1) extents
+  const R *h[kGenDims];            // level-l spacings (grid.cpp:60-65)
+  const R *r[kGenDims];            // level-l ratios (grid.cpp:66-71)
+  const R *th[kGenDims];           // level-(l-1) Thomas factors (kernels.hpp:107-135),
+  const R *tf[kGenDims];           // null where the dimension does not refine
+  const R *ti[kGenDims];
+  uint64_t tbase[1 << kGenDims];   // class type bases (grid.cpp:151-162)
+  uint32_t cext[1 << kGenDims][kGenDims]; // class type extents
+
+  __host__ __device__ uint64_t nodes() const {
+    return uint64_t(n[0]) * n[1] * n[2] * n[3];
+  }
+  __host__ __device__ uint64_t coarse_nodes() const {
+    return uint64_t(m[0]) * m[1] * m[2] * m[3];
+  }
+};
+
+__device__ __forceinline__ void gen_decode(uint64_t i, const uint32_t *e, uint32_t *p) {
+#pragma unroll
+  for (int d = 0; d < kGenDims; ++d) {
+    p[d] = uint32_t(i % e[d]);
+    i /= e[d];
+  }
+}
+
+template <typename R>
+__device__ __forceinline__ unsigned gen_mask(const Gen4Geom<R> &g, const uint32_t *p) {
+  unsigned mask = 0;
+#pragma unroll
+  for (int d = 0; d < kGenDims; ++d)
+    if (!is_coarse(p[d], g.n[d]))
+      mask |= 1u << d;
+  return mask;
+}
+
+// class_slot (grid.hpp:149-164)
+template <typename R>
+__device__ __forceinline__ uint64_t gen_slot(const Gen4Geom<R> &g, const uint32_t *p,
+                                             unsigned mask) {
+  uint64_t idx = 0, mult = 1;
+#pragma unroll
+  for (int d = 0; d < kGenDims; ++d) {
+    const uint32_t w = ((mask >> d) & 1) ? fine_rank(p[d]) : coarse_rank(p[d]);
+    idx += w * mult;
+    mult *= g.cext[mask][d];
+  }
+  return g.tbase[mask] + idx;
+}
+
+// interpolate_node (kernels.hpp:193-223): corners at p +- 1 along the fine
+// dims (bit q of the corner id -> +1 on the q-th fine dim), reduced pairwise
+// a + t*(b - a), lowest fine dim first.  `at(q)` reads the level-l value at
+// lattice position q (all corners are coarse nodes).
+template <typename R, typename At>
+__device__ R gen_interp(const Gen4Geom<R> &g, const uint32_t *p, unsigned mask, At &&at) {
+  int fd[kGenDims];
+  int k = 0;
+#pragma unroll
+  for (int d = 0; d < kGenDims; ++d)
+    if ((mask >> d) & 1)
+      fd[k++] = d;
+  R corner[1 << kGenDims];
+  for (int c = 0; c < (1 << k); ++c) {
+    uint32_t q[kGenDims];
+#pragma unroll
+    for (int d = 0; d < kGenDims; ++d)
+      q[d] = p[d];
+    for (int b = 0; b < k; ++b)
+      q[fd[b]] = ((c >> b) & 1) ? p[fd[b]] + 1 : p[fd[b]] - 1;
+    corner[c] = at(q);
+  }
+  int width = 1 << k;
+  for (int b = 0; b < k; ++b) {
+    const int d = fd[b];
+    const R t = g.r[d][p[d] - 1];
+    width >>= 1;
+    for (int i = 0; i < width; ++i)
+      corner[i] = lerp(corner[2 * i], corner[2 * i + 1], t);
+  }
+  return corner[0];
+}
+
+template <typename R>
+__device__ __forceinline__ uint64_t gen_lattice_off(const Gen4Geom<R> &g, const uint32_t *q) {
+  return q[0] + uint64_t(g.n[0]) * (q[1] + uint64_t(g.n[1]) * (q[2] + uint64_t(g.n[2]) * q[3]));
+}
+
+// decompose: coefficients + vec(C) field + class store
+template <typename R>
+__global__ void gen_coef_kernel(Gen4Geom<R> g, const R *__restrict__ a, R *__restrict__ W,
+                                R *__restrict__ cls) {
+  const uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= g.nodes())
+    return;
+  uint32_t p[kGenDims];
+  gen_decode(i, g.n, p);
+  const unsigned mask = gen_mask(g, p);
+  if (!mask) {
+    W[i] = R(0);
+    return;
+  }
+  const R ip = gen_interp(g, p, mask, [&](const uint32_t *q) { return a[gen_lattice_off(g, q)]; });
+  const R coef = sub(a[i], ip);
+  W[i] = coef;
+  cls[gen_slot(g, p, mask)] = coef;
+}
+
+// recompose: vec(C) field from the class (null class = zeros)
+template <typename R>
+__global__ void gen_load_kernel(Gen4Geom<R> g, const R *__restrict__ cls, R *__restrict__ W) {
+  const uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= g.nodes())
+    return;
+  uint32_t p[kGenDims];
+  gen_decode(i, g.n, p);
+  const unsigned mask = gen_mask(g, p);
+  W[i] = (mask && cls) ? cls[gen_slot(g, p, mask)] : R(0);
+}
+
+// R*M along dim d: input extents e (e[d] = n[d]), output extents e with
+// e[d] = m[d]; one thread per output node
+template <typename R>
+__global__ void gen_mass_kernel(Gen4Geom<R> g, int d, uint4 e4, const R *__restrict__ in,
+                                R *__restrict__ out) {
+  const uint32_t e[kGenDims] = {e4.x, e4.y, e4.z, e4.w};
+  uint32_t oe[kGenDims] = {e4.x, e4.y, e4.z, e4.w};
+  const uint32_t n = g.n[d];
+  oe[d] = g.m[d];
+  const uint64_t total = uint64_t(oe[0]) * oe[1] * oe[2] * oe[3];
+  const uint64_t o = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (o >= total)
+    return;
+  uint32_t p[kGenDims];
+  gen_decode(o, oe, p);
+  uint64_t base = 0, str = 1, sd = 1;
+#pragma unroll
+  for (int k = 0; k < kGenDims; ++k) {
+    if (k == d)
+      sd = str;
+    else
+      base += p[k] * str;
+    str *= e[k];
+  }
+  const uint32_t q = coarse_pos(p[d], n);
+  out[o] = masstrans_at<R>([&](uint32_t j) { return in[base + j * sd]; }, q, n, g.h[d], g.r[d]);
+}
+
+// Thomas along dim d of the compact coarse lattice, in place; one thread per
+// fiber (thomas_fiber, kernels.hpp:143-151)
+template <typename R>
+__global__ void gen_thomas_kernel(Gen4Geom<R> g, int d, R *__restrict__ f) {
+  const uint32_t mm = g.m[d];
+  const uint64_t fibers = g.coarse_nodes() / mm;
+  const uint64_t t = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (t >= fibers)
+    return;
+  uint64_t rest = t, base = 0, str = 1, sd = 1;
+#pragma unroll
+  for (int k = 0; k < kGenDims; ++k) {
+    if (k == d) {
+      sd = str;
+    } else {
+      base += (rest % g.m[k]) * str;
+      rest /= g.m[k];
+    }
+    str *= g.m[k];
+  }
+  R *v = f + base;
+  const R *h = g.th[d], *fwd = g.tf[d], *ip = g.ti[d];
+  R prev = v[0];
+  for (uint32_t i = 1; i < mm; ++i) {
+    const R x = add(v[i * sd], mul(fwd[i], prev));
+    v[i * sd] = x;
+    prev = x;
+  }
+  R next = mul(prev, ip[mm - 1]);
+  v[(mm - 1) * sd] = next;
+  for (uint32_t i = mm - 1; i-- > 0;) {
+    const R x = mul(sub(v[i * sd], mul(h[i], next)), ip[i]);
+    v[i * sd] = x;
+    next = x;
+  }
+}
+
+// decompose apply_pack: P[i] = a[off(i)] + z[i]
+template <typename R>
+__global__ void gen_apply_kernel(Gen4Geom<R> g, const R *__restrict__ a,
+                                 const R *__restrict__ z, R *__restrict__ P) {
+  const uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= g.coarse_nodes())
+    return;
+  uint32_t c[kGenDims], q[kGenDims];
+  gen_decode(i, g.m, c);
+#pragma unroll
+  for (int d = 0; d < kGenDims; ++d)
+    q[d] = coarse_pos(c[d], g.n[d]);
+  P[i] = add(a[gen_lattice_off(g, q)], z[i]);
+}
+
+// recompose unapply_expand on the compact coarse lattice: z <- prev - z
+template <typename R>
+__global__ void gen_unapply_kernel(uint64_t count, const R *__restrict__ prev, R *__restrict__ z) {
+  const uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i < count)
+    z[i] = sub(prev[i], z[i]);
+}
+
+// recompose: scatter_class + inverse gpk_sweep from the corrected coarse
+// lattice cz (compact, level-(l-1) extents)
+template <typename R>
+__global__ void gen_rgpk_kernel(Gen4Geom<R> g, const R *__restrict__ cz,
+                                const R *__restrict__ cls, R *__restrict__ out) {
+  const uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= g.nodes())
+    return;
+  uint32_t p[kGenDims];
+  gen_decode(i, g.n, p);
+  const unsigned mask = gen_mask(g, p);
+  auto at = [&](const uint32_t *q) {
+    return cz[coarse_rank(q[0]) +
+              uint64_t(g.m[0]) * (coarse_rank(q[1]) +
+                                  uint64_t(g.m[1]) * (coarse_rank(q[2]) +
+                                                      uint64_t(g.m[2]) * coarse_rank(q[3])))];
+  };
+  if (!mask) {
+    out[i] = at(p);
+    return;
+  }
+  const R ip = gen_interp(g, p, mask, at);
+  out[i] = add(ip, cls ? cls[gen_slot(g, p, mask)] : R(0));
+}
+
+// unit-level compute_coefficients / restore_coefficients in place
+// (kernels.hpp:284-310): corners are coarse nodes, never written
+template <typename R>
+__global__ void gen_gpk_inplace_kernel(Gen4Geom<R> g, R *a, int inverse) {
+  const uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= g.nodes())
+    return;
+  uint32_t p[kGenDims];
+  gen_decode(i, g.n, p);
+  const unsigned mask = gen_mask(g, p);
+  if (!mask)
+    return;
+  const R ip = gen_interp(g, p, mask, [&](const uint32_t *q) { return a[gen_lattice_off(g, q)]; });
+  a[i] = inverse ? add(ip, a[i]) : sub(a[i], ip);
+}
+
+// unit-level masstrans_apply along dim 0 (kernels.hpp:328-412): the vec(C)
+// input (all-coarse nodes as 0) and the optional fused class copy
+template <typename R>
+__global__ void gen_vecc_kernel(Gen4Geom<R> g, const R *__restrict__ in, R *__restrict__ W,
+                                R *__restrict__ coef) {
+  const uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= g.nodes())
+    return;
+  uint32_t p[kGenDims];
+  gen_decode(i, g.n, p);
+  const unsigned mask = gen_mask(g, p);
+  const R x = in[i];
+  W[i] = mask ? x : R(0);
+  if (mask && coef)
+    coef[gen_slot(g, p, mask)] = x;
+}
+
+// reorder / to_natural (grid.hpp:177-196): coarse-first index of natural
+// node i is its coarse rank (all-coarse nodes) or C + its class slot
+template <typename R>
+__global__ void gen_reorder_kernel(Gen4Geom<R> g, int to_natural, const R *__restrict__ in,
+                                   R *__restrict__ out) {
+  const uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= g.nodes())
+    return;
+  uint32_t p[kGenDims];
+  gen_decode(i, g.n, p);
+  const unsigned mask = gen_mask(g, p);
+  const uint64_t k =
+      mask ? g.coarse_nodes() + gen_slot(g, p, mask)
+           : coarse_rank(p[0]) +
+                 uint64_t(g.m[0]) * (coarse_rank(p[1]) +
+                                     uint64_t(g.m[1]) * (coarse_rank(p[2]) +
+                                                         uint64_t(g.m[2]) * coarse_rank(p[3])));
+  if (to_natural)
+    out[i] = in[k];
+  else
+    out[k] = in[i];
+}
+
+} // namespace mgrg

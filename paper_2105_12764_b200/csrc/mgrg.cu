@@ -32,6 +32,7 @@
 #include "kernels4.cuh"
 #include "lean.cuh"
 #include "thomas_fiber.cuh"
+#include "gen4.cuh"
 
 using namespace mgrg;
 
@@ -89,9 +90,6 @@ mgrg_status build_hierarchy(const mgrg_grid_desc &desc, Hierarchy &H) {
   if (nd < 1 || nd > 4)
     return fail(MGRG_INVALID_GRID, "grid must have 1..4 dimensions, got " +
                                        std::to_string(nd));
-  if (nd == 4)
-    return fail(MGRG_UNSUPPORTED,
-                "4-D (spatiotemporal) grids are outside this path's scope");
   H.nd = nd;
   std::vector<std::vector<double>> coords(nd);
   const double *cp = desc.coords;
@@ -185,6 +183,7 @@ template <typename R> struct PlanT {
   std::vector<std::array<const Stencil<R> *, 3>> sten; // [l][kd] merged R*M tables
   std::vector<std::array<const LeanW<R> *, 3>> lean;   // [l][kd] lean tables (padded)
   std::vector<std::array<ThomasLean<R>, 3>> tlean;     // [l][kd] chunked Thomas tables
+  std::vector<Gen4Geom<R>> g4;                         // [l] 4-D levels (gen4.cuh)
   R *d_geom = nullptr;
 };
 
@@ -206,6 +205,8 @@ struct mgrg_plan {
   bool fast = false;      // MGRG_FLAG_FAST: FMA arithmetic policy
   uint32_t zchunk = 32;
   bool lean = false;      // dyadic x/y(/z) refinement: lean warp-tiled kernels (lean.cuh)
+  bool gen = false;       // 4-D grid: generic per-pass kernels (gen4.cuh)
+  uint64_t offW = 0, offW2 = 0; // gen: two level-L lattices (vec(C) field, mass ping-pong)
   mgrg_status deferred = MGRG_OK;         // SingularSystem found at build time
   std::string deferred_msg;
   PlanT<float> pf;
@@ -507,6 +508,82 @@ template <typename R> mgrg_status upload_geometry(mgrg_plan *p) {
                           : reinterpret_cast<const LeanW<R> *>(base + refs[l].lw[kd]);
     }
     fill_layout(g);
+  }
+  return MGRG_OK;
+}
+
+// 4-D plans (gen4.cuh): per level the spacings/ratios of every dimension,
+// the level-(l-1) Thomas factors of the refining ones and the class layout
+// (make_class_layout, grid.cpp:140-165) over all four dimensions.
+template <typename R> mgrg_status upload_geometry_gen(mgrg_plan *p) {
+  const Hierarchy &H = p->H;
+  const int L = H.L;
+  std::vector<R> buf;
+  auto push = [&](const std::vector<R> &v) {
+    size_t off = buf.size();
+    buf.insert(buf.end(), v.begin(), v.end());
+    buf.resize((buf.size() + 31) & ~size_t(31), R(0));
+    return off;
+  };
+  constexpr size_t kNone = size_t(-1);
+  struct Ref {
+    size_t h[kGenDims], r[kGenDims], th[kGenDims], tf[kGenDims], ti[kGenDims];
+  };
+  std::vector<Ref> refs(L + 1);
+  for (int l = 1; l <= L; ++l)
+    for (int d = 0; d < kGenDims; ++d) {
+      Ref &f = refs[l];
+      f.h[d] = f.r[d] = f.th[d] = f.tf[d] = f.ti[d] = kNone;
+      std::vector<R> h(H.h[d][l].begin(), H.h[d][l].end());
+      std::vector<R> r(H.r[d][l].begin(), H.r[d][l].end());
+      f.h[d] = push(h);
+      f.r[d] = push(r);
+      if (H.ext[l - 1][d] < H.ext[l][d]) {
+        std::vector<R> th, tf, ti;
+        std::string err;
+        if (!thomas_factors<R>(H.h[d][l - 1], th, tf, ti, err) && p->deferred == MGRG_OK) {
+          p->deferred = MGRG_SINGULAR_SYSTEM;
+          p->deferred_msg = err;
+        }
+        if (th.empty())
+          th.push_back(R(0));
+        f.th[d] = push(th);
+        f.tf[d] = push(tf);
+        f.ti[d] = push(ti);
+      }
+    }
+  if (buf.empty())
+    buf.resize(32, R(0));
+  p->geom_bytes = buf.size() * sizeof(R);
+  CUDA_TRY(cudaMalloc(&p->d_geom, p->geom_bytes));
+  CUDA_TRY(cudaMemcpy(p->d_geom, buf.data(), p->geom_bytes, cudaMemcpyHostToDevice));
+  const R *base = static_cast<const R *>(p->d_geom);
+  auto at = [&](size_t o) { return o == kNone ? nullptr : base + o; };
+  PlanT<R> &P = pt<R>(p);
+  P.g4.assign(L + 1, Gen4Geom<R>{});
+  for (int l = 1; l <= L; ++l) {
+    Gen4Geom<R> &g = P.g4[l];
+    for (int d = 0; d < kGenDims; ++d) {
+      g.n[d] = uint32_t(H.ext[l][d]);
+      g.m[d] = uint32_t(H.ext[l - 1][d]);
+      g.h[d] = at(refs[l].h[d]);
+      g.r[d] = at(refs[l].r[d]);
+      g.th[d] = at(refs[l].th[d]);
+      g.tf[d] = at(refs[l].tf[d]);
+      g.ti[d] = at(refs[l].ti[d]);
+    }
+    uint64_t off = 0;
+    g.tbase[0] = 0;
+    for (unsigned mask = 1; mask < (1u << kGenDims); ++mask) {
+      uint64_t count = 1;
+      for (int d = 0; d < kGenDims; ++d) {
+        const uint64_t n = g.n[d];
+        g.cext[mask][d] = uint32_t(((mask >> d) & 1) ? n - coarse_extent(n) : coarse_extent(n));
+        count *= g.cext[mask][d];
+      }
+      g.tbase[mask] = off;
+      off += count;
+    }
   }
   return MGRG_OK;
 }
@@ -897,9 +974,121 @@ mgrg_status Recorder::end() {
   return MGRG_OK;
 }
 
+// ---- 4-D levels (gen4.cuh) -------------------------------------------------
+
+inline unsigned gen_blocks(uint64_t n) { return unsigned((n + 255) / 256); }
+
+// R*M along every refining dimension, dims ascending (masstrans_dim0 then
+// masstrans_later, refactor.hpp:251-346), ping-pong between W and W2;
+// returns the buffer holding the load vector on the coarse lattice
+template <typename R>
+R *gen_mass_all(mgrg_plan *p, const Gen4Geom<R> &g, int l, Recorder &rec, cudaStream_t s,
+                mgrg_status &st) {
+  R *cur = ws<R>(p, p->offW), *oth = ws<R>(p, p->offW2);
+  uint32_t e[kGenDims] = {g.n[0], g.n[1], g.n[2], g.n[3]};
+  for (int d = 0; d < kGenDims; ++d) {
+    if (!(g.m[d] < g.n[d]))
+      continue;
+    uint64_t out = 1;
+    for (int k = 0; k < kGenDims; ++k)
+      out *= k == d ? g.m[d] : e[k];
+    if ((st = rec.begin(MGRG_K_DEC_LEVEL, l, 0)))
+      return nullptr;
+    gen_mass_kernel<R><<<gen_blocks(out), 256, 0, s>>>(g, d, make_uint4(e[0], e[1], e[2], e[3]),
+                                                       cur, oth);
+    if ((st = rec.end()))
+      return nullptr;
+    e[d] = g.m[d];
+    std::swap(cur, oth);
+  }
+  // Thomas along every refining dimension, in place on the coarse lattice
+  for (int d = 0; d < kGenDims; ++d) {
+    if (!(g.m[d] < g.n[d]))
+      continue;
+    if ((st = rec.begin(MGRG_K_THOMAS_X + std::min(d, 2), l, 0)))
+      return nullptr;
+    gen_thomas_kernel<R><<<gen_blocks(g.coarse_nodes() / g.m[d]), 256, 0, s>>>(g, d, cur);
+    if ((st = rec.end()))
+      return nullptr;
+  }
+  return cur;
+}
+
+template <typename R>
+mgrg_status run_gen_decompose(mgrg_plan *p, const R *d_in, R *d_cls, cudaStream_t s) {
+  PlanT<R> &P = pt<R>(p);
+  const int L = p->H.L;
+  Recorder rec{p, s};
+  mgrg_status st = MGRG_OK;
+  for (int l = L; l >= 1; --l) {
+    const Gen4Geom<R> &g = P.g4[l];
+    const R *a = l == L ? d_in : level_buf<R>(p, l);
+    R *Pout = l == 1 ? d_cls : level_buf<R>(p, l - 1);
+    R *cls = d_cls + p->nodes[l - 1];
+    if ((st = rec.begin(MGRG_K_DEC_LEVEL, l, 0)))
+      return st;
+    gen_coef_kernel<R><<<gen_blocks(g.nodes()), 256, 0, s>>>(g, a, ws<R>(p, p->offW), cls);
+    if ((st = rec.end()))
+      return st;
+    R *z = gen_mass_all<R>(p, g, l, rec, s, st);
+    if (st)
+      return st;
+    if ((st = rec.begin(MGRG_K_DEC_LEVEL, l, 0)))
+      return st;
+    gen_apply_kernel<R><<<gen_blocks(g.coarse_nodes()), 256, 0, s>>>(g, a, z, Pout);
+    if ((st = rec.end()))
+      return st;
+  }
+  CUDA_TRY(cudaGetLastError());
+  p->last_launches = rec.launches;
+  return MGRG_OK;
+}
+
+template <typename R>
+mgrg_status run_gen_recompose(mgrg_plan *p, const R *d_cls, int k, R *d_out, cudaStream_t s) {
+  PlanT<R> &P = pt<R>(p);
+  const int L = p->H.L;
+  Recorder rec{p, s};
+  mgrg_status st = MGRG_OK;
+  for (int l = 1; l <= L; ++l) {
+    const Gen4Geom<R> &g = P.g4[l];
+    const R *prev = l == 1 ? d_cls : level_buf<R>(p, l - 1);
+    R *out = l == L ? d_out : level_buf<R>(p, l);
+    const R *cls = l <= k ? d_cls + p->nodes[l - 1] : nullptr;
+    const R *cz = prev; // classes above k are zero: z = +0, a' = a_{l-1} exactly
+    if (cls) {
+      if ((st = rec.begin(MGRG_K_REC_LOAD, l, 0)))
+        return st;
+      gen_load_kernel<R><<<gen_blocks(g.nodes()), 256, 0, s>>>(g, cls, ws<R>(p, p->offW));
+      if ((st = rec.end()))
+        return st;
+      R *z = gen_mass_all<R>(p, g, l, rec, s, st);
+      if (st)
+        return st;
+      if ((st = rec.begin(MGRG_K_REC_LOAD, l, 0)))
+        return st;
+      gen_unapply_kernel<R><<<gen_blocks(g.coarse_nodes()), 256, 0, s>>>(g.coarse_nodes(), prev,
+                                                                          z);
+      if ((st = rec.end()))
+        return st;
+      cz = z;
+    }
+    if ((st = rec.begin(MGRG_K_REC_GPK, l, 0)))
+      return st;
+    gen_rgpk_kernel<R><<<gen_blocks(g.nodes()), 256, 0, s>>>(g, cz, cls, out);
+    if ((st = rec.end()))
+      return st;
+  }
+  CUDA_TRY(cudaGetLastError());
+  p->last_launches = rec.launches;
+  return MGRG_OK;
+}
+
 template <typename R>
 mgrg_status run_decompose(mgrg_plan *p, const R *d_in, R *d_cls, cudaStream_t s,
                           bool top_done = false) {
+  if (p->gen)
+    return run_gen_decompose<R>(p, d_in, d_cls, s);
   PlanT<R> &P = pt<R>(p);
   const int L = p->H.L;
   R *F = ws<R>(p, p->offF);
@@ -959,6 +1148,8 @@ mgrg_status run_decompose(mgrg_plan *p, const R *d_in, R *d_cls, cudaStream_t s,
 template <typename R>
 mgrg_status run_recompose(mgrg_plan *p, const R *d_cls, int k, R *d_out,
                           cudaStream_t s) {
+  if (p->gen)
+    return run_gen_recompose<R>(p, d_cls, k, d_out, s);
   PlanT<R> &P = pt<R>(p);
   const int L = p->H.L;
   R *F = ws<R>(p, p->offF);
@@ -1087,6 +1278,38 @@ mgrg_status mgrg_plan_create(const mgrg_grid_desc *desc, mgrg_plan **out) {
     return st;
   const Hierarchy &H = p->H;
   const int nd = H.nd, L = H.L;
+  auto al = [](uint64_t n) { return (n + 63) & ~uint64_t(63); };
+  if (nd == 4) {
+    // 4-D: generic per-pass kernels (gen4.cuh); both policies bit-exact
+    p->gen = true;
+    p->fast = (desc->flags & MGRG_FLAG_FAST) != 0;
+    p->kext.assign(L + 1, {1, 1, 1});
+    p->nodes.assign(L + 1, 1);
+    for (int l = 0; l <= L; ++l)
+      for (int d = 0; d < nd; ++d)
+        p->nodes[l] *= H.ext[l][d];
+    DeviceGuard guard(p->device);
+    mgrg_status st = p->dtype == MGRG_F32 ? upload_geometry_gen<float>(p.get())
+                                          : upload_geometry_gen<double>(p.get());
+    if (st)
+      return st;
+    // workspace: A = N_{L-1}, B = N_{L-2} (level ping-pong), W, W2 = N_L
+    const uint64_t nA = p->nodes[L - 1], nB = L >= 2 ? p->nodes[L - 2] : 1;
+    p->offA = 0;
+    p->offB = al(nA);
+    p->offW = p->offB + al(nB);
+    p->offW2 = p->offW + al(p->nodes[L]);
+    p->offF = p->offW2;
+    p->ws_bytes = (p->offW2 + al(p->nodes[L])) * p->esize;
+    cudaError_t e = cudaMalloc(&p->d_ws, p->ws_bytes);
+    if (e != cudaSuccess) {
+      cudaFree(p->d_geom);
+      return fail(e == cudaErrorMemoryAllocation ? MGRG_OUT_OF_MEMORY : MGRG_CUDA_ERROR,
+                  std::string("workspace allocation: ") + cudaGetErrorString(e));
+    }
+    *out = p.release();
+    return MGRG_OK;
+  }
   // kernel dims: user dims in order, padded to 3
   for (int kd = 0; kd < 3; ++kd)
     p->kmap[kd] = kd < nd ? kd : -1;
@@ -1133,7 +1356,6 @@ mgrg_status mgrg_plan_create(const mgrg_grid_desc *desc, mgrg_plan **out) {
   // workspace: A = N_{L-1}, B = N_{L-2}, F = N_{L-1}
   const uint64_t nA = p->nodes[L - 1];
   const uint64_t nB = L >= 2 ? p->nodes[L - 2] : 1;
-  auto al = [](uint64_t n) { return (n + 63) & ~uint64_t(63); };
   p->offA = 0;
   p->offB = al(nA);
   p->offF = p->offB + al(nB);
@@ -1414,6 +1636,8 @@ mgrg_status decompose_host_pipelined(mgrg_plan *p, const R *h_in, R *h_cls) {
 }
 
 template <typename R> bool pipelined_ok(mgrg_plan *p) {
+  if (p->gen)
+    return false;
   const int L = p->H.L;
   const LevelGeom<R> &g = pt<R>(p).geom[L];
   return p->fast && p->lean && p->refine == 7u && lean_level(g) && g.n[2] > 1 &&
@@ -1487,6 +1711,13 @@ static mgrg_status check_level(const mgrg_plan *p, int32_t level) {
 extern "C++" {
 template <typename R>
 static mgrg_status gpk_t(mgrg_plan *p, int level, int inverse, void *d, cudaStream_t s) {
+  if (p->gen) {
+    const Gen4Geom<R> &g = pt<R>(p).g4[level];
+    gen_gpk_inplace_kernel<R><<<gen_blocks(g.nodes()), 256, 0, s>>>(g, static_cast<R *>(d),
+                                                                    inverse);
+    CUDA_TRY(cudaGetLastError());
+    return MGRG_OK;
+  }
   const LevelGeom<R> &g = pt<R>(p).geom[level];
   const uint64_t n = g.nodes();
   gpk_inplace_kernel<R><<<unsigned((n + 255) / 256), 256, 0, s>>>(g, static_cast<R *>(d),
@@ -1514,6 +1745,32 @@ extern "C++" {
 template <typename R>
 static mgrg_status masstrans_t(mgrg_plan *p, int level, int kd, const void *in, void *out,
                                int fused, void *coef, cudaStream_t s) {
+  if (p->gen) {
+    // input extents: dims < kd coarse, dims >= kd level-l (kernels.hpp:340-352)
+    const Gen4Geom<R> &g = pt<R>(p).g4[level];
+    uint32_t e[kGenDims];
+    uint64_t ein = 1, eout = 1;
+    for (int d = 0; d < kGenDims; ++d) {
+      e[d] = d < kd ? g.m[d] : g.n[d];
+      ein *= e[d];
+      eout *= d == kd ? g.m[d] : e[d];
+    }
+    const R *src = static_cast<const R *>(in);
+    if (!(g.m[kd] < g.n[kd])) { // identity transfer (kernels.hpp:351-354)
+      CUDA_TRY(cudaMemcpyAsync(out, src, ein * sizeof(R), cudaMemcpyDeviceToDevice, s));
+      return MGRG_OK;
+    }
+    if (kd == 0) {
+      R *W = ws<R>(p, p->offW);
+      gen_vecc_kernel<R><<<gen_blocks(g.nodes()), 256, 0, s>>>(
+          g, src, W, fused ? static_cast<R *>(coef) : nullptr);
+      src = W;
+    }
+    gen_mass_kernel<R><<<gen_blocks(eout), 256, 0, s>>>(
+        g, kd, make_uint4(e[0], e[1], e[2], e[3]), src, static_cast<R *>(out));
+    CUDA_TRY(cudaGetLastError());
+    return MGRG_OK;
+  }
   const LevelGeom<R> &g = pt<R>(p).geom[level];
   uint32_t e[3];
   for (int d = 0; d < 3; ++d)
@@ -1555,6 +1812,15 @@ mgrg_status mgrg_masstrans(mgrg_plan *p, int32_t level, int32_t dim, const void 
 extern "C++" {
 template <typename R>
 static mgrg_status solve_t(mgrg_plan *p, int level, int kd, void *f, cudaStream_t s) {
+  if (p->gen) {
+    const Gen4Geom<R> &g = pt<R>(p).g4[level];
+    if (!(g.m[kd] < g.n[kd]))
+      return MGRG_OK; // identity transfer (kernels.hpp:434-435)
+    gen_thomas_kernel<R><<<gen_blocks(g.coarse_nodes() / g.m[kd]), 256, 0, s>>>(
+        g, kd, static_cast<R *>(f));
+    CUDA_TRY(cudaGetLastError());
+    return MGRG_OK;
+  }
   const LevelGeom<R> &g = pt<R>(p).geom[level];
   if (!((g.refine >> kd) & 1))
     return MGRG_OK; // identity transfer (kernels.hpp:434-435)
@@ -1619,6 +1885,18 @@ mgrg_status mgrg_reorder(mgrg_plan *p, int32_t level, int32_t dir, const void *d
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   const uint64_t n = p->nodes[level];
   const unsigned blocks = unsigned((n + 255) / 256);
+  if (p->gen) {
+    if (p->dtype == MGRG_F32)
+      gen_reorder_kernel<float><<<blocks, 256, 0, s>>>(p->pf.g4[level], dir,
+                                                       static_cast<const float *>(d_in),
+                                                       static_cast<float *>(d_out));
+    else
+      gen_reorder_kernel<double><<<blocks, 256, 0, s>>>(p->pd.g4[level], dir,
+                                                        static_cast<const double *>(d_in),
+                                                        static_cast<double *>(d_out));
+    CUDA_TRY(cudaGetLastError());
+    return MGRG_OK;
+  }
   if (p->dtype == MGRG_F32)
     reorder_kernel<float><<<blocks, 256, 0, s>>>(p->pf.geom[level], dir,
                                                  static_cast<const float *>(d_in),

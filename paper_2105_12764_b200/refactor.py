@@ -219,6 +219,39 @@ def decompose(grid: TensorGrid, opt: RefactorOptions | None = None) -> Refactore
                           plan.levels, classes, flat)
 
 
+def decompose_spatiotemporal(snapshots, time_coords,
+                             opt: RefactorOptions | None = None) -> RefactoredData:
+    """mgr::decompose_spatiotemporal (refactor.hpp:536-567): stack the
+    snapshots along a trailing time dimension and decompose the stacked grid
+    (spatial dimensions before the temporal one at every level).  A 3-D
+    snapshot series becomes a 4-D grid (csrc/gen4.cuh)."""
+    if len(snapshots) < 2:
+        raise errors.ShapeError("need at least 2 snapshots")
+    if len(time_coords) != len(snapshots):
+        raise errors.ShapeError("time coordinate count does not match snapshots")
+    first = snapshots[0]
+    if first.ndims() + 1 > kMaxDims:
+        raise errors.InvalidGrid("too many dimensions after stacking time")
+    for s in snapshots:
+        same = tuple(s.shape) == tuple(first.shape) and len(s.coords) == len(first.coords)
+        same = same and all(np.array_equal(np.asarray(a, dtype=np.float64),
+                                           np.asarray(b, dtype=np.float64))
+                            for a, b in zip(s.coords, first.coords))
+        if not same:
+            raise errors.ShapeError("snapshots must share shape and coordinates")
+    shape = tuple(first.shape) + (len(snapshots),)
+    coords = [np.asarray(c, dtype=np.float64) for c in first.coords]
+    coords.append(np.asarray(time_coords, dtype=np.float64))
+    if _is_torch(first.values):
+        import torch
+
+        values = torch.cat([s.values.reshape(-1) for s in snapshots])
+    else:
+        values = np.concatenate([np.asarray(s.values).reshape(-1) for s in snapshots])
+    stacked = make_grid(shape, values, coords, 2)
+    return decompose(stacked, opt)
+
+
 def _all_uniform(g) -> bool:
     for d, n in enumerate(g.shape):
         c = np.asarray(g.coords[d], dtype=np.float64)

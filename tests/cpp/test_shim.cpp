@@ -18,6 +18,8 @@ int mgrref_decompose_f64(int, const uint64_t *, const double *, int, const doubl
                          double *, int *);
 int mgrref_decompose_f32(int, const uint64_t *, const double *, int, const float *,
                          float *, int *);
+int mgrref_spatiotemporal_f64(int, const uint64_t *, const double *, int, const double *,
+                              const double *, double *, int *);
 }
 
 #define CHECK(c)                                                               \
@@ -82,6 +84,41 @@ int main() {
   check_case<float>({65, 40}, true, 2);
   check_case<double>({129}, true, 3);
   check_case<float>({12, 10, 9}, false, 4);
+  check_case<double>({9, 5, 3, 6}, true, 5); // 4-D grids
+  check_case<float>({17, 9, 5, 3}, false, 6);
+  // decompose_spatiotemporal (refactor.hpp:536-567) against the reference's own
+  {
+    const mgr::Shape sh{9, 5, 5};
+    const int T = 5;
+    std::vector<mgr::TensorGrid<double>> snaps;
+    std::vector<double> all, tc;
+    for (int t = 0; t < T; ++t) {
+      std::vector<double> v(9 * 5 * 5);
+      for (std::size_t k = 0; k < v.size(); ++k)
+        v[k] = std::cos(0.05 * double(k) + 0.3 * t);
+      all.insert(all.end(), v.begin(), v.end());
+      snaps.push_back(mgr::make_grid<double>(sh, v));
+      tc.push_back(0.5 * t + 0.1 * t * t);
+    }
+    const auto r = mgr::decompose_spatiotemporal(snaps, tc);
+    std::vector<uint64_t> s64(sh.begin(), sh.end());
+    std::vector<double> ref(all.size());
+    int L = 0;
+    CHECK(mgrref_spatiotemporal_f64(3, s64.data(), nullptr, T, tc.data(), all.data(),
+                                    ref.data(), &L) == 0);
+    CHECK(std::size_t(L) == r.levels);
+    std::size_t off = 0;
+    for (const auto &c : r.classes) {
+      CHECK(std::memcmp(c.data(), ref.data() + off, c.size() * sizeof(double)) == 0);
+      off += c.size();
+    }
+    try {
+      mgr::decompose_spatiotemporal(std::vector<mgr::TensorGrid<double>>{snaps[0]}, {0.0});
+      CHECK(false);
+    } catch (const mgr::ShapeError &e) {
+      CHECK(e.code() == "ShapeError");
+    }
+  }
   // errors keep the reference's types and codes
   try {
     mgr::make_grid<double>({2, 2}, std::vector<double>(4));

@@ -37,7 +37,13 @@ CASES = [
     ((2, 5, 9), True, 0), ((12, 10, 9), False, 0), ((12, 10, 9), True, 0),
     ((17, 9, 5), True, 0), ((17, 17, 17), False, 0), ((17, 17, 17), True, 1),
     ((9, 9, 33), True, 0),
+    # 4-D (the stacked grids of decompose_spatiotemporal, refactor.hpp:536-567)
+    ((5, 5, 5, 5), False, 0), ((9, 5, 3, 6), True, 0), ((6, 7, 9, 10), True, 0),
+    ((17, 9, 5, 3), False, 0), ((9, 9, 9, 9), True, 2), ((5, 3, 2, 9), False, 0),
 ]
+
+# decompose_spatiotemporal series: (snapshot shape, snapshot count, nonuniform)
+ST_CASES = [((9, 5, 5), 5, True), ((17, 9), 3, False), ((5, 5, 5), 2, False)]
 
 
 def main() -> None:
@@ -74,8 +80,27 @@ def main() -> None:
     arrays["fig2_coords"] = np.arange(5, dtype=np.float64)
     arrays["fig2_classes"], _ = oracle.decompose(arrays["fig2_values"], (5,),
                                                  [arrays["fig2_coords"]], impl="ref")
+    # decompose_spatiotemporal of the reference (values snapshot-major)
+    for i, (shape, T, nonuni) in enumerate(ST_CASES):
+        seed = 5000 + 31 * i
+        n = int(np.prod(shape))
+        coords = ([oracle.ref_random_increasing_coords(s, seed + d)
+                   for d, s in enumerate(shape)] if nonuni else None)
+        tc = oracle.ref_random_increasing_coords(T, seed + 9)
+        v64 = oracle.ref_random_vector(n * T, seed)
+        for dt in ("float64", "float32"):
+            v = v64.astype(dt)
+            cls, L = oracle.ref_spatiotemporal(v, shape, tc, coords)
+            arrays[f"st{i}_{dt}_values"] = v
+            arrays[f"st{i}_{dt}_classes"] = cls
+            arrays[f"st{i}_{dt}_levels"] = np.array([L])
+        arrays[f"st{i}_shape"] = np.array(shape, dtype=np.int64)
+        arrays[f"st{i}_time"] = tc
+        if coords is not None:
+            arrays[f"st{i}_coords"] = np.concatenate(coords)
     out = os.path.join(HERE, "refactor_golden.npz")
-    np.savez_compressed(out, ncases=np.array([len(CASES)]), **arrays)
+    np.savez_compressed(out, ncases=np.array([len(CASES)]), nst=np.array([len(ST_CASES)]),
+                        **arrays)
     print(f"wrote {out}: {len(arrays)} arrays, {os.path.getsize(out)} bytes")
 
 

@@ -21,6 +21,7 @@ CASES = [  # (name, shape, dtype, nonuniform)
     ("c2d_f32", (33, 17), "float32", False),
     ("c2d_f64_nonuni", (12, 10), "float64", True),
     ("c1d_f64", (65,), "float64", False),
+    ("c4d_f32_nonuni", (9, 5, 3, 6), "float32", True),
 ]
 
 

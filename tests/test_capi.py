@@ -58,7 +58,6 @@ def _create(shape, dtype=4, coords=None, levels=0):
     ((5, 1), None, 1, "need at least 2"),
     ((), None, 1, "1..4 dimensions"),
     ((5,), [np.array([0.0, 1.0, 1.0, 2.0, 3.0])], 1, "not strictly increasing at index 1"),
-    ((3, 3, 3, 3), None, 14, "4-D"),
 ])
 def test_plan_validation_mirrors_reference(shape, coords, code, msg):
     """validate_grid_geometry (grid.cpp:14-36) -> InvalidGrid, before any

@@ -16,6 +16,7 @@ CASES = [  # (shape, dtype, nonuniform, error bound)
     ((65, 33), "float64", False, 1e-6),
     ((12, 10, 9), "float32", False, 5e-4),
     ((129,), "float64", True, 1e-9),
+    ((9, 5, 5, 5), "float64", False, 1e-4),  # 4-D
 ]
 
 

@@ -14,7 +14,8 @@ import pytest
 from paper_2105_12764_b200 import container, errors
 
 GOLD = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "mgrf")
-NAMES = ["c3d_f64", "c3d_f32_nonuni", "c2d_f32", "c2d_f64_nonuni", "c1d_f64"]
+NAMES = ["c3d_f64", "c3d_f32_nonuni", "c2d_f32", "c2d_f64_nonuni", "c1d_f64",
+         "c4d_f32_nonuni"]
 
 
 def _case(name):
