@@ -148,6 +148,37 @@ mgrg_status mgrg_apply_correction(mgrg_plan *plan, uint64_t count,
 mgrg_status mgrg_reorder(mgrg_plan *plan, int32_t level, int32_t direction,
                          const void *d_in, void *d_out, void *stream);
 
+/* ---- cooperative multi-GPU decompose ----------------
+ * cooperative_decompose (parallel.hpp:227-230, parallel_impl.hpp:691-808):
+ * every worker (one GPU, one plan for the WHOLE grid) owns a z slab of the
+ * level lattices and runs these steps in lockstep with its neighbours; the
+ * host (paper_2105_12764_b200/coop.py) moves the halo planes and the Thomas
+ * carries between GPUs (NCCL send/recv or peer copies).  Results are
+ * bit-identical to mgrg_decompose of the whole grid (exact policy).
+ *
+ * mgrg_coop_level: level `level` (3-D, odd extents, z refining) on coarse
+ * planes [c0, c1): coefficients, class-`level` stores of fine planes
+ * [2c0, 2c1), packed coarse values, the load vector, and its x and y
+ * solves.  Reads fine planes [2c0-2, 2c1] of the level array: d_level is the
+ * caller's finest-level buffer at level L, NULL below (the plan's level
+ * buffer, see mgrg_plan_level_buffer).  c0 (and c1 unless it is the last
+ * coarse plane + 1) must be even multiples of a power of two >= 1.
+ * mgrg_coop_thomas_z: the z solve of coarse planes [c0, c1) for xy fibers
+ * [f0, f1): direction 0 = forward elimination (carry_in = the previous
+ * worker's last forward plane, NULL when c0 == 0; carry_out = this worker's
+ * last forward plane); direction 1 = back substitution fused with apply_pack
+ * (carry_in = the next worker's first solved plane, NULL at the top; carry_out
+ * = this worker's first solved plane).  Carries are full xy planes (m0*m1
+ * elements) indexed by fiber. */
+mgrg_status mgrg_coop_level(mgrg_plan *plan, int32_t level, uint32_t c0, uint32_t c1,
+                            const void *d_level, void *d_classes, void *stream);
+mgrg_status mgrg_coop_thomas_z(mgrg_plan *plan, int32_t level, uint32_t c0, uint32_t c1,
+                               uint64_t f0, uint64_t f1, int32_t direction,
+                               const void *d_carry_in, void *d_carry_out, void *d_classes,
+                               void *stream);
+/* Device pointer of the plan's packed level-`level` buffer (1 <= level < L). */
+mgrg_status mgrg_plan_level_buffer(mgrg_plan *plan, int32_t level, void **d_ptr);
+
 /* ---- diagnostics ------------------------------------------------------- */
 /* Thread-local message of the last failing call ("" if none). */
 const char *mgrg_last_error(void);

@@ -10,6 +10,9 @@ from .errors import (CorruptFile, Error, InvalidBound, InvalidFusion, InvalidGri
                      InvalidLevel, IoError, MissingClass, ShapeError, SingularSystem,
                      TooManyWorkers, WorkerFailure)
 from .plan import Plan
+from .coop import (CommReport, CoopOptions, Partition, PartitionScheme,
+                   cooperative_decompose, grouped_decompose, make_partitions,
+                   split_dims_of)
 from .container import (CompressionReport, CompressResult, DecompressResult, ReadResult,
                         RefactorFileHeader, compress, crc32, decompress, read_refactored,
                         read_refactored_header, write_refactored)
@@ -24,7 +27,8 @@ from .parallel import (BlockShardedRefactor, embarrassing_decompose, embarrassin
 __all__ = [
     "Plan", "TensorGrid", "RefactoredData", "RefactorOptions", "PassStats",
     "LevelPassStats", "PhaseCounters", "ReconstructionReport", "decompose", "recompose",
-    "decompose_spatiotemporal",
+    "decompose_spatiotemporal", "cooperative_decompose", "CoopOptions", "CommReport",
+    "PartitionScheme", "Partition", "make_partitions", "split_dims_of", "grouped_decompose",
     "recompose_with_report", "make_grid", "uniform_coords", "value_range",
     "weighted_l2_norm", "errors", "Error", "InvalidGrid", "InvalidLevel", "ShapeError",
     "InvalidFusion", "SingularSystem", "TooManyWorkers", "WorkerFailure", "CorruptFile",

@@ -24,6 +24,7 @@ EXPORTS = (
     "mgrg_decompose", "mgrg_recompose", "mgrg_decompose_host",
     "mgrg_recompose_host", "mgrg_gpk", "mgrg_masstrans", "mgrg_solve",
     "mgrg_apply_correction", "mgrg_reorder", "mgrg_last_error",
+    "mgrg_coop_level", "mgrg_coop_thomas_z", "mgrg_plan_level_buffer",
     "mgrg_status_name", "mgrg_plan_last_launches", "mgrg_version",
     "mgrg_plan_set_profiling", "mgrg_plan_profile_reset", "mgrg_plan_profile_read",
     "mgrg_crc32", "mgrg_class_crc32", "mgrg_write_refactored", "mgrg_read_refactored",
@@ -67,6 +68,7 @@ def lib() -> ctypes.CDLL:
                 "(the refactoring path has no CPU fallback)")
         L = ctypes.CDLL(LIB_PATH)
         vp, i32, u64 = ctypes.c_void_p, ctypes.c_int32, ctypes.c_uint64
+        u32 = ctypes.c_uint32
         sig = {
             "mgrg_plan_create": [ctypes.POINTER(GridDesc), ctypes.POINTER(vp)],
             "mgrg_plan_destroy": [vp],
@@ -83,6 +85,9 @@ def lib() -> ctypes.CDLL:
             "mgrg_solve": [vp, i32, i32, vp, vp],
             "mgrg_apply_correction": [vp, u64, vp, vp, i32, vp],
             "mgrg_reorder": [vp, i32, i32, vp, vp, vp],
+            "mgrg_coop_level": [vp, i32, u32, u32, vp, vp, vp],
+            "mgrg_coop_thomas_z": [vp, i32, u32, u32, u64, u64, i32, vp, vp, vp, vp],
+            "mgrg_plan_level_buffer": [vp, i32, ctypes.POINTER(ctypes.c_void_p)],
             "mgrg_plan_last_launches": [vp, ctypes.POINTER(u64)],
             "mgrg_plan_set_profiling": [vp, i32],
             "mgrg_plan_profile_reset": [vp],

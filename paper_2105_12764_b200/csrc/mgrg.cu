@@ -1909,6 +1909,179 @@ mgrg_status mgrg_reorder(mgrg_plan *p, int32_t level, int32_t dir, const void *d
   return MGRG_OK;
 }
 
+// ---- cooperative multi-GPU decompose -----------------
+
+} // extern "C"
+
+namespace {
+
+// z solve of one worker's coarse planes for fibers [f0, f1) of the xy plane
+// (thomas_fiber, kernels.hpp:143-151, in the reference's order: bit-exact).
+// dir 0: v[c] += fwd[c] * v[c-1]; carry_out = v[c1-1].  dir 1: v[m-1] *= ip,
+// v[c] = (v[c] - h[c] * v[c+1]) * ip[c], then P[c] += v[c] (apply_pack);
+// carry_out = v[c0].
+template <typename R>
+__global__ void coop_tz_kernel(R *__restrict__ f, R *__restrict__ P, ThomasGeom<R> t,
+                               uint64_t m01, uint32_t c0, uint32_t c1, uint64_t f0,
+                               uint64_t f1, int dir, const R *__restrict__ cin,
+                               R *__restrict__ cout) {
+  const uint64_t xy = f0 + uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (xy >= f1)
+    return;
+  R *v = f + xy;
+  const uint32_t mm = t.m;
+  if (dir == 0) {
+    R prev = cin ? cin[xy] : R(0);
+    for (uint32_t c = c0; c < c1; ++c) {
+      R x = v[c * m01];
+      if (c > 0)
+        x = add(x, mul(t.fwd[c], prev));
+      v[c * m01] = x;
+      prev = x;
+    }
+    if (cout)
+      cout[xy] = prev;
+  } else {
+    R next = cin ? cin[xy] : R(0);
+    for (uint32_t c = c1; c-- > c0;) {
+      R x = v[c * m01];
+      x = c == mm - 1 ? mul(x, t.ip[c]) : mul(sub(x, mul(t.h[c], next)), t.ip[c]);
+      v[c * m01] = x;
+      P[xy + c * m01] = add(P[xy + c * m01], x);
+      next = x;
+    }
+    if (cout)
+      cout[xy] = next;
+  }
+}
+
+template <typename R>
+mgrg_status coop_level_t(mgrg_plan *p, int l, uint32_t c0, uint32_t c1, const R *d_level,
+                         R *d_cls, cudaStream_t s) {
+  PlanT<R> &P = pt<R>(p);
+  const int L = p->H.L;
+  const LevelGeom<R> &g = P.geom[l];
+  if (!(p->lean && p->refine == 7u && lean_level(g)))
+    return fail(MGRG_UNSUPPORTED, "cooperative levels need a 3-D grid with odd extents "
+                                  "refining in every dimension");
+  const uint32_t m2 = g.m[2];
+  if (!(c0 < c1 && c1 <= m2))
+    return fail(MGRG_INVALID_ARGUMENT, "coarse plane range out of bounds");
+  const R *a = l == L ? d_level : level_buf<R>(p, l);
+  if (!a)
+    return fail(MGRG_INVALID_ARGUMENT, "null level array");
+  if ((reinterpret_cast<uintptr_t>(a) & 15) != 0)
+    return fail(MGRG_INVALID_ARGUMENT, "level array must be 16-byte aligned");
+  R *Pout = l == 1 ? d_cls : level_buf<R>(p, l - 1);
+  R *F = ws<R>(p, p->offF);
+  R *cls = d_cls + p->nodes[l - 1];
+  LeanTiles t = lean_tiles<R>(g.m[0], g.m[1], g.m[2], true);
+  uint32_t zc = t.zc;
+  while (zc > 1 && (c0 % zc || (c1 < m2 && c1 % zc)))
+    zc >>= 1;
+  t.zc = zc;
+  t.tz0 = c0 / zc;
+  t.ntz = (c1 - c0 + zc - 1) / zc;
+  const unsigned blocks = unsigned((t.warps() + kLeanWPB - 1) / kLeanWPB);
+  if (p->fast)
+    lean_dec_kernel<R, true, true><<<blocks, 32 * kLeanWPB, lean_dec_smem<R>(), s>>>(
+        g, P.lean[l][0], P.lean[l][1], P.lean[l][2], P.sten[l][0], P.sten[l][1], P.sten[l][2],
+        a, cls, Pout, F, t);
+  else
+    lean_dec_kernel<R, true, false><<<blocks, 32 * kLeanWPB, lean_dec_smem<R>(), s>>>(
+        g, P.lean[l][0], P.lean[l][1], P.lean[l][2], P.sten[l][0], P.sten[l][1], P.sten[l][2],
+        a, cls, Pout, F, t);
+  CUDA_TRY(cudaGetLastError());
+  // x and y solves of the worker's planes: the exact-order kernels on the
+  // sub-lattice (the FAST chunked kernels assume a 16-byte aligned lattice)
+  LevelGeom<R> gs = g;
+  gs.m[2] = c1 - c0;
+  R *Fs = F + uint64_t(c0) * g.m[0] * g.m[1];
+  for (int kd = 0; kd < 2; ++kd)
+    launch_thomas<R>(false, gs, P.thom[l][kd], P.tlean[l][kd], kd, Fs, Epi::none, nullptr,
+                     nullptr, s);
+  CUDA_TRY(cudaGetLastError());
+  return MGRG_OK;
+}
+
+template <typename R>
+mgrg_status coop_tz_t(mgrg_plan *p, int l, uint32_t c0, uint32_t c1, uint64_t f0, uint64_t f1,
+                      int dir, const R *cin, R *cout, R *d_cls, cudaStream_t s) {
+  PlanT<R> &P = pt<R>(p);
+  const LevelGeom<R> &g = P.geom[l];
+  const uint64_t m01 = uint64_t(g.m[0]) * g.m[1];
+  if (!(c0 < c1 && c1 <= g.m[2]) || f1 > m01 || f0 >= f1)
+    return fail(MGRG_INVALID_ARGUMENT, "plane or fiber range out of bounds");
+  R *Pout = l == 1 ? d_cls : level_buf<R>(p, l - 1);
+  R *F = ws<R>(p, p->offF);
+  coop_tz_kernel<R><<<unsigned((f1 - f0 + 255) / 256), 256, 0, s>>>(
+      F, Pout, P.thom[l][2], m01, c0, c1, f0, f1, dir, cin, cout);
+  CUDA_TRY(cudaGetLastError());
+  return MGRG_OK;
+}
+
+} // namespace
+
+extern "C" {
+
+mgrg_status mgrg_coop_level(mgrg_plan *p, int32_t level, uint32_t c0, uint32_t c1,
+                            const void *d_level, void *d_classes, void *stream) {
+  g_last_error.clear();
+  if (mgrg_status st = check_plan(p))
+    return st;
+  if (mgrg_status st = check_level(p, level))
+    return st;
+  if (!d_classes)
+    return fail(MGRG_INVALID_ARGUMENT, "null device buffer");
+  if (p->deferred)
+    return fail(p->deferred, p->deferred_msg);
+  if (p->gen)
+    return fail(MGRG_UNSUPPORTED, "cooperative decompose of 4-D grids");
+  DeviceGuard guard(p->device);
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  return p->dtype == MGRG_F32
+             ? coop_level_t<float>(p, level, c0, c1, static_cast<const float *>(d_level),
+                                   static_cast<float *>(d_classes), s)
+             : coop_level_t<double>(p, level, c0, c1, static_cast<const double *>(d_level),
+                                    static_cast<double *>(d_classes), s);
+}
+
+mgrg_status mgrg_coop_thomas_z(mgrg_plan *p, int32_t level, uint32_t c0, uint32_t c1,
+                               uint64_t f0, uint64_t f1, int32_t direction,
+                               const void *d_carry_in, void *d_carry_out, void *d_classes,
+                               void *stream) {
+  g_last_error.clear();
+  if (mgrg_status st = check_plan(p))
+    return st;
+  if (mgrg_status st = check_level(p, level))
+    return st;
+  if (!d_classes)
+    return fail(MGRG_INVALID_ARGUMENT, "null device buffer");
+  if (p->gen)
+    return fail(MGRG_UNSUPPORTED, "cooperative decompose of 4-D grids");
+  DeviceGuard guard(p->device);
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  return p->dtype == MGRG_F32
+             ? coop_tz_t<float>(p, level, c0, c1, f0, f1, direction,
+                                static_cast<const float *>(d_carry_in),
+                                static_cast<float *>(d_carry_out),
+                                static_cast<float *>(d_classes), s)
+             : coop_tz_t<double>(p, level, c0, c1, f0, f1, direction,
+                                 static_cast<const double *>(d_carry_in),
+                                 static_cast<double *>(d_carry_out),
+                                 static_cast<double *>(d_classes), s);
+}
+
+mgrg_status mgrg_plan_level_buffer(mgrg_plan *p, int32_t level, void **d_ptr) {
+  if (mgrg_status st = check_plan(p))
+    return st;
+  if (level < 1 || level >= p->H.L || !d_ptr)
+    return fail(MGRG_INVALID_ARGUMENT, "level buffer index outside [1, L)");
+  *d_ptr = p->dtype == MGRG_F32 ? static_cast<void *>(level_buf<float>(p, level))
+                                : static_cast<void *>(level_buf<double>(p, level));
+  return MGRG_OK;
+}
+
 } // extern "C"
 
 #include "container.cuh"
