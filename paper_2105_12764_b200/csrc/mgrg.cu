@@ -1147,7 +1147,7 @@ mgrg_status run_decompose(mgrg_plan *p, const R *d_in, R *d_cls, cudaStream_t s,
 
 template <typename R>
 mgrg_status run_recompose(mgrg_plan *p, const R *d_cls, int k, R *d_out,
-                          cudaStream_t s) {
+                          cudaStream_t s, int lmax = -1) {
   if (p->gen)
     return run_gen_recompose<R>(p, d_cls, k, d_out, s);
   PlanT<R> &P = pt<R>(p);
@@ -1155,7 +1155,7 @@ mgrg_status run_recompose(mgrg_plan *p, const R *d_cls, int k, R *d_out,
   R *F = ws<R>(p, p->offF);
   Recorder rec{p, s};
   const uint64_t es = sizeof(R);
-  for (int l = 1; l <= L; ++l) {
+  for (int l = 1; l <= (lmax < 0 ? L : lmax); ++l) {
     const LevelGeom<R> &g = P.geom[l];
     const uint64_t Fn = g.nodes(), Cn = g.coarse_nodes();
     const R *prev = l == 1 ? d_cls : level_buf<R>(p, l - 1);
@@ -1543,11 +1543,17 @@ mgrg_status mgrg_recompose(mgrg_plan *p, const void *d_classes, int32_t k,
                                      static_cast<double *>(d_values), s);
 }
 
+// host-API staging: [in | out] with the second half 256-byte aligned (the
+// lean finest-level kernels store 2-element vectors)
+static uint64_t stage_half(const mgrg_plan *p) {
+  return (p->nodes[p->H.L] + 63) & ~uint64_t(63);
+}
+
 static mgrg_status ensure_stage(mgrg_plan *p) {
   if (p->d_stage)
     return MGRG_OK;
   const uint64_t n = p->nodes[p->H.L];
-  cudaError_t e = cudaMalloc(&p->d_stage, 2 * n * p->esize);
+  cudaError_t e = cudaMalloc(&p->d_stage, (stage_half(p) + n) * p->esize);
   if (e != cudaSuccess)
     return fail(e == cudaErrorMemoryAllocation ? MGRG_OUT_OF_MEMORY : MGRG_CUDA_ERROR,
                 std::string("staging allocation: ") + cudaGetErrorString(e));
@@ -1576,12 +1582,18 @@ mgrg_status decompose_host_pipelined(mgrg_plan *p, const R *h_in, R *h_cls) {
   const int L = p->H.L;
   const LevelGeom<R> &g = P.geom[L];
   const uint64_t N = p->nodes[L], nxy = uint64_t(g.n[0]) * g.n[1];
-  R *din = static_cast<R *>(p->d_stage), *dcls = din + N;
+  R *din = static_cast<R *>(p->d_stage), *dcls = din + stage_half(p);
   R *clsL = dcls + p->nodes[L - 1];
   R *Pout = L == 1 ? dcls : level_buf<R>(p, L - 1);
   R *F = ws<R>(p, p->offF);
   const LeanTiles t = lean_tiles<R>(g.m[0], g.m[1], g.m[2], true);
-  const int G = int(std::min<uint32_t>(t.ntz, 8));
+  // slab groups: 16 measured best on B200 + PCIe 5 (8: 122 ms, 16: 112 ms for
+  // 1025^3 f32); MGRG_PIPE_G overrides (1..16, the event arrays' size)
+  static const int kG = [] {
+    const char *e = std::getenv("MGRG_PIPE_G");
+    return e ? std::max(1, std::min(16, std::atoi(e))) : 16;
+  }();
+  const int G = int(std::min<uint32_t>(t.ntz, uint32_t(kG)));
   const uint32_t n2 = g.n[2], m2 = g.m[2];
   auto chunk0 = [&](int q) { return uint32_t((uint64_t(q) * t.ntz) / G); };
   auto fplane = [&](uint32_t c) { return std::min<uint32_t>(2 * c * t.zc, n2); };
@@ -1635,12 +1647,105 @@ mgrg_status decompose_host_pipelined(mgrg_plan *p, const R *h_in, R *h_cls) {
   return MGRG_OK;
 }
 
-template <typename R> bool pipelined_ok(mgrg_plan *p) {
+// Pipelined host-buffer recompose (dyadic 3-D finest level, all classes):
+// classes 0..L-1 go up first and the coarse levels run while class L goes up
+// in z slab groups; the finest level's load vector is built per group as its
+// pieces (plus one halo rank) land, then the solves, then the finest level is
+// written per group and each group's output planes go down while later
+// groups are still being interpolated.
+template <typename R>
+mgrg_status recompose_host_pipelined(mgrg_plan *p, const R *h_cls, R *h_out) {
+  PlanT<R> &P = pt<R>(p);
+  const int L = p->H.L;
+  const LevelGeom<R> &g = P.geom[L];
+  const uint64_t N = p->nodes[L], nxy = uint64_t(g.n[0]) * g.n[1];
+  R *dcls = static_cast<R *>(p->d_stage), *dout = dcls + stage_half(p);
+  R *F = ws<R>(p, p->offF);
+  const R *prev = L == 1 ? dcls : level_buf<R>(p, L - 1);
+  const R *clsL = dcls + p->nodes[L - 1];
+  const uint32_t m2 = g.m[2], n2 = g.n[2];
+  cudaStream_t sc = p->own_stream;
+  // uploads: classes 0..L-1, then class L by rload chunk groups
+  CUDA_TRY(cudaMemcpyAsync(dcls, h_cls, p->nodes[L - 1] * sizeof(R), cudaMemcpyHostToDevice,
+                           p->s_in));
+  CUDA_TRY(cudaEventRecord(p->ev_done, p->s_in));
+  const LeanTiles tr = lean_rtiles<R>(g.m[0], g.m[1], m2, true);
+  const int G = int(std::min<uint32_t>(tr.ntz, 16));
+  auto rchunk0 = [&](int q) { return uint32_t((uint64_t(q) * tr.ntz) / G); };
+  for (int q = 0; q < G; ++q) {
+    const uint32_t zr0 = rchunk0(q) * tr.zc, zr1 = q == G - 1 ? m2 : rchunk0(q + 1) * tr.zc;
+    for (unsigned ty = 1; ty < 8; ++ty) {
+      const uint32_t nz = (ty & 4) ? m2 - 1 : m2;
+      const uint32_t a = std::min(zr0, nz), b = q == G - 1 ? nz : std::min(zr1, nz);
+      if (b <= a)
+        continue;
+      const uint64_t S = uint64_t(g.tex[ty]) * g.tey[ty];
+      const uint64_t off = p->nodes[L - 1] + g.tbase[ty] + S * a;
+      CUDA_TRY(cudaMemcpyAsync(dcls + off, h_cls + off, S * (b - a) * sizeof(R),
+                               cudaMemcpyHostToDevice, p->s_in));
+    }
+    CUDA_TRY(cudaEventRecord(p->ev_in[q], p->s_in));
+  }
+  // coarse levels as soon as classes 0..L-1 are resident
+  CUDA_TRY(cudaStreamWaitEvent(sc, p->ev_done, 0));
+  if (L > 1)
+    if (mgrg_status st = run_recompose<R>(p, dcls, L, dout, sc, L - 1))
+      return st;
+  // finest load vector per group: chunk range [c0, c1) reads class ranks
+  // c0-1 .. c1 (the next group's first rank)
+  for (int q = 0; q < G; ++q) {
+    CUDA_TRY(cudaStreamWaitEvent(sc, p->ev_in[std::min(q + 1, G - 1)], 0));
+    LeanTiles t = tr;
+    t.tz0 = rchunk0(q);
+    t.ntz = rchunk0(q + 1) - rchunk0(q);
+    if (q == G - 1)
+      t.ntz = tr.ntz - t.tz0;
+    const unsigned blocks = unsigned((t.warps() + kLeanWPB - 1) / kLeanWPB);
+    auto k = p->fast ? lean_rload_kernel<R, true, true> : lean_rload_kernel<R, true, false>;
+    k<<<blocks, 32 * kLeanWPB, 0, sc>>>(g, P.lean[L][0], P.lean[L][1], P.lean[L][2],
+                                        P.sten[L][0], P.sten[L][1], P.sten[L][2], clsL, F, t);
+    CUDA_TRY(cudaGetLastError());
+  }
+  for (int i = 0; i < p->nrefine; ++i) {
+    const int kd = p->refine_dims[i];
+    const bool last = i == p->nrefine - 1;
+    launch_thomas<R>(p->fast, g, P.thom[L][kd], P.tlean[L][kd], kd, F,
+                     last ? Epi::sub : Epi::none, prev, F, sc);
+  }
+  CUDA_TRY(cudaGetLastError());
+  // finest level per group, each group's planes [2c0, 2c1) down at once
+  const LeanTiles tg = lean_gtiles<R>(g.m[0], g.m[1], m2, true);
+  const int H = int(std::min<uint32_t>(tg.ntz, 16));
+  auto gchunk0 = [&](int q) { return uint32_t((uint64_t(q) * tg.ntz) / H); };
+  for (int q = 0; q < H; ++q) {
+    LeanTiles t = tg;
+    t.tz0 = gchunk0(q);
+    t.ntz = (q == H - 1 ? tg.ntz : gchunk0(q + 1)) - t.tz0;
+    const unsigned blocks = unsigned((t.warps() + kLeanWPB - 1) / kLeanWPB);
+    auto k = p->fast ? lean_rgpk_kernel<R, true, true, true>
+                     : lean_rgpk_kernel<R, true, true, false>;
+    k<<<blocks, 32 * kLeanWPB, 0, sc>>>(g, P.lean[L][0], P.lean[L][1], P.lean[L][2], F, clsL,
+                                        dout, t);
+    CUDA_TRY(cudaGetLastError());
+    CUDA_TRY(cudaEventRecord(p->ev_dec[q], sc));
+    CUDA_TRY(cudaStreamWaitEvent(p->s_out, p->ev_dec[q], 0));
+    const uint32_t z0 = std::min<uint32_t>(2 * t.tz0 * tg.zc, n2);
+    const uint32_t z1 = q == H - 1 ? n2 : std::min<uint32_t>(2 * gchunk0(q + 1) * tg.zc, n2);
+    if (z1 > z0)
+      CUDA_TRY(cudaMemcpyAsync(h_out + z0 * nxy, dout + z0 * nxy, (z1 - z0) * nxy * sizeof(R),
+                               cudaMemcpyDeviceToHost, p->s_out));
+  }
+  CUDA_TRY(cudaStreamSynchronize(p->s_out));
+  CUDA_TRY(cudaStreamSynchronize(sc));
+  return MGRG_OK;
+}
+
+template <typename R> bool pipelined_ok(mgrg_plan *p, bool need_fast = true) {
   if (p->gen)
     return false;
   const int L = p->H.L;
   const LevelGeom<R> &g = pt<R>(p).geom[L];
-  return p->fast && p->lean && p->refine == 7u && lean_level(g) && g.n[2] > 1 &&
+  return (p->fast || !need_fast) && p->lean && p->refine == 7u && lean_level(g) && g.n[2] > 1 &&
          p->nodes[L] >= (uint64_t(1) << 22) && g_pipelined_host;
 }
 } // extern "C++"
@@ -1664,7 +1769,7 @@ mgrg_status mgrg_decompose_host(mgrg_plan *p, const void *h_values, void *h_clas
                : decompose_host_pipelined<double>(p, static_cast<const double *>(h_values),
                                                   static_cast<double *>(h_classes));
   const uint64_t bytes = p->nodes[p->H.L] * p->esize;
-  char *din = static_cast<char *>(p->d_stage), *dout = din + bytes;
+  char *din = static_cast<char *>(p->d_stage), *dout = din + stage_half(p) * p->esize;
   CUDA_TRY(cudaMemcpyAsync(din, h_values, bytes, cudaMemcpyHostToDevice, p->own_stream));
   if (mgrg_status st = mgrg_decompose(p, din, dout, p->own_stream))
     return st;
@@ -1688,7 +1793,14 @@ mgrg_status mgrg_recompose_host(mgrg_plan *p, const void *h_classes, int32_t k,
   if (mgrg_status st = ensure_stage(p))
     return st;
   const uint64_t bytes = p->nodes[p->H.L] * p->esize;
-  char *din = static_cast<char *>(p->d_stage), *dout = din + bytes;
+  char *din = static_cast<char *>(p->d_stage), *dout = din + stage_half(p) * p->esize;
+  if (k == p->H.L && p->lean && !p->gen &&
+      (p->dtype == MGRG_F32 ? pipelined_ok<float>(p, false) : pipelined_ok<double>(p, false)))
+    return p->dtype == MGRG_F32
+               ? recompose_host_pipelined<float>(p, static_cast<const float *>(h_classes),
+                                                 static_cast<float *>(h_values))
+               : recompose_host_pipelined<double>(p, static_cast<const double *>(h_classes),
+                                                  static_cast<double *>(h_values));
   // only classes 0..k are read (refactor.hpp:483-485): copy that prefix
   const uint64_t used = p->nodes[k] * p->esize;
   CUDA_TRY(cudaMemcpyAsync(din, h_classes, used, cudaMemcpyHostToDevice, p->own_stream));
