@@ -32,6 +32,7 @@
 #include "kernels4.cuh"
 #include "lean.cuh"
 #include "thomas_fiber.cuh"
+#include "thomas_exact.cuh"
 #include "gen4.cuh"
 
 using namespace mgrg;
@@ -637,6 +638,12 @@ int g_thomas_fiber = [] {
   const char *e = std::getenv("MGRG_TFIBER");
   return e ? std::atoi(e) : 1;
 }();
+// exact-policy resident Thomas (thomas_exact.cuh; MGRG_TEXACT=0 disables,
+// 2 also uses it for y / z fibers)
+int g_thomas_exact = [] {
+  const char *e = std::getenv("MGRG_TEXACT");
+  return e ? std::atoi(e) : 1;
+}();
 // pipelined host-buffer decompose (MGRG_PIPELINE=0 disables)
 int g_pipelined_host = [] {
   const char *e = std::getenv("MGRG_PIPELINE");
@@ -876,6 +883,19 @@ void launch_thomas(bool fast, const LevelGeom<R> &g, const ThomasGeom<R> &t,
     launch_tf<R>(kd, tl, nfib, uint32_t(mx), uint32_t(my), epi, base, out, f, s);
     return;
   }
+  if (!fast && g_thomas_exact && (kd == 0 || g_thomas_exact > 1) && te_fits<R>(kd, t.m) &&
+      (reinterpret_cast<uintptr_t>(f) & 15) == 0) {
+    // exact order, fibers resident in shared memory (thomas_exact.cuh); x
+    // fibers only by default: for y / z the thread-per-fiber streaming kernel
+    // measured faster (0.48 / 0.87 ms vs 0.73 / 1.26 ms at 1025^3 f32)
+    const uint64_t nfib = kd == 0 ? my * mz : (kd == 1 ? mx * mz : mx * my);
+    const unsigned blocks = unsigned((nfib + te_nf<R>() - 1) / te_nf<R>());
+    auto k = kd == 0 ? thomas_exact_kernel<R, 0>
+                     : (kd == 1 ? thomas_exact_kernel<R, 1> : thomas_exact_kernel<R, 2>);
+    k<<<blocks, kTeThreads, te_smem<R>(kd, t.m), s>>>(f, t, nfib, uint32_t(mx), uint32_t(my),
+                                                      epi, base, out);
+    return;
+  }
   if (kd == 0) {
     const uint64_t nf = my * mz;
     if (fast && try_scan<R>(0, t, 1, 1, 0, nf, f, epi, base, out, s))
@@ -923,6 +943,8 @@ template <typename R> void set_thomas_attrs() {
   cudaFuncSetAttribute(thomas_cols_kernel<R, true>,
                        cudaFuncAttributeMaxDynamicSharedMemorySize, lim);
   set_tf_attrs<R>();
+  for (auto k : {thomas_exact_kernel<R, 0>, thomas_exact_kernel<R, 1>, thomas_exact_kernel<R, 2>})
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 74 * 1024);
   cudaFuncSetAttribute(thomas_small_kernel<R>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        96 * 1024);
 }
