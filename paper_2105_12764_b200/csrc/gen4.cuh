@@ -13,7 +13,8 @@
 //                       (masstrans_window, kernels.hpp:158-185); one pass per
 //                       dimension that refines, ping-pong between buffers
 //              solve d: Thomas along d on the coarse lattice
-//                       (thomas_fiber, kernels.hpp:143-151), in place
+//                       (thomas_fiber, kernels.hpp:143-151), in place, with
+//                       the 3-D family's exact-order Thomas kernels
 //              apply  : a_{l-1}[i] = a_l[off(i)] + z[i]  (refactor.hpp:380-399)
 //   recompose  load   : W = class value at fine nodes, 0 elsewhere
 //              mass/solve as above, then a' = a_{l-1} - z  (refactor.hpp:404-422)
@@ -23,8 +24,7 @@
 // All arithmetic is the reference expression through the _rn intrinsics, so
 // both policies are bit-identical to the reference on 4-D grids (the FAST
 // tolerance is met trivially).  The lattices are compact and dim-0-fastest,
-// so each pass reads and writes unit-stride along dim 0; the Thomas pass for
-// d > 0 has consecutive threads on consecutive fibers (coalesced).
+// so each pass reads and writes unit-stride along dim 0.
 #pragma once
 
 #include <cstdint>
@@ -55,6 +55,17 @@ template <typename R> struct Gen4Geom {
 };
 
 __device__ __forceinline__ void gen_decode(uint64_t i, const uint32_t *e, uint32_t *p) {
+  if ((i >> 32) == 0) { // 32-bit divisions (a 64-bit one is a long call)
+    uint32_t j = uint32_t(i);
+#pragma unroll
+    for (int d = 0; d < kGenDims - 1; ++d) {
+      const uint32_t qd = j / e[d];
+      p[d] = j - qd * e[d];
+      j = qd;
+    }
+    p[kGenDims - 1] = j;
+    return;
+  }
 #pragma unroll
   for (int d = 0; d < kGenDims; ++d) {
     p[d] = uint32_t(i % e[d]);
@@ -87,36 +98,36 @@ __device__ __forceinline__ uint64_t gen_slot(const Gen4Geom<R> &g, const uint32_
 }
 
 // interpolate_node (kernels.hpp:193-223): corners at p +- 1 along the fine
-// dims (bit q of the corner id -> +1 on the q-th fine dim), reduced pairwise
-// a + t*(b - a), lowest fine dim first.  `at(q)` reads the level-l value at
-// lattice position q (all corners are coarse nodes).
+// dims, reduced pairwise a + t*(b - a), lowest fine dim first.  Corner c
+// carries bit d for dimension d (all four, statically indexed: no local
+// memory); only the 2^k corners of the k fine dims are loaded, and a
+// non-fine dimension's reduction step keeps the even corner unchanged, which
+// pairs and orders the lerps exactly like the reference's compacted corner
+// index.  `at(q)` reads the level-l value at lattice position q.
 template <typename R, typename At>
-__device__ R gen_interp(const Gen4Geom<R> &g, const uint32_t *p, unsigned mask, At &&at) {
-  int fd[kGenDims];
-  int k = 0;
+__device__ __forceinline__ R gen_interp(const Gen4Geom<R> &g, const uint32_t *p, unsigned mask,
+                                        At &&at) {
+  R c[1 << kGenDims];
 #pragma unroll
-  for (int d = 0; d < kGenDims; ++d)
-    if ((mask >> d) & 1)
-      fd[k++] = d;
-  R corner[1 << kGenDims];
-  for (int c = 0; c < (1 << k); ++c) {
-    uint32_t q[kGenDims];
+  for (int ci = 0; ci < (1 << kGenDims); ++ci) {
+    c[ci] = R(0);
+    if ((unsigned(ci) & ~mask) == 0) {
+      uint32_t q[kGenDims];
 #pragma unroll
-    for (int d = 0; d < kGenDims; ++d)
-      q[d] = p[d];
-    for (int b = 0; b < k; ++b)
-      q[fd[b]] = ((c >> b) & 1) ? p[fd[b]] + 1 : p[fd[b]] - 1;
-    corner[c] = at(q);
+      for (int d = 0; d < kGenDims; ++d)
+        q[d] = ((mask >> d) & 1) ? (((ci >> d) & 1) ? p[d] + 1 : p[d] - 1) : p[d];
+      c[ci] = at(q);
+    }
   }
-  int width = 1 << k;
-  for (int b = 0; b < k; ++b) {
-    const int d = fd[b];
-    const R t = g.r[d][p[d] - 1];
-    width >>= 1;
-    for (int i = 0; i < width; ++i)
-      corner[i] = lerp(corner[2 * i], corner[2 * i + 1], t);
+#pragma unroll
+  for (int d = 0; d < kGenDims; ++d) {
+    const bool fine = (mask >> d) & 1;
+    const R t = fine ? g.r[d][p[d] - 1] : R(0);
+#pragma unroll
+    for (int i = 0; i < ((1 << kGenDims) >> (d + 1)); ++i)
+      c[i] = fine ? lerp(c[2 * i], c[2 * i + 1], t) : c[2 * i];
   }
-  return corner[0];
+  return c[0];
 }
 
 template <typename R>
@@ -182,43 +193,6 @@ __global__ void gen_mass_kernel(Gen4Geom<R> g, int d, uint4 e4, const R *__restr
   }
   const uint32_t q = coarse_pos(p[d], n);
   out[o] = masstrans_at<R>([&](uint32_t j) { return in[base + j * sd]; }, q, n, g.h[d], g.r[d]);
-}
-
-// Thomas along dim d of the compact coarse lattice, in place; one thread per
-// fiber (thomas_fiber, kernels.hpp:143-151)
-template <typename R>
-__global__ void gen_thomas_kernel(Gen4Geom<R> g, int d, R *__restrict__ f) {
-  const uint32_t mm = g.m[d];
-  const uint64_t fibers = g.coarse_nodes() / mm;
-  const uint64_t t = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (t >= fibers)
-    return;
-  uint64_t rest = t, base = 0, str = 1, sd = 1;
-#pragma unroll
-  for (int k = 0; k < kGenDims; ++k) {
-    if (k == d) {
-      sd = str;
-    } else {
-      base += (rest % g.m[k]) * str;
-      rest /= g.m[k];
-    }
-    str *= g.m[k];
-  }
-  R *v = f + base;
-  const R *h = g.th[d], *fwd = g.tf[d], *ip = g.ti[d];
-  R prev = v[0];
-  for (uint32_t i = 1; i < mm; ++i) {
-    const R x = add(v[i * sd], mul(fwd[i], prev));
-    v[i * sd] = x;
-    prev = x;
-  }
-  R next = mul(prev, ip[mm - 1]);
-  v[(mm - 1) * sd] = next;
-  for (uint32_t i = mm - 1; i-- > 0;) {
-    const R x = mul(sub(v[i * sd], mul(h[i], next)), ip[i]);
-    v[i * sd] = x;
-    next = x;
-  }
 }
 
 // decompose apply_pack: P[i] = a[off(i)] + z[i]

@@ -1000,6 +1000,25 @@ mgrg_status Recorder::end() {
 
 inline unsigned gen_blocks(uint64_t n) { return unsigned((n + 255) / 256); }
 
+// Thomas along dim d of the compact coarse lattice with the 3-D family's
+// exact-order kernels: x fibers resident in shared memory, the others one
+// thread per fiber with consecutive threads on consecutive inner nodes
+template <typename R> void gen_launch_thomas(const Gen4Geom<R> &g, int d, R *f, cudaStream_t s) {
+  const ThomasGeom<R> t{g.th[d], g.tf[d], g.ti[d], g.m[d]};
+  const uint64_t nfib = g.coarse_nodes() / g.m[d];
+  if (d == 0 && te_fits<R>(0, t.m) && (reinterpret_cast<uintptr_t>(f) & 15) == 0) {
+    thomas_exact_kernel<R, 0><<<unsigned((nfib + te_nf<R>() - 1) / te_nf<R>()), kTeThreads,
+                                te_smem<R>(0, t.m), s>>>(f, t, nfib, g.m[0], g.m[1], Epi::none,
+                                                         nullptr, nullptr);
+    return;
+  }
+  uint64_t inner = 1;
+  for (int k = 0; k < d; ++k)
+    inner *= g.m[k];
+  thomas_strided_kernel<R><<<unsigned((nfib + 127) / 128), 128, 0, s>>>(
+      f, t, inner, inner, inner * g.m[d], nfib, Epi::none, nullptr, nullptr);
+}
+
 // R*M along every refining dimension, dims ascending (masstrans_dim0 then
 // masstrans_later, refactor.hpp:251-346), ping-pong between W and W2;
 // returns the buffer holding the load vector on the coarse lattice
@@ -1029,7 +1048,7 @@ R *gen_mass_all(mgrg_plan *p, const Gen4Geom<R> &g, int l, Recorder &rec, cudaSt
       continue;
     if ((st = rec.begin(MGRG_K_THOMAS_X + std::min(d, 2), l, 0)))
       return nullptr;
-    gen_thomas_kernel<R><<<gen_blocks(g.coarse_nodes() / g.m[d]), 256, 0, s>>>(g, d, cur);
+    gen_launch_thomas<R>(g, d, cur, s);
     if ((st = rec.end()))
       return nullptr;
   }
@@ -1329,6 +1348,10 @@ mgrg_status mgrg_plan_create(const mgrg_grid_desc *desc, mgrg_plan **out) {
       return fail(e == cudaErrorMemoryAllocation ? MGRG_OUT_OF_MEMORY : MGRG_CUDA_ERROR,
                   std::string("workspace allocation: ") + cudaGetErrorString(e));
     }
+    if (p->dtype == MGRG_F32)
+      set_thomas_attrs<float>();
+    else
+      set_thomas_attrs<double>();
     *out = p.release();
     return MGRG_OK;
   }
@@ -1950,8 +1973,7 @@ static mgrg_status solve_t(mgrg_plan *p, int level, int kd, void *f, cudaStream_
     const Gen4Geom<R> &g = pt<R>(p).g4[level];
     if (!(g.m[kd] < g.n[kd]))
       return MGRG_OK; // identity transfer (kernels.hpp:434-435)
-    gen_thomas_kernel<R><<<gen_blocks(g.coarse_nodes() / g.m[kd]), 256, 0, s>>>(
-        g, kd, static_cast<R *>(f));
+    gen_launch_thomas<R>(g, kd, static_cast<R *>(f), s);
     CUDA_TRY(cudaGetLastError());
     return MGRG_OK;
   }
