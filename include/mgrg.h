@@ -179,6 +179,23 @@ mgrg_status mgrg_coop_thomas_z(mgrg_plan *plan, int32_t level, uint32_t c0, uint
 /* Device pointer of the plan's packed level-`level` buffer (1 <= level < L). */
 mgrg_status mgrg_plan_level_buffer(mgrg_plan *plan, int32_t level, void **d_ptr);
 
+/* Fault hook of cooperative runs (CoopOptions::fault_injector,
+ * parallel.hpp:68-70): called at every phase entry ("level", "solve",
+ * "tail", "serial"); a non-zero return aborts the run as WORKER_FAILURE. */
+typedef int (*mgrg_fault_fn)(void *ctx, int32_t worker, const char *phase, int32_t level);
+/* cooperative_decompose (parallel_impl.hpp:691-808) of a host grid by
+ * `workers` workers, worker w on device (desc->device + w) mod the visible
+ * devices (several workers may share a GPU), driven from the calling thread
+ * with the steps above; classes (N elements, class l at N_{l-1}) written to
+ * h_classes, bit-identical to mgrg_decompose_host of the whole grid (exact
+ * policy).  remote_elements (optional) = elements moved between distinct
+ * workers (CommReport).  TOO_MANY_WORKERS as make_partitions
+ * (parallel.cpp:41-55). */
+mgrg_status mgrg_cooperative_decompose_host(const mgrg_grid_desc *desc, int32_t workers,
+                                            const void *h_values, void *h_classes,
+                                            mgrg_fault_fn fault, void *fault_ctx,
+                                            uint64_t *remote_elements);
+
 /* ---- diagnostics ------------------------------------------------------- */
 /* Thread-local message of the last failing call ("" if none). */
 const char *mgrg_last_error(void);

@@ -25,6 +25,7 @@ EXPORTS = (
     "mgrg_recompose_host", "mgrg_gpk", "mgrg_masstrans", "mgrg_solve",
     "mgrg_apply_correction", "mgrg_reorder", "mgrg_last_error",
     "mgrg_coop_level", "mgrg_coop_thomas_z", "mgrg_plan_level_buffer",
+    "mgrg_cooperative_decompose_host",
     "mgrg_status_name", "mgrg_plan_last_launches", "mgrg_version",
     "mgrg_plan_set_profiling", "mgrg_plan_profile_reset", "mgrg_plan_profile_read",
     "mgrg_crc32", "mgrg_class_crc32", "mgrg_write_refactored", "mgrg_read_refactored",
@@ -88,6 +89,8 @@ def lib() -> ctypes.CDLL:
             "mgrg_coop_level": [vp, i32, u32, u32, vp, vp, vp],
             "mgrg_coop_thomas_z": [vp, i32, u32, u32, u64, u64, i32, vp, vp, vp, vp],
             "mgrg_plan_level_buffer": [vp, i32, ctypes.POINTER(ctypes.c_void_p)],
+            "mgrg_cooperative_decompose_host": [ctypes.POINTER(GridDesc), i32, vp, vp, vp, vp,
+                                                ctypes.POINTER(u64)],
             "mgrg_plan_last_launches": [vp, ctypes.POINTER(u64)],
             "mgrg_plan_set_profiling": [vp, i32],
             "mgrg_plan_profile_reset": [vp],

@@ -326,11 +326,64 @@ def _fault(opt, w, phase, level):
             raise errors.WorkerFailure(f"worker {w} failed in {phase}: {ex}") from ex
 
 
+_FAULT_FN = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.c_void_p, ctypes.c_int32, ctypes.c_char_p,
+                             ctypes.c_int32)
+
+
+def _native_cooperative(grid, workers, opt, device):
+    """mgrg_cooperative_decompose_host: the same steps driven by the native
+    runtime (csrc/coop_host.cuh), worker w on device (device + w) mod the
+    visible GPUs."""
+    from .plan import Plan
+    from .refactor import RefactoredData
+
+    shape = tuple(int(s) for s in grid.shape)
+    vals = grid.values
+    host = vals.detach().cpu().numpy() if hasattr(vals, "detach") else np.asarray(vals)
+    host = np.ascontiguousarray(host.reshape(-1))
+    coords = [np.asarray(c, dtype=np.float64) for c in grid.coords]
+    desc = _lib.GridDesc()
+    desc.ndims = len(shape)
+    desc.dtype = host.dtype.itemsize
+    for i, n in enumerate(shape):
+        desc.shape[i] = n
+    flat_c = np.ascontiguousarray(np.concatenate(coords))
+    desc.coords = flat_c.ctypes.data
+    desc.levels = int(opt.levels or 0)
+    desc.device = device
+    desc.flags = 1 if opt.fast else 0
+    err = []
+
+    def hook(ctx, w, phase, level):
+        try:
+            opt.fault_injector(int(w), phase.decode(), int(level))
+            return 0
+        except Exception as ex:  # surfaces as WorkerFailure
+            err.append(ex)
+            return 1
+
+    cb = _FAULT_FN(hook) if opt.fault_injector is not None else None
+    out = np.empty_like(host)
+    moved = ctypes.c_uint64(0)
+    _lib.check(_lib.lib().mgrg_cooperative_decompose_host(
+        ctypes.byref(desc), workers, host.ctypes.data, out.ctypes.data,
+        ctypes.cast(cb, ctypes.c_void_p) if cb else None, None, ctypes.byref(moved)))
+    if opt.report is not None:
+        opt.report.add("native", int(moved.value), True)
+    plan = Plan(shape, host.dtype, coords=coords, levels=opt.levels, device=device)
+    classes = [out[x] for x in plan.class_slices()]
+    L = plan.levels
+    plan.close()
+    return RefactoredData(shape, coords, L, classes, out)
+
+
 def cooperative_decompose(grid, workers: int, opt: CoopOptions | None = None,
                           transport=None, device: int = 0):
     """mgr::cooperative_decompose (parallel_impl.hpp:691-808).  Returns the
     RefactoredData on worker 0 (None on the other ranks).  Without a
-    transport: all `workers` run in this process on `device`; with
+    transport: the native runtime (mgrg_cooperative_decompose_host) drives
+    all `workers` from this thread, worker w on device (device + w) mod the
+    visible GPUs; LocalTransport(W): the same in Python on one device;
     DistTransport: one worker per rank (call on every rank)."""
     import torch
 
@@ -339,7 +392,12 @@ def cooperative_decompose(grid, workers: int, opt: CoopOptions | None = None,
     opt = opt or CoopOptions()
     _validate_geometry(grid.shape, grid.coords, 2)
     make_partitions(grid.shape, workers, opt.scheme)  # reference validation
-    tp = transport or LocalTransport(workers)
+    if transport is None:
+        if opt.report is not None:
+            opt.report.workers, opt.report.scheme = workers, opt.scheme
+            opt.report.total_grid_elements = int(np.prod(grid.shape))
+        return _native_cooperative(grid, workers, opt, device)
+    tp = transport
     if tp.workers != workers:
         raise errors.TooManyWorkers(f"transport has {tp.workers} workers, asked for {workers}")
     shape = tuple(int(s) for s in grid.shape)

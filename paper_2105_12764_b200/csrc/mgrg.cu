@@ -2240,5 +2240,6 @@ mgrg_status mgrg_plan_level_buffer(mgrg_plan *p, int32_t level, void **d_ptr) {
 
 } // extern "C"
 
+#include "coop_host.cuh"
 #include "container.cuh"
 #include "compress.cuh"

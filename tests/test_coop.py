@@ -149,13 +149,20 @@ def test_cooperative_equals_serial(shape, workers, dtype, nonuni):
     g = make_grid(shape, rng.random(int(np.prod(shape))).astype(dtype), coords)
     serial = decompose(g)
     rep = coop.CommReport()
-    r = coop.cooperative_decompose(g, workers, coop.CoopOptions(report=rep))
+    r = coop.cooperative_decompose(g, workers, coop.CoopOptions(report=rep),
+                                   transport=coop.LocalTransport(workers))
     assert r.levels == serial.levels
     for l in range(r.levels + 1):
         assert np.array_equal(np.asarray(r.classes[l]), np.asarray(serial.classes[l])), l
-    if workers > 1 and coop.coop_levels(
-            [tuple(int(x) for x in e) for e in _level_shapes(shape)], workers):
+    split = workers > 1 and coop.coop_levels(
+        [tuple(int(x) for x in e) for e in _level_shapes(shape)], workers)
+    if split:
         assert rep.phases["classes"].elements > 0
+    # the native runtime (csrc/coop_host.cuh): same classes
+    nrep = coop.CommReport()
+    n = coop.cooperative_decompose(g, workers, coop.CoopOptions(report=nrep))
+    assert np.array_equal(np.asarray(n.flat), np.asarray(serial.flat))
+    assert (nrep.phases["native"].elements > 0) == bool(split)
 
 
 @pytest.mark.gpu
@@ -165,7 +172,10 @@ def test_cooperative_level_cap_and_fast_policy():
     rng = np.random.default_rng(5)
     g = make_grid((33, 33, 65), rng.random(33 * 33 * 65).astype("float32"))
     serial = decompose(g, RefactorOptions(levels=3))
-    r = coop.cooperative_decompose(g, 4, coop.CoopOptions(levels=3))
+    r = coop.cooperative_decompose(g, 4, coop.CoopOptions(levels=3),
+                                   transport=coop.LocalTransport(4))
+    nat = coop.cooperative_decompose(g, 4, coop.CoopOptions(levels=3))
+    assert np.array_equal(np.asarray(nat.flat), np.asarray(serial.flat))
     assert r.levels == 3
     assert all(np.array_equal(np.asarray(a), np.asarray(b))
                for a, b in zip(r.classes, serial.classes))
@@ -187,6 +197,9 @@ def test_cooperative_fault_injection_is_worker_failure():
             raise RuntimeError("injected")
 
     with pytest.raises(errors.WorkerFailure):
+        coop.cooperative_decompose(g, 2, coop.CoopOptions(fault_injector=boom),
+                                   transport=coop.LocalTransport(2))
+    with pytest.raises(errors.WorkerFailure):  # native runtime, C callback
         coop.cooperative_decompose(g, 2, coop.CoopOptions(fault_injector=boom))
 
 
