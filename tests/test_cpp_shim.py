@@ -49,3 +49,26 @@ def test_cpp_pipeline_shim_matches_reference(tmp_path, oracle_mod):
     out = subprocess.run([exe, str(tmp_path)], capture_output=True, text=True, timeout=300)
     assert out.returncode == 0, out.stderr
     assert "pipeline ok" in out.stdout
+
+
+PARSRC = os.path.join(ROOT, "tests", "cpp", "test_parallel_shim.cpp")
+
+
+def test_parallel_header_compiles_standalone():
+    subprocess.run(["g++", "-std=c++17", "-fsyntax-only", "-Wall", "-Wextra",
+                    "-I", os.path.join(ROOT, "include"), PARSRC], check=True)
+
+
+@pytest.mark.gpu
+def test_cpp_parallel_shim_matches_reference(tmp_path, oracle_mod):
+    """cooperative_decompose / grouped_decompose through the C++ drop-in
+    (native cooperative runtime) equal the reference's serial decompose."""
+    if not oracle_mod.available("ref"):
+        pytest.skip("oracle/_ref not built")
+    exe = str(tmp_path / "test_parallel_shim")
+    subprocess.run(["g++", "-std=c++17", "-O2", "-I", os.path.join(ROOT, "include"), PARSRC,
+                    "-L", PKG, "-lmgrg", "-L", REF, "-lmgr_ref", "-pthread",
+                    f"-Wl,-rpath,{PKG}:{REF}", "-o", exe], check=True)
+    out = subprocess.run([exe], capture_output=True, text=True, timeout=300)
+    assert out.returncode == 0, out.stderr
+    assert "parallel shim ok" in out.stdout
