@@ -104,6 +104,45 @@ __device__ __forceinline__ R stencil_eval(const Stencil<R> &s, R t0, R t1, R t2,
   }
 }
 
+// Pieces of the exact merged stencil, to share the fine-neighbour mass
+// products of adjacent outputs: mr(c) (the q+1 term of output c) equals
+// ml(c+1) (the q'-1 term of output c+1, q' = q+2) bit for bit -- same
+// coefficients h[q], 2(h[q]+h[q+1]), h[q+1] (one table value each), same
+// taps, same operation order -- so each is evaluated once.  st_combine(s,
+// t0..t3, st_ml(s, t0, t1, t2), st_mr(s, t2, t3, t4)) == stencil_eval<R,
+// false>(s, t0, .., t4) for every stencil.
+template <typename R>
+__device__ __forceinline__ R st_ml(const Stencil<R> &s, R t0, R t1, R t2) {
+  return add(add(mul(s.hm2, t0), mul(s.dm1, t1)), mul(s.hm1, t2));
+}
+template <typename R>
+__device__ __forceinline__ R st_mr(const Stencil<R> &s, R t2, R t3, R t4) {
+  return add(add(mul(s.h0, t2), mul(s.dp1, t3)), mul(s.hp1, t4));
+}
+template <typename R>
+__device__ __forceinline__ R st_combine(const Stencil<R> &s, R t0, R t1, R t2, R t3, R ml,
+                                        R mr) {
+  if (s.flags == ST_INTERIOR) {
+    R v = add(add(mul(s.hm1, t1), mul(s.d0, t2)), mul(s.h0, t3));
+    v = add(v, mul(s.cl, ml));
+    return add(v, mul(s.cr, mr));
+  }
+  if (s.flags & ST_SHIFT)
+    return add(mul(s.hm1, t0), mul(s.d0, t1));
+  R v;
+  if (s.flags & ST_LEFT)
+    v = add(mul(s.d0, t2), mul(s.h0, t3));
+  else if (s.flags & ST_RIGHT)
+    v = add(mul(s.hm1, t1), mul(s.d0, t2));
+  else
+    v = add(add(mul(s.hm1, t1), mul(s.d0, t2)), mul(s.h0, t3));
+  if (s.flags & ST_HASL)
+    v = add(v, mul(s.cl, ml));
+  if (s.flags & ST_HASR)
+    v = add(v, mul(s.cr, mr));
+  return v;
+}
+
 // Balanced tiling: tile t of nt over m outputs covers [t*m/nt, (t+1)*m/nt).
 __device__ __forceinline__ uint32_t tile_lo(uint32_t t, uint32_t nt, uint32_t m) {
   return uint32_t((uint64_t(t) * m) / nt);

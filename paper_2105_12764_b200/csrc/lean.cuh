@@ -112,22 +112,55 @@ template <typename R, bool FAST>
 __device__ __forceinline__ R lean_xpass(const W5r<R> &wx, const Stencil<R> &sx, R ce, R co) {
   const R em = __shfl_up_sync(0xffffffffu, ce, 1);
   const R om = __shfl_up_sync(0xffffffffu, co, 1);
-  const R ep = __shfl_down_sync(0xffffffffu, ce, 1);
-  return pstencil<R, FAST>(wx, sx, em, om, ce, co, ep);
+  if constexpr (FAST) {
+    const R ep = __shfl_down_sync(0xffffffffu, ce, 1);
+    return pstencil<R, FAST>(wx, sx, em, om, ce, co, ep);
+  } else { // the q+1 term is the next lane's q-1 term (st_ml)
+    const R ml = st_ml(sx, em, om, ce);
+    const R mr = __shfl_down_sync(0xffffffffu, ml, 1);
+    return st_combine(sx, em, om, ce, co, ml, mr);
+  }
 }
 // Same on a row whose even nodes are kept (coarse in every other dim): the
 // even taps are zero.
 template <typename R, bool FAST>
 __device__ __forceinline__ R lean_xpass_odd(const W5r<R> &wx, const Stencil<R> &sx, R co) {
   const R om = __shfl_up_sync(0xffffffffu, co, 1);
-  if constexpr (FAST)
+  if constexpr (FAST) {
     return fma(wx.w3, co, wx.w1 * om);
-  else
-    return stencil_eval<R, false>(sx, R(0), om, R(0), co, R(0));
+  } else {
+    const R ml = st_ml(sx, R(0), om, R(0));
+    const R mr = __shfl_down_sync(0xffffffffu, ml, 1);
+    return st_combine(sx, R(0), om, R(0), co, ml, mr);
+  }
 }
 
 // Merged R*M along y of the band's x results, output row j (y stencil row
 // cy0 + j; rows past the level are clamped -- their outputs are not stored)
+// All TY outputs of the band; the exact policy carries output j's q+1 term
+// as output j+1's q-1 term (st_ml / st_mr), one stencil live at a time.
+template <typename R, bool FAST, int TY>
+__device__ __forceinline__ void lean_ypass_all(const W5r<R> *wy, const Stencil<R> *__restrict__ sy,
+                                               int cy0, int m1, const R *X, R *Y) {
+  if constexpr (FAST) {
+#pragma unroll
+    for (int j = 0; j < TY; ++j)
+      Y[j] = pstencil<R, true>(wy[j], Stencil<R>{}, X[2 * j], X[2 * j + 1], X[2 * j + 2],
+                               X[2 * j + 3], X[2 * j + 4]);
+  } else {
+    R ml = R(0);
+#pragma unroll
+    for (int j = 0; j < TY; ++j) {
+      const Stencil<R> s = sy[min(cy0 + j, m1 - 1)];
+      if (j == 0)
+        ml = st_ml(s, X[0], X[1], X[2]);
+      const R mr = st_mr(s, X[2 * j + 2], X[2 * j + 3], X[2 * j + 4]);
+      Y[j] = st_combine(s, X[2 * j], X[2 * j + 1], X[2 * j + 2], X[2 * j + 3], ml, mr);
+      ml = mr;
+    }
+  }
+}
+
 template <typename R, bool FAST>
 __device__ __forceinline__ R lean_ypass(const W5r<R> *wy, const Stencil<R> *__restrict__ sy,
                                         int row, const R *X, int j) {
@@ -281,9 +314,7 @@ __device__ __forceinline__ void lean_plane(
       ((r & 1) ? po.bo1 : po.bo0)[uint32_t(ex_o * rr)] = co;
     X[r] = kept ? lean_xpass_odd<R, FAST>(wx, sx, co) : lean_xpass<R, FAST>(wx, sx, ce, co);
   }
-#pragma unroll
-  for (int j = 0; j < TY; ++j)
-    Y[j] = lean_ypass<R, FAST>(wy, sy, min(cy0 + j, m1 - 1), X, j);
+  lean_ypass_all<R, FAST, TY>(wy, sy, cy0, m1, X, Y);
 }
 
 // ---------------------------------------------------------------------------
@@ -397,7 +428,7 @@ __global__ void __launch_bounds__(32 * kLeanWPB, 3)
   for (int r = 0; r < NR; ++r)
     WLe[r] = WLo[r] = R(0);
   R accM[TY], acc0[TY]; // FAST: partial f of outputs k-1 and k at step k
-  R YEm2[TY], YOm1[TY], YEm1[TY]; // exact: y results of planes 2k-4, 2k-3, 2k-2
+  R YEm2[TY], YOm1[TY], YEm1[TY]; // exact: carried q-1 term; y results of planes 2k-3, 2k-2
 #pragma unroll
   for (int j = 0; j < TY; ++j)
     accM[j] = acc0[j] = YEm2[j] = YOm1[j] = YEm1[j] = R(0);
@@ -499,16 +530,20 @@ __global__ void __launch_bounds__(32 * kLeanWPB, 3)
         accM[i] = fma(b1, YO[i], fma(b2, YE[i], acc0[i]));
         acc0[i] = c0 * YE[i];
       }
-    } else { // exact: output k-1 from the five planes 2k-4 .. 2k
+    } else { // exact: output k-1 from planes 2k-3 .. 2k; its q-1 term is
+      // output k-2's q+1 term, carried in YEm2 (st_ml / st_mr; computed from
+      // step cz0 on, where output cz0-1's q+1 term is output cz0's q-1 term)
+      const bool need = k >= 1 && k >= cz0 && k - 1 < cz1;
       Stencil<R> sk{};
-      if (emit)
+      if (need)
         sk = szt[k - 1];
 #pragma unroll
       for (int i = 0; i < TY; ++i) {
+        const R mr = st_mr(sk, YEm1[i], YO[i], YE[i]);
         if (emit && cy0 + i < cy1)
           fq[int64_t(m0) * i + m01 * (k - 1)] =
-              stencil_eval<R, false>(sk, YEm2[i], YOm1[i], YEm1[i], YO[i], YE[i]);
-        YEm2[i] = YEm1[i];
+              st_combine(sk, R(0), YOm1[i], YEm1[i], YO[i], YEm2[i], mr);
+        YEm2[i] = mr;
         YOm1[i] = YO[i];
         YEm1[i] = YE[i];
       }
@@ -574,7 +609,7 @@ __global__ void __launch_bounds__(32 * kLeanWPB, LEAN_RL_MINB)
   const int cz0 = Z3 ? int(tzc) * tl.zc : 0;
   const int cz1 = Z3 ? min(cz0 + tl.zc, m2) : 1;
   R accM[TY], acc0[TY];          // FAST: partial f of outputs k-1 and k
-  R YEm2[TY], YOm1[TY], YEm1[TY]; // exact: y results of planes 2k-4, 2k-3, 2k-2
+  R YEm2[TY], YOm1[TY], YEm1[TY]; // exact: carried q-1 term; y results of planes 2k-3, 2k-2
 #pragma unroll
   for (int j = 0; j < TY; ++j)
     accM[j] = acc0[j] = YEm2[j] = YOm1[j] = YEm1[j] = R(0);
@@ -635,9 +670,7 @@ __global__ void __launch_bounds__(32 * kLeanWPB, LEAN_RL_MINB)
           X[r] = lean_xpass<R, FAST>(wx, sx, ce, co);
         }
       }
-#pragma unroll
-      for (int j = 0; j < TY; ++j)
-        YE[j] = lean_ypass<R, FAST>(wy, syt, min(cy0 + j, m1 - 1), X, j);
+      lean_ypass_all<R, FAST, TY>(wy, syt, cy0, m1, X, YE);
     }
     if constexpr (!Z3) {
 #pragma unroll
@@ -657,9 +690,7 @@ __global__ void __launch_bounds__(32 * kLeanWPB, LEAN_RL_MINB)
         const R co = (vo && rv) ? uoO[r] : R(0);
         X[r] = lean_xpass<R, FAST>(wx, sx, ce, co);
       }
-#pragma unroll
-      for (int j = 0; j < TY; ++j)
-        YO[j] = lean_ypass<R, FAST>(wy, syt, min(cy0 + j, m1 - 1), X, j);
+      lean_ypass_all<R, FAST, TY>(wy, syt, cy0, m1, X, YO);
     }
     const bool emit = outl && k - 1 >= cz0 && k - 1 < cz1;
     if constexpr (FAST) {
@@ -674,16 +705,18 @@ __global__ void __launch_bounds__(32 * kLeanWPB, LEAN_RL_MINB)
         accM[j] = fma(b1, YO[j], fma(b2, YE[j], acc0[j]));
         acc0[j] = c0 * YE[j];
       }
-    } else { // exact: output k-1 from the five planes 2k-4 .. 2k
+    } else { // exact: as in lean_dec_kernel (q-1 term carried in YEm2)
+      const bool need = k >= 1 && k >= cz0 && k - 1 < cz1;
       Stencil<R> sk{};
-      if (emit)
+      if (need)
         sk = szt[k - 1];
 #pragma unroll
       for (int j = 0; j < TY; ++j) {
+        const R mr = st_mr(sk, YEm1[j], YO[j], YE[j]);
         if (emit && cy0 + j < cy1)
           fq[int64_t(m0) * j + m01 * (k - 1)] =
-              stencil_eval<R, false>(sk, YEm2[j], YOm1[j], YEm1[j], YO[j], YE[j]);
-        YEm2[j] = YEm1[j];
+              st_combine(sk, R(0), YOm1[j], YEm1[j], YO[j], YEm2[j], mr);
+        YEm2[j] = mr;
         YOm1[j] = YO[j];
         YEm1[j] = YE[j];
       }
