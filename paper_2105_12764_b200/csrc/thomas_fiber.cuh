@@ -151,6 +151,44 @@ __global__ void __launch_bounds__(kTfThreads, sizeof(R) == 4 ? 2 : 1)
   const bool contiguous = DIM == 2 || (F0 % m0) + uint64_t(nf) <= m0;
   const uint64_t ntot = nfib * m;
 
+  // DIM 1, 2: position-major tile [i][fiber]; with 32 contiguous fibers of
+  // DIM 2 each position row is fetched as its 16-byte aligned superset (NCK
+  // chunks, one LDGSTS.128 each: ~4x fewer copy operations than element
+  // copies) and read back at the row's shift.  The same staging brings the
+  // epilogue's base rows in while the solve runs.
+  constexpr bool SUPR = NF == 32 && DIM == 2;
+  auto stage_rows = [&](const R *src) {
+    if (SUPR && contiguous) {
+      constexpr int RPR = 32 / NCK; // rows per warp copy instruction
+      const int lane = tid & 31;
+      for (uint32_t i0 = w; i0 < m; i0 += NCH * RPR) {
+        const uint32_t i = i0 + uint32_t(lane / NCK) * NCH;
+        const int c = lane % NCK;
+        if (lane < RPR * NCK && i < m) {
+          const uint64_t s0 = (F0row + ps * i) & ~uint64_t(V - 1);
+          const uint64_t g = s0 + uint64_t(c) * V;
+          R *d = tile + size_t(i) * RW + c * V;
+          if (g + V <= ntot) {
+            cp_async16(d, src + g);
+          } else {
+#pragma unroll
+            for (int e = 0; e < V; ++e)
+              if (g + e < ntot)
+                cp_async(d + e, src + g + e);
+          }
+        }
+      }
+    } else {
+      for (uint32_t i = w; i < m; i += NCH)
+        cp_async(tile + size_t(i) * NF + fi, src + fa + ps * i);
+    }
+  };
+  auto row_at = [&](uint32_t i) -> R {
+    if (SUPR && contiguous)
+      return tile[size_t(i) * RW + int((F0row + ps * i) & uint64_t(V - 1)) + fi];
+    return tile[size_t(i) * NF + fi];
+  };
+
   if (TSM)
     tf_copy_in(stab, t.tab, tf_tab_elems<R>(m), tid);
   R v[CH];
@@ -164,49 +202,14 @@ __global__ void __launch_bounds__(kTfThreads, sizeof(R) == 4 ? 2 : 1)
 #pragma unroll
     for (int k = 0; k < CH; ++k)
       v[k] = uint32_t(k) < ln ? tp[k] : R(0);
-  } else if (NF == 32 && DIM == 2 && contiguous) {
-    // position-major tile [i][RW]: position i's 32 fibers are one contiguous
-    // run; it is fetched as the 16-byte aligned superset (NCK chunks, one
-    // LDGSTS.128 each: ~4x fewer copy operations than element copies) and
-    // read back at the row's shift
-    constexpr int RPR = 32 / NCK; // rows per warp copy instruction
-    const int lane = tid & 31;
-    for (uint32_t i0 = w; i0 < m; i0 += NCH * RPR) {
-      const uint32_t i = i0 + uint32_t(lane / NCK) * NCH;
-      const int c = lane % NCK;
-      if (lane < RPR * NCK && i < m) {
-        const uint64_t s0 = (F0row + ps * i) & ~uint64_t(V - 1);
-        const uint64_t g = s0 + uint64_t(c) * V;
-        R *d = tile + size_t(i) * RW + c * V;
-        if (g + V <= ntot) {
-          cp_async16(d, f + g);
-        } else {
-#pragma unroll
-          for (int e = 0; e < V; ++e)
-            if (g + e < ntot)
-              cp_async(d + e, f + g + e);
-        }
-      }
-    }
-    cp_async_commit();
-    cp_async_wait<0>();
-    __syncthreads();
-#pragma unroll
-    for (int k = 0; k < CH; ++k) {
-      const uint32_t i = a + k;
-      const int sh = int((F0row + ps * i) & uint64_t(V - 1));
-      v[k] = uint32_t(k) < len ? tile[size_t(i) * RW + sh + fi] : R(0);
-    }
   } else {
-    // position-major tile [i][fiber]: each position is one coalesced row
-    for (uint32_t i = w; i < m; i += NCH)
-      cp_async(tile + size_t(i) * NF + fi, f + fa + ps * i);
+    stage_rows(f);
     cp_async_commit();
     cp_async_wait<0>();
     __syncthreads();
 #pragma unroll
     for (int k = 0; k < CH; ++k)
-      v[k] = uint32_t(k) < len ? tile[size_t(a + k) * NF + fi] : R(0);
+      v[k] = uint32_t(k) < len ? row_at(a + k) : R(0);
   }
 
   // ---- forward, zero carry-in
@@ -218,7 +221,12 @@ __global__ void __launch_bounds__(kTfThreads, sizeof(R) == 4 ? 2 : 1)
     v[k] = acc;
   }
   carry[w * NF + fi] = acc;
-  __syncthreads();
+  __syncthreads(); // every thread has read its tile values
+  const bool pre = DIM != 0 && epi != Epi::none;
+  if (pre) { // the epilogue's base rows, in flight during the solve
+    stage_rows(base);
+    cp_async_commit();
+  }
   R c = R(0);
   for (int k = 0; k < w; ++k)
     c = fma(pfend[k], c, carry[k * NF + fi]);
@@ -273,32 +281,24 @@ __global__ void __launch_bounds__(kTfThreads, sizeof(R) == 4 ? 2 : 1)
       const R z = tile[e];
       dst[e] = epi == Epi::none ? z : (epi == Epi::add ? bs[e] + z : bs[e] - z);
     }
-  } else if (fi < nf) {
-    R *p = (epi == Epi::none ? f : out) + fa + ps * a;
-    const R *q = base + fa + ps * a;
-    if (epi == Epi::none) {
+  } else {
+    if (pre) {
+      cp_async_wait<0>();
+      __syncthreads();
+    }
+    if (fi < nf) {
+      R *p = (epi == Epi::none ? f : out) + fa + ps * a;
 #pragma unroll
       for (int k = 0; k < CH; ++k) {
-        if (uint32_t(k) < len)
-          *p = v[k];
+        if (uint32_t(k) < len) {
+          if (epi == Epi::none) {
+            *p = v[k];
+          } else {
+            const R b = row_at(a + k);
+            *p = epi == Epi::add ? b + v[k] : b - v[k];
+          }
+        }
         p += ps;
-      }
-    } else {
-      // base values in batches of 8 (bounded registers, 8 loads in flight)
-#pragma unroll
-      for (int k0 = 0; k0 < CH; k0 += 8) {
-        R bv[8];
-#pragma unroll
-        for (int k = k0; k < k0 + 8 && k < CH; ++k) {
-          bv[k - k0] = uint32_t(k) < len ? *q : R(0);
-          q += ps;
-        }
-#pragma unroll
-        for (int k = k0; k < k0 + 8 && k < CH; ++k) {
-          if (uint32_t(k) < len)
-            *p = epi == Epi::add ? bv[k - k0] + v[k] : bv[k - k0] - v[k];
-          p += ps;
-        }
       }
     }
   }
