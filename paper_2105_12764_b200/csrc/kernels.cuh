@@ -482,18 +482,26 @@ __global__ void __launch_bounds__(128)
   }
   v = mul(v, __ldg(t.ip + M - 1));
   epi_store(epi, f, base, out, st + uint64_t(M - 1) * S, v);
+  const bool ep = epi != Epi::none;
   for (int32_t i0 = int32_t(M) - 2; i0 >= 0; i0 -= B) {
-    R buf[B];
+    R buf[B], bb[B];
+    // the batch's solution inputs and (last solve) epilogue bases together
 #pragma unroll
     for (int b = 0; b < B; ++b)
-      if (i0 - b >= 0)
+      if (i0 - b >= 0) {
         buf[b] = fp[uint64_t(i0 - b) * S];
+        bb[b] = ep ? base[st + uint64_t(i0 - b) * S] : R(0);
+      }
 #pragma unroll
     for (int b = 0; b < B; ++b)
       if (i0 - b >= 0) {
         const uint32_t i = i0 - b;
         v = mul(sub(buf[b], mul(__ldg(t.h + i), v)), __ldg(t.ip + i));
-        epi_store(epi, f, base, out, st + uint64_t(i) * S, v);
+        const uint64_t idx = st + uint64_t(i) * S;
+        if (!ep)
+          f[idx] = v;
+        else
+          out[idx] = epi == Epi::add ? add(bb[b], v) : sub(bb[b], v);
       }
   }
 }
