@@ -438,9 +438,8 @@ __global__ void __launch_bounds__(CX *CY)
 // Thomas solves (thomas_fiber, kernels.hpp:143-151), batched over fibers.
 // ---------------------------------------------------------------------------
 template <typename R>
-__device__ __forceinline__ void epi_store(Epi epi, R *__restrict__ f,
-                                          const R *__restrict__ base,
-                                          R *__restrict__ out, uint64_t idx, R z) {
+__device__ __forceinline__ void epi_store(Epi epi, R *f, const R *base, R *out, uint64_t idx,
+                                          R z) {
   if (epi == Epi::none)
     f[idx] = z;
   else if (epi == Epi::add)
@@ -456,9 +455,9 @@ __device__ __forceinline__ void epi_store(Epi epi, R *__restrict__ f,
 // backward sweep, which reads them in reverse).
 template <typename R, int B = 8>
 __global__ void __launch_bounds__(128)
-    thomas_strided_kernel(R *__restrict__ f, ThomasGeom<R> t, uint64_t S,
-                          uint32_t inner, uint64_t ostride, uint64_t nfibers, Epi epi,
-                          const R *__restrict__ base, R *__restrict__ out) {
+    thomas_strided_kernel(R *f, ThomasGeom<R> t, uint64_t S, uint32_t inner,
+                          uint64_t ostride, uint64_t nfibers, Epi epi, const R *base, R *out) {
+  // f, base and out may alias (the epilogues write in place): no __restrict__
   const uint64_t k = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
   if (k >= nfibers)
     return;
@@ -513,8 +512,8 @@ __global__ void __launch_bounds__(128)
 // back coalesced.
 template <typename R>
 __global__ void __launch_bounds__(128)
-    thomas_x_kernel(R *__restrict__ f, ThomasGeom<R> t, uint64_t nfibers, Epi epi,
-                    const R *__restrict__ base, R *__restrict__ out) {
+    thomas_x_kernel(R *f, ThomasGeom<R> t, uint64_t nfibers, Epi epi, const R *base,
+                    R *out) { // f, base, out may alias
   __shared__ R tile_all[4][32][33];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   auto tile = tile_all[w];
