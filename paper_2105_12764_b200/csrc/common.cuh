@@ -108,4 +108,13 @@ template <int N> __device__ __forceinline__ void cp_async_wait() {
   asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
 }
 
+// Programmatic dependent launch: kernels of the level loop are launched
+// with programmatic stream serialization, so a kernel's CTAs are scheduled
+// while its predecessor drains; every such kernel waits here (first
+// statement) until the predecessor's writes are visible.  A no-op for
+// ordinary launches.
+__device__ __forceinline__ void pdl_wait() {
+  asm volatile("griddepcontrol.wait;\n" ::: "memory");
+}
+
 } // namespace mgrg

@@ -332,6 +332,7 @@ __global__ void __launch_bounds__(32 * kLeanWPB, 3)
                     const Stencil<R> *__restrict__ sxt, const Stencil<R> *__restrict__ syt,
                     const Stencil<R> *__restrict__ szt, const R *__restrict__ in,
                     R *__restrict__ cls, R *__restrict__ P, R *__restrict__ f, LeanTiles tl) {
+  pdl_wait();
   constexpr int TY = lean_ty<R>(), NR = 2 * TY + 3;
   constexpr int V = LeanStage<R>::V, SLOT = NR * LeanStage<R>::RP;
   extern __shared__ __align__(16) unsigned char lean_raw_sm[];
@@ -568,6 +569,7 @@ __global__ void __launch_bounds__(32 * kLeanWPB, LEAN_RL_MINB)
                       const Stencil<R> *__restrict__ sxt, const Stencil<R> *__restrict__ syt,
                       const Stencil<R> *__restrict__ szt, const R *__restrict__ cls,
                       R *__restrict__ f, LeanTiles tl) {
+  pdl_wait();
   constexpr int TY = lean_ty_rl<R>(), NR = 2 * TY + 3;
   const int lane = threadIdx.x & 31;
   const uint64_t wid = uint64_t(blockIdx.x) * kLeanWPB + (threadIdx.x >> 5);
@@ -760,6 +762,7 @@ __global__ void __launch_bounds__(32 * kLeanWPB, 4)
                      const LeanW<R> *__restrict__ ly, const LeanW<R> *__restrict__ lz,
                      const R *__restrict__ coarse, const R *__restrict__ cls,
                      R *__restrict__ out, LeanTiles tl) {
+  pdl_wait();
   constexpr int TG = lean_tg<R>(), NF = 2 * TG + 1; // fine rows incl. halo row 2cy1
   const int lane = threadIdx.x & 31;
   const uint64_t wid = uint64_t(blockIdx.x) * kLeanWPB + (threadIdx.x >> 5);

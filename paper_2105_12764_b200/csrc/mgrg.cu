@@ -638,6 +638,31 @@ int g_thomas_fiber = [] {
   const char *e = std::getenv("MGRG_TFIBER");
   return e ? std::atoi(e) : 1;
 }();
+// programmatic dependent launch of the level-loop kernels (MGRG_PDL=0 disables)
+int g_pdl = [] {
+  const char *e = std::getenv("MGRG_PDL");
+  return e ? std::atoi(e) : 1;
+}();
+
+// Launch with programmatic stream serialization: the kernel's CTAs may be
+// scheduled before its stream predecessor has finished; the kernel waits in
+// pdl_wait() (common.cuh) before touching any data.
+template <typename... KArgs, typename... Args>
+void launch_pdl(void (*k)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                Args &&...args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = g_pdl ? 1 : 0;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  cudaLaunchKernelEx(&cfg, k, std::forward<Args>(args)...);
+}
+
 // exact-policy resident Thomas (thomas_exact.cuh; MGRG_TEXACT=0 disables,
 // 2 also uses it for y / z fibers)
 int g_thomas_exact = [] {
@@ -704,8 +729,8 @@ void launch_lean_dec(bool fast, const LevelGeom<R> &g, const std::array<const Le
   const unsigned blocks = unsigned((t.warps() + kLeanWPB - 1) / kLeanWPB);
   auto k = z3 ? (fast ? lean_dec_kernel<R, true, true> : lean_dec_kernel<R, true, false>)
               : (fast ? lean_dec_kernel<R, false, true> : lean_dec_kernel<R, false, false>);
-  k<<<blocks, 32 * kLeanWPB, lean_dec_smem<R>(), s>>>(g, st[0], st[1], st[2], sc[0], sc[1],
-                                                      sc[2], in, cls, P, f, t);
+  launch_pdl(k, blocks, 32 * kLeanWPB, lean_dec_smem<R>(), s, g, st[0], st[1], st[2], sc[0],
+             sc[1], sc[2], in, cls, P, f, t);
 }
 template <typename R>
 void launch_lean_rload(bool fast, const LevelGeom<R> &g,
@@ -717,7 +742,8 @@ void launch_lean_rload(bool fast, const LevelGeom<R> &g,
   const unsigned blocks = unsigned((t.warps() + kLeanWPB - 1) / kLeanWPB);
   auto k = z3 ? (fast ? lean_rload_kernel<R, true, true> : lean_rload_kernel<R, true, false>)
               : (fast ? lean_rload_kernel<R, false, true> : lean_rload_kernel<R, false, false>);
-  k<<<blocks, 32 * kLeanWPB, 0, s>>>(g, st[0], st[1], st[2], sc[0], sc[1], sc[2], cls, f, t);
+  launch_pdl(k, blocks, 32 * kLeanWPB, 0, s, g, st[0], st[1], st[2], sc[0], sc[1], sc[2], cls, f,
+             t);
 }
 template <typename R>
 void launch_lean_rgpk(bool fast, const LevelGeom<R> &g,
@@ -738,7 +764,7 @@ void launch_lean_rgpk(bool fast, const LevelGeom<R> &g,
                     : lean_rgpk_kernel<R, false, true, false>)
             : (fast ? lean_rgpk_kernel<R, false, false, true>
                     : lean_rgpk_kernel<R, false, false, false>);
-  k<<<blocks, 32 * kLeanWPB, 0, s>>>(g, st[0], st[1], st[2], coarse, cls, out, t);
+  launch_pdl(k, blocks, 32 * kLeanWPB, 0, s, g, st[0], st[1], st[2], coarse, cls, out, t);
 }
 template <typename R>
 void launch_rl2(bool fast, const LevelGeom<R> &g,
@@ -820,10 +846,9 @@ template <typename R> bool ts_fits(const LevelGeom<R> &g) {
 template <typename R>
 void launch_thomas_small(const LevelGeom<R> &g, const std::array<ThomasGeom<R>, 3> &t, R *f,
                          Epi epi, const R *base, R *out, cudaStream_t s) {
-  thomas_small_kernel<R><<<1, kTsThreads,
-                           ts_smem<R>(g.coarse_nodes(), uint64_t(g.m[0]) + g.m[1] + g.m[2]),
-                           s>>>(
-      f, t[0], t[1], t[2], g.m[0], g.m[1], g.m[2], g.refine, epi, base, out);
+  launch_pdl(thomas_small_kernel<R>, 1, kTsThreads,
+             ts_smem<R>(g.coarse_nodes(), uint64_t(g.m[0]) + g.m[1] + g.m[2]), s, f, t[0], t[1],
+             t[2], g.m[0], g.m[1], g.m[2], g.refine, epi, base, out);
 }
 
 template <typename R, int DIM, int CH, int NF> auto tf_kernel() {
@@ -857,7 +882,7 @@ void launch_tf(int kd, const ThomasLean<R> &tl, uint64_t nfib, uint32_t mx, uint
   const unsigned blocks = unsigned((nfib + nf - 1) / nf);
   auto k = kd == 0 ? tf_pick<R, 0>(ch, nf) : (kd == 1 ? tf_pick<R, 1>(ch, nf)
                                                       : tf_pick<R, 2>(ch, nf));
-  k<<<blocks, kTfThreads, tf_smem<R>(kd, tl.m), s>>>(f, tl, nfib, mx, my, epi, base, out);
+  launch_pdl(k, blocks, kTfThreads, tf_smem<R>(kd, tl.m), s, f, tl, nfib, mx, my, epi, base, out);
 }
 template <typename R> void set_tf_attrs() {
   const int lim = int(tf_limit<R>());

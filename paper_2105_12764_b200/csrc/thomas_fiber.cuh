@@ -113,6 +113,7 @@ template <typename R, int DIM, int CH, int NF>
 __global__ void __launch_bounds__(kTfThreads, sizeof(R) == 4 ? 2 : 1)
     thomas_fiber_kernel(R *__restrict__ f, ThomasLean<R> t, uint64_t nfib, uint32_t m0,
                         uint32_t m1, Epi epi, const R *base, R *out) {
+  pdl_wait();
   constexpr int NCH = kTfThreads / NF;
   constexpr bool TSM = NF == 32; // coefficient table in shared memory
   extern __shared__ __align__(16) unsigned char tf_raw[];
@@ -324,6 +325,7 @@ __global__ void __launch_bounds__(kTsThreads)
     thomas_small_kernel(R *__restrict__ f, ThomasGeom<R> tx, ThomasGeom<R> ty,
                         ThomasGeom<R> tz, uint32_t m0, uint32_t m1, uint32_t m2,
                         uint32_t refine, Epi epi, const R *base, R *out) {
+  pdl_wait();
   extern __shared__ __align__(16) unsigned char ts_raw[];
   R *s = reinterpret_cast<R *>(ts_raw);
   const uint32_t n = m0 * m1 * m2;
