@@ -457,6 +457,7 @@ template <typename R, int B = 8>
 __global__ void __launch_bounds__(128)
     thomas_strided_kernel(R *f, ThomasGeom<R> t, uint64_t S, uint32_t inner,
                           uint64_t ostride, uint64_t nfibers, Epi epi, const R *base, R *out) {
+  pdl_wait();
   // f, base and out may alias (the epilogues write in place): no __restrict__
   const uint64_t k = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
   if (k >= nfibers)

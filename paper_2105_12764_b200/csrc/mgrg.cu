@@ -917,8 +917,8 @@ void launch_thomas(bool fast, const LevelGeom<R> &g, const ThomasGeom<R> &t,
     const unsigned blocks = unsigned((nfib + te_nf<R>() - 1) / te_nf<R>());
     auto k = kd == 0 ? thomas_exact_kernel<R, 0>
                      : (kd == 1 ? thomas_exact_kernel<R, 1> : thomas_exact_kernel<R, 2>);
-    k<<<blocks, kTeThreads, te_smem<R>(kd, t.m), s>>>(f, t, nfib, uint32_t(mx), uint32_t(my),
-                                                      epi, base, out);
+    launch_pdl(k, blocks, kTeThreads, te_smem<R>(kd, t.m), s, f, t, nfib, uint32_t(mx),
+               uint32_t(my), epi, base, out);
     return;
   }
   if (kd == 0) {
@@ -940,8 +940,8 @@ void launch_thomas(bool fast, const LevelGeom<R> &g, const ThomasGeom<R> &t,
     const uint64_t nf = mx * (kd == 1 ? mz : my);
     if (fast && kd == 1 && try_scan<R>(1, t, S, mx, mx * my, nf, f, epi, base, out, s))
       return;
-    thomas_strided_kernel<R><<<unsigned((nf + 127) / 128), 128, 0, s>>>(
-        f, t, S, uint32_t(mx), ostride, nf, epi, base, out);
+    launch_pdl(thomas_strided_kernel<R, 8>, unsigned((nf + 127) / 128), 128, 0, s, f, t, S,
+               uint32_t(mx), ostride, nf, epi, base, out);
   }
 }
 

@@ -43,6 +43,7 @@ template <typename R, int DIM>
 __global__ void __launch_bounds__(kTeThreads, 3)
     thomas_exact_kernel(R *f, ThomasGeom<R> t, uint64_t nfib, uint32_t m0, uint32_t m1,
                         Epi epi, const R *base, R *out) {
+  pdl_wait();
   // f, base and out may alias (epilogues write in place)
   constexpr int NF = te_nf<R>();
   constexpr int V = 16 / int(sizeof(R));
