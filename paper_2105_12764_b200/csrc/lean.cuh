@@ -900,7 +900,10 @@ __global__ void __launch_bounds__(32 * kLeanWPB, 4)
 inline int lean_zc(uint64_t xy_tiles, uint32_t m2, bool z3) {
   if (!z3)
     return 1;
-  const uint64_t want = 148ull * 32; // warps
+#ifndef LEAN_ZC_WANT
+#define LEAN_ZC_WANT 32
+#endif
+  const uint64_t want = 148ull * LEAN_ZC_WANT; // warps
   int zc = kLeanZC;
   while (zc > LEAN_ZC_MIN && xy_tiles * ((m2 + zc - 1) / zc) < want)
     zc /= 2;
