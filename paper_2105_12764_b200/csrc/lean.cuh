@@ -734,7 +734,15 @@ __global__ void __launch_bounds__(32 * kLeanWPB, LEAN_RL_MINB)
 // coarse row cy1 for the last odd row) through a chunk of coarse planes;
 // the interpolant of the previous even plane is carried in registers.
 // CLS = false: classes above classes_used (all zero): pure prolongation.
-template <typename R> __host__ __device__ constexpr int lean_tg() { return sizeof(R) == 4 ? 4 : 2; }
+#ifndef LEAN_RG_TG
+#define LEAN_RG_TG 4
+#endif
+#ifndef LEAN_RG_MINB
+#define LEAN_RG_MINB 4
+#endif
+template <typename R> __host__ __device__ constexpr int lean_tg() {
+  return sizeof(R) == 4 ? LEAN_RG_TG : 2;
+}
 constexpr int kLeanGOut = 31;
 
 template <typename R, bool ALIGNED>
@@ -757,7 +765,7 @@ __device__ __forceinline__ void lean_store_pair(R *p, R e, R o, bool we, bool wo
 }
 
 template <typename R, bool Z3, bool CLS, bool FAST>
-__global__ void __launch_bounds__(32 * kLeanWPB, 4)
+__global__ void __launch_bounds__(32 * kLeanWPB, LEAN_RG_MINB)
     lean_rgpk_kernel(LevelGeom<R> g, const LeanW<R> *__restrict__ lx,
                      const LeanW<R> *__restrict__ ly, const LeanW<R> *__restrict__ lz,
                      const R *__restrict__ coarse, const R *__restrict__ cls,
