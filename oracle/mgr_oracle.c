@@ -8,8 +8,10 @@
 #include "mgr_oracle.h"
 
 #include <math.h>
+#include <pthread.h>
 #include <stdlib.h>
 #include <string.h>
+#include <unistd.h>
 
 /* status codes: keep in sync with include/mgrg.h (errors.hpp:27-37) */
 enum {
@@ -198,6 +200,71 @@ static uint64_t class_slot(const layout_t *c, int nd, const uint64_t *lshape,
     mult *= c->ext[mask][d];
   }
   return c->base[mask] + idx;
+}
+
+/* ---- row-parallel loops (pthreads) ----------------------------------------
+ * The engine's row loops (GPK rows, mass-transfer fibers, Thomas fibers,
+ * pack / expand / scatter elements) are independent: every element is
+ * computed by exactly the reference expression in the reference order, so
+ * splitting a loop over threads never changes a value.  This only makes the
+ * checker fast enough to run at the BASELINE sizes (1025^3) inside the GPU
+ * test suite.  Small loops run on the calling thread. */
+static int g_threads = 0; /* 0 = all online CPUs */
+
+int mgro_set_threads(int n) {
+  int old = g_threads;
+  g_threads = n < 0 ? 0 : n;
+  return old;
+}
+
+typedef void (*range_fn)(void *ctx, int64_t lo, int64_t hi);
+typedef struct {
+  range_fn fn;
+  void *ctx;
+  int64_t lo, hi;
+} par_job;
+
+static void *par_tramp(void *p) {
+  par_job *j = (par_job *)p;
+  j->fn(j->ctx, j->lo, j->hi);
+  return NULL;
+}
+
+/* fn over [0, n) split in contiguous ranges; `work` = elements touched, the
+ * serial cutoff. */
+static void par_for(int64_t n, uint64_t work, range_fn fn, void *ctx) {
+  int T = g_threads;
+  if (T <= 0) {
+    long c = sysconf(_SC_NPROCESSORS_ONLN);
+    T = c > 0 ? (int)c : 1;
+  }
+  if (T > 64)
+    T = 64;
+  if ((int64_t)T > n)
+    T = (int)n;
+  if (T <= 1 || work < (1u << 18)) {
+    if (n > 0)
+      fn(ctx, 0, n);
+    return;
+  }
+  pthread_t th[64];
+  par_job job[64];
+  int started[64] = {0};
+  for (int t = 0; t < T; ++t) {
+    job[t].fn = fn;
+    job[t].ctx = ctx;
+    job[t].lo = n * t / T;
+    job[t].hi = n * (t + 1) / T;
+    if (t > 0)
+      started[t] = pthread_create(&th[t], NULL, par_tramp, &job[t]) == 0;
+  }
+  fn(ctx, job[0].lo, job[0].hi);
+  for (int t = 1; t < T; ++t) {
+    if (started[t])
+      pthread_join(th[t], NULL);
+    else
+      fn(ctx, job[t].lo, job[t].hi); /* thread creation failed: run inline */
+  }
 }
 
 int mgro_hierarchy(int ndims, const uint64_t *shape, const double *coords,

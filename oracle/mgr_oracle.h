@@ -96,6 +96,10 @@ int mgro_reorder_f64(int ndims, const uint64_t *shape, const double *coords,
                      int levels_cap, int level, int direction,
                      const double *in, double *out);
 
+/* Worker threads of the engine's row-parallel loops (0 = all online CPUs,
+ * 1 = serial); returns the previous setting.  Never changes a value. */
+int mgro_set_threads(int n);
+
 #ifdef __cplusplus
 }
 #endif
