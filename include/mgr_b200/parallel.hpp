@@ -19,6 +19,7 @@
 #include <array>
 #include <functional>
 #include <map>
+#include <sstream>
 #include <string>
 #include <utility>
 #include <vector>
@@ -115,11 +116,45 @@ struct CommPhaseStats {
   std::uint64_t local_elements = 0;
   double seconds = 0;
 };
+// Idle workers per pipeline stage of one ordered sweep (parallel.hpp:44-50).
+struct IdleRecord {
+  std::size_t level = 0;
+  std::size_t dim = 0;
+  std::vector<int> idle_per_stage;
+};
 struct CommReport {
   int workers = 0;
   PartitionScheme scheme = PartitionScheme::block;
   std::map<std::string, CommPhaseStats> phases;
+  std::vector<IdleRecord> idle;
   std::uint64_t total_grid_elements = 0;
+  // parallel.cpp:264-292: the same keys, order and number formatting
+  // (std::ostream defaults) as the reference, so tools that parse the
+  // reference's report (mgrf.cpp:150-158) read this one.
+  std::string to_json() const {
+    std::ostringstream os;
+    os << "{\"workers\":" << workers << ",\"scheme\":\"" << to_string(scheme)
+       << "\",\"grid_elements\":" << total_grid_elements << ",\"phases\":{";
+    bool first = true;
+    for (const auto &[name, st] : phases) {
+      os << (first ? "" : ",") << "\"" << name << "\":{\"messages\":" << st.messages
+         << ",\"elements\":" << st.elements << ",\"local_elements\":" << st.local_elements
+         << ",\"seconds\":" << st.seconds << "}";
+      first = false;
+    }
+    os << "},\"idle\":[";
+    first = true;
+    for (const auto &rec : idle) {
+      os << (first ? "" : ",") << "{\"level\":" << rec.level << ",\"dim\":" << rec.dim
+         << ",\"idle_per_stage\":[";
+      for (std::size_t i = 0; i < rec.idle_per_stage.size(); ++i)
+        os << (i ? "," : "") << rec.idle_per_stage[i];
+      os << "]}";
+      first = false;
+    }
+    os << "]}";
+    return os.str();
+  }
 };
 
 // parallel.hpp:61-71
@@ -164,15 +199,23 @@ RefactoredData<Real> cooperative_decompose(const TensorGrid<Real> &grid, int wor
     flat.insert(flat.end(), grid.coords[d].begin(), grid.coords[d].end());
   }
   desc.coords = flat.data();
-  desc.levels = opt.levels ? int32_t(*opt.levels) : 0;
+  desc.levels = b200_detail::levels_arg(opt.levels);
   desc.device = opt.device;
   desc.flags = opt.fast ? MGRG_FLAG_FAST : 0;
   std::vector<Real> out(grid.values.size());
   std::uint64_t moved = 0;
+  const auto t0 = std::chrono::steady_clock::now();
   b200_detail::check(mgrg_cooperative_decompose_host(
       &desc, workers, grid.values.data(), out.data(),
       opt.fault_injector ? &b200_detail::fault_trampoline : nullptr,
       const_cast<CoopOptions *>(&opt), &moved));
+  const double secs =
+      std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+  // class layout of the whole-grid plan
+  mgrg_plan *p = b200_detail::plan_for<Real>(grid.shape, grid.coords, opt.levels, opt.device,
+                                             opt.fast);
+  int32_t L = 0;
+  b200_detail::check(mgrg_plan_levels(p, &L));
   if (opt.report) {
     opt.report->workers = workers;
     opt.report->scheme = opt.scheme;
@@ -180,12 +223,31 @@ RefactoredData<Real> cooperative_decompose(const TensorGrid<Real> &grid, int wor
     auto &ph = opt.report->phases["device"];
     ph.messages += 1;
     ph.elements += moved;
+    ph.seconds += secs;
+    // idle workers per stage of the ordered (chained) z solves, the one
+    // sweep the runtime orders across workers (compute_idle_records,
+    // parallel.cpp:217-258, for the runtime's z-slab partition): stage s of
+    // the chain at a cooperative level is worker s's slab, so W - 1 workers
+    // wait in every stage (fewer active when a slab holds no coarse plane)
+    int32_t q = 0;
+    std::vector<uint64_t> bounds(std::size_t(workers) + 1);
+    b200_detail::check(mgrg_coop_schedule(p, workers, &q, bounds.data()));
+    opt.report->idle.clear();
+    for (int j = 0; j < q; ++j) {
+      uint64_t ls[4] = {1, 1, 1, 1};
+      b200_detail::check(mgrg_plan_level_shape(p, L - j - 1, ls));
+      IdleRecord rec;
+      rec.level = std::size_t(L - j);
+      rec.dim = 2;
+      rec.idle_per_stage.assign(std::size_t(workers), workers);
+      for (int r = 0; r < workers; ++r) {
+        const uint64_t c0 = bounds[r] >> (j + 1);
+        const uint64_t c1 = r == workers - 1 ? ls[2] : bounds[r + 1] >> (j + 1);
+        rec.idle_per_stage[r] = workers - (c1 > c0 ? 1 : 0);
+      }
+      opt.report->idle.push_back(std::move(rec));
+    }
   }
-  // class layout of the whole-grid plan
-  mgrg_plan *p = b200_detail::plan_for<Real>(grid.shape, grid.coords, opt.levels, opt.device,
-                                             opt.fast);
-  int32_t L = 0;
-  b200_detail::check(mgrg_plan_levels(p, &L));
   std::vector<uint64_t> off(std::size_t(L) + 2);
   b200_detail::check(mgrg_plan_class_offsets(p, off.data()));
   RefactoredData<Real> r;
@@ -198,8 +260,10 @@ RefactoredData<Real> cooperative_decompose(const TensorGrid<Real> &grid, int wor
 }
 
 // mgr::grouped_decompose (parallel_impl.hpp:849-885): K groups of S
-// cooperating workers, block i to group i mod K (the runtime spreads each
-// group's workers over the visible GPUs).
+// cooperating workers run concurrently, one host thread per group, block i
+// to group i mod K; group g's workers start at GPU g * S (mod the visible
+// GPUs) so concurrent groups land on distinct devices when there are enough.
+// The first failure stops the groups and surfaces as WorkerFailure.
 template <typename Real>
 std::vector<RefactoredData<Real>>
 grouped_decompose(const std::vector<TensorGrid<Real>> &blocks, int num_groups, int group_size,
@@ -207,19 +271,37 @@ grouped_decompose(const std::vector<TensorGrid<Real>> &blocks, int num_groups, i
   if (num_groups < 1 || group_size < 1)
     throw TooManyWorkers("group shape must be positive");
   std::vector<RefactoredData<Real>> out(blocks.size());
+  int32_t ndev = 1;
+  if (mgrg_device_count(&ndev) != MGRG_OK || ndev < 1)
+    ndev = 1;
+  std::atomic<bool> failed{false};
+  std::mutex err_mu;
+  std::string err;
+  std::vector<std::thread> threads;
   const int groups = std::max(1, std::min<int>(num_groups, int(blocks.size())));
-  for (std::size_t i = 0; i < blocks.size(); ++i) {
-    CoopOptions o;
-    o.scheme = scheme;
-    (void)groups;
-    try {
-      out[i] = cooperative_decompose(blocks[i], group_size, o);
-    } catch (const WorkerFailure &) {
-      throw;
-    } catch (const std::exception &e) {
-      throw WorkerFailure(e.what());
-    }
-  }
+  for (int g = 0; g < groups; ++g)
+    threads.emplace_back([&, g] {
+      for (std::size_t i = std::size_t(g); i < blocks.size(); i += std::size_t(groups)) {
+        if (failed.load())
+          break;
+        try {
+          CoopOptions o;
+          o.scheme = scheme;
+          o.device = (g * group_size) % int(ndev);
+          out[i] = cooperative_decompose(blocks[i], group_size, o);
+        } catch (const std::exception &e) {
+          std::lock_guard<std::mutex> lk(err_mu);
+          err = e.what();
+          failed.store(true);
+          break;
+        }
+      }
+      release_plans();
+    });
+  for (auto &t : threads)
+    t.join();
+  if (failed.load())
+    throw WorkerFailure(err);
   return out;
 }
 

@@ -136,7 +136,26 @@ inline RefactorFileHeader read_refactored_header(const std::string &path) {
 template <typename Real>
 std::uint64_t write_refactored_t(const RefactoredData<Real> &r, const std::string &path) {
   mgrg_plan *p = b200_detail::plan_for<Real>(r.shape, r.coords, r.levels, 0, false);
+  int32_t L = 0;
+  b200_detail::check(mgrg_plan_levels(p, &L));
+  if (std::size_t(L) != r.levels)
+    throw InvalidLevel("container has " + std::to_string(r.levels) +
+                       " levels; grid supports " + std::to_string(L));
+  // the device writer streams all L+1 classes from one buffer: a prefix
+  // (read_refactored(path, k < L)) or a mis-sized class is rejected here
+  // instead of reading past the caller's vectors
+  if (r.classes.size() != std::size_t(L) + 1)
+    throw MissingClass("write_refactored needs all " + std::to_string(L + 1) +
+                       " classes; got " + std::to_string(r.classes.size()));
+  std::vector<uint64_t> off(std::size_t(L) + 2);
+  b200_detail::check(mgrg_plan_class_offsets(p, off.data()));
+  for (int l = 0; l <= L; ++l)
+    if (r.classes[l].size() != off[l + 1] - off[l])
+      throw ShapeError("class " + std::to_string(l) + " has " +
+                       std::to_string(r.classes[l].size()) + " entries, expected " +
+                       std::to_string(off[l + 1] - off[l]));
   std::vector<Real> flat;
+  flat.reserve(off[L + 1]);
   for (const auto &c : r.classes)
     flat.insert(flat.end(), c.begin(), c.end());
   std::uint64_t n = 0;

@@ -31,6 +31,7 @@
 #include <stdexcept>
 #include <string>
 #include <thread>
+#include <tuple>
 #include <type_traits>
 #include <vector>
 
@@ -228,13 +229,18 @@ struct RefactorOptions {
 namespace b200_detail {
 
 // One plan per (geometry, dtype, levels, device, policy), reused across
-// calls like a long-lived engine; plans are not shared between threads.
+// calls like a long-lived engine; plans are not shared between threads.  The
+// per-thread cache is a small LRU (plan_cache_capacity(), default 4 plans):
+// a plan owns its geometry tables, a workspace of about N/4 elements and,
+// after a host-buffer call, a 2N staging buffer, so a caller cycling through
+// many distinct block geometries (config 5's coordinate slices) must not pin
+// them all.  The evicted plan is destroyed (its device memory freed).
 struct PlanKey {
   Shape shape;
   std::vector<double> coords;
   int dtype, levels, device, fast;
-  bool operator<(const PlanKey &o) const {
-    return std::tie(shape, coords, dtype, levels, device, fast) <
+  bool operator==(const PlanKey &o) const {
+    return std::tie(shape, coords, dtype, levels, device, fast) ==
            std::tie(o.shape, o.coords, o.dtype, o.levels, o.device, o.fast);
   }
 };
@@ -243,6 +249,15 @@ struct PlanDeleter {
 };
 using PlanPtr = std::unique_ptr<mgrg_plan, PlanDeleter>;
 
+inline std::size_t &plan_cache_capacity_ref() {
+  thread_local std::size_t cap = 4;
+  return cap;
+}
+inline std::vector<std::pair<PlanKey, PlanPtr>> &plan_cache() { // most recent last
+  thread_local std::vector<std::pair<PlanKey, PlanPtr>> cache;
+  return cache;
+}
+
 inline bool is_uniform(const Shape &shape, const std::vector<std::vector<double>> &c) {
   for (std::size_t d = 0; d < shape.size(); ++d)
     if (c[d] != uniform_coords(shape[d]))
@@ -250,20 +265,33 @@ inline bool is_uniform(const Shape &shape, const std::vector<std::vector<double>
   return true;
 }
 
+// RefactorOptions::levels as the reference reads it (grid.cpp:99-102): an
+// engaged count below 1 is InvalidLevel; counts beyond the grid's depth are
+// capped by the hierarchy, so clamp before narrowing to the C ABI's int32.
+inline int32_t levels_arg(std::optional<std::size_t> levels) {
+  if (!levels)
+    return 0; // full depth
+  if (*levels < 1)
+    throw InvalidLevel("level count must be at least 1");
+  return int32_t(std::min<std::size_t>(*levels, 64));
+}
+
 template <typename Real>
 mgrg_plan *plan_for(const Shape &shape, const std::vector<std::vector<double>> &coords,
                     std::optional<std::size_t> levels, int device, bool fast) {
   static_assert(std::is_same_v<Real, float> || std::is_same_v<Real, double>,
                 "Real must be float or double");
-  thread_local std::map<PlanKey, PlanPtr> cache;
-  PlanKey key{shape, {}, int(sizeof(Real)), levels ? int(*levels) : 0, device, fast};
+  auto &cache = plan_cache();
+  PlanKey key{shape, {}, int(sizeof(Real)), levels_arg(levels), device, fast};
   const bool uni = is_uniform(shape, coords);
   if (!uni)
     for (const auto &c : coords)
       key.coords.insert(key.coords.end(), c.begin(), c.end());
-  auto it = cache.find(key);
-  if (it != cache.end())
-    return it->second.get();
+  for (std::size_t i = 0; i < cache.size(); ++i)
+    if (cache[i].first == key) {
+      std::rotate(cache.begin() + i, cache.begin() + i + 1, cache.end());
+      return cache.back().second.get();
+    }
   mgrg_grid_desc desc{};
   desc.ndims = int32_t(shape.size());
   desc.dtype = sizeof(Real) == 4 ? MGRG_F32 : MGRG_F64;
@@ -273,45 +301,59 @@ mgrg_plan *plan_for(const Shape &shape, const std::vector<std::vector<double>> &
   desc.levels = key.levels;
   desc.device = device;
   desc.flags = fast ? MGRG_FLAG_FAST : 0;
+  const std::size_t cap = std::max<std::size_t>(1, plan_cache_capacity_ref());
+  while (cache.size() >= cap) // free before allocating the new plan
+    cache.erase(cache.begin());
   mgrg_plan *p = nullptr;
   check(mgrg_plan_create(&desc, &p));
-  cache.emplace(key, PlanPtr(p));
+  cache.emplace_back(std::move(key), PlanPtr(p));
   return p;
 }
 
-// The documented traffic composition (refactor.hpp:223-421, README passes).
-inline void fill_stats(PassStats &stats, mgrg_plan *p, std::size_t nd) {
-  stats.levels.clear();
+// The per-level traffic counters the reference engine accumulates
+// (refactor.hpp:223-421): decompose clears stats and appends levels finest
+// first; recompose appends levels coarsest first without clearing
+// (refactor.hpp:159-199).  The GPU kernels fuse these phases; the counters
+// report the reference's documented composition, which acceptance criterion
+// 9 (acceptance.cpp:336-374) checks.
+inline LevelPassStats level_stats(mgrg_plan *p, int l, std::size_t nd) {
+  uint64_t ls[4] = {1, 1, 1, 1}, cs[4] = {1, 1, 1, 1};
+  check(mgrg_plan_level_shape(p, l, ls));
+  check(mgrg_plan_level_shape(p, l - 1, cs));
+  uint64_t F = 1, C = 1;
+  for (std::size_t d = 0; d < nd; ++d) {
+    F *= ls[d];
+    C *= cs[d];
+  }
+  LevelPassStats s;
+  s.level = std::size_t(l);
+  s.level_elements = F;
+  s.coefficient = {F, F - C};
+  s.fused_copy = {0, F - C};
+  s.masstrans.resize(nd);
+  s.solve.resize(nd);
+  uint64_t cur = F;
+  for (std::size_t d = 0; d < nd; ++d)
+    if (cs[d] < ls[d]) {
+      const uint64_t out = cur / ls[d] * cs[d];
+      s.masstrans[d] = {cur, out};
+      s.solve[d] = {2 * C, 2 * C};
+      cur = out;
+    }
+  s.apply = {2 * C, C};
+  return s;
+}
+
+inline void fill_stats(PassStats &stats, mgrg_plan *p, std::size_t nd, bool recompose) {
   int32_t L = 0;
-  mgrg_plan_levels(p, &L);
-  for (int l = L; l >= 1; --l) {
-    uint64_t ls[4] = {1, 1, 1, 1}, cs[4] = {1, 1, 1, 1};
-    mgrg_plan_level_shape(p, l, ls);
-    mgrg_plan_level_shape(p, l - 1, cs);
-    uint64_t F = 1, C = 1;
-    for (std::size_t d = 0; d < nd; ++d) {
-      F *= ls[d];
-      C *= cs[d];
-    }
-    LevelPassStats s;
-    s.level = std::size_t(l);
-    s.level_elements = F;
-    s.coefficient = {F, F - C};
-    s.fused_copy = {0, F - C};
-    uint64_t cur = F;
-    for (std::size_t d = 0; d < nd; ++d) {
-      if (cs[d] < ls[d]) {
-        const uint64_t out = cur / ls[d] * cs[d];
-        s.masstrans.push_back({cur, out});
-        s.solve.push_back({2 * C, 2 * C});
-        cur = out;
-      } else {
-        s.masstrans.push_back({});
-        s.solve.push_back({});
-      }
-    }
-    s.apply = {2 * C, C};
-    stats.levels.push_back(s);
+  check(mgrg_plan_levels(p, &L));
+  if (!recompose) {
+    stats.levels.clear();
+    for (int l = L; l >= 1; --l)
+      stats.levels.push_back(level_stats(p, l, nd));
+  } else {
+    for (int l = 1; l <= L; ++l)
+      stats.levels.push_back(level_stats(p, l, nd));
   }
 }
 
@@ -341,7 +383,7 @@ RefactoredData<Real> decompose(const TensorGrid<Real> &grid,
   for (int l = 0; l <= L; ++l)
     out.classes.emplace_back(flat.begin() + off[l], flat.begin() + off[l + 1]);
   if (opt.stats)
-    b200_detail::fill_stats(*opt.stats, p, grid.shape.size());
+    b200_detail::fill_stats(*opt.stats, p, grid.shape.size(), false);
   return out;
 }
 
@@ -378,43 +420,55 @@ TensorGrid<Real> recompose(const RefactoredData<Real> &r, std::size_t classes_us
   g.values.resize(num_elements(r.shape));
   b200_detail::check(
       mgrg_recompose_host(p, flat.data(), int32_t(classes_used), g.values.data()));
+  if (opt.stats)
+    b200_detail::fill_stats(*opt.stats, p, r.shape.size(), true);
   return g;
 }
 
 // mgr::recompose_with_report (refactor.hpp:500-534); the weighted-L2 norm
 // (grid.hpp:198-244) is a host-side reporting metric.
-template <typename Real>
-double weighted_l2_norm(const TensorGrid<Real> &g) {
+namespace b200_detail {
+// detail::mass_fiber (grid.hpp:198-214) with Weight = Real = double: the
+// reference's coefficients and evaluation order, so the norm is bit-identical.
+inline void mass_fiber(const double *in, double *out, const double *h, std::size_t n) {
+  if (n == 1) {
+    out[0] = in[0];
+    return;
+  }
+  out[0] = double(2 * h[0]) * in[0] + double(h[0]) * in[1];
+  for (std::size_t i = 1; i + 1 < n; ++i)
+    out[i] = double(h[i - 1]) * in[i - 1] + double(2 * (h[i - 1] + h[i])) * in[i] +
+             double(h[i]) * in[i + 1];
+  out[n - 1] = double(h[n - 2]) * in[n - 2] + double(2 * h[n - 2]) * in[n - 1];
+}
+} // namespace b200_detail
+
+// mgr::weighted_l2_norm (grid.hpp:218-244): sqrt(v^T (M_0 x M_1 x ...) v)
+// with the finest-level mass matrices, accumulated in double.
+template <typename Real> double weighted_l2_norm(const TensorGrid<Real> &g) {
   std::vector<double> w(g.values.begin(), g.values.end());
   const std::size_t nd = g.shape.size();
   std::size_t stride = 1;
   for (std::size_t d = 0; d < nd; ++d) {
     const std::size_t n = g.shape[d];
-    const auto &c = g.coords[d];
-    std::vector<double> out(w.size());
+    std::vector<double> h(n > 1 ? n - 1 : 0), fin(n), fout(n);
+    for (std::size_t i = 0; i + 1 < n; ++i)
+      h[i] = g.coords[d][i + 1] - g.coords[d][i];
     const std::size_t outer = w.size() / (n * stride);
     for (std::size_t o = 0; o < outer; ++o)
       for (std::size_t s = 0; s < stride; ++s) {
         const std::size_t b = o * n * stride + s;
-        for (std::size_t i = 0; i < n; ++i) {
-          double v = 0;
-          if (i > 0) {
-            const double h = c[i] - c[i - 1];
-            v += h * w[b + (i - 1) * stride] + 2 * h * w[b + i * stride];
-          }
-          if (i + 1 < n) {
-            const double h = c[i + 1] - c[i];
-            v += 2 * h * w[b + i * stride] + h * w[b + (i + 1) * stride];
-          }
-          out[b + i * stride] = v;
-        }
+        for (std::size_t i = 0; i < n; ++i)
+          fin[i] = w[b + i * stride];
+        b200_detail::mass_fiber(fin.data(), fout.data(), h.data(), n);
+        for (std::size_t i = 0; i < n; ++i)
+          w[b + i * stride] = fout[i];
       }
-    w.swap(out);
     stride *= n;
   }
   double dot = 0;
   for (std::size_t i = 0; i < w.size(); ++i)
-    dot += w[i] * double(g.values[i]);
+    dot += w[i] * static_cast<double>(g.values[i]);
   return std::sqrt(std::max(dot, 0.0));
 }
 
@@ -477,18 +531,36 @@ decompose_spatiotemporal(const std::vector<TensorGrid<Real>> &snapshots,
   return decompose(make_grid(std::move(shape), std::move(values), std::move(coords), 2), opt);
 }
 
+// Per-thread plan cache capacity (see b200_detail::plan_for); returns the
+// previous value.  Shrinking takes effect at the next plan creation.
+inline std::size_t set_plan_cache_capacity(std::size_t plans) {
+  std::size_t &c = b200_detail::plan_cache_capacity_ref();
+  const std::size_t old = c;
+  c = std::max<std::size_t>(1, plans);
+  return old;
+}
+// Destroy this thread's cached plans (frees their device memory).
+inline void release_plans() { b200_detail::plan_cache().clear(); }
+
 // mgr::embarrassing_decompose (parallel_impl.hpp:810-847): a pool of
-// min(workers, blocks, visible GPUs) host threads, one GPU each, claiming
-// blocks from a shared counter; result i == decompose(blocks[i]); the first
-// failure stops the pool and surfaces as WorkerFailure.
+// min(workers, blocks, visible GPUs) host threads, thread w driving GPU
+// (opt.device + w) mod the visible GPUs (one B200 is saturated by one block,
+// so more threads than GPUs would only contend), claiming blocks from a
+// shared counter; result i == decompose(blocks[i]); the first failure stops
+// the pool and surfaces as WorkerFailure.  Each pool thread releases its
+// plans on exit.
 template <typename Real>
 std::vector<RefactoredData<Real>>
 embarrassing_decompose(const std::vector<TensorGrid<Real>> &blocks, int workers,
-                       const RefactorOptions &opt = {}, int devices = 1) {
+                       const RefactorOptions &opt = {}) {
   std::vector<RefactoredData<Real>> out(blocks.size());
   if (blocks.empty())
     return out;
-  const int pool = std::max(1, std::min<int>({workers, int(blocks.size()), devices}));
+  int32_t ndev = 0;
+  b200_detail::check(mgrg_device_count(&ndev));
+  if (ndev < 1)
+    throw CudaError("no CUDA device visible");
+  const int pool = std::max(1, std::min<int>({workers, int(blocks.size()), int(ndev)}));
   std::atomic<std::size_t> next{0};
   std::atomic<bool> failed{false};
   std::mutex err_mu;
@@ -499,19 +571,20 @@ embarrassing_decompose(const std::vector<TensorGrid<Real>> &blocks, int workers,
       for (;;) {
         const std::size_t i = next.fetch_add(1);
         if (i >= blocks.size() || failed.load())
-          return;
+          break;
         try {
           RefactorOptions o = opt;
           o.stats = nullptr;
-          o.device = opt.device + w;
+          o.device = (opt.device + w) % int(ndev);
           out[i] = decompose(blocks[i], o);
         } catch (const std::exception &e) {
           std::lock_guard<std::mutex> lk(err_mu);
           err = e.what();
           failed.store(true);
-          return;
+          break;
         }
       }
+      release_plans();
     });
   for (auto &t : threads)
     t.join();

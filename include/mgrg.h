@@ -287,6 +287,66 @@ mgrg_status mgrg_decompress_host(mgrg_plan *plan, const uint8_t *bytes, uint64_t
                                  void *h_values, double *error_bound, double *bin,
                                  double *measured, int32_t *codec);
 
+/* ---- devices, cooperative schedule ---------------------------------------
+ * Visible CUDA devices (embarrassing_decompose's worker -> GPU map,
+ * parallel_impl.hpp:810-847: one host thread per GPU). */
+mgrg_status mgrg_device_count(int32_t *count);
+/* The slab schedule mgrg_cooperative_decompose_host uses for this plan's grid
+ * and `workers` workers: *q = number of cooperative (top) levels (0: worker 0
+ * runs the whole decompose), bounds[0..workers] = finest-plane z slab
+ * boundaries (bounds has workers + 1 entries; untouched when *q == 0).  The
+ * C++ drop-in derives CommReport::idle (parallel.cpp:217-258) from it. */
+mgrg_status mgrg_coop_schedule(const mgrg_plan *plan, int32_t workers, int32_t *q,
+                               uint64_t *bounds);
+
+/* ---- block metadata gather over NCCL --------------------
+ * The one collective of the block-sharded path: every rank holds whole
+ * blocks (embarrassing_decompose, parallel_impl.hpp:810-847), and a single
+ * ncclAllGather of fixed-size per-block records tells every rank where every
+ * block's classes are and how large they are (the MGRF class records,
+ * pipeline.cpp:180-206, without the payload).  No bulk data crosses GPUs. */
+#define MGRG_MAX_CLASSES 32
+typedef struct mgrg_block_meta {
+  int64_t block_id;                         /* -1: padding record          */
+  int32_t rank;                             /* producing rank              */
+  int32_t dtype;                            /* 4 | 8                       */
+  int32_t ndims;
+  int32_t levels;                           /* L; classes 0..L             */
+  uint64_t origin[4];                       /* block origin in the field   */
+  uint64_t shape[4];
+  uint64_t class_bytes[MGRG_MAX_CLASSES];   /* class l byte length         */
+  uint32_t class_crc32[MGRG_MAX_CLASSES];   /* mgr::crc32 of class l bytes */
+  uint32_t checksum;                        /* crc32 of class_crc32[0..L]  */
+  uint32_t reserved;
+  double decompose_ms;                      /* device time, caller-supplied */
+  double recompose_ms;
+} mgrg_block_meta;
+/* Fill `meta` for a decomposed block: geometry and class byte lengths from
+ * the plan, per-class CRC-32 of d_classes on the GPU (synchronous on
+ * `stream`), the checksum of the CRCs; origin (ndims entries, may be NULL =
+ * zeros), block id and timings from the caller. */
+mgrg_status mgrg_block_meta_fill(mgrg_plan *plan, const void *d_classes, int64_t block_id,
+                                 int32_t rank, const uint64_t *origin, double decompose_ms,
+                                 double recompose_ms, mgrg_block_meta *meta, void *stream);
+/* One communicator per rank, one rank per GPU (NCCL over NVLink/NVSwitch).
+ * Rank 0 makes the unique id; the caller ships its 128 bytes to the other
+ * ranks (MPI, a TCP store, a file) before every rank calls mgrg_comm_init. */
+typedef struct mgrg_comm mgrg_comm;
+#define MGRG_COMM_ID_BYTES 128
+mgrg_status mgrg_comm_unique_id(uint8_t id[MGRG_COMM_ID_BYTES]);
+mgrg_status mgrg_comm_init(const uint8_t id[MGRG_COMM_ID_BYTES], int32_t nranks,
+                           int32_t rank, int32_t device, mgrg_comm **comm);
+mgrg_status mgrg_comm_destroy(mgrg_comm *comm);
+mgrg_status mgrg_comm_size(const mgrg_comm *comm, int32_t *nranks, int32_t *rank);
+/* All-gather of `per_rank` records from every rank (pad with block_id = -1
+ * when ranks hold different block counts): all[r * per_rank + i] = rank r's
+ * mine[i].  Host buffers in and out; one ncclAllGather on the comm's device,
+ * ordered after `stream` (may be NULL) and synchronous.  MGRG_NCCL_ERROR on
+ * a collective failure. */
+mgrg_status mgrg_comm_allgather_block_meta(mgrg_comm *comm, const mgrg_block_meta *mine,
+                                           int32_t per_rank, mgrg_block_meta *all,
+                                           void *stream);
+
 #ifdef __cplusplus
 }
 #endif

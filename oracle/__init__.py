@@ -376,3 +376,31 @@ def ref_decompress(data: bytes, n_elements, dtype):
     if rc < 0:
         raise OracleError(int(-rc), "mgrref_decompress")
     return out
+
+
+def ref_pass_stats(values: np.ndarray, shape, coords=None, levels_cap: int = 0,
+                   recompose: bool = False):
+    """The reference engine's PassStats (refactor.hpp:223-421) of a decompose
+    (+ a full recompose into the same stats when `recompose`): list of
+    per-level dicts in the reference's record order."""
+    lib = _lib("ref")
+    nd = len(shape)
+    v = np.ascontiguousarray(values, dtype=np.float64)
+    cflat, cptr = _coords_arr(shape, coords)
+    w = 8 + 4 * nd
+    out = np.zeros(128 * w, dtype=np.uint64)
+    n = ctypes.c_int(0)
+    fn = lib.mgrref_pass_stats_f64
+    fn.restype = ctypes.c_int
+    _check(fn(nd, _shape_arr(shape), cptr, int(levels_cap), _ptr(v), int(bool(recompose)),
+              _ptr(out), 128, ctypes.byref(n)), "pass_stats")
+    recs = []
+    for i in range(n.value):
+        o = [int(x) for x in out[i * w:(i + 1) * w]]
+        recs.append({"level": o[0], "level_elements": o[1], "coefficient": (o[2], o[3]),
+                     "fused_copy": (o[4], o[5]),
+                     "masstrans": [(o[6 + 2 * d], o[7 + 2 * d]) for d in range(nd)],
+                     "solve": [(o[6 + 2 * nd + 2 * d], o[7 + 2 * nd + 2 * d])
+                               for d in range(nd)],
+                     "apply": (o[6 + 4 * nd], o[7 + 4 * nd])})
+    return recs

@@ -450,6 +450,101 @@ int64_t mgrref_decompress(const uint8_t *bytes, uint64_t n, void *values, uint64
     return -15;
   }
 }
+// PassStats of the reference engine (refactor.hpp:223-421): decompose of the
+// given f64 grid (levels cap 0 = full), then -- when `recompose` -- a full
+// recompose into the SAME stats object (it appends without clearing).  Per
+// level record (finest first for the decompose part): level, elements,
+// coefficient in/out, fused_copy in/out, then nd x (masstrans in, out),
+// nd x (solve in, out), apply in/out = 8 + 4 nd words.  *nlevels = records.
+int mgrref_pass_stats_f64(int nd, const uint64_t *shape, const double *coords, int levels_cap,
+                          const double *values, int recompose, uint64_t *out, int cap_records,
+                          int *nlevels) {
+  try {
+    mgr::TensorGrid<double> g;
+    g.shape = to_shape(nd, shape);
+    g.coords = to_coords(nd, shape, coords);
+    g.values.assign(values, values + mgr::num_elements(g.shape));
+    mgr::PassStats st;
+    mgr::RefactorOptions opt;
+    if (levels_cap > 0)
+      opt.levels = std::size_t(levels_cap);
+    opt.stats = &st;
+    const auto r = mgr::decompose(g, opt);
+    if (recompose)
+      (void)mgr::recompose(r, r.levels, opt);
+    *nlevels = int(st.levels.size());
+    const std::size_t w = 8 + 4 * std::size_t(nd);
+    for (std::size_t i = 0; i < st.levels.size() && int(i) < cap_records; ++i) {
+      const auto &lv = st.levels[i];
+      uint64_t *o = out + i * w;
+      o[0] = lv.level;
+      o[1] = lv.level_elements;
+      o[2] = lv.coefficient.in;
+      o[3] = lv.coefficient.out;
+      o[4] = lv.fused_copy.in;
+      o[5] = lv.fused_copy.out;
+      for (int d = 0; d < nd; ++d) {
+        o[6 + 2 * d] = lv.masstrans[d].in;
+        o[7 + 2 * d] = lv.masstrans[d].out;
+        o[6 + 2 * nd + 2 * d] = lv.solve[d].in;
+        o[7 + 2 * nd + 2 * d] = lv.solve[d].out;
+      }
+      o[6 + 4 * nd] = lv.apply.in;
+      o[7 + 4 * nd] = lv.apply.out;
+    }
+    return 0;
+  } catch (const mgr::Error &e) {
+    return code_of(e);
+  } catch (...) {
+    return 15;
+  }
+}
+
+// mgr::weighted_l2_norm (grid.hpp:218-244) of an f64 grid.
+double mgrref_weighted_l2_norm_f64(int nd, const uint64_t *shape, const double *coords,
+                                   const double *values) {
+  mgr::TensorGrid<double> g;
+  g.shape = to_shape(nd, shape);
+  g.coords = to_coords(nd, shape, coords);
+  g.values.assign(values, values + mgr::num_elements(g.shape));
+  return mgr::weighted_l2_norm(g);
+}
+
+// CommReport::to_json (parallel.cpp:264-292) of a report built from plain
+// fields: phases as (name, messages, elements, local, seconds), idle records
+// as (level, dim, stages, counts...).  Writes at most cap bytes (NUL-ended).
+int mgrref_comm_report_json(int workers, int scheme, uint64_t grid_elements, int nphases,
+                            const char *const *names, const uint64_t *counts,
+                            const double *seconds, int nidle, const uint64_t *idle_words,
+                            char *out, uint64_t cap) {
+  mgr::CommReport rep;
+  rep.workers = workers;
+  rep.scheme = scheme ? mgr::PartitionScheme::shifted_round_robin : mgr::PartitionScheme::block;
+  rep.total_grid_elements = grid_elements;
+  for (int i = 0; i < nphases; ++i) {
+    auto &ph = rep.phases[names[i]];
+    ph.messages = counts[3 * i];
+    ph.elements = counts[3 * i + 1];
+    ph.local_elements = counts[3 * i + 2];
+    ph.seconds = seconds[i];
+  }
+  const uint64_t *w = idle_words;
+  for (int i = 0; i < nidle; ++i) {
+    mgr::IdleRecord rec;
+    rec.level = w[0];
+    rec.dim = w[1];
+    for (uint64_t k = 0; k < w[2]; ++k)
+      rec.idle_per_stage.push_back(int(w[3 + k]));
+    w += 3 + w[2];
+    rep.idle.push_back(std::move(rec));
+  }
+  const std::string j = rep.to_json();
+  if (j.size() + 1 > cap)
+    return 3;
+  std::memcpy(out, j.c_str(), j.size() + 1);
+  return 0;
+}
+
 uint32_t mgrref_crc32(const uint8_t *data, uint64_t n) {
   return mgr::crc32(std::span<const uint8_t>(data, n));
 }

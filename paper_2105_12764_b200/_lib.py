@@ -32,6 +32,9 @@ EXPORTS = (
     "mgrg_compress", "mgrg_free", "mgrg_decompress", "mgrg_crc32_host",
     "mgrg_write_refactored_host", "mgrg_read_refactored_host", "mgrg_compress_host",
     "mgrg_decompress_host",
+    "mgrg_device_count", "mgrg_coop_schedule", "mgrg_block_meta_fill",
+    "mgrg_comm_unique_id", "mgrg_comm_init", "mgrg_comm_destroy", "mgrg_comm_size",
+    "mgrg_comm_allgather_block_meta",
 )
 
 KERNEL_KINDS = {0: "dec_level", 1: "thomas_x", 2: "thomas_y", 3: "thomas_z",
@@ -55,6 +58,28 @@ class GridDesc(ctypes.Structure):
 
 
 MGRG_FLAG_FAST = 1
+MGRG_MAX_CLASSES = 32
+MGRG_COMM_ID_BYTES = 128
+
+
+class BlockMeta(ctypes.Structure):
+    """mgrg_block_meta (include/mgrg.h): the fixed-size per-block record of
+    the block-sharded path's one all-gather."""
+    _fields_ = [
+        ("block_id", ctypes.c_int64),
+        ("rank", ctypes.c_int32),
+        ("dtype", ctypes.c_int32),
+        ("ndims", ctypes.c_int32),
+        ("levels", ctypes.c_int32),
+        ("origin", ctypes.c_uint64 * 4),
+        ("shape", ctypes.c_uint64 * 4),
+        ("class_bytes", ctypes.c_uint64 * MGRG_MAX_CLASSES),
+        ("class_crc32", ctypes.c_uint32 * MGRG_MAX_CLASSES),
+        ("checksum", ctypes.c_uint32),
+        ("reserved", ctypes.c_uint32),
+        ("decompose_ms", ctypes.c_double),
+        ("recompose_ms", ctypes.c_double),
+    ]
 
 
 _lib = None
@@ -106,6 +131,16 @@ def lib() -> ctypes.CDLL:
             "mgrg_decompress": [vp, vp, u64, vp, ctypes.POINTER(ctypes.c_double),
                                 ctypes.POINTER(ctypes.c_double),
                                 ctypes.POINTER(ctypes.c_double), ctypes.POINTER(i32)],
+            "mgrg_device_count": [ctypes.POINTER(i32)],
+            "mgrg_coop_schedule": [vp, i32, ctypes.POINTER(i32), vp],
+            "mgrg_block_meta_fill": [vp, vp, ctypes.c_int64, i32, vp, ctypes.c_double,
+                                     ctypes.c_double, ctypes.POINTER(BlockMeta), vp],
+            "mgrg_comm_unique_id": [vp],
+            "mgrg_comm_init": [vp, i32, i32, i32, ctypes.POINTER(vp)],
+            "mgrg_comm_destroy": [vp],
+            "mgrg_comm_size": [vp, ctypes.POINTER(i32), ctypes.POINTER(i32)],
+            "mgrg_comm_allgather_block_meta": [vp, ctypes.POINTER(BlockMeta), i32,
+                                               ctypes.POINTER(BlockMeta), vp],
         }
         for name, args in sig.items():
             fn = getattr(L, name)

@@ -34,7 +34,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
     if not force and up_to_date():
         return LIB
     nvcc = os.environ.get("NVCC", "nvcc")
-    cmd = [nvcc, *NVCC_FLAGS, "-o", LIB, os.path.join(CSRC, "mgrg.cu"), "-lz"]
+    cmd = [nvcc, *NVCC_FLAGS, "-o", LIB, os.path.join(CSRC, "mgrg.cu"), "-lz", "-lnccl"]
     if verbose:
         print(" ".join(cmd))
     subprocess.run(cmd, check=True)

@@ -123,7 +123,7 @@ def write_refactored(r, path, device: int = 0) -> int:
     """mgr::write_refactored (pipeline.cpp:208-215) of a RefactoredData."""
     import torch
 
-    from .refactor import _plan_for, _validate_geometry, uniform_coords
+    from .refactor import _plan_for, _validate_geometry, flat_if_current, uniform_coords
 
     _validate_geometry(r.shape, r.coords, 2)
     uni = all(np.array_equal(np.asarray(c, dtype=np.float64), uniform_coords(n))
@@ -133,7 +133,16 @@ def write_refactored(r, path, device: int = 0) -> int:
     plan = _plan_for(r.shape, None if uni else r.coords, dt, int(r.levels), device)
     if plan.levels != r.levels:
         raise errors.InvalidLevel(f"container levels {r.levels} do not match the grid")
-    flat = r.flat
+    if len(r.classes) != plan.levels + 1:
+        raise errors.MissingClass(f"write_refactored needs all {plan.levels + 1} classes; "
+                                  f"got {len(r.classes)}")
+    offs = plan.class_offsets
+    for l, c in enumerate(r.classes):
+        n = c.numel() if hasattr(c, "is_cuda") else np.asarray(c).size
+        if n != offs[l + 1] - offs[l]:
+            raise errors.ShapeError(f"class {l} has {n} entries, expected "
+                                    f"{offs[l + 1] - offs[l]}")
+    flat = flat_if_current(r, plan)
     if flat is None:
         parts = [c.reshape(-1) if hasattr(c, "is_cuda") else
                  torch.from_numpy(np.ascontiguousarray(c).reshape(-1)) for c in r.classes]

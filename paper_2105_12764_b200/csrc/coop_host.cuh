@@ -192,6 +192,17 @@ mgrg_status mgrg_cooperative_decompose_host(const mgrg_grid_desc *desc, int32_t 
     mgrg_plan_level_buffer(wk[w].p, l, &ptr);
     return static_cast<char *>(ptr);
   };
+  // Define every byte the level kernels may stage: their 16-byte row chunks
+  // straddle the first / last plane a worker holds, so the neighbouring
+  // (never used) bytes must not be uninitialised memory (compute-sanitizer
+  // initcheck).  One HBM-speed pass per worker buffer.
+  for (int w = 0; w < W; ++w) {
+    DeviceGuard g(wk[w].dev);
+    COOP_CUDA(cudaMemset(wk[w].in, 0, N * es));
+    for (int l = L - 1; l >= std::max(1, L - 2); --l)
+      COOP_CUDA(cudaMemset(level_arr(w, l), 0,
+                           G.ls[l][0] * G.ls[l][1] * G.ls[l][2] * es));
+  }
   // upload: fine planes [2c0 - 2, 2c1] of the finest level
   {
     const uint64_t nxy = G.ls[L][0] * G.ls[L][1], n2 = G.ls[L][2];

@@ -633,16 +633,22 @@ void launch_rec_gpk(const LevelGeom<R> &g, const R *coarse, const R *cls, R *out
 static_assert(sizeof(Stencil<float>) % sizeof(float) == 0, "stencil layout");
 static_assert(sizeof(Stencil<double>) % sizeof(double) == 0, "stencil layout");
 
-// experiment knob: chunked fiber-resident Thomas (MGRG_TFIBER=0 disables)
-int g_thomas_fiber = [] {
-  const char *e = std::getenv("MGRG_TFIBER");
-  return e ? std::atoi(e) : 1;
-}();
+// Tuning / A-B knobs.  Release builds use the measured defaults and never
+// read the environment; a debug build (-DMGRG_DEBUG_KNOBS) lets an A/B run
+// override a knob.  No knob changes a value-affecting contract (the
+// arithmetic policy is the caller's MGRG_FLAG_FAST, nothing else).
+int knob(const char *name, int dflt) {
+#ifdef MGRG_DEBUG_KNOBS
+  if (const char *e = std::getenv(name))
+    return std::atoi(e);
+#endif
+  (void)name;
+  return dflt;
+}
+// chunked fiber-resident Thomas (MGRG_TFIBER=0 disables)
+int g_thomas_fiber = knob("MGRG_TFIBER", 1);
 // programmatic dependent launch of the level-loop kernels (MGRG_PDL=0 disables)
-int g_pdl = [] {
-  const char *e = std::getenv("MGRG_PDL");
-  return e ? std::atoi(e) : 1;
-}();
+int g_pdl = knob("MGRG_PDL", 1);
 
 // Launch with programmatic stream serialization: the kernel's CTAs may be
 // scheduled before its stream predecessor has finished; the kernel waits in
@@ -665,20 +671,11 @@ void launch_pdl(void (*k)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStr
 
 // exact-policy resident Thomas (thomas_exact.cuh; MGRG_TEXACT=0 disables,
 // 2 also uses it for y / z fibers)
-int g_thomas_exact = [] {
-  const char *e = std::getenv("MGRG_TEXACT");
-  return e ? std::atoi(e) : 1;
-}();
+int g_thomas_exact = knob("MGRG_TEXACT", 1);
 // pipelined host-buffer decompose (MGRG_PIPELINE=0 disables)
-int g_pipelined_host = [] {
-  const char *e = std::getenv("MGRG_PIPELINE");
-  return e ? std::atoi(e) : 1;
-}();
+int g_pipelined_host = knob("MGRG_PIPELINE", 1);
 // experiment knob: one-launch Thomas for small lattices (MGRG_TSMALL=0 disables)
-int g_thomas_small = [] {
-  const char *e = std::getenv("MGRG_TSMALL");
-  return e ? std::atoi(e) : 1;
-}();
+int g_thomas_small = knob("MGRG_TSMALL", 1);
 constexpr uint32_t kZChunk = 32; // coarse-z planes per CTA of the pair-lane kernels
 template <typename R> constexpr int pair_cy() { return sizeof(R) == 4 ? 16 : 8; }
 
@@ -1401,22 +1398,17 @@ mgrg_status mgrg_plan_create(const mgrg_grid_desc *desc, mgrg_plan **out) {
   p->tile = nd == 1 ? TileKind::t128x1 : TileKind::t32x8;
   p->pair_path = (p->refine & 3u) == 3u;
   p->fast = (desc->flags & MGRG_FLAG_FAST) != 0;
-  if (const char *fe = std::getenv("MGRG_FAST"))
-    p->fast = std::atoi(fe) != 0;
-  if (const char *gp = std::getenv("MGRG_GENERIC"))
-    if (std::atoi(gp) != 0)
-      p->pair_path = false;
+  if (knob("MGRG_GENERIC", 0) != 0)
+    p->pair_path = false;
   {
     // lean family: x, y (and z) refine; used on every level whose extents
     // are all odd (coarse = even positions), see lean_level()
     p->lean = p->refine == 7u || (p->refine == 3u && p->kext[L][2] == 1);
-    if (const char *le = std::getenv("MGRG_LEAN"))
-      p->lean = p->lean && std::atoi(le) != 0;
+    p->lean = p->lean && knob("MGRG_LEAN", 1) != 0;
   }
   p->zchunk = nd == 3 ? 32 : 1;
-  if (const char *zc = std::getenv("MGRG_ZCHUNK"))
-    if (nd == 3 && std::atoi(zc) > 0)
-      p->zchunk = uint32_t(std::atoi(zc));
+  if (nd == 3 && knob("MGRG_ZCHUNK", 0) > 0)
+    p->zchunk = uint32_t(knob("MGRG_ZCHUNK", 0));
 
   DeviceGuard guard(p->device);
   mgrg_status st = p->dtype == MGRG_F32 ? upload_geometry<float>(p.get())
@@ -1659,10 +1651,7 @@ mgrg_status decompose_host_pipelined(mgrg_plan *p, const R *h_in, R *h_cls) {
   const LeanTiles t = lean_tiles<R>(g.m[0], g.m[1], g.m[2], true);
   // slab groups: 16 measured best on B200 + PCIe 5 (8: 122 ms, 16: 112 ms for
   // 1025^3 f32); MGRG_PIPE_G overrides (1..16, the event arrays' size)
-  static const int kG = [] {
-    const char *e = std::getenv("MGRG_PIPE_G");
-    return e ? std::max(1, std::min(16, std::atoi(e))) : 16;
-  }();
+  static const int kG = std::max(1, std::min(16, knob("MGRG_PIPE_G", 16)));
   const int G = int(std::min<uint32_t>(t.ntz, uint32_t(kG)));
   const uint32_t n2 = g.n[2], m2 = g.m[2];
   auto chunk0 = [&](int q) { return uint32_t((uint64_t(q) * t.ntz) / G); };
@@ -2268,3 +2257,4 @@ mgrg_status mgrg_plan_level_buffer(mgrg_plan *p, int32_t level, void **d_ptr) {
 #include "coop_host.cuh"
 #include "container.cuh"
 #include "compress.cuh"
+#include "comm.cuh"

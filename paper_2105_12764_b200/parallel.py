@@ -136,6 +136,7 @@ class BlockMeta:
     class_crc32: list     # crc32 of every class payload (pipeline.cpp:13-28 polynomial)
     decompose_us: int = 0
     recompose_us: int = 0
+    checksum: int = 0     # crc32 of the class CRCs (filled by block_meta)
 
     def pack(self) -> np.ndarray:
         if self.levels + 1 > MAX_CLASSES // 2:
@@ -191,6 +192,129 @@ def gather_metadata(records, max_blocks_per_rank: int, group=None, device=None):
     allr = out.cpu().numpy().reshape(world * max_blocks_per_rank, META_WORDS)
     metas = [BlockMeta.unpack(r) for r in allr if r[0] >= 0]
     return sorted(metas, key=lambda m: m.block)
+
+
+# ---------------------------------------------------------------------------
+# the native gather: libmgrg's NCCL communicator (include/mgrg.h mgrg_comm_*)
+# ---------------------------------------------------------------------------
+def _to_c(m: BlockMeta):
+    from . import _lib
+
+    c = _lib.BlockMeta()
+    c.block_id, c.rank, c.dtype = m.block, m.rank, m.dtype_bytes
+    c.ndims, c.levels = len(m.shape), m.levels
+    for d in range(len(m.shape)):
+        c.origin[d], c.shape[d] = int(m.origin[d]), int(m.shape[d])
+    for l in range(m.levels + 1):
+        c.class_bytes[l] = int(m.class_bytes[l])
+        c.class_crc32[l] = int(m.class_crc32[l]) & 0xFFFFFFFF
+    c.decompose_ms, c.recompose_ms = m.decompose_us / 1e3, m.recompose_us / 1e3
+    return c
+
+
+def _from_c(c) -> BlockMeta:
+    nd, L = int(c.ndims), int(c.levels)
+    return BlockMeta(block=int(c.block_id), rank=int(c.rank), origin=tuple(c.origin[:nd]),
+                     shape=tuple(c.shape[:nd]), dtype_bytes=int(c.dtype), levels=L,
+                     class_bytes=list(c.class_bytes[:L + 1]),
+                     class_crc32=list(c.class_crc32[:L + 1]),
+                     decompose_us=int(round(c.decompose_ms * 1e3)),
+                     recompose_us=int(round(c.recompose_ms * 1e3)))
+
+
+def block_meta(plan, d_classes, block: int, rank: int, origin=None,
+               decompose_ms: float = 0.0, recompose_ms: float = 0.0,
+               stream=None) -> BlockMeta:
+    """The block's metadata record from the device class buffer:
+    mgrg_block_meta_fill (per-class CRC-32 on the GPU, geometry from the
+    plan)."""
+    import ctypes
+
+    from . import _lib
+    from .plan import _stream_ptr, _tensor_ptr
+
+    c = _lib.BlockMeta()
+    org = None
+    if origin is not None:
+        org = (ctypes.c_uint64 * 4)(*[int(x) for x in origin])
+    _lib.check(_lib.lib().mgrg_block_meta_fill(
+        plan._h, _tensor_ptr(d_classes), int(block), int(rank), org,
+        float(decompose_ms), float(recompose_ms), ctypes.byref(c),
+        _stream_ptr(stream, plan.device)))
+    m = _from_c(c)
+    m.checksum = int(c.checksum)
+    return m
+
+
+class NativeMetaComm:
+    """One NCCL communicator per rank inside libmgrg (mgrg_comm_init), for
+    the block-sharded path's one collective: the metadata all-gather
+    (mgrg_comm_allgather_block_meta).  The 128-byte unique id made by rank 0
+    is shipped to the other ranks through the process group's own
+    transport."""
+
+    def __init__(self, rank: int, world: int, device: int, uid: bytes):
+        import ctypes
+
+        from . import _lib
+
+        self.rank, self.world, self.device = int(rank), int(world), int(device)
+        self._h = ctypes.c_void_p()
+        buf = (ctypes.c_uint8 * _lib.MGRG_COMM_ID_BYTES).from_buffer_copy(uid)
+        _lib.check(_lib.lib().mgrg_comm_init(buf, self.world, self.rank, self.device,
+                                             ctypes.byref(self._h)))
+
+    @staticmethod
+    def unique_id() -> bytes:
+        import ctypes
+
+        from . import _lib
+
+        buf = (ctypes.c_uint8 * _lib.MGRG_COMM_ID_BYTES)()
+        _lib.check(_lib.lib().mgrg_comm_unique_id(buf))
+        return bytes(buf)
+
+    @classmethod
+    def from_process_group(cls, group=None, device: int | None = None):
+        import torch
+        import torch.distributed as dist
+
+        rank, world = dist.get_rank(group), dist.get_world_size(group)
+        obj = [cls.unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=dist.get_global_rank(group, 0)
+                                   if group is not None else 0, group=group)
+        dev = torch.cuda.current_device() if device is None else int(device)
+        return cls(rank, world, dev, obj[0])
+
+    def allgather(self, records, per_rank: int):
+        """Every rank's records (this rank's `records`, padded to per_rank),
+        ordered by block index."""
+        from . import _lib
+
+        mine = (_lib.BlockMeta * max(1, per_rank))()
+        for i in range(per_rank):
+            mine[i].block_id = -1
+        for i, m in enumerate(records):
+            mine[i] = _to_c(m)
+        out = (_lib.BlockMeta * max(1, per_rank * self.world))()
+        _lib.check(_lib.lib().mgrg_comm_allgather_block_meta(self._h, mine, int(per_rank),
+                                                             out, None))
+        metas = [_from_c(out[i]) for i in range(per_rank * self.world)
+                 if out[i].block_id >= 0]
+        return sorted(metas, key=lambda m: m.block)
+
+    def close(self):
+        from . import _lib
+
+        if self._h:
+            _lib.lib().mgrg_comm_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
 
 
 # ---------------------------------------------------------------------------
@@ -322,6 +446,11 @@ class BlockShardedRefactor:
             out[i] = r
         return out
 
-    def finish(self):
-        """The metadata all-gather: every rank learns every block's record."""
+    def finish(self, comm: "NativeMetaComm | None" = None):
+        """The metadata all-gather: every rank learns every block's record --
+        through libmgrg's own NCCL communicator when one is given (the C-ABI
+        path a C++ caller uses), else through the process group (gloo in the
+        CPU tests)."""
+        if comm is not None:
+            return comm.allgather(self.records, self.max_per_rank)
         return gather_metadata(self.records, self.max_per_rank, self.group, self.device)

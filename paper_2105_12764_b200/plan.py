@@ -22,11 +22,13 @@ def _dtype_name(dtype) -> str:
     raise errors.InvalidArgument(f"unsupported dtype {dtype}")
 
 
-def _stream_ptr(stream):
+def _stream_ptr(stream, device=None):
+    """The stream to launch on: torch's current stream OF THE PLAN'S DEVICE
+    when none is given (not the current device's)."""
     if stream is None:
         import torch
 
-        return ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+        return ctypes.c_void_p(torch.cuda.current_stream(device).cuda_stream)
     if isinstance(stream, int):
         return ctypes.c_void_p(stream)
     return ctypes.c_void_p(stream.cuda_stream)
@@ -66,7 +68,7 @@ class Plan:
             self._coords = np.ascontiguousarray(
                 np.concatenate([np.asarray(c, dtype=np.float64) for c in coords]))
             desc.coords = self._coords.ctypes.data
-        desc.levels = 0 if levels is None else int(levels)
+        desc.levels = 0 if levels is None else min(int(levels), 64)
         if levels is not None and int(levels) < 1:
             raise errors.InvalidLevel("level count must be at least 1")
         desc.device = self.device
@@ -160,6 +162,11 @@ class Plan:
             raise errors.InvalidArgument(f"{what} has dtype {t.dtype}, plan is {self.dtype}")
         if t.numel() < n:
             raise errors.ShapeError(f"{what} has {t.numel()} elements, need {n}")
+        if not t.is_cuda or t.device.index != self.device:
+            raise errors.InvalidArgument(
+                f"{what} is on {t.device}, plan is on cuda:{self.device}")
+        if not t.is_contiguous():
+            raise errors.InvalidArgument(f"{what} must be contiguous")
 
     def decompose(self, values, classes=None, stream=None):
         """mgr::decompose on device buffers; returns the flat class tensor."""
@@ -170,7 +177,7 @@ class Plan:
             classes = torch.empty(self.num_elements, dtype=values.dtype, device=values.device)
         self._check_tensor(classes, self.num_elements, "classes")
         _lib.check(_lib.lib().mgrg_decompose(self._h, _tensor_ptr(values),
-                                             _tensor_ptr(classes), _stream_ptr(stream)))
+                                             _tensor_ptr(classes), _stream_ptr(stream, self.device)))
         return classes
 
     def recompose(self, classes, classes_used=None, out=None, stream=None):
@@ -186,7 +193,7 @@ class Plan:
             out = torch.empty(self.num_elements, dtype=classes.dtype, device=classes.device)
         self._check_tensor(out, self.num_elements, "values")
         _lib.check(_lib.lib().mgrg_recompose(self._h, _tensor_ptr(classes), k,
-                                             _tensor_ptr(out), _stream_ptr(stream)))
+                                             _tensor_ptr(out), _stream_ptr(stream, self.device)))
         return out
 
     # -- host entry points (numpy) ----------------------------------------------
@@ -220,7 +227,7 @@ class Plan:
         self._check_tensor(classes, self.class_offsets[k + 1], "classes")
         out = (ctypes.c_uint32 * (k + 1))()
         _lib.check(_lib.lib().mgrg_class_crc32(self._h, _tensor_ptr(classes), k, out,
-                                               _stream_ptr(stream)))
+                                               _stream_ptr(stream, self.device)))
         return [int(x) for x in out]
 
     def write_refactored(self, classes, path) -> int:
@@ -289,19 +296,19 @@ class Plan:
     def gpk(self, level: int, values, inverse: bool = False, stream=None):
         """compute_coefficients / restore_coefficients in place."""
         _lib.check(_lib.lib().mgrg_gpk(self._h, level, int(inverse), _tensor_ptr(values),
-                                       _stream_ptr(stream)))
+                                       _stream_ptr(stream, self.device)))
         return values
 
     def masstrans(self, level: int, dim: int, inp, out, fused_copy=False, coef=None,
                   stream=None):
         _lib.check(_lib.lib().mgrg_masstrans(
             self._h, level, dim, _tensor_ptr(inp), _tensor_ptr(out), int(fused_copy),
-            _tensor_ptr(coef) if coef is not None else None, _stream_ptr(stream)))
+            _tensor_ptr(coef) if coef is not None else None, _stream_ptr(stream, self.device)))
         return out
 
     def solve(self, level: int, dim: int, f, stream=None):
         _lib.check(_lib.lib().mgrg_solve(self._h, level, dim, _tensor_ptr(f),
-                                         _stream_ptr(stream)))
+                                         _stream_ptr(stream, self.device)))
         return f
 
     def apply_correction(self, values, z, sign: int = 1, stream=None):
@@ -310,11 +317,11 @@ class Plan:
                 f"correction length {z.numel()} does not match {values.numel()} nodes")
         _lib.check(_lib.lib().mgrg_apply_correction(
             self._h, values.numel(), _tensor_ptr(values), _tensor_ptr(z), int(sign),
-            _stream_ptr(stream)))
+            _stream_ptr(stream, self.device)))
         return values
 
     def reorder(self, level: int, values, out, to_natural: bool = False, stream=None):
         _lib.check(_lib.lib().mgrg_reorder(self._h, level, int(to_natural),
                                            _tensor_ptr(values), _tensor_ptr(out),
-                                           _stream_ptr(stream)))
+                                           _stream_ptr(stream, self.device)))
         return out

@@ -171,33 +171,48 @@ def _plan_for(shape, coords, dtype, levels, device) -> Plan:
     return p
 
 
-def _fill_stats(stats: PassStats, plan: Plan):
-    """The documented per-level traffic composition (refactor.hpp:223-421,
-    README "passes"), from the plan geometry."""
-    stats.levels.clear()
+def _level_stats(plan: Plan, l: int) -> LevelPassStats:
     nd = len(plan.shape)
-    for l in range(plan.levels, 0, -1):
-        ls, cs = plan.level_shape(l), plan.level_shape(l - 1)
-        F, C = int(np.prod(ls)), int(np.prod(cs))
-        lv = LevelPassStats(level=l, level_elements=F)
-        lv.coefficient = PhaseCounters(F, F - C)
-        lv.fused_copy = PhaseCounters(0, F - C)
-        cur = F
-        for d in range(nd):
-            if cs[d] < ls[d]:
-                out = cur // ls[d] * cs[d]
-                lv.masstrans.append(PhaseCounters(cur, out))
-                lv.solve.append(PhaseCounters(2 * C, 2 * C))
-                cur = out
-            else:
-                lv.masstrans.append(PhaseCounters())
-                lv.solve.append(PhaseCounters())
-        lv.apply = PhaseCounters(2 * C, C)
-        stats.levels.append(lv)
+    ls, cs = plan.level_shape(l), plan.level_shape(l - 1)
+    F, C = int(np.prod(ls)), int(np.prod(cs))
+    lv = LevelPassStats(level=l, level_elements=F)
+    lv.coefficient = PhaseCounters(F, F - C)
+    lv.fused_copy = PhaseCounters(0, F - C)
+    cur = F
+    for d in range(nd):
+        if cs[d] < ls[d]:
+            out = cur // ls[d] * cs[d]
+            lv.masstrans.append(PhaseCounters(cur, out))
+            lv.solve.append(PhaseCounters(2 * C, 2 * C))
+            cur = out
+        else:
+            lv.masstrans.append(PhaseCounters())
+            lv.solve.append(PhaseCounters())
+    lv.apply = PhaseCounters(2 * C, C)
+    return lv
+
+
+def _fill_stats(stats: PassStats, plan: Plan, recompose: bool = False):
+    """The per-level traffic counters the reference engine accumulates
+    (refactor.hpp:223-421): decompose clears and appends levels finest
+    first; recompose appends levels coarsest first without clearing
+    (refactor.hpp:159-199).  Acceptance criterion 9 (acceptance.cpp:336-374)
+    checks this composition."""
+    if not recompose:
+        stats.levels.clear()
+        stats.levels.extend(_level_stats(plan, l) for l in range(plan.levels, 0, -1))
+    else:
+        stats.levels.extend(_level_stats(plan, l) for l in range(1, plan.levels + 1))
 
 
 def _is_torch(x) -> bool:
     return hasattr(x, "is_cuda")
+
+
+def _on_plan_device(t, plan: Plan):
+    if t.is_cuda and t.device.index == plan.device:
+        return t.contiguous()
+    return t.to(f"cuda:{plan.device}").contiguous()
 
 
 def decompose(grid: TensorGrid, opt: RefactorOptions | None = None) -> RefactoredData:
@@ -209,7 +224,8 @@ def decompose(grid: TensorGrid, opt: RefactorOptions | None = None) -> Refactore
     plan = _plan_for(grid.shape, grid.coords if not _all_uniform(grid) else None,
                      dtype, opt.levels, opt.device)
     if _is_torch(vals):
-        flat = plan.decompose(vals.reshape(-1))
+        # a block handed to another GPU's worker moves to that GPU first
+        flat = plan.decompose(_on_plan_device(vals.reshape(-1), plan))
     else:
         flat = plan.decompose_host(np.asarray(vals).reshape(-1))
     if opt.stats is not None:
@@ -260,9 +276,41 @@ def _all_uniform(g) -> bool:
     return True
 
 
+def _addr(a) -> int:
+    return a.data_ptr() if _is_torch(a) else int(a.__array_interface__["data"][0])
+
+
+def flat_if_current(r: RefactoredData, plan: Plan, upto: int | None = None):
+    """r.flat when classes 0..upto are all still views of it at their class
+    offsets (N_{l-1}) -- i.e. nobody replaced a class array (quantized,
+    zeroed, loaded from elsewhere); None otherwise.  The reference treats
+    the classes as the data (refactor.hpp:18-32), so a stale flat buffer
+    must never be used in their place."""
+    flat = r.flat
+    if flat is None:
+        return None
+    upto = r.levels if upto is None else upto
+    if len(r.classes) < upto + 1 or _is_torch(flat) != _is_torch(r.classes[0]):
+        return None
+    offs = plan.class_offsets
+    es = flat.element_size() if _is_torch(flat) else flat.itemsize
+    base = _addr(flat)
+    for l in range(upto + 1):
+        c = r.classes[l]
+        n = c.numel() if _is_torch(c) else c.size
+        if n != offs[l + 1] - offs[l] or (n and _addr(c) != base + offs[l] * es):
+            return None
+        if _is_torch(c) and (not c.is_contiguous() or c.dtype != flat.dtype):
+            return None
+        if not _is_torch(c) and (not c.flags.c_contiguous or c.dtype != flat.dtype):
+            return None
+    return flat
+
+
 def _flat_classes(r: RefactoredData, k: int, plan: Plan):
-    if r.flat is not None:
-        return r.flat
+    flat = flat_if_current(r, plan, k)
+    if flat is not None:
+        return flat
     parts = r.classes[: k + 1]
     if parts and _is_torch(parts[0]):
         import torch
@@ -287,9 +335,11 @@ def recompose(r: RefactoredData, classes_used: int,
                      first.dtype, r.levels, opt.device)
     flat = _flat_classes(r, classes_used, plan)
     if _is_torch(flat):
-        vals = plan.recompose(flat, classes_used)
+        vals = plan.recompose(_on_plan_device(flat, plan), classes_used)
     else:
         vals = plan.recompose_host(np.asarray(flat), classes_used)
+    if opt.stats is not None:
+        _fill_stats(opt.stats, plan, recompose=True)
     return TensorGrid(tuple(r.shape), r.coords, vals)
 
 

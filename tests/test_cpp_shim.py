@@ -72,3 +72,27 @@ def test_cpp_parallel_shim_matches_reference(tmp_path, oracle_mod):
     out = subprocess.run([exe], capture_output=True, text=True, timeout=300)
     assert out.returncode == 0, out.stderr
     assert "parallel shim ok" in out.stdout
+
+
+DSRC = os.path.join(ROOT, "tests", "cpp", "test_dropin_contract.cpp")
+
+
+def test_dropin_contract_compiles_standalone():
+    subprocess.run(["g++", "-std=c++20", "-fsyntax-only", "-Wall", "-Wextra",
+                    "-I", os.path.join(ROOT, "include"), DSRC], check=True)
+
+
+@pytest.mark.gpu
+def test_cpp_dropin_contract_matches_reference(tmp_path, oracle_mod):
+    """PassStats (decompose + recompose), weighted_l2_norm, level validation,
+    the bounded plan cache, the parallel drivers and CommReport::to_json
+    against the reference library."""
+    if not oracle_mod.available("ref"):
+        pytest.skip("oracle/_ref not built")
+    exe = str(tmp_path / "test_dropin")
+    subprocess.run(["g++", "-std=c++20", "-O2", "-I", os.path.join(ROOT, "include"), DSRC,
+                    "-L", PKG, "-lmgrg", "-L", REF, "-lmgr_ref", "-lz", "-pthread",
+                    f"-Wl,-rpath,{PKG}:{REF}", "-o", exe], check=True)
+    out = subprocess.run([exe, str(tmp_path)], capture_output=True, text=True, timeout=600)
+    assert out.returncode == 0, out.stderr
+    assert "dropin ok" in out.stdout

@@ -1,0 +1,137 @@
+"""Drop-in contract details of the Python API and the C ABI that need a
+GPU: PassStats through decompose AND recompose against the reference
+engine's counters (acceptance criterion 9, acceptance.cpp:336-374); class
+arrays replaced after decompose are what recompose / write_refactored use
+(the reference treats classes as the data); tensors on the wrong device are
+rejected; the block metadata record (GPU CRC) and the native NCCL all-gather
+(world size 1 on one GPU -- the multi-rank path is the same call)."""
+import zlib
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+def _stats_as_dicts(st):
+    def pc(c):
+        return (c.in_, c.out)
+
+    return [{"level": lv.level, "level_elements": lv.level_elements,
+             "coefficient": pc(lv.coefficient), "fused_copy": pc(lv.fused_copy),
+             "masstrans": [pc(c) for c in lv.masstrans], "solve": [pc(c) for c in lv.solve],
+             "apply": pc(lv.apply)} for lv in st.levels]
+
+
+@pytest.mark.parametrize("shape,nonuni,cap", [((17, 17, 17), False, 0), ((12, 10, 9), False, 0),
+                                              ((33, 17), True, 0), ((65,), False, 3),
+                                              ((9, 5, 3, 6), True, 0)])
+def test_pass_stats_decompose_and_recompose_match_reference(oracle_mod, shape, nonuni, cap):
+    if not oracle_mod.available("ref"):
+        pytest.skip("oracle/_ref not built")
+    from paper_2105_12764_b200 import refactor as R
+
+    rng = np.random.default_rng(9000)
+    coords = ([np.cumsum(rng.uniform(0.1, 1.0, n)) for n in shape] if nonuni else None)
+    v = rng.random(int(np.prod(shape)))
+    g = R.make_grid(shape, v, coords)
+    st = R.PassStats()
+    opt = R.RefactorOptions(levels=cap or None, stats=st)
+    r = R.decompose(g, opt)
+    assert _stats_as_dicts(st) == oracle_mod.ref_pass_stats(v, shape, coords, cap)
+    R.recompose(r, r.levels, opt)
+    assert _stats_as_dicts(st) == oracle_mod.ref_pass_stats(v, shape, coords, cap,
+                                                            recompose=True)
+
+
+@pytest.mark.parametrize("host", [True, False])
+def test_replaced_class_arrays_are_used(oracle_mod, host):
+    import torch
+
+    from paper_2105_12764_b200 import container, refactor as R
+
+    shape = (17, 9, 9)
+    v = np.random.default_rng(1).random(int(np.prod(shape)))
+    vals = v if host else torch.from_numpy(v).cuda()
+    r = R.decompose(R.make_grid(shape, vals))
+    L = r.levels
+    # zero the finest class in place of the original array (a quantizer would)
+    r.classes[L] = np.zeros_like(r.classes[L]) if host else torch.zeros_like(r.classes[L])
+    got = R.recompose(r, L).values
+    got = got if host else got.cpu().numpy()
+    ref_c, _ = oracle_mod.decompose(v, shape)
+    offs = oracle_mod.class_offsets(shape, L)
+    ref_c[offs[L]:offs[L + 1]] = 0
+    assert np.array_equal(got, oracle_mod.recompose(ref_c, shape, L, L))
+    # and a container written from it holds the replaced class
+    import tempfile, os
+    with tempfile.TemporaryDirectory() as td:
+        p = os.path.join(td, "z.mgrf")
+        container.write_refactored(r, p)
+        back = container.read_refactored(p)
+        cl = back.data.classes[L]
+        cl = cl.cpu().numpy() if hasattr(cl, "cpu") else np.asarray(cl)
+        assert not cl.any()
+
+
+def test_wrong_device_and_noncontiguous_tensors_rejected():
+    import torch
+
+    from paper_2105_12764_b200 import Plan, errors
+
+    plan = Plan((17, 9), "float64", device=0)
+    with pytest.raises(errors.InvalidArgument):
+        plan.decompose(torch.zeros(17 * 9, dtype=torch.float64))  # host tensor
+    x = torch.zeros(9, 17 * 2, dtype=torch.float64, device="cuda")[:, ::2]
+    with pytest.raises(errors.InvalidArgument):
+        plan.decompose(x.reshape(-1) if x.is_contiguous() else x.t())
+    plan.close()
+
+
+def test_block_meta_and_native_allgather_world1():
+    import torch
+
+    from paper_2105_12764_b200 import Plan, parallel
+
+    shape = (33, 17, 9)
+    v = torch.rand(int(np.prod(shape)), dtype=torch.float32, device="cuda")
+    plan = Plan(shape, "float32", device=0)
+    c = plan.decompose(v)
+    m = parallel.block_meta(plan, c, block=3, rank=0, origin=(32, 0, 8),
+                            decompose_ms=1.5, recompose_ms=2.25)
+    host = c.cpu().numpy()
+    offs = plan.class_offsets
+    crcs = [zlib.crc32(host[offs[l]:offs[l + 1]].view(np.uint8)) for l in range(plan.levels + 1)]
+    assert m.class_crc32 == crcs
+    assert m.class_bytes == [4 * (offs[l + 1] - offs[l]) for l in range(plan.levels + 1)]
+    le = b"".join(int(x).to_bytes(4, "little") for x in crcs)
+    assert m.checksum == zlib.crc32(le)
+    assert m.origin == (32, 0, 8) and m.shape == shape and m.levels == plan.levels
+    comm = parallel.NativeMetaComm(0, 1, 0, parallel.NativeMetaComm.unique_id())
+    other = parallel.BlockMeta(block=1, rank=0, origin=(0, 0, 0), shape=shape, dtype_bytes=4,
+                               levels=m.levels, class_bytes=m.class_bytes,
+                               class_crc32=m.class_crc32, decompose_us=10, recompose_us=20)
+    got = comm.allgather([m, other], per_rank=3)  # one padding record
+    assert [g.block for g in got] == [1, 3]
+    assert got[1].class_crc32 == m.class_crc32 and got[1].decompose_us == 1500
+    assert got[0].recompose_us == 20
+    comm.close()
+    plan.close()
+
+
+def test_coop_schedule_matches_runtime_rule():
+    import ctypes
+
+    from paper_2105_12764_b200 import Plan, _lib, coop
+
+    plan = Plan((33, 33, 33), "float64", device=0)
+    q = ctypes.c_int32(0)
+    bounds = (ctypes.c_uint64 * 3)()
+    _lib.check(_lib.lib().mgrg_coop_schedule(plan._h, 2, ctypes.byref(q), bounds))
+    shapes = [plan.level_shape(l) for l in range(plan.levels + 1)]
+    assert q.value == coop.coop_levels(shapes, 2) == 4
+    assert list(bounds) == coop.slab_bounds(33, 2, 4) == [0, 16, 32]
+    n = ctypes.c_int32(0)
+    _lib.check(_lib.lib().mgrg_device_count(ctypes.byref(n)))
+    assert n.value >= 1
+    plan.close()
