@@ -404,3 +404,24 @@ def ref_pass_stats(values: np.ndarray, shape, coords=None, levels_cap: int = 0,
                                for d in range(nd)],
                      "apply": (o[6 + 4 * nd], o[7 + 4 * nd])})
     return recs
+
+
+def embarrassing_roundtrip_blocks_f32(blocks, shape, workers: int, coords=None):
+    """Reference embarrassing_decompose + threaded recompose of the given
+    same-shape f32 blocks (`blocks`: one C-contiguous array of nblocks * N
+    values; `coords`: nblocks * sum(shape) doubles or None); returns
+    (t_dec, t_rec) seconds (block copies excluded from the timing)."""
+    lib = _lib("ref")
+    v = np.ascontiguousarray(blocks, dtype=np.float32)
+    n = int(np.prod(shape))
+    nblocks = v.size // n
+    fn = lib.mgrref_embarrassing_roundtrip_coords_f32
+    fn.argtypes = [ctypes.c_int, ctypes.c_void_p, ctypes.c_int, ctypes.c_int,
+                   ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
+                   ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_double)]
+    c = None if coords is None else np.ascontiguousarray(coords, dtype=np.float64)
+    td, tr = ctypes.c_double(), ctypes.c_double()
+    _check(fn(len(shape), _shape_arr(shape), nblocks, workers,
+              None if c is None else _ptr(c), _ptr(v), None, None, ctypes.byref(td),
+              ctypes.byref(tr)), "embarrassing_roundtrip")
+    return td.value, tr.value

@@ -321,18 +321,39 @@ int mgrref_solve_f32(int nd, const uint64_t *s, const double *c, int cap, int l,
 // block, each block an independent 3-D grid of the same shape; `workers`
 // threads.  Used by bench.py --impl reference to time the reference on all
 // host cores.  values/classes: nblocks * N elements back to back.
+int mgrref_embarrassing_roundtrip_coords_f32(int nd, const uint64_t *shape, int nblocks,
+                                             int workers, const double *coords,
+                                             const float *values, float *classes,
+                                             float *recomposed, double *t_dec,
+                                             double *t_rec);
+
 int mgrref_embarrassing_roundtrip_f32(int nd, const uint64_t *shape,
                                       int nblocks, int workers,
                                       const float *values, float *classes,
                                       float *recomposed, double *t_dec,
                                       double *t_rec) {
+  return mgrref_embarrassing_roundtrip_coords_f32(nd, shape, nblocks, workers, nullptr, values,
+                                                  classes, recomposed, t_dec, t_rec);
+}
+
+// The same with per-block coordinates (`coords`: nblocks consecutive
+// sets of sum(shape) doubles, e.g. slices of a larger field's global
+// coordinates; NULL = uniform_coords per block).
+int mgrref_embarrassing_roundtrip_coords_f32(int nd, const uint64_t *shape, int nblocks,
+                                             int workers, const double *coords,
+                                             const float *values, float *classes,
+                                             float *recomposed, double *t_dec,
+                                             double *t_rec) {
   try {
     const mgr::Shape s = to_shape(nd, shape);
     const std::size_t n = mgr::num_elements(s);
+    std::size_t csum = 0;
+    for (int d = 0; d < nd; ++d)
+      csum += shape[d];
     std::vector<mgr::TensorGrid<float>> blocks(nblocks);
     for (int b = 0; b < nblocks; ++b) {
       blocks[b].shape = s;
-      blocks[b].coords = to_coords(nd, shape, nullptr);
+      blocks[b].coords = to_coords(nd, shape, coords ? coords + b * csum : nullptr);
       blocks[b].values.assign(values + b * n, values + (b + 1) * n);
     }
     const auto t0 = std::chrono::steady_clock::now();
