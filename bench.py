@@ -451,6 +451,47 @@ def other_configs(args, device):
     return out
 
 
+def roofline_report(prof, plans, K, ms_step, arith):
+    """Roofline of the dominant kernel launch (largest total device time over
+    the timed region, from the plans' CUDA-event launch records), the whole
+    step against its algorithmic bytes (decompose
+    s*[2F + (2D+2)C], recompose s*[3F + (2D+1)C] per level, summed over the
+    step's blocks) and the top launches."""
+    peak, peak_kind = hbm_peak()
+    groups = {}
+    for kname, lvl, ms, by in prof:
+        g = groups.setdefault((kname, lvl), [0.0, 0, by])
+        g[0] += ms
+        g[1] += 1
+    (dk, dl), (dtot, dcnt, dbytes) = max(groups.items(), key=lambda kv: kv[1][0])
+    davg = dtot / dcnt
+    achieved = dbytes / (davg * 1e-3) / 1e9
+    alg_step = 0
+    for plan in plans:
+        offs = plan.class_offsets
+        esize = 4 if plan.dtype == "float32" else 8
+        D = sum(1 for n in plan.shape if n >= 3)
+        for lv in range(1, plan.levels + 1):
+            Fn, Cn = offs[lv + 1], offs[lv]
+            alg_step += esize * ((2 * Fn + (2 * D + 2) * Cn) + (3 * Fn + (2 * D + 1) * Cn))
+    traffic = ncu_traffic().get(f"{dk}/L{dl}/{arith}")
+    roofline = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak,
+                "unit": "GB/s", "frac": round(achieved / peak, 4),
+                "traffic": traffic, "kernel": f"{dk} level {dl}",
+                "algorithmic_bytes_per_launch": dbytes,
+                "avg_launch_ms": round(davg, 4), "share_of_step": round(dtot / K / ms_step, 3),
+                "peak_source": f"{peak_kind} (MEASURED_PEAKS.json hbm_gbs)"
+                if peak_kind == "measured" else "fallback 6.65 TB/s (B200_PROFILING.md)"}
+    step_roofline = {"algorithmic_bytes_per_step": alg_step,
+                     "achieved_GBps": round(alg_step / (ms_step * 1e-3) / 1e9, 1),
+                     "frac": round(alg_step / (ms_step * 1e-3) / 1e9 / peak, 4)}
+    per_kernel = {}
+    for (kname, lvl), (tot, cnt, by) in sorted(groups.items(), key=lambda kv: -kv[1][0])[:12]:
+        per_kernel[f"{kname}/L{lvl}"] = {"ms": round(tot / cnt, 4),
+                                         "GBps": round(by / (tot / cnt * 1e-3) / 1e9, 1)}
+    return roofline, step_roofline, per_kernel
+
+
 def run_ours(args, rank, world, local_rank):
     import torch
 
@@ -472,18 +513,20 @@ def run_ours(args, rank, world, local_rank):
     d_out = torch.empty(N, dtype=torch.float32, device=device)
     stream = torch.cuda.current_stream(device)
 
-    # per-block metadata record (gathered with NCCL every step when N > 1):
-    # block id, origin[3], shape[3], dtype bytes, L, class offsets 0..L+1
-    meta = np.zeros(64, dtype=np.int64)
-    meta[0] = rank
-    meta[1:4] = [1024 * (rank & 1), 1024 * ((rank >> 1) & 1), 1024 * ((rank >> 2) & 1)]
-    meta[4:7] = SHAPE
-    meta[7] = esize
-    meta[8] = L
-    offs = plan.class_offsets
-    meta[9:9 + len(offs)] = offs
-    d_meta = torch.from_numpy(meta).to(device)
-    d_meta_all = torch.empty(world * meta.size, dtype=torch.int64, device=device)
+    # per-block metadata record (include/mgrg.h mgrg_block_meta: geometry,
+    # class byte lengths, per-class CRC-32 computed on the GPU), all-gathered
+    # every step when N > 1 through libmgrg's own NCCL communicator
+    # (mgrg_comm_allgather_block_meta) -- the path's one collective
+    comm = None
+    meta = None
+    if dist is not None:
+        from paper_2105_12764_b200 import parallel as par
+
+        plan.decompose(d_in, d_cls, stream)
+        meta = par.block_meta(plan, d_cls, block=rank, rank=rank,
+                              origin=(1024 * (rank & 1), 1024 * ((rank >> 1) & 1),
+                                      1024 * ((rank >> 2) & 1)), stream=stream)
+        comm = par.NativeMetaComm.from_process_group(device=local_rank)
 
     def step(ev_d=None, ev_r=None):
         plan.decompose(d_in, d_cls, stream)
@@ -492,8 +535,8 @@ def run_ours(args, rank, world, local_rank):
         plan.recompose(d_cls, L, d_out, stream)
         if ev_r is not None:
             ev_r.record(stream)
-        if dist is not None:
-            dist.all_gather_into_tensor(d_meta_all, d_meta)
+        if comm is not None:
+            comm.allgather([meta], 1)
 
     for _ in range(max(3, args.warmup)):
         step()
@@ -551,39 +594,8 @@ def run_ours(args, rank, world, local_rank):
     dec_gbs = world * nbytes / (dmed * 1e-3) / 1e9
     rec_gbs = world * nbytes / (rmed * 1e-3) / 1e9
 
-    # roofline of the dominant kernel launch (largest total device time)
-    peak, peak_kind = hbm_peak()
-    groups = {}
-    for kname, lvl, ms, by in prof:
-        g = groups.setdefault((kname, lvl), [0.0, 0, by])
-        g[0] += ms
-        g[1] += 1
-    (dk, dl), (dtot, dcnt, dbytes) = max(groups.items(), key=lambda kv: kv[1][0])
-    davg = dtot / dcnt
-    achieved = dbytes / (davg * 1e-3) / 1e9
-    # algorithmic bytes of one step from the hierarchy:
-    # decompose s*[2F + (2D+2)C], recompose s*[3F + (2D+1)C] per level
-    offs = plan.class_offsets
-    D = sum(1 for n in SHAPE if n >= 3)
-    alg_step = 0
-    for lv in range(1, L + 1):
-        Fn, Cn = offs[lv + 1], offs[lv]
-        alg_step += esize * ((2 * Fn + (2 * D + 2) * Cn) + (3 * Fn + (2 * D + 1) * Cn))
-    traffic = ncu_traffic().get(f"{dk}/L{dl}/{args.arith}")
-    roofline = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak,
-                "unit": "GB/s", "frac": round(achieved / peak, 4),
-                "traffic": traffic, "kernel": f"{dk} level {dl}",
-                "algorithmic_bytes_per_launch": dbytes,
-                "avg_launch_ms": round(davg, 4), "share_of_step": round(dtot / K / ms_step, 3),
-                "peak_source": f"{peak_kind} (MEASURED_PEAKS.json hbm_gbs)"
-                if peak_kind == "measured" else "fallback 6.65 TB/s (B200_PROFILING.md)"}
-    step_roofline = {"algorithmic_bytes_per_step": alg_step,
-                     "achieved_GBps": round(alg_step / (ms_step * 1e-3) / 1e9, 1),
-                     "frac": round(alg_step / (ms_step * 1e-3) / 1e9 / peak, 4)}
-    per_kernel = {}
-    for (kname, lvl), (tot, cnt, by) in sorted(groups.items(), key=lambda kv: -kv[1][0])[:12]:
-        per_kernel[f"{kname}/L{lvl}"] = {"ms": round(tot / cnt, 4),
-                                         "GBps": round(by / (tot / cnt * 1e-3) / 1e9, 1)}
+    roofline, step_roofline, per_kernel = roofline_report(
+        prof, [plan], K, ms_step, args.arith)
 
     e2e = None
     if not args.no_e2e:
@@ -616,7 +628,8 @@ def run_ours(args, rank, world, local_rank):
             "dtype": "f32", "data": "synthetic",
             "config": {"workload": WORKLOAD, "shape": list(SHAPE), "levels": L,
                        "blocks_per_gpu": 1, "step": "decompose + full recompose"
-                       + (" + NCCL all_gather of per-block metadata" if world > 1 else ""),
+                       + (" + NCCL all-gather of the per-block metadata records "
+                          "(libmgrg mgrg_comm_allgather_block_meta)" if world > 1 else ""),
                        "l2": "inputs (4.3 GB) larger than L2; no flush",
                        "parallelism": f"embarrassing x{world}"},
             "decompose_GBps": round(dec_gbs, 2), "recompose_GBps": round(rec_gbs, 2),
@@ -629,7 +642,191 @@ def run_ours(args, rank, world, local_rank):
             "other_configs": others,
         }
         print(json.dumps(out), flush=True)
+    if comm is not None:
+        comm.close()
     plan.close()
+
+# ---------------------------------------------------------------------------
+# BASELINE config 5: one 2049x2049x1025 f64 field split across the GPUs
+# ---------------------------------------------------------------------------
+C5_SHAPE = (2049, 2049, 1025)
+C5_PARTS = (2, 2, 2)
+C5_WORKLOAD = ("3D 2049x2049x1025 fp64 single field split 2x2x2 into 8 plane-sharing "
+               "1025x1025x513 blocks dealt round-robin to the GPUs (strong scaling), "
+               "decompose + full recompose (BASELINE configs[4])")
+
+
+def c5_factors():
+    """Separable fp64 factors of the smooth field on the GLOBAL uniform
+    coordinates (i/2048, j/2048, k/1024) -- no per-rank offset: one field."""
+    c1, c2 = (0.35, 0.4, 0.45), (0.7, 0.65, 0.6)
+    fac, xs = [], []
+    for d, n in enumerate(C5_SHAPE):
+        x = np.arange(n, dtype=np.float64) / (n - 1)
+        xs.append(x)
+        fac.append((np.exp(-30 * (x - c1[d]) ** 2), np.exp(-25 * (x - c2[d]) ** 2),
+                    np.sin(2 * np.pi * x)))
+    return fac, xs
+
+
+def make_block_device(fac, spec, device, dtype):
+    """Block `spec` (origin, shape) of the separable field on the device."""
+    import torch
+
+    sl = [slice(o, o + n) for o, n in zip(spec.origin, spec.shape)]
+    t = [[torch.from_numpy(np.ascontiguousarray(f[sl[d]])).to(device) for f in fac[d]]
+         for d in range(3)]
+    nx, ny, nz = spec.shape
+    out = torch.empty(nz, ny, nx, dtype=getattr(torch, dtype), device=device)
+    for z0 in range(0, nz, 32):
+        z1 = min(nz, z0 + 32)
+        acc = None
+        for term, w in ((0, 1.0), (1, 0.6), (2, 0.2)):
+            p = (w * t[2][term][z0:z1, None, None] * t[1][term][None, :, None]
+                 * t[0][term][None, None, :])
+            acc = p if acc is None else acc + p
+        out[z0:z1] = acc.to(out.dtype)
+    return out.reshape(-1)
+
+
+def run_config5(args, rank, world, local_rank):
+    """Strong scaling of BASELINE config 5: the 8 blocks of the one field are
+    dealt round-robin to the ranks (parallel.assign_blocks); a step is, on
+    every rank, decompose + full recompose of each of its blocks followed by
+    the per-block metadata all-gather (libmgrg's NCCL communicator, N > 1).
+    value = 2 x field bytes (shared planes counted once) / the slowest rank's
+    step time."""
+    import torch
+
+    from paper_2105_12764_b200 import Plan
+    from paper_2105_12764_b200 import parallel as par
+
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+    device = torch.device("cuda", local_rank)
+    torch.cuda.set_device(device)
+    dt = "float64"
+    fac, xs = c5_factors()
+    specs = par.split_blocks(C5_SHAPE, C5_PARTS)
+    mine = par.assign_blocks(len(specs), rank, world)
+    stream = torch.cuda.current_stream(device)
+    blocks = []
+    for b in mine:
+        sp = specs[b]
+        coords = [xs[d][sp.origin[d]:sp.origin[d] + sp.shape[d]] for d in range(3)]
+        plan = Plan(sp.shape, dt, coords=coords, device=local_rank,
+                    fast=args.arith == "fast")
+        v = make_block_device(fac, sp, device, dt)
+        blocks.append({"spec": sp, "plan": plan, "in": v, "cls": torch.empty_like(v)})
+    nmax = max(int(np.prod(sp.shape)) for sp in specs)
+    scratch = torch.empty(nmax, dtype=torch.float64, device=device)
+
+    comm, metas = None, []
+    for blk in blocks:
+        blk["plan"].decompose(blk["in"], blk["cls"], stream)
+        metas.append(par.block_meta(blk["plan"], blk["cls"], block=blk["spec"].index,
+                                    rank=rank, origin=blk["spec"].origin, stream=stream))
+    per_rank = -(-len(specs) // world)
+    if dist is not None:
+        comm = par.NativeMetaComm.from_process_group(device=local_rank)
+
+    def step():
+        for blk in blocks:
+            p = blk["plan"]
+            p.decompose(blk["in"], blk["cls"], stream)
+            p.recompose(blk["cls"], p.levels, scratch[:p.num_elements], stream)
+        if comm is not None:
+            comm.allgather(metas, per_rank)
+
+    for _ in range(max(3, args.warmup)):
+        step()
+    torch.cuda.synchronize()
+    launches = 0
+    for blk in blocks:
+        p = blk["plan"]
+        p.decompose(blk["in"], blk["cls"], stream)
+        launches += p.last_launches
+        p.recompose(blk["cls"], p.levels, scratch[:p.num_elements], stream)
+        launches += p.last_launches
+    torch.cuda.synchronize()
+    K = args.steps
+    for blk in blocks:
+        blk["plan"].set_profiling(True, top_levels=2)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    sampler = ClockSampler(local_rank)
+    sampler.start()
+    time.sleep(0.2)
+    if dist is not None:
+        dist.barrier()
+    torch.cuda.synchronize()
+    e0.record(stream)
+    for _ in range(K):
+        step()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    if dist is not None:
+        dist.barrier()
+    clocks = sampler.stop()
+    total_ms = e0.elapsed_time(e1)
+    prof = []
+    for blk in blocks:
+        prof += blk["plan"].profile(reset=True)
+        blk["plan"].set_profiling(False)
+    t = torch.tensor([total_ms], dtype=torch.float64, device=device)
+    if dist is not None:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    total_ms = t.item()
+    ms_step = total_ms / K
+    field_bytes = int(np.prod(C5_SHAPE)) * 8
+    value = 2 * field_bytes / (ms_step * 1e-3) / 1e9
+    roofline, step_roofline, per_kernel = roofline_report(
+        prof, [b["plan"] for b in blocks], K, ms_step, args.arith)
+    # size-independent check of what was timed: every block's lossless round
+    # trip (FAST policy: within 1e-12 of the block's range)
+    worst = 0.0
+    for blk in blocks:
+        p = blk["plan"]
+        p.decompose(blk["in"], blk["cls"], stream)
+        r = p.recompose(blk["cls"], p.levels, scratch[:p.num_elements], stream)
+        rng = (blk["in"].max() - blk["in"].min()).item()
+        worst = max(worst, ((r - blk["in"]).abs().max() / rng).item())
+    w = torch.tensor([worst], dtype=torch.float64, device=device)
+    if dist is not None:
+        dist.all_reduce(w, op=dist.ReduceOp.MAX)
+    gathered = comm.allgather(metas, per_rank) if comm is not None else metas
+    if rank == 0:
+        out = {
+            "metric": METRIC, "value": round(value, 2), "unit": "GB/s", "n_gpus": world,
+            "steps": K, "warmup": max(3, args.warmup), "ms_per_step": round(ms_step, 4),
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+            "dtype": "f64", "data": "synthetic",
+            "config": {"workload": C5_WORKLOAD, "shape": list(C5_SHAPE),
+                       "blocks": len(specs), "block_shape": list(specs[0].shape),
+                       "blocks_per_gpu": len(mine), "levels": blocks[0]["plan"].levels,
+                       "step": "decompose + full recompose of every block"
+                       + (" + NCCL all-gather of the per-block metadata records" if world > 1
+                          else ""),
+                       "l2": "blocks (4.3 GB each) larger than L2; no flush",
+                       "parallelism": f"embarrassing x{world}",
+                       "field_bytes": field_bytes},
+            "roundtrip_rel_err": w.item(), "arith": args.arith,
+            "roofline": roofline, "step_roofline": step_roofline, "per_kernel": per_kernel,
+            "cpu_baseline": None,
+            "e2e": {"value": None, "unit": "GB/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0,
+                    "note": "config 5 is device-resident only (69 GB of blocks per GPU at "
+                            "N=1); the host-buffer e2e is measured on the headline config"},
+            "gpu_launches": launches * K,
+            "metadata_records": len(gathered),
+            "clocks": clocks,
+        }
+        print(json.dumps(out), flush=True)
+    if comm is not None:
+        comm.close()
+    for blk in blocks:
+        blk["plan"].close()
+
 
 
 def main():
@@ -638,6 +835,10 @@ def main():
     ap.add_argument("--steps", type=int, default=100)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--config", type=int, choices=[4, 5], default=4,
+                    help="4 (default, the headline): one 1025^3 f32 block per GPU, weak "
+                         "scaling; 5: the 2049x2049x1025 f64 field split into 8 blocks "
+                         "across the GPUs, strong scaling")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     ap.add_argument("--no-e2e", action="store_true", help="skip the host-buffer leg")
     ap.add_argument("--no-others", action="store_true",
@@ -660,7 +861,10 @@ def main():
         torch.cuda.set_device(local_rank)
         dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
     try:
-        run_ours(args, rank, world, local_rank)
+        if args.config == 5:
+            run_config5(args, rank, world, local_rank)
+        else:
+            run_ours(args, rank, world, local_rank)
     finally:
         if world > 1:
             import torch.distributed as dist

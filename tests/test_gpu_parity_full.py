@@ -222,3 +222,41 @@ def test_targeted_instantiations(shape, dtype, nonuni, oracle_mod):
             _check_field(plan.recompose(d_ref, k), ref_r, not fast, tol_abs,
                          f"{'fast' if fast else 'exact'} recompose k={k}")
         plan.close()
+
+
+@pytest.mark.parametrize("fast", [False, True])
+def test_config5_split_decompose_recompose_assemble_downscaled(oracle_mod, fast):
+    """Config 5's pipeline on a downscaled field (129x129x65 f64, split 2x2x2
+    into 65x65x33 blocks with their global coordinate slices, as bench.py
+    --config 5 does at 2049x2049x1025): every block's classes against the
+    oracle's decompose of that block (exact policy bit-identical, FAST within
+    1e-12 of the range), its full recompose, and the assembled field equal to
+    the input (shared planes from the lower block)."""
+    import torch
+
+    from paper_2105_12764_b200 import Plan
+    from paper_2105_12764_b200 import parallel as par
+
+    shape = (129, 129, 65)
+    coords = [_uniform(n) for n in shape]
+    v = _smooth_field_separable(shape, coords, np.float64)
+    rng = float(v.max() - v.min())
+    specs = par.split_blocks(shape, (2, 2, 2))
+    assert [s.shape for s in specs] == [(65, 65, 33)] * 8
+    rec_blocks = {}
+    for sp in specs:
+        g = par.block_grid(v, shape, coords, sp)
+        plan = Plan(sp.shape, "float64", coords=g.coords, device=0, fast=fast)
+        d = torch.from_numpy(g.values).cuda()
+        c = plan.decompose(d)
+        ref_c, L = oracle_mod.decompose(g.values, sp.shape, g.coords)
+        assert L == plan.levels
+        got = c.cpu().numpy()
+        if fast:
+            assert float(np.abs(got - ref_c).max()) <= 1e-12 * rng
+        else:
+            assert np.array_equal(got, ref_c)
+        rec_blocks[sp.index] = plan.recompose(c).cpu().numpy()
+        plan.close()
+    back = par.assemble_blocks(rec_blocks, specs, shape)
+    assert float(np.abs(back - v).max()) <= 1e-12 * rng
