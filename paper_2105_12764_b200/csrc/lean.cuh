@@ -29,7 +29,13 @@
 
 namespace mgrg {
 
-template <typename R> __host__ __device__ constexpr int lean_ty() { return sizeof(R) == 4 ? 4 : 2; } // coarse y rows per warp band
+#ifndef LEAN_TY_F32
+#define LEAN_TY_F32 3 // measured: 3 = 2.13 ms, 4 = 2.19 ms at L10 (MINB 3; 4 CTAs/SM spill-free variants are slower)
+#endif
+#ifndef LEAN_DEC_MINB
+#define LEAN_DEC_MINB 3
+#endif
+template <typename R> __host__ __device__ constexpr int lean_ty() { return sizeof(R) == 4 ? LEAN_TY_F32 : 2; } // coarse y rows per warp band
 #ifndef LEAN_ZC_MAX
 #define LEAN_ZC_MAX 32
 #endif
@@ -329,7 +335,7 @@ template <typename R> __host__ __device__ constexpr size_t lean_dec_smem() {
 }
 
 template <typename R, bool Z3, bool FAST>
-__global__ void __launch_bounds__(32 * kLeanWPB, 3)
+__global__ void __launch_bounds__(32 * kLeanWPB, LEAN_DEC_MINB)
     lean_dec_kernel(LevelGeom<R> g, const LeanW<R> *__restrict__ lx,
                     const LeanW<R> *__restrict__ ly, const LeanW<R> *__restrict__ lz,
                     const Stencil<R> *__restrict__ sxt, const Stencil<R> *__restrict__ syt,
@@ -738,10 +744,13 @@ __global__ void __launch_bounds__(32 * kLeanWPB, LEAN_RL_MINB)
 // the interpolant of the previous even plane is carried in registers.
 // CLS = false: classes above classes_used (all zero): pure prolongation.
 #ifndef LEAN_RG_TG
-#define LEAN_RG_TG 4
+#define LEAN_RG_TG 3 // measured with LEAN_RG_PF=1: TG 2 / 3 / 4 = 1.90 / 1.75 / 1.92 ms at L10
 #endif
 #ifndef LEAN_RG_MINB
-#define LEAN_RG_MINB 4
+#define LEAN_RG_MINB 3 // with TG 3 + prefetch: 3 (143 regs) 1.72 ms, 4 (128) 1.76, 5 (96) 2.46
+#endif
+#ifndef LEAN_RG_PF
+#define LEAN_RG_PF 1 // the loads of step k+1 are issued before step k computes
 #endif
 template <typename R> __host__ __device__ constexpr int lean_tg() {
   return sizeof(R) == 4 ? LEAN_RG_TG : 2;
@@ -815,83 +824,107 @@ __global__ void __launch_bounds__(32 * kLeanWPB, LEAN_RG_MINB)
 
   const int cz0 = Z3 ? int(tzc) * tl.zc : 0;
   const int cz1 = Z3 ? min(cz0 + tl.zc, m2) : 1;
-  R WLe[NF], WLo[NF];
   // step k: even plane 2k (coarse plane k) and, for k > cz0, the odd plane
   // 2k-1 between coarse planes k-1 and k
   const int kend = Z3 ? min(cz1, m2 - 1) : 0;
-  for (int k = cz0; k <= kend; ++k) {
-    R We[NF], Wo[NF];
-    {
-      R c[TG + 1];
-      const R *cp = coarse + m01 * k + qe;
+  // All of a step's inputs -- the TG+1 coarse rows and the 7 TG class rows
+  // of both planes -- are loaded in ONE batch at addresses that are always
+  // valid (planes clamped; unused values are discarded), so a step exposes
+  // one load latency instead of three (ncu: 68 % long-scoreboard stalls on
+  // the lerp, shuffle and class-add consumers of three dependent batches);
+  // with LEAN_RG_PF the batch of step k+1 is issued before step k computes.
+  struct In {
+    R c[TG + 1], v[7][TG];
+  };
+  auto load = [&](int k, In &in) {
+    const R *cp = coarse + m01 * k + qe;
 #pragma unroll
-      for (int i = 0; i <= TG; ++i)
-        c[i] = __ldg(cp + int64_t(m0) * crow[i]);
-#pragma unroll
-      for (int i = 0; i <= TG; ++i) {
-        const R cn = __shfl_down_sync(0xffffffffu, c[i], 1);
-        We[2 * i] = c[i];
-        Wo[2 * i] = plerp<R, FAST>(c[i], cn, txr);
-      }
+    for (int i = 0; i <= TG; ++i)
+      in.c[i] = __ldg(cp + int64_t(m0) * crow[i]);
+    if constexpr (CLS) {
+      const int64_t ke = min(k, m2 - 1), zr = max(k - 1, 0);
+      const R *c1 = cls + g.tbase[1] + qo + int64_t(m0 - 1) * (int64_t(m1) * ke);
+      const R *c2 = cls + g.tbase[2] + qe + int64_t(m0) * (int64_t(m1 - 1) * ke);
+      const R *c3 = cls + g.tbase[3] + qo + int64_t(m0 - 1) * (int64_t(m1 - 1) * ke);
 #pragma unroll
       for (int i = 0; i < TG; ++i) {
-        We[2 * i + 1] = plerp<R, FAST>(We[2 * i], We[2 * i + 2], tyr[i]);
-        Wo[2 * i + 1] = plerp<R, FAST>(Wo[2 * i], Wo[2 * i + 2], tyr[i]);
+        in.v[0][i] = __ldg(c1 + int64_t(m0 - 1) * crow[i]);
+        in.v[1][i] = __ldg(c2 + int64_t(m0) * rfo[i]);
+        in.v[2][i] = __ldg(c3 + int64_t(m0 - 1) * rfo[i]);
       }
+      if constexpr (Z3) {
+        const R *c4 = cls + g.tbase[4] + qe + int64_t(m0) * (int64_t(m1) * zr);
+        const R *c5 = cls + g.tbase[5] + qo + int64_t(m0 - 1) * (int64_t(m1) * zr);
+        const R *c6 = cls + g.tbase[6] + qe + int64_t(m0) * (int64_t(m1 - 1) * zr);
+        const R *c7 = cls + g.tbase[7] + qo + int64_t(m0 - 1) * (int64_t(m1 - 1) * zr);
+#pragma unroll
+        for (int i = 0; i < TG; ++i) {
+          in.v[3][i] = __ldg(c4 + int64_t(m0) * crow[i]);
+          in.v[4][i] = __ldg(c5 + int64_t(m0 - 1) * crow[i]);
+          in.v[5][i] = __ldg(c6 + int64_t(m0) * rfo[i]);
+          in.v[6][i] = __ldg(c7 + int64_t(m0 - 1) * rfo[i]);
+        }
+      }
+    }
+  };
+  R WLe[NF], WLo[NF];
+  In cur;
+  load(cz0, cur);
+  for (int k = cz0; k <= kend; ++k) {
+#if LEAN_RG_PF
+    In nxt;
+    if (k < kend)
+      load(k + 1, nxt);
+#endif
+    R We[NF], Wo[NF];
+#pragma unroll
+    for (int i = 0; i <= TG; ++i) {
+      const R cn = __shfl_down_sync(0xffffffffu, cur.c[i], 1);
+      We[2 * i] = cur.c[i];
+      Wo[2 * i] = plerp<R, FAST>(cur.c[i], cn, txr);
+    }
+#pragma unroll
+    for (int i = 0; i < TG; ++i) {
+      We[2 * i + 1] = plerp<R, FAST>(We[2 * i], We[2 * i + 2], tyr[i]);
+      Wo[2 * i + 1] = plerp<R, FAST>(Wo[2 * i], Wo[2 * i + 2], tyr[i]);
     }
     // ---- even plane 2k (written when k < cz1)
     if (k < cz1) {
-      const R *c1 = cls + g.tbase[1] + qo + int64_t(m0 - 1) * (int64_t(m1) * k);
-      const R *c2 = cls + g.tbase[2] + qe + int64_t(m0) * (int64_t(m1 - 1) * k);
-      const R *c3 = cls + g.tbase[3] + qo + int64_t(m0 - 1) * (int64_t(m1 - 1) * k);
-      R v1[TG], v2[TG], v3[TG];
-#pragma unroll
-      for (int i = 0; i < TG; ++i) {
-        v1[i] = CLS ? __ldg(c1 + int64_t(m0 - 1) * crow[i]) : R(0);
-        v2[i] = CLS ? __ldg(c2 + int64_t(m0) * rfo[i]) : R(0);
-        v3[i] = CLS ? __ldg(c3 + int64_t(m0 - 1) * rfo[i]) : R(0);
-      }
       R *op = out + int64_t(2 * k) * nxy + int64_t(2 * cy0) * n0 + 2 * qc;
 #pragma unroll
       for (int i = 0; i < TG; ++i) {
+        const R v1 = CLS ? cur.v[0][i] : R(0), v2 = CLS ? cur.v[1][i] : R(0),
+                v3 = CLS ? cur.v[2][i] : R(0);
         // even row 2(cy0+i): parity of (2k + 2(cy0+i)) is even -> aligned
         if ((wrow >> (2 * i)) & 1u)
-          lean_store_pair<R, true>(op + int64_t(2 * i) * n0, We[2 * i], padd<R, FAST>(Wo[2 * i], v1[i]), own,
-                                   ownO);
+          lean_store_pair<R, true>(op + int64_t(2 * i) * n0, We[2 * i],
+                                   padd<R, FAST>(Wo[2 * i], v1), own, ownO);
         if ((wrow >> (2 * i + 1)) & 1u)
-          lean_store_pair<R, false>(op + int64_t(2 * i + 1) * n0, padd<R, FAST>(We[2 * i + 1], v2[i]),
-                                    padd<R, FAST>(Wo[2 * i + 1], v3[i]), own, ownO);
+          lean_store_pair<R, false>(op + int64_t(2 * i + 1) * n0,
+                                    padd<R, FAST>(We[2 * i + 1], v2),
+                                    padd<R, FAST>(Wo[2 * i + 1], v3), own, ownO);
       }
     }
     // ---- odd plane 2k-1
     if (Z3 && k > cz0) {
       const R tz = __ldg(&lz[k - 1 + 2].t);
-      const int64_t zr = k - 1;
-      const R *c4 = cls + g.tbase[4] + qe + int64_t(m0) * (int64_t(m1) * zr);
-      const R *c5 = cls + g.tbase[5] + qo + int64_t(m0 - 1) * (int64_t(m1) * zr);
-      const R *c6 = cls + g.tbase[6] + qe + int64_t(m0) * (int64_t(m1 - 1) * zr);
-      const R *c7 = cls + g.tbase[7] + qo + int64_t(m0 - 1) * (int64_t(m1 - 1) * zr);
-      R v4[TG], v5[TG], v6[TG], v7[TG];
-#pragma unroll
-      for (int i = 0; i < TG; ++i) {
-        v4[i] = CLS ? __ldg(c4 + int64_t(m0) * crow[i]) : R(0);
-        v5[i] = CLS ? __ldg(c5 + int64_t(m0 - 1) * crow[i]) : R(0);
-        v6[i] = CLS ? __ldg(c6 + int64_t(m0) * rfo[i]) : R(0);
-        v7[i] = CLS ? __ldg(c7 + int64_t(m0 - 1) * rfo[i]) : R(0);
-      }
       R *op = out + int64_t(2 * k - 1) * nxy + int64_t(2 * cy0) * n0 + 2 * qc;
 #pragma unroll
       for (int i = 0; i < TG; ++i) {
+        const R v4 = CLS ? cur.v[3][i] : R(0), v5 = CLS ? cur.v[4][i] : R(0),
+                v6 = CLS ? cur.v[5][i] : R(0), v7 = CLS ? cur.v[6][i] : R(0);
         // odd plane: even rows misaligned, odd rows aligned
         if ((wrow >> (2 * i)) & 1u)
-          lean_store_pair<R, false>(op + int64_t(2 * i) * n0,
-                                    padd<R, FAST>(plerp<R, FAST>(WLe[2 * i], We[2 * i], tz), v4[i]),
-                                    padd<R, FAST>(plerp<R, FAST>(WLo[2 * i], Wo[2 * i], tz), v5[i]), own, ownO);
+          lean_store_pair<R, false>(
+              op + int64_t(2 * i) * n0,
+              padd<R, FAST>(plerp<R, FAST>(WLe[2 * i], We[2 * i], tz), v4),
+              padd<R, FAST>(plerp<R, FAST>(WLo[2 * i], Wo[2 * i], tz), v5), own, ownO);
         if ((wrow >> (2 * i + 1)) & 1u)
-          lean_store_pair<R, true>(op + int64_t(2 * i + 1) * n0,
-                                   padd<R, FAST>(plerp<R, FAST>(WLe[2 * i + 1], We[2 * i + 1], tz), v6[i]),
-                                   padd<R, FAST>(plerp<R, FAST>(WLo[2 * i + 1], Wo[2 * i + 1], tz), v7[i]), own,
-                                   ownO);
+          lean_store_pair<R, true>(
+              op + int64_t(2 * i + 1) * n0,
+              padd<R, FAST>(plerp<R, FAST>(WLe[2 * i + 1], We[2 * i + 1], tz), v6),
+              padd<R, FAST>(plerp<R, FAST>(WLo[2 * i + 1], Wo[2 * i + 1], tz), v7), own,
+              ownO);
       }
     }
 #pragma unroll
@@ -899,6 +932,12 @@ __global__ void __launch_bounds__(32 * kLeanWPB, LEAN_RG_MINB)
       WLe[r] = We[r];
       WLo[r] = Wo[r];
     }
+#if LEAN_RG_PF
+    cur = nxt;
+#else
+    if (k < kend)
+      load(k + 1, cur);
+#endif
   }
 }
 
