@@ -558,8 +558,15 @@ def run_ours(args, rank, world, local_rank):
     e_start = torch.cuda.Event(enable_timing=True)
     e_end = torch.cuda.Event(enable_timing=True)
     # per-launch events on the top two levels only (every launch of the
-    # small levels bracketed by events would add ~0.7 ms to a 9 ms step)
+    # small levels bracketed by events would add ~0.7 ms to a 9 ms step);
+    # with --graphs the timed region replays captured graphs (profiling would
+    # bypass them), and the per-launch profile comes from a separate pass
     plan.set_profiling(True, top_levels=2)
+    if args.graphs:  # the capture call records the profiling events into the graphs
+        plan.profile(reset=True)
+        plan.set_graphs(True)
+        step()
+        torch.cuda.synchronize()
     sampler = ClockSampler(local_rank)
     sampler.start()
     time.sleep(0.2)
@@ -581,8 +588,13 @@ def run_ours(args, rank, world, local_rank):
         dec_ms.append(prev.elapsed_time(evs[i][0]))
         rec_ms.append(evs[i][0].elapsed_time(evs[i][1]))
         prev = evs[i][1]
+    # graphs: the records are the capture call's launches, timed by the last
+    # replay of the timed region (one step); streams: every step's launches
     prof = plan.profile(reset=True)
+    prof_steps = 1 if args.graphs else K
     plan.set_profiling(False)
+    if args.graphs:
+        plan.set_graphs(False)
 
     t = torch.tensor([total_ms, statistics.median(dec_ms), statistics.median(rec_ms)],
                      dtype=torch.float64, device=device)
@@ -595,7 +607,7 @@ def run_ours(args, rank, world, local_rank):
     rec_gbs = world * nbytes / (rmed * 1e-3) / 1e9
 
     roofline, step_roofline, per_kernel = roofline_report(
-        prof, [plan], K, ms_step, args.arith)
+        prof, [plan], prof_steps, ms_step, args.arith)
 
     e2e = None
     if not args.no_e2e:
@@ -634,6 +646,7 @@ def run_ours(args, rank, world, local_rank):
                        "parallelism": f"embarrassing x{world}"},
             "decompose_GBps": round(dec_gbs, 2), "recompose_GBps": round(rec_gbs, 2),
             "roundtrip_rel_err": rt_err, "arith": args.arith,
+            "launch_mode": "cuda-graph replay" if args.graphs else "PDL stream launches",
             "roofline": roofline, "step_roofline": step_roofline,
             "per_kernel": per_kernel,
             "cpu_baseline": cpu, "e2e": e2e,
@@ -839,6 +852,9 @@ def main():
                     help="4 (default, the headline): one 1025^3 f32 block per GPU, weak "
                          "scaling; 5: the 2049x2049x1025 f64 field split into 8 blocks "
                          "across the GPUs, strong scaling")
+    ap.add_argument("--graphs", action="store_true",
+                    help="replay the level loops as captured CUDA graphs (A/B against "
+                         "programmatic-dependent stream launches)")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     ap.add_argument("--no-e2e", action="store_true", help="skip the host-buffer leg")
     ap.add_argument("--no-others", action="store_true",

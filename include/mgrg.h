@@ -201,6 +201,15 @@ mgrg_status mgrg_cooperative_decompose_host(const mgrg_grid_desc *desc, int32_t 
 const char *mgrg_last_error(void);
 /* Status name as the reference spells the exception ("InvalidGrid", ...). */
 const char *mgrg_status_name(mgrg_status status);
+/* CUDA-graph replay (enable != 0): mgrg_decompose / mgrg_recompose capture
+ * their level loop (the ~L*5 dependent launches) once per (operation, buffer
+ * pointers, classes_used) into a graph on a plan-owned stream and replay it,
+ * ordered after and before the caller's stream by events; at most 8 graphs
+ * are kept per plan.  Values are identical with and without graphs.  With
+ * per-launch profiling on, the profiling events are captured into the graph:
+ * the records then hold the launches of the capturing call, timed by the
+ * LAST replay. */
+mgrg_status mgrg_plan_set_graphs(mgrg_plan *plan, int32_t enable);
 /* Kernel launches the last decompose/recompose issued on this plan. */
 mgrg_status mgrg_plan_last_launches(const mgrg_plan *plan, uint64_t *launches);
 /* Per-launch device timing.  With profiling on, every kernel the plan

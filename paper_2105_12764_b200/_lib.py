@@ -34,7 +34,7 @@ EXPORTS = (
     "mgrg_decompress_host",
     "mgrg_device_count", "mgrg_coop_schedule", "mgrg_block_meta_fill",
     "mgrg_comm_unique_id", "mgrg_comm_init", "mgrg_comm_destroy", "mgrg_comm_size",
-    "mgrg_comm_allgather_block_meta",
+    "mgrg_comm_allgather_block_meta", "mgrg_plan_set_graphs",
 )
 
 KERNEL_KINDS = {0: "dec_level", 1: "thomas_x", 2: "thomas_y", 3: "thomas_z",
@@ -118,6 +118,7 @@ def lib() -> ctypes.CDLL:
                                                 ctypes.POINTER(u64)],
             "mgrg_plan_last_launches": [vp, ctypes.POINTER(u64)],
             "mgrg_plan_set_profiling": [vp, i32],
+            "mgrg_plan_set_graphs": [vp, i32],
             "mgrg_plan_profile_reset": [vp],
             "mgrg_plan_profile_read": [vp, u64, vp, vp, vp, vp, ctypes.POINTER(u64)],
             "mgrg_crc32": [vp, u64, ctypes.POINTER(ctypes.c_uint32), vp],

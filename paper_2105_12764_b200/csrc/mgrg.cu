@@ -233,6 +233,20 @@ struct mgrg_plan {
   std::vector<Prof> prof;
   std::vector<cudaEvent_t> event_pool;
   size_t prof_used = 0;
+  // CUDA-graph replay of the level loop (mgrg_plan_set_graphs): one
+  // instantiated graph per (operation, buffers, k), most recent last
+  bool graphs = false;
+  struct Graph {
+    int op; // 0 decompose, 1 recompose
+    const void *a;
+    void *b;
+    int32_t k;
+    cudaGraphExec_t exec;
+    uint64_t launches;
+  };
+  std::vector<Graph> graph_cache;
+  cudaStream_t graph_stream = nullptr;
+  cudaEvent_t graph_ev[2] = {nullptr, nullptr};
 };
 
 namespace {
@@ -647,6 +661,15 @@ int knob(const char *name, int dflt) {
 }
 // chunked fiber-resident Thomas (MGRG_TFIBER=0 disables)
 int g_thomas_fiber = knob("MGRG_TFIBER", 1);
+// Profiling event record: inside a stream capture (graph replay mode) the
+// record must be an EXTERNAL event-record node to be timeable.
+cudaError_t prof_record(cudaEvent_t e, cudaStream_t s) {
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  cudaStreamIsCapturing(s, &cs);
+  return cs == cudaStreamCaptureStatusActive
+             ? cudaEventRecordWithFlags(e, s, cudaEventRecordExternal)
+             : cudaEventRecord(e, s);
+}
 // programmatic dependent launch of the level-loop kernels (MGRG_PDL=0 disables)
 int g_pdl = knob("MGRG_PDL", 1);
 
@@ -1006,7 +1029,7 @@ mgrg_status Recorder::begin(int kind, int level, uint64_t bytes) {
   mgrg_plan::Prof pr{kind, level, bytes, p->event_pool[p->prof_used],
                      p->event_pool[p->prof_used + 1]};
   p->prof_used += 2;
-  CUDA_TRY(cudaEventRecord(pr.e0, s));
+  CUDA_TRY(prof_record(pr.e0, s));
   p->prof.push_back(pr);
   return MGRG_OK;
 }
@@ -1014,7 +1037,7 @@ mgrg_status Recorder::begin(int kind, int level, uint64_t bytes) {
 mgrg_status Recorder::end() {
   if (!active)
     return MGRG_OK;
-  CUDA_TRY(cudaEventRecord(p->prof.back().e1, s));
+  CUDA_TRY(prof_record(p->prof.back().e1, s));
   return MGRG_OK;
 }
 
@@ -1467,6 +1490,13 @@ mgrg_status mgrg_plan_destroy(mgrg_plan *p) {
     }
     if (p->ev_done)
       cudaEventDestroy(p->ev_done);
+    for (auto &gr : p->graph_cache)
+      cudaGraphExecDestroy(gr.exec);
+    if (p->graph_stream)
+      cudaStreamDestroy(p->graph_stream);
+    for (cudaEvent_t e : p->graph_ev)
+      if (e)
+        cudaEventDestroy(e);
   }
   delete p;
   return MGRG_OK;
@@ -1546,8 +1576,12 @@ mgrg_status mgrg_plan_profile_read(mgrg_plan *p, uint64_t cap, int32_t *kinds,
   DeviceGuard guard(p->device);
   if (count)
     *count = p->prof.size();
-  if (!p->prof.empty())
-    CUDA_TRY(cudaEventSynchronize(p->prof.back().e1));
+  // (a device sync, not an event sync: events recorded by replayed graph
+  // nodes cannot be host-synchronized)
+  if (!p->prof.empty()) {
+    DeviceGuard guard(p->device);
+    CUDA_TRY(cudaDeviceSynchronize());
+  }
   for (uint64_t i = 0; i < p->prof.size() && i < cap; ++i) {
     const auto &pr = p->prof[i];
     if (kinds)
@@ -1565,6 +1599,81 @@ mgrg_status mgrg_plan_profile_read(mgrg_plan *p, uint64_t cap, int32_t *kinds,
   return MGRG_OK;
 }
 
+} // extern "C"
+
+namespace {
+constexpr size_t kGraphCache = 8;
+
+// Run `body` (which launches the level loop on the stream it is given) as a
+// replayed CUDA graph: captured once per (op, a, b, k) on the plan's graph
+// stream -- the caller's stream may be the legacy default stream, which
+// cannot be captured -- and launched there between two event hand-offs.
+template <typename Body>
+mgrg_status run_graphed(mgrg_plan *p, int op, const void *a, void *b, int32_t k,
+                        cudaStream_t s, Body body) {
+  if (!p->graph_stream) {
+    CUDA_TRY(cudaStreamCreateWithFlags(&p->graph_stream, cudaStreamNonBlocking));
+    for (cudaEvent_t &e : p->graph_ev)
+      CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  }
+  auto &cache = p->graph_cache;
+  size_t hit = cache.size();
+  for (size_t i = 0; i < cache.size(); ++i)
+    if (cache[i].op == op && cache[i].a == a && cache[i].b == b && cache[i].k == k)
+      hit = i;
+  if (hit == cache.size()) {
+    if (cache.size() >= kGraphCache) {
+      cudaGraphExecDestroy(cache.front().exec);
+      cache.erase(cache.begin());
+    }
+    cudaGraph_t graph = nullptr;
+    CUDA_TRY(cudaStreamBeginCapture(p->graph_stream, cudaStreamCaptureModeThreadLocal));
+    const mgrg_status st = body(p->graph_stream);
+    const cudaError_t ce = cudaStreamEndCapture(p->graph_stream, &graph);
+    if (st != MGRG_OK) {
+      if (graph)
+        cudaGraphDestroy(graph);
+      return st;
+    }
+    if (ce != cudaSuccess)
+      return fail(MGRG_CUDA_ERROR, std::string("graph capture: ") + cudaGetErrorString(ce));
+    cudaGraphExec_t exec = nullptr;
+    const cudaError_t ie = cudaGraphInstantiate(&exec, graph, 0);
+    cudaGraphDestroy(graph);
+    if (ie != cudaSuccess)
+      return fail(MGRG_CUDA_ERROR, std::string("graph instantiate: ") + cudaGetErrorString(ie));
+    cache.push_back({op, a, b, k, exec, p->last_launches});
+    hit = cache.size() - 1;
+  } else if (hit + 1 != cache.size()) {
+    std::rotate(cache.begin() + hit, cache.begin() + hit + 1, cache.end());
+    hit = cache.size() - 1;
+  }
+  CUDA_TRY(cudaEventRecord(p->graph_ev[0], s));
+  CUDA_TRY(cudaStreamWaitEvent(p->graph_stream, p->graph_ev[0], 0));
+  CUDA_TRY(cudaGraphLaunch(cache[hit].exec, p->graph_stream));
+  CUDA_TRY(cudaEventRecord(p->graph_ev[1], p->graph_stream));
+  CUDA_TRY(cudaStreamWaitEvent(s, p->graph_ev[1], 0));
+  p->last_launches = cache[hit].launches;
+  return MGRG_OK;
+}
+} // namespace
+
+extern "C" {
+
+mgrg_status mgrg_plan_set_graphs(mgrg_plan *p, int32_t enable) {
+  g_last_error.clear();
+  if (mgrg_status st = check_plan(p))
+    return st;
+  DeviceGuard guard(p->device);
+  p->graphs = enable != 0;
+  if (!p->graphs) {
+    for (auto &gr : p->graph_cache)
+      cudaGraphExecDestroy(gr.exec);
+    p->graph_cache.clear();
+  }
+  return MGRG_OK;
+}
+
 mgrg_status mgrg_decompose(mgrg_plan *p, const void *d_values, void *d_classes,
                            void *stream) {
   g_last_error.clear();
@@ -1576,11 +1685,16 @@ mgrg_status mgrg_decompose(mgrg_plan *p, const void *d_values, void *d_classes,
     return fail(p->deferred, p->deferred_msg);
   DeviceGuard guard(p->device);
   cudaStream_t s = static_cast<cudaStream_t>(stream);
-  return p->dtype == MGRG_F32
-             ? run_decompose<float>(p, static_cast<const float *>(d_values),
-                                    static_cast<float *>(d_classes), s)
-             : run_decompose<double>(p, static_cast<const double *>(d_values),
-                                     static_cast<double *>(d_classes), s);
+  auto body = [&](cudaStream_t q) {
+    return p->dtype == MGRG_F32
+               ? run_decompose<float>(p, static_cast<const float *>(d_values),
+                                      static_cast<float *>(d_classes), q)
+               : run_decompose<double>(p, static_cast<const double *>(d_values),
+                                       static_cast<double *>(d_classes), q);
+  };
+  if (p->graphs)
+    return run_graphed(p, 0, d_values, d_classes, 0, s, body);
+  return body(s);
 }
 
 mgrg_status mgrg_recompose(mgrg_plan *p, const void *d_classes, int32_t k,
@@ -1598,11 +1712,16 @@ mgrg_status mgrg_recompose(mgrg_plan *p, const void *d_classes, int32_t k,
     return fail(p->deferred, p->deferred_msg);
   DeviceGuard guard(p->device);
   cudaStream_t s = static_cast<cudaStream_t>(stream);
-  return p->dtype == MGRG_F32
-             ? run_recompose<float>(p, static_cast<const float *>(d_classes), k,
-                                    static_cast<float *>(d_values), s)
-             : run_recompose<double>(p, static_cast<const double *>(d_classes), k,
-                                     static_cast<double *>(d_values), s);
+  auto body = [&](cudaStream_t q) {
+    return p->dtype == MGRG_F32
+               ? run_recompose<float>(p, static_cast<const float *>(d_classes), k,
+                                      static_cast<float *>(d_values), q)
+               : run_recompose<double>(p, static_cast<const double *>(d_classes), k,
+                                       static_cast<double *>(d_values), q);
+  };
+  if (p->graphs)
+    return run_graphed(p, 1, d_classes, d_values, k, s, body);
+  return body(s);
 }
 
 // host-API staging: [in | out] with the second half 256-byte aligned (the

@@ -123,6 +123,11 @@ class Plan:
         return n.value
 
     # -- per-launch profiling ------------------------------------------------------
+    def set_graphs(self, enable=True):
+        """Replay decompose / recompose as captured CUDA graphs (one per
+        buffers + classes_used; mgrg_plan_set_graphs)."""
+        _lib.check(_lib.lib().mgrg_plan_set_graphs(self._h, int(bool(enable))))
+
     def set_profiling(self, enable=True, top_levels=None):
         """Per-launch CUDA-event timing; top_levels=k profiles only the
         launches of levels L .. L-k+1."""

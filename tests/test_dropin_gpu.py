@@ -135,3 +135,36 @@ def test_coop_schedule_matches_runtime_rule():
     _lib.check(_lib.lib().mgrg_device_count(ctypes.byref(n)))
     assert n.value >= 1
     plan.close()
+
+
+@pytest.mark.parametrize("shape,dt,fast", [((65, 33, 17), "float32", True),
+                                           ((33, 17, 9), "float64", False),
+                                           ((257, 129), "float64", True)])
+def test_graph_replay_identical(shape, dt, fast):
+    """mgrg_plan_set_graphs: captured-graph replay gives the same bits as the
+    stream launches, for repeated calls, a second buffer set (new capture)
+    and every classes_used."""
+    import torch
+
+    from paper_2105_12764_b200 import Plan
+
+    v = torch.rand(int(np.prod(shape)), dtype=getattr(torch, dt), device="cuda")
+    plan = Plan(shape, dt, fast=fast)
+    c0 = plan.decompose(v)
+    r0 = [plan.recompose(c0, k) for k in range(plan.levels + 1)]
+    plan.set_graphs(True)
+    c1 = torch.empty_like(c0)
+    for _ in range(3):
+        plan.decompose(v, c1)
+        assert torch.equal(c1, c0)
+    v2 = v.clone()
+    c2 = plan.decompose(v2)
+    assert torch.equal(c2, c0)
+    out = torch.empty_like(v)
+    for k in range(plan.levels + 1):
+        for _ in range(2):
+            plan.recompose(c1, k, out)
+            assert torch.equal(out, r0[k])
+    assert plan.last_launches > 0
+    plan.set_graphs(False)
+    plan.close()
