@@ -209,23 +209,28 @@ template <typename R> struct LeanStage {
 // take the unchecked path; near the array ends chunks before element 0 are
 // skipped (invalid columns) and chunks crossing the end go element-wise.
 template <typename R, int NR>
-__device__ __forceinline__ void lean_stage_plane(R *slot, const R *__restrict__ pb, int q,
+__device__ __forceinline__ void lean_stage_plane(R *slot, const R *__restrict__ in,
+                                                 const R *__restrict__ pb, int q,
                                                  const int *rowoff, bool interior,
                                                  int64_t pbase, int64_t ntot, int lane) {
   constexpr int V = LeanStage<R>::V, NCH = LeanStage<R>::NCH, RP = LeanStage<R>::RP;
   // lane c copies chunk c (and c + 32 when NCH > 32) of every row
-  const R *gl = pb - q + lane * V; // 16-byte aligned element of the plane
   R *sl = slot + lane * V;
   if (interior) {
+    // 32-bit element indices (lean plans have N < 2^32): chunk c of row r
+    // starts at ((pbase + rowoff[r]) & ~(V-1)) + c*V = (pbase + rowoff[r] +
+    // c*V) & ~(V-1) -- one add, one mask and one wide multiply-add per copy
+    const uint32_t pl = uint32_t(pbase) + uint32_t(lane * V);
     if (lane < NCH) {
 #pragma unroll
       for (int r = 0; r < NR; ++r)
-        cp_async16(sl + r * RP, gl + ((q + rowoff[r]) & ~(V - 1)));
+        cp_async16(sl + r * RP, in + ((pl + uint32_t(rowoff[r])) & ~uint32_t(V - 1)));
     }
     if (NCH > 32 && lane + 32 < NCH) {
 #pragma unroll
       for (int r = 0; r < NR; ++r)
-        cp_async16(sl + r * RP + 32 * V, gl + ((q + rowoff[r]) & ~(V - 1)) + 32 * V);
+        cp_async16(sl + r * RP + 32 * V,
+                   in + ((pl + uint32_t(rowoff[r] + 32 * V)) & ~uint32_t(V - 1)));
     }
     return;
   }
@@ -248,10 +253,13 @@ __device__ __forceinline__ void lean_stage_plane(R *slot, const R *__restrict__ 
   }
 }
 
-// Class/packed stores of one plane: row r of the band writes its even node
-// to be[r&1] + ex_e*(r>>1) and its odd node to bo[r&1] + ex_o*(r>>1).
+// Class/packed stores of one plane as 32-bit element indices (lean plans
+// have N < 2^32; indices may wrap below zero for masked rows): row r of the
+// band writes its even node to (r even: pe0, else cls)[ie[r&1] + ex_e*(r>>1)]
+// and its odd node to cls[io[r&1] + ex_o*(r>>1)].
 template <typename R> struct PlaneOut {
-  R *be0, *bo0, *be1, *bo1; // even rows (e, o), odd rows (e, o)
+  R *pe0;                     // even rows' even nodes: P (even plane) or cls
+  uint32_t ie0, io0, ie1, io1; // even rows (e, o), odd rows (e, o)
 };
 
 // ---------------------------------------------------------------------------
@@ -265,7 +273,8 @@ __device__ __forceinline__ void lean_plane(
     const R *__restrict__ slot, int q, const int *rowoff, R txr, const R *tyr,
     const W5r<R> &wx, const W5r<R> *wy, const Stencil<R> &sx,
     const Stencil<R> *__restrict__ sy, int cy0, int m1, bool ve, bool vo, uint32_t stmask_e,
-    uint32_t stmask_o, const PlaneOut<R> &po, int ex_e, int ex_o, R *We, R *Wo,
+    uint32_t stmask_o, const PlaneOut<R> &po, R *__restrict__ cls, int ex_e, int ex_o, R *We,
+    R *Wo,
     const R *WLe, const R *WLo, R tz, R *Y) {
   constexpr int NR = 2 * TY + 3;
   constexpr int RP = LeanStage<R>::RP;
@@ -318,9 +327,10 @@ __device__ __forceinline__ void lean_plane(
     const R co = vo ? psub<R, FAST>(u[r].o, wo) : R(0);
     const int rr = r >> 1;
     if ((stmask_e >> r) & 1u)
-      ((r & 1) ? po.be1 : po.be0)[uint32_t(ex_e * rr)] = kept ? u[r].e : ce;
+      ((r & 1) ? cls : po.pe0)[((r & 1) ? po.ie1 : po.ie0) + uint32_t(ex_e * rr)] =
+          kept ? u[r].e : ce;
     if ((stmask_o >> r) & 1u)
-      ((r & 1) ? po.bo1 : po.bo0)[uint32_t(ex_o * rr)] = co;
+      cls[((r & 1) ? po.io1 : po.io0) + uint32_t(ex_o * rr)] = co;
     X[r] = kept ? lean_xpass_odd<R, FAST>(wx, sx, co) : lean_xpass<R, FAST>(wx, sx, ce, co);
   }
   lean_ypass_all<R, FAST, TY>(wy, sy, cy0, m1, X, Y);
@@ -426,8 +436,8 @@ __global__ void __launch_bounds__(32 * kLeanWPB, LEAN_DEC_MINB)
       const int64_t pbase = int64_t(p) * nxy;
       const bool interior = pbase + rlo >= 0 && pbase + rhi <= ntot;
       const int slot = j % 3;
-      lean_stage_plane<R, NR>(ring + slot * SLOT, in + pbase, int(pbase & (V - 1)), rowoff,
-                              interior, pbase, ntot, lane);
+      lean_stage_plane<R, NR>(ring + slot * SLOT, in, in + pbase, int(pbase & (V - 1)),
+                              rowoff, interior, pbase, ntot, lane);
     }
     cp_async_commit();
   };
@@ -461,13 +471,14 @@ __global__ void __launch_bounds__(32 * kLeanWPB, LEAN_DEC_MINB)
         const bool own = pe >= 2 * cz0 && pe < 2 * cz1;
         const int64_t yb = int64_t(cy0) - 1; // rank of band row 0
         PlaneOut<R> po;
-        po.be0 = P + qc + int64_t(m0) * (yb + int64_t(m1) * k);
-        po.bo0 = cls + g.tbase[1] + qc + int64_t(m0 - 1) * (yb + int64_t(m1) * k);
-        po.be1 = cls + g.tbase[2] + qc + int64_t(m0) * (yb + int64_t(m1 - 1) * k);
-        po.bo1 = cls + g.tbase[3] + qc + int64_t(m0 - 1) * (yb + int64_t(m1 - 1) * k);
+        po.pe0 = P;
+        po.ie0 = uint32_t(qc + int64_t(m0) * (yb + int64_t(m1) * k));
+        po.io0 = uint32_t(g.tbase[1] + qc + int64_t(m0 - 1) * (yb + int64_t(m1) * k));
+        po.ie1 = uint32_t(g.tbase[2] + qc + int64_t(m0) * (yb + int64_t(m1 - 1) * k));
+        po.io1 = uint32_t(g.tbase[3] + qc + int64_t(m0 - 1) * (yb + int64_t(m1 - 1) * k));
         lean_plane<R, TY, true, FAST>(ring + js * SLOT, q_of(pe), rowoff, txr, tyr, wx, wy, sx,
                                       syt, cy0, m1, ve,
-                                vo, own ? st_e : 0u, own ? st_o : 0u, po, m0, m0 - 1, We, Wo,
+                                vo, own ? st_e : 0u, own ? st_o : 0u, po, cls, m0, m0 - 1, We, Wo,
                                 nullptr, nullptr, R(0), YE);
       } else {
 #pragma unroll
@@ -500,13 +511,14 @@ __global__ void __launch_bounds__(32 * kLeanWPB, LEAN_DEC_MINB)
         const int64_t yb = int64_t(cy0) - 1;
         const int64_t zr = k - 1;
         PlaneOut<R> po;
-        po.be0 = cls + g.tbase[4] + qc + int64_t(m0) * (yb + int64_t(m1) * zr);
-        po.bo0 = cls + g.tbase[5] + qc + int64_t(m0 - 1) * (yb + int64_t(m1) * zr);
-        po.be1 = cls + g.tbase[6] + qc + int64_t(m0) * (yb + int64_t(m1 - 1) * zr);
-        po.bo1 = cls + g.tbase[7] + qc + int64_t(m0 - 1) * (yb + int64_t(m1 - 1) * zr);
+        po.pe0 = cls;
+        po.ie0 = uint32_t(g.tbase[4] + qc + int64_t(m0) * (yb + int64_t(m1) * zr));
+        po.io0 = uint32_t(g.tbase[5] + qc + int64_t(m0 - 1) * (yb + int64_t(m1) * zr));
+        po.ie1 = uint32_t(g.tbase[6] + qc + int64_t(m0) * (yb + int64_t(m1 - 1) * zr));
+        po.io1 = uint32_t(g.tbase[7] + qc + int64_t(m0 - 1) * (yb + int64_t(m1 - 1) * zr));
         lean_plane<R, TY, false, FAST>(ring + js * SLOT, q_of(pz), rowoff, txr, tyr, wx, wy, sx,
                                        syt, cy0, m1, ve,
-                                 vo, own ? st_e : 0u, own ? st_o : 0u, po, m0, m0 - 1, We,
+                                 vo, own ? st_e : 0u, own ? st_o : 0u, po, cls, m0, m0 - 1, We,
                                  Wo, WLe, WLo, __ldg(&lzk->t), YO);
       } else {
 #pragma unroll

@@ -1428,6 +1428,9 @@ mgrg_status mgrg_plan_create(const mgrg_grid_desc *desc, mgrg_plan **out) {
     // are all odd (coarse = even positions), see lean_level()
     p->lean = p->refine == 7u || (p->refine == 3u && p->kext[L][2] == 1);
     p->lean = p->lean && knob("MGRG_LEAN", 1) != 0;
+    // the lean kernels index the level array and class buffer with 32-bit
+    // element offsets
+    p->lean = p->lean && p->nodes[L] < (uint64_t(1) << 32);
   }
   p->zchunk = nd == 3 ? 32 : 1;
   if (nd == 3 && knob("MGRG_ZCHUNK", 0) > 0)
