@@ -453,7 +453,7 @@ __global__ void __launch_bounds__(32 * kLeanWPB, LEAN_DEC_MINB)
   for (int j = 0; j < TY; ++j)
     accM[j] = acc0[j] = YEm2[j] = YOm1[j] = YEm1[j] = R(0);
   const int64_t m01 = int64_t(m0) * m1;
-  R *fq = f + qc + int64_t(m0) * cy0;
+  const uint32_t fq0 = uint32_t(qc + m0 * cy0); // f index of output row cy0 (may wrap: masked)
 
   issue(0);
   issue(1);
@@ -496,7 +496,7 @@ __global__ void __launch_bounds__(32 * kLeanWPB, LEAN_DEC_MINB)
 #pragma unroll
       for (int i = 0; i < TY; ++i)
         if (outl && cy0 + i < cy1)
-          fq[int64_t(m0) * i] = YE[i];
+          f[fq0 + uint32_t(m0 * i)] = YE[i];
       break;
     }
     // ================= odd plane 2k - 1 =================
@@ -548,7 +548,7 @@ __global__ void __launch_bounds__(32 * kLeanWPB, LEAN_DEC_MINB)
       for (int i = 0; i < TY; ++i) {
         const R out = fma(a3, YO[i], fma(a4, YE[i], accM[i]));
         if (emit && cy0 + i < cy1)
-          fq[int64_t(m0) * i + m01 * (k - 1)] = out;
+          f[fq0 + uint32_t(m0 * i) + uint32_t(m01) * uint32_t(k - 1)] = out;
         accM[i] = fma(b1, YO[i], fma(b2, YE[i], acc0[i]));
         acc0[i] = c0 * YE[i];
       }
@@ -563,7 +563,7 @@ __global__ void __launch_bounds__(32 * kLeanWPB, LEAN_DEC_MINB)
       for (int i = 0; i < TY; ++i) {
         const R mr = st_mr(sk, YEm1[i], YO[i], YE[i]);
         if (emit && cy0 + i < cy1)
-          fq[int64_t(m0) * i + m01 * (k - 1)] =
+          f[fq0 + uint32_t(m0 * i) + uint32_t(m01) * uint32_t(k - 1)] =
               st_combine(sk, R(0), YOm1[i], YEm1[i], YO[i], YEm2[i], mr);
         YEm2[i] = mr;
         YOm1[i] = YO[i];
@@ -637,7 +637,7 @@ __global__ void __launch_bounds__(32 * kLeanWPB, LEAN_RL_MINB)
   for (int j = 0; j < TY; ++j)
     accM[j] = acc0[j] = YEm2[j] = YOm1[j] = YEm1[j] = R(0);
   const int64_t m01 = int64_t(m0) * m1;
-  R *fq = f + qc + int64_t(m0) * cy0;
+  const uint32_t fq0 = uint32_t(qc + m0 * cy0); // f index of output row cy0 (may wrap: masked)
 
   // class row offsets of band row r (rank cy0 - 1 + (r >> 1) clamped into
   // the type's y range; invalid rows are masked), loop invariant
@@ -649,7 +649,6 @@ __global__ void __launch_bounds__(32 * kLeanWPB, LEAN_RL_MINB)
     oe[r] = uint32_t(m0) * rk;
     oo[r] = uint32_t(m0 - 1) * rk;
   }
-  const R *cbe = cls + qe, *cbo = cls + qo;
 
   for (int k = Z3 ? cz0 - 1 : 0; k <= (Z3 ? cz1 : 0); ++k) {
     R YE[TY], YO[TY];
@@ -658,25 +657,27 @@ __global__ void __launch_bounds__(32 * kLeanWPB, LEAN_RL_MINB)
     const bool ov = Z3 && k >= cz0 && pz >= 1 && pz < n2;
     // ---- both planes' loads first (one batch of independent loads per
     // step); invalid planes read a valid one and are zeroed below
-    const int64_t ke = ev ? k : 0, ko = ov ? k - 1 : 0;
-    const R *b1 = cbo + g.tbase[1] + int64_t(m0 - 1) * (int64_t(m1) * ke);
-    const R *b2 = cbe + g.tbase[2] + int64_t(m0) * (int64_t(m1 - 1) * ke);
-    const R *b3 = cbo + g.tbase[3] + int64_t(m0 - 1) * (int64_t(m1 - 1) * ke);
+    // 32-bit element indices into the class buffer (lean plans: N < 2^32)
+    const uint32_t ke = ev ? uint32_t(k) : 0u, ko = ov ? uint32_t(k - 1) : 0u;
+    const uint32_t b1 = qo + uint32_t(g.tbase[1]) + uint32_t(m0 - 1) * (uint32_t(m1) * ke);
+    const uint32_t b2 = qe + uint32_t(g.tbase[2]) + uint32_t(m0) * (uint32_t(m1 - 1) * ke);
+    const uint32_t b3 = qo + uint32_t(g.tbase[3]) + uint32_t(m0 - 1) * (uint32_t(m1 - 1) * ke);
     R ueE[NR], uoE[NR], ueO[NR], uoO[NR];
 #pragma unroll
     for (int r = 0; r < NR; ++r) {
-      ueE[r] = (r & 1) ? __ldg(b2 + oe[r]) : R(0); // even rows: kept nodes
-      uoE[r] = __ldg(((r & 1) ? b3 : b1) + oo[r]);
+      ueE[r] = (r & 1) ? __ldg(cls + (b2 + oe[r])) : R(0); // even rows: kept nodes
+      uoE[r] = __ldg(cls + (((r & 1) ? b3 : b1) + oo[r]));
     }
     if constexpr (Z3) {
-      const R *b4 = cbe + g.tbase[4] + int64_t(m0) * (int64_t(m1) * ko);
-      const R *b5 = cbo + g.tbase[5] + int64_t(m0 - 1) * (int64_t(m1) * ko);
-      const R *b6 = cbe + g.tbase[6] + int64_t(m0) * (int64_t(m1 - 1) * ko);
-      const R *b7 = cbo + g.tbase[7] + int64_t(m0 - 1) * (int64_t(m1 - 1) * ko);
+      const uint32_t b4 = qe + uint32_t(g.tbase[4]) + uint32_t(m0) * (uint32_t(m1) * ko);
+      const uint32_t b5 = qo + uint32_t(g.tbase[5]) + uint32_t(m0 - 1) * (uint32_t(m1) * ko);
+      const uint32_t b6 = qe + uint32_t(g.tbase[6]) + uint32_t(m0) * (uint32_t(m1 - 1) * ko);
+      const uint32_t b7 =
+          qo + uint32_t(g.tbase[7]) + uint32_t(m0 - 1) * (uint32_t(m1 - 1) * ko);
 #pragma unroll
       for (int r = 0; r < NR; ++r) {
-        ueO[r] = __ldg(((r & 1) ? b6 : b4) + oe[r]);
-        uoO[r] = __ldg(((r & 1) ? b7 : b5) + oo[r]);
+        ueO[r] = __ldg(cls + (((r & 1) ? b6 : b4) + oe[r]));
+        uoO[r] = __ldg(cls + (((r & 1) ? b7 : b5) + oo[r]));
       }
     }
     // ---- even plane
@@ -699,7 +700,7 @@ __global__ void __launch_bounds__(32 * kLeanWPB, LEAN_RL_MINB)
 #pragma unroll
       for (int j = 0; j < TY; ++j)
         if (outl && cy0 + j < cy1)
-          fq[int64_t(m0) * j] = YE[j];
+          f[fq0 + uint32_t(m0 * j)] = YE[j];
       break;
     }
     const LeanW<R> *lzk = lz + k + 1;
@@ -724,7 +725,7 @@ __global__ void __launch_bounds__(32 * kLeanWPB, LEAN_RL_MINB)
       for (int j = 0; j < TY; ++j) {
         const R out = fma(a3, YO[j], fma(a4, YE[j], accM[j]));
         if (emit && cy0 + j < cy1)
-          fq[int64_t(m0) * j + m01 * (k - 1)] = out;
+          f[fq0 + uint32_t(m0 * j) + uint32_t(m01) * uint32_t(k - 1)] = out;
         accM[j] = fma(b1, YO[j], fma(b2, YE[j], acc0[j]));
         acc0[j] = c0 * YE[j];
       }
@@ -737,7 +738,7 @@ __global__ void __launch_bounds__(32 * kLeanWPB, LEAN_RL_MINB)
       for (int j = 0; j < TY; ++j) {
         const R mr = st_mr(sk, YEm1[j], YO[j], YE[j]);
         if (emit && cy0 + j < cy1)
-          fq[int64_t(m0) * j + m01 * (k - 1)] =
+          f[fq0 + uint32_t(m0 * j) + uint32_t(m01) * uint32_t(k - 1)] =
               st_combine(sk, R(0), YOm1[j], YEm1[j], YO[j], YEm2[j], mr);
         YEm2[j] = mr;
         YOm1[j] = YO[j];
@@ -848,33 +849,35 @@ __global__ void __launch_bounds__(32 * kLeanWPB, LEAN_RG_MINB)
   struct In {
     R c[TG + 1], v[7][TG];
   };
+  // 32-bit element indices (lean plans: N < 2^32)
   auto load = [&](int k, In &in) {
-    const R *cp = coarse + m01 * k + qe;
+    const uint32_t cp = uint32_t(m01) * uint32_t(k) + uint32_t(qe);
 #pragma unroll
     for (int i = 0; i <= TG; ++i)
-      in.c[i] = __ldg(cp + int64_t(m0) * crow[i]);
+      in.c[i] = __ldg(coarse + (cp + uint32_t(m0 * crow[i])));
     if constexpr (CLS) {
-      const int64_t ke = min(k, m2 - 1), zr = max(k - 1, 0);
-      const R *c1 = cls + g.tbase[1] + qo + int64_t(m0 - 1) * (int64_t(m1) * ke);
-      const R *c2 = cls + g.tbase[2] + qe + int64_t(m0) * (int64_t(m1 - 1) * ke);
-      const R *c3 = cls + g.tbase[3] + qo + int64_t(m0 - 1) * (int64_t(m1 - 1) * ke);
+      const uint32_t ke = uint32_t(min(k, m2 - 1)), zr = uint32_t(max(k - 1, 0));
+      const uint32_t um0 = uint32_t(m0), um1 = uint32_t(m1);
+      const uint32_t c1 = uint32_t(g.tbase[1]) + qo + (um0 - 1) * (um1 * ke);
+      const uint32_t c2 = uint32_t(g.tbase[2]) + qe + um0 * ((um1 - 1) * ke);
+      const uint32_t c3 = uint32_t(g.tbase[3]) + qo + (um0 - 1) * ((um1 - 1) * ke);
 #pragma unroll
       for (int i = 0; i < TG; ++i) {
-        in.v[0][i] = __ldg(c1 + int64_t(m0 - 1) * crow[i]);
-        in.v[1][i] = __ldg(c2 + int64_t(m0) * rfo[i]);
-        in.v[2][i] = __ldg(c3 + int64_t(m0 - 1) * rfo[i]);
+        in.v[0][i] = __ldg(cls + (c1 + (um0 - 1) * uint32_t(crow[i])));
+        in.v[1][i] = __ldg(cls + (c2 + um0 * uint32_t(rfo[i])));
+        in.v[2][i] = __ldg(cls + (c3 + (um0 - 1) * uint32_t(rfo[i])));
       }
       if constexpr (Z3) {
-        const R *c4 = cls + g.tbase[4] + qe + int64_t(m0) * (int64_t(m1) * zr);
-        const R *c5 = cls + g.tbase[5] + qo + int64_t(m0 - 1) * (int64_t(m1) * zr);
-        const R *c6 = cls + g.tbase[6] + qe + int64_t(m0) * (int64_t(m1 - 1) * zr);
-        const R *c7 = cls + g.tbase[7] + qo + int64_t(m0 - 1) * (int64_t(m1 - 1) * zr);
+        const uint32_t c4 = uint32_t(g.tbase[4]) + qe + um0 * (um1 * zr);
+        const uint32_t c5 = uint32_t(g.tbase[5]) + qo + (um0 - 1) * (um1 * zr);
+        const uint32_t c6 = uint32_t(g.tbase[6]) + qe + um0 * ((um1 - 1) * zr);
+        const uint32_t c7 = uint32_t(g.tbase[7]) + qo + (um0 - 1) * ((um1 - 1) * zr);
 #pragma unroll
         for (int i = 0; i < TG; ++i) {
-          in.v[3][i] = __ldg(c4 + int64_t(m0) * crow[i]);
-          in.v[4][i] = __ldg(c5 + int64_t(m0 - 1) * crow[i]);
-          in.v[5][i] = __ldg(c6 + int64_t(m0) * rfo[i]);
-          in.v[6][i] = __ldg(c7 + int64_t(m0 - 1) * rfo[i]);
+          in.v[3][i] = __ldg(cls + (c4 + um0 * uint32_t(crow[i])));
+          in.v[4][i] = __ldg(cls + (c5 + (um0 - 1) * uint32_t(crow[i])));
+          in.v[5][i] = __ldg(cls + (c6 + um0 * uint32_t(rfo[i])));
+          in.v[6][i] = __ldg(cls + (c7 + (um0 - 1) * uint32_t(rfo[i])));
         }
       }
     }
@@ -902,17 +905,17 @@ __global__ void __launch_bounds__(32 * kLeanWPB, LEAN_RG_MINB)
     }
     // ---- even plane 2k (written when k < cz1)
     if (k < cz1) {
-      R *op = out + int64_t(2 * k) * nxy + int64_t(2 * cy0) * n0 + 2 * qc;
+      const uint32_t op = uint32_t(2 * k) * uint32_t(nxy) + uint32_t(2 * cy0 * n0 + 2 * qc);
 #pragma unroll
       for (int i = 0; i < TG; ++i) {
         const R v1 = CLS ? cur.v[0][i] : R(0), v2 = CLS ? cur.v[1][i] : R(0),
                 v3 = CLS ? cur.v[2][i] : R(0);
         // even row 2(cy0+i): parity of (2k + 2(cy0+i)) is even -> aligned
         if ((wrow >> (2 * i)) & 1u)
-          lean_store_pair<R, true>(op + int64_t(2 * i) * n0, We[2 * i],
+          lean_store_pair<R, true>(out + (op + uint32_t(2 * i * n0)), We[2 * i],
                                    padd<R, FAST>(Wo[2 * i], v1), own, ownO);
         if ((wrow >> (2 * i + 1)) & 1u)
-          lean_store_pair<R, false>(op + int64_t(2 * i + 1) * n0,
+          lean_store_pair<R, false>(out + (op + uint32_t((2 * i + 1) * n0)),
                                     padd<R, FAST>(We[2 * i + 1], v2),
                                     padd<R, FAST>(Wo[2 * i + 1], v3), own, ownO);
       }
@@ -920,7 +923,8 @@ __global__ void __launch_bounds__(32 * kLeanWPB, LEAN_RG_MINB)
     // ---- odd plane 2k-1
     if (Z3 && k > cz0) {
       const R tz = __ldg(&lz[k - 1 + 2].t);
-      R *op = out + int64_t(2 * k - 1) * nxy + int64_t(2 * cy0) * n0 + 2 * qc;
+      const uint32_t op =
+          uint32_t(2 * k - 1) * uint32_t(nxy) + uint32_t(2 * cy0 * n0 + 2 * qc);
 #pragma unroll
       for (int i = 0; i < TG; ++i) {
         const R v4 = CLS ? cur.v[3][i] : R(0), v5 = CLS ? cur.v[4][i] : R(0),
@@ -928,12 +932,12 @@ __global__ void __launch_bounds__(32 * kLeanWPB, LEAN_RG_MINB)
         // odd plane: even rows misaligned, odd rows aligned
         if ((wrow >> (2 * i)) & 1u)
           lean_store_pair<R, false>(
-              op + int64_t(2 * i) * n0,
+              out + (op + uint32_t(2 * i * n0)),
               padd<R, FAST>(plerp<R, FAST>(WLe[2 * i], We[2 * i], tz), v4),
               padd<R, FAST>(plerp<R, FAST>(WLo[2 * i], Wo[2 * i], tz), v5), own, ownO);
         if ((wrow >> (2 * i + 1)) & 1u)
           lean_store_pair<R, true>(
-              op + int64_t(2 * i + 1) * n0,
+              out + (op + uint32_t((2 * i + 1) * n0)),
               padd<R, FAST>(plerp<R, FAST>(WLe[2 * i + 1], We[2 * i + 1], tz), v6),
               padd<R, FAST>(plerp<R, FAST>(WLo[2 * i + 1], Wo[2 * i + 1], tz), v7), own,
               ownO);
