@@ -390,6 +390,31 @@ def run_e2e(plan, d_in, d_out, N, nbytes, L, K, dist, device, world):
     return e2e
 
 
+def run_dropin(fast: bool, steps: int = 2, warmup: int = 1):
+    """The C++ source drop-in as a reference caller uses it (tests/cpp/
+    bench_dropin.cpp: pageable std::vector input, per-class std::vector
+    output, mgr::decompose + mgr::recompose with every class), host
+    wall-clock per step -- what `#include "mgr_b200/refactor.hpp"` gives a
+    caller of the reference API at 1025^3 f32."""
+    import subprocess
+
+    src = os.path.join(ROOT, "tests", "cpp", "bench_dropin.cpp")
+    pkg = os.path.join(ROOT, "paper_2105_12764_b200")
+    exe = os.path.join(ROOT, "build", "bench_dropin")
+    if not os.path.exists(exe) or os.path.getmtime(exe) < max(
+            os.path.getmtime(src), os.path.getmtime(os.path.join(pkg, "libmgrg.so")),
+            os.path.getmtime(os.path.join(ROOT, "include", "mgr_b200", "refactor.hpp"))):
+        os.makedirs(os.path.dirname(exe), exist_ok=True)
+        subprocess.run(["g++", "-std=c++17", "-O2", "-I", os.path.join(ROOT, "include"), src,
+                        "-L", pkg, "-lmgrg", "-pthread", f"-Wl,-rpath,{pkg}", "-o", exe],
+                       check=True, capture_output=True)
+    out = subprocess.run([exe, str(SHAPE[0]), str(steps), str(warmup), str(int(fast))],
+                         capture_output=True, text=True, timeout=600)
+    if out.returncode != 0:
+        raise RuntimeError(out.stderr.strip()[-200:])
+    return json.loads(out.stdout.strip().splitlines()[-1])
+
+
 def other_configs(args, device):
     """Device dec + rec throughput of BASELINE configs 1, 2, 3 and the config-5
     block (secondary lines of the report; parity for them is in
@@ -616,6 +641,24 @@ def run_ours(args, rank, world, local_rank):
         except (RuntimeError, MemoryError) as ex:  # e.g. pinned host memory exhausted
             e2e = {"value": None, "unit": "GB/s", "error": str(ex)[:200]}
 
+    dropin = None
+    if rank == 0 and world == 1 and not args.no_e2e:
+        try:
+            dropin = {}
+            for pol in ("exact", "fast"):
+                r = run_dropin(pol == "fast")
+                dropin[pol] = {"value": round(r["GBps"], 3), "unit": "GB/s",
+                               "ms_per_step": r["ms_per_step"],
+                               "decompose_ms": r["decompose_ms"],
+                               "recompose_ms": r["recompose_ms"], "steps": r["steps"],
+                               "alloc_vector_ms": r.get("alloc_vector_ms"),
+                               "alloc_prefaulted_ms": r.get("alloc_prefaulted_ms")}
+            dropin["how"] = ("C++ drop-in include/mgr_b200/refactor.hpp: pageable std::vector "
+                             "in, per-class std::vector out (mgr::decompose + mgr::recompose, "
+                             "host wall clock incl. output allocation); tests/cpp/bench_dropin.cpp")
+        except (RuntimeError, OSError, ValueError, subprocess.SubprocessError) as ex:
+            dropin = {"value": None, "error": str(ex)[:200]}
+
     others = None
     if rank == 0 and world == 1 and not args.no_others:
         plan.close()
@@ -649,7 +692,7 @@ def run_ours(args, rank, world, local_rank):
             "launch_mode": "cuda-graph replay" if args.graphs else "PDL stream launches",
             "roofline": roofline, "step_roofline": step_roofline,
             "per_kernel": per_kernel,
-            "cpu_baseline": cpu, "e2e": e2e,
+            "cpu_baseline": cpu, "e2e": e2e, "dropin_e2e": dropin,
             "gpu_launches": launches_per_step * K,
             "clocks": clocks,
             "other_configs": others,

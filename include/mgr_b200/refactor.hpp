@@ -35,6 +35,10 @@
 #include <type_traits>
 #include <vector>
 
+#if defined(__linux__)
+#include <sys/mman.h>
+#endif
+
 #include "../mgrg.h"
 
 namespace mgr {
@@ -357,6 +361,50 @@ inline void fill_stats(PassStats &stats, mgrg_plan *p, std::size_t nd, bool reco
   }
 }
 
+// An n-element value-initialised std::vector<Real> (the reference's output
+// type) whose pages are first faulted in by all host threads: a fresh
+// multi-GB std::vector otherwise spends ~0.4 s per GB page-faulting inside
+// its single-threaded zero fill (profiles/r2/host_probe.json).  Populating
+// the reserved storage is a kernel operation on memory the vector owns; no
+// element is touched before resize() constructs it.
+inline void prefault(void *p, std::size_t bytes) {
+#if defined(__linux__)
+#ifndef MADV_POPULATE_WRITE
+#define MADV_POPULATE_WRITE 23
+#endif
+  const std::size_t pg = 4096;
+  const std::uintptr_t a = (reinterpret_cast<std::uintptr_t>(p) + pg - 1) & ~(pg - 1);
+  const std::uintptr_t e = (reinterpret_cast<std::uintptr_t>(p) + bytes) & ~(pg - 1);
+  if (e <= a)
+    return;
+#ifdef MADV_HUGEPAGE
+  (void)madvise(reinterpret_cast<void *>(a), e - a, MADV_HUGEPAGE); // 2 MiB faults where THP allows
+#endif
+  const unsigned T = std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
+  const std::size_t per = ((e - a) / T + (2u << 20) - 1) & ~std::size_t((2u << 20) - 1);
+  std::vector<std::thread> th;
+  for (unsigned t = 0; t < T; ++t) {
+    const std::uintptr_t s0 = a + t * per, s1 = std::min<std::uintptr_t>(e, s0 + per);
+    if (s1 > s0)
+      th.emplace_back([=] { (void)madvise(reinterpret_cast<void *>(s0), s1 - s0, MADV_POPULATE_WRITE); });
+  }
+  for (auto &x : th)
+    x.join();
+#else
+  (void)p;
+  (void)bytes;
+#endif
+}
+template <typename Real> std::vector<Real> make_output_vector(std::size_t n) {
+  std::vector<Real> v;
+  if (n * sizeof(Real) >= (std::size_t(64) << 20)) {
+    v.reserve(n);
+    prefault(v.data(), n * sizeof(Real));
+  }
+  v.resize(n);
+  return v;
+}
+
 } // namespace b200_detail
 
 // mgr::decompose (refactor.hpp:462-474)
@@ -374,14 +422,18 @@ RefactoredData<Real> decompose(const TensorGrid<Real> &grid,
   b200_detail::check(mgrg_plan_levels(p, &L));
   std::vector<uint64_t> off(std::size_t(L) + 2);
   b200_detail::check(mgrg_plan_class_offsets(p, off.data()));
-  std::vector<Real> flat(grid.values.size());
-  b200_detail::check(mgrg_decompose_host(p, grid.values.data(), flat.data()));
   RefactoredData<Real> out;
   out.shape = grid.shape;
   out.coords = grid.coords;
   out.levels = std::size_t(L);
-  for (int l = 0; l <= L; ++l)
-    out.classes.emplace_back(flat.begin() + off[l], flat.begin() + off[l + 1]);
+  // the classes are written in place, one host buffer per class
+  std::vector<void *> dst(std::size_t(L) + 1);
+  out.classes.resize(std::size_t(L) + 1);
+  for (int l = 0; l <= L; ++l) {
+    out.classes[l] = b200_detail::make_output_vector<Real>(off[l + 1] - off[l]);
+    dst[l] = out.classes[l].data();
+  }
+  b200_detail::check(mgrg_decompose_host_classes(p, grid.values.data(), dst.data()));
   if (opt.stats)
     b200_detail::fill_stats(*opt.stats, p, grid.shape.size(), false);
   return out;
@@ -406,20 +458,20 @@ TensorGrid<Real> recompose(const RefactoredData<Real> &r, std::size_t classes_us
                        " levels; grid supports " + std::to_string(L));
   std::vector<uint64_t> off(std::size_t(L) + 2);
   b200_detail::check(mgrg_plan_class_offsets(p, off.data()));
-  std::vector<Real> flat(off[classes_used + 1]);
+  std::vector<const void *> src(classes_used + 1);
   for (std::size_t l = 0; l <= classes_used; ++l) {
     if (r.classes[l].size() != off[l + 1] - off[l])
       throw ShapeError("class " + std::to_string(l) + " has " +
                        std::to_string(r.classes[l].size()) + " entries, expected " +
                        std::to_string(off[l + 1] - off[l]));
-    std::copy(r.classes[l].begin(), r.classes[l].end(), flat.begin() + off[l]);
+    src[l] = r.classes[l].data();
   }
   TensorGrid<Real> g;
   g.shape = r.shape;
   g.coords = r.coords;
-  g.values.resize(num_elements(r.shape));
-  b200_detail::check(
-      mgrg_recompose_host(p, flat.data(), int32_t(classes_used), g.values.data()));
+  g.values = b200_detail::make_output_vector<Real>(num_elements(r.shape));
+  b200_detail::check(mgrg_recompose_host_classes(p, src.data(), int32_t(classes_used),
+                                                 g.values.data()));
   if (opt.stats)
     b200_detail::fill_stats(*opt.stats, p, r.shape.size(), true);
   return g;

@@ -117,11 +117,22 @@ mgrg_status mgrg_recompose(mgrg_plan *plan, const void *d_classes,
 
 /* ---- host-buffer entry points (what the reference's callers pass) -------
  * Same semantics; host -> device copy, the device path, device -> host copy,
- * synchronous.  Pinned host memory gives full PCIe bandwidth. */
+ * synchronous.  Pinned host memory (cudaHostAlloc / cudaHostRegister) is
+ * DMA'd directly; pageable memory streams through plan-owned pinned rings
+ * with multi-threaded host copies overlapping the DMA and the kernels. */
 mgrg_status mgrg_decompose_host(mgrg_plan *plan, const void *h_values,
                                 void *h_classes);
 mgrg_status mgrg_recompose_host(mgrg_plan *plan, const void *h_classes,
                                 int32_t classes_used, void *h_values);
+/* The same with the classes in separate host buffers, one per class, as
+ * RefactoredData::classes holds them (refactor.hpp:18-30): h_classes[l]
+ * points to class l's nodes (offsets[l+1] - offsets[l] elements of
+ * mgrg_plan_class_offsets), l = 0..L for decompose, 0..classes_used for
+ * recompose (others are not read).  No flat concatenation is made. */
+mgrg_status mgrg_decompose_host_classes(mgrg_plan *plan, const void *h_values,
+                                        void *const *h_classes);
+mgrg_status mgrg_recompose_host_classes(mgrg_plan *plan, const void *const *h_classes,
+                                        int32_t classes_used, void *h_values);
 
 /* ---- unit-level kernels (kernels.hpp), device buffers, for parity ---------
  * compute_coefficients / restore_coefficients (kernels.hpp:284-310): in place

@@ -17,7 +17,9 @@
 #include <cmath>
 #include <cstdio>
 #include <cstring>
+#include <map>
 #include <memory>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -34,6 +36,7 @@
 #include "thomas_fiber.cuh"
 #include "thomas_exact.cuh"
 #include "gen4.cuh"
+#include "hostio.cuh"
 
 using namespace mgrg;
 
@@ -221,6 +224,7 @@ struct mgrg_plan {
   cudaStream_t own_stream = nullptr;
   cudaStream_t s_in = nullptr, s_out = nullptr; // host-API copy streams (pipelined path)
   cudaEvent_t ev_in[16] = {}, ev_dec[16] = {}, ev_done = nullptr;
+  std::unique_ptr<mgrg::HostXfer> xfer; // pinned rings for pageable host buffers
   uint64_t last_launches = 0;
   // per-launch profiling (mgrg_plan_set_profiling)
   bool profiling = false;
@@ -455,6 +459,22 @@ template <typename R> mgrg_status upload_geometry(mgrg_plan *p) {
               Q[8 * (i - 1) + 4] = R(pr);
             }
             Tps[w] = R(pr);
+          }
+          // cluster-segment multipliers (thomas_cluster_kernel): products of
+          // the per-position factors over each 16-chunk segment
+          if (tf_cl(mm) > 1) {
+            const int cl = tf_cl(mm);
+            const uint32_t seg = 16u * uint32_t(ch);
+            R *Tmf = Tps + nch, *Tmb = Tmf + cl;
+            for (int r = 0; r < cl; ++r) {
+              double pf = 1.0, pb = 1.0;
+              for (uint32_t i = uint32_t(r) * seg; i < uint32_t(r + 1) * seg; ++i) {
+                pf *= double(Q[8 * i]);
+                pb *= double(Q[8 * i + 2]);
+              }
+              Tmf[r] = R(pf);
+              Tmb[r] = R(pb);
+            }
           }
           refs[l].tl[kd] = push(tl);
         }
@@ -856,7 +876,7 @@ bool try_scan(int kd, const ThomasGeom<R> &t, uint64_t S, uint64_t inner, uint64
   }
 }
 
-template <typename R> constexpr size_t tf_limit() { return 200 * 1024; }
+template <typename R> constexpr size_t tf_limit() { return 224 * 1024; }
 
 // small coarse lattices: one CTA solves every dimension (thomas_small_kernel)
 template <typename R> bool ts_fits(const LevelGeom<R> &g) {
@@ -871,48 +891,116 @@ void launch_thomas_small(const LevelGeom<R> &g, const std::array<ThomasGeom<R>, 
              t[2], g.m[0], g.m[1], g.m[2], g.refine, epi, base, out);
 }
 
-template <typename R, int DIM, int CH, int NF> auto tf_kernel() {
-  return thomas_fiber_kernel<R, DIM, CH, NF>;
+template <typename R, int DIM, int CH> auto tf_kernel() {
+  return thomas_fiber_kernel<R, DIM, CH, 32>;
 }
 template <typename R, int DIM>
-void (*tf_pick(int ch, int nf))(R *, ThomasLean<R>, uint64_t, uint32_t, uint32_t, Epi,
-                                const R *, R *) {
-  if (nf == 4) {
-    switch (ch) {
-    case 5: return tf_kernel<R, DIM, 5, 4>();
-    case 9: return tf_kernel<R, DIM, 9, 4>();
-    case 17: return tf_kernel<R, DIM, 17, 4>();
-    default: return tf_kernel<R, DIM, 33, 4>();
-    }
-  }
+void (*tf_pick(int ch))(R *, ThomasLean<R>, uint64_t, uint32_t, uint32_t, Epi, const R *, R *) {
   switch (ch) {
-  case 1: return tf_kernel<R, DIM, 1, 32>();
-  case 2: return tf_kernel<R, DIM, 2, 32>();
-  case 3: return tf_kernel<R, DIM, 3, 32>();
-  case 5: return tf_kernel<R, DIM, 5, 32>();
-  case 9: return tf_kernel<R, DIM, 9, 32>();
-  case 17: return tf_kernel<R, DIM, 17, 32>();
-  default: return tf_kernel<R, DIM, 33, 32>();
+  case 1: return tf_kernel<R, DIM, 1>();
+  case 2: return tf_kernel<R, DIM, 2>();
+  case 3: return tf_kernel<R, DIM, 3>();
+  case 5: return tf_kernel<R, DIM, 5>();
+  case 9: return tf_kernel<R, DIM, 9>();
+  case 17: return tf_kernel<R, DIM, 17>();
+  default: return tf_kernel<R, DIM, 33>();
   }
+}
+// long fibers: cluster of cl CTAs, chunk length 17 or 33
+template <typename R, int DIM, int CH>
+void (*tc_pick_cl(int cl))(R *, ThomasLean<R>, uint64_t, uint32_t, uint32_t, Epi, const R *,
+                           R *) {
+  switch (cl) {
+  case 2: return thomas_cluster_kernel<R, DIM, CH, 2>;
+  case 4: return thomas_cluster_kernel<R, DIM, CH, 4>;
+  default: return thomas_cluster_kernel<R, DIM, CH, 8>;
+  }
+}
+template <typename R, int DIM>
+void (*tc_pick(int ch, int cl))(R *, ThomasLean<R>, uint64_t, uint32_t, uint32_t, Epi,
+                                const R *, R *) {
+  return ch <= 17 ? tc_pick_cl<R, DIM, 17>(cl) : tc_pick_cl<R, DIM, 33>(cl);
+}
+template <typename R> size_t tc_smem_of(int kd, int ch) {
+  if (ch <= 17)
+    return kd == 0 ? tc_smem<R, 0, 17>() : (kd == 1 ? tc_smem<R, 1, 17>() : tc_smem<R, 2, 17>());
+  return kd == 0 ? tc_smem<R, 0, 33>() : (kd == 1 ? tc_smem<R, 1, 33>() : tc_smem<R, 2, 33>());
+}
+// smem of the chunked-Thomas launch for a fiber length (either kernel)
+template <typename R> size_t tf_launch_smem(int kd, uint32_t m) {
+  return tf_cl(m) > 1 ? tc_smem_of<R>(kd, tf_ch(m)) : tf_smem<R>(kd, m);
 }
 template <typename R>
 void launch_tf(int kd, const ThomasLean<R> &tl, uint64_t nfib, uint32_t mx, uint32_t my,
                Epi epi, const R *base, R *out, R *f, cudaStream_t s) {
-  const int nf = tf_nf(tl.m), ch = std::max(tf_ch(tl.m), nf == 4 ? 5 : 1);
-  const unsigned blocks = unsigned((nfib + nf - 1) / nf);
-  auto k = kd == 0 ? tf_pick<R, 0>(ch, nf) : (kd == 1 ? tf_pick<R, 1>(ch, nf)
-                                                      : tf_pick<R, 2>(ch, nf));
-  launch_pdl(k, blocks, kTfThreads, tf_smem<R>(kd, tl.m), s, f, tl, nfib, mx, my, epi, base, out);
+  const int ch = tf_ch(tl.m), cl = tf_cl(tl.m);
+  const unsigned groups = unsigned((nfib + 31) / 32);
+  if (cl > 1) {
+    auto k = kd == 0 ? tc_pick<R, 0>(ch, cl)
+                     : (kd == 1 ? tc_pick<R, 1>(ch, cl) : tc_pick<R, 2>(ch, cl));
+    cudaLaunchConfig_t cfg = {};
+    // persistent: as many clusters as are co-resident (queried once per
+    // instantiation), each walking the 32-fiber groups
+    static std::mutex mu;
+    static std::map<const void *, int> resident;
+    int nres = 0;
+    {
+      std::lock_guard<std::mutex> lk(mu);
+      auto it = resident.find(reinterpret_cast<const void *>(k));
+      if (it == resident.end()) {
+        cudaLaunchConfig_t q = {};
+        q.gridDim = dim3(unsigned(cl));
+        q.blockDim = dim3(kTfThreads);
+        q.dynamicSmemBytes = tc_smem_of<R>(kd, ch);
+        cudaLaunchAttribute qa[1];
+        qa[0].id = cudaLaunchAttributeClusterDimension;
+        qa[0].val.clusterDim.x = unsigned(cl);
+        qa[0].val.clusterDim.y = 1;
+        qa[0].val.clusterDim.z = 1;
+        q.attrs = qa;
+        q.numAttrs = 1;
+        if (cudaOccupancyMaxActiveClusters(&nres, k, &q) != cudaSuccess || nres < 1) {
+          cudaGetLastError();
+          nres = 1;
+        }
+        resident[reinterpret_cast<const void *>(k)] = nres;
+      } else {
+        nres = it->second;
+      }
+    }
+    cfg.gridDim = dim3(std::min<unsigned>(groups, unsigned(nres)) * unsigned(cl));
+    cfg.blockDim = dim3(kTfThreads);
+    cfg.dynamicSmemBytes = tc_smem_of<R>(kd, ch);
+    cfg.stream = s;
+    cudaLaunchAttribute at[2];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = g_pdl ? 1 : 0;
+    at[1].id = cudaLaunchAttributeClusterDimension;
+    at[1].val.clusterDim.x = unsigned(cl);
+    at[1].val.clusterDim.y = 1;
+    at[1].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 2;
+    cudaLaunchKernelEx(&cfg, k, f, tl, nfib, mx, my, epi, base, out);
+    return;
+  }
+  auto k = kd == 0 ? tf_pick<R, 0>(ch) : (kd == 1 ? tf_pick<R, 1>(ch) : tf_pick<R, 2>(ch));
+  launch_pdl(k, groups, kTfThreads, tf_smem<R>(kd, tl.m), s, f, tl, nfib, mx, my, epi, base, out);
 }
 template <typename R> void set_tf_attrs() {
   const int lim = int(tf_limit<R>());
-  for (int nf : {32, 4})
-    for (int ch : {1, 2, 3, 5, 9, 17, 33}) {
-      cudaFuncSetAttribute(tf_pick<R, 0>(ch, nf), cudaFuncAttributeMaxDynamicSharedMemorySize,
+  for (int ch : {1, 2, 3, 5, 9, 17, 33}) {
+    cudaFuncSetAttribute(tf_pick<R, 0>(ch), cudaFuncAttributeMaxDynamicSharedMemorySize, lim);
+    cudaFuncSetAttribute(tf_pick<R, 1>(ch), cudaFuncAttributeMaxDynamicSharedMemorySize, lim);
+    cudaFuncSetAttribute(tf_pick<R, 2>(ch), cudaFuncAttributeMaxDynamicSharedMemorySize, lim);
+  }
+  for (int ch : {17, 33})
+    for (int cl : {2, 4, 8}) {
+      cudaFuncSetAttribute(tc_pick<R, 0>(ch, cl), cudaFuncAttributeMaxDynamicSharedMemorySize,
                            lim);
-      cudaFuncSetAttribute(tf_pick<R, 1>(ch, nf), cudaFuncAttributeMaxDynamicSharedMemorySize,
+      cudaFuncSetAttribute(tc_pick<R, 1>(ch, cl), cudaFuncAttributeMaxDynamicSharedMemorySize,
                            lim);
-      cudaFuncSetAttribute(tf_pick<R, 2>(ch, nf), cudaFuncAttributeMaxDynamicSharedMemorySize,
+      cudaFuncSetAttribute(tc_pick<R, 2>(ch, cl), cudaFuncAttributeMaxDynamicSharedMemorySize,
                            lim);
     }
 }
@@ -922,7 +1010,7 @@ void launch_thomas(bool fast, const LevelGeom<R> &g, const ThomasGeom<R> &t,
                    const ThomasLean<R> &tl, int kd, R *f, Epi epi, const R *base, R *out,
                    cudaStream_t s) {
   const uint64_t mx = g.m[0], my = g.m[1], mz = g.m[2];
-  if (fast && tl.tab && tf_ch(tl.m) && tf_smem<R>(kd, tl.m) <= tf_limit<R>() &&
+  if (fast && tl.tab && tf_ch(tl.m) && tf_launch_smem<R>(kd, tl.m) <= tf_limit<R>() &&
       g_thomas_fiber) {
     const uint64_t nfib = kd == 0 ? my * mz : (kd == 1 ? mx * mz : mx * my);
     launch_tf<R>(kd, tl, nfib, uint32_t(mx), uint32_t(my), epi, base, out, f, s);
@@ -1475,6 +1563,7 @@ mgrg_status mgrg_plan_destroy(mgrg_plan *p) {
     return MGRG_OK;
   {
     DeviceGuard guard(p->device);
+    p->xfer.reset(); // joins the download worker before its stream goes
     for (cudaEvent_t e : p->event_pool)
       cudaEventDestroy(e);
     cudaFree(p->d_geom);
@@ -1749,23 +1838,30 @@ static mgrg_status ensure_stage(mgrg_plan *p) {
     CUDA_TRY(cudaEventCreateWithFlags(&p->ev_dec[i], cudaEventDisableTiming));
   }
   CUDA_TRY(cudaEventCreateWithFlags(&p->ev_done, cudaEventDisableTiming));
+  p->xfer.reset(new HostXfer(p->device));
+  p->xfer->init(p->s_out, n * p->esize);
   return MGRG_OK;
 }
 
 extern "C++" {
-// Pipelined host-buffer decompose (FAST, dyadic 3-D finest level): the input
+// Pipelined host-buffer decompose (either policy, dyadic 3-D finest level): the input
 // goes up in z slabs on one copy stream, the finest-level kernel runs per
 // slab group as soon as its planes (plus one halo plane) are resident, and
 // each group's finished class-L pieces (z-major within every class type) go
 // down on the other copy stream while later slabs are still uploading --
 // PCIe carries both directions at once.  The finest level's Thomas solves
 // and the coarser levels follow; classes 0..L-1 (1/8 of the data) last.
+// Host buffers are HostViews (hostio.cuh): pinned ones are DMA'd directly,
+// pageable ones through the plan's pinned rings; uploads are issued one slab
+// ahead of the kernel that needs them, so with pageable memory the host
+// copies of later slabs overlap the kernels and downloads of earlier ones.
 template <typename R>
-mgrg_status decompose_host_pipelined(mgrg_plan *p, const R *h_in, R *h_cls) {
+mgrg_status decompose_host_pipelined(mgrg_plan *p, const HostView &hin, const HostView &hcls) {
   PlanT<R> &P = pt<R>(p);
+  HostXfer &X = *p->xfer;
   const int L = p->H.L;
   const LevelGeom<R> &g = P.geom[L];
-  const uint64_t N = p->nodes[L], nxy = uint64_t(g.n[0]) * g.n[1];
+  const uint64_t nxy = uint64_t(g.n[0]) * g.n[1];
   R *din = static_cast<R *>(p->d_stage), *dcls = din + stage_half(p);
   R *clsL = dcls + p->nodes[L - 1];
   R *Pout = L == 1 ? dcls : level_buf<R>(p, L - 1);
@@ -1779,27 +1875,33 @@ mgrg_status decompose_host_pipelined(mgrg_plan *p, const R *h_in, R *h_cls) {
   auto chunk0 = [&](int q) { return uint32_t((uint64_t(q) * t.ntz) / G); };
   auto fplane = [&](uint32_t c) { return std::min<uint32_t>(2 * c * t.zc, n2); };
   cudaStream_t sc = p->own_stream;
-  // uploads
-  for (int q = 0; q < G; ++q) {
-    const uint32_t z0 = fplane(chunk0(q)), z1 = q == G - 1 ? n2 : fplane(chunk0(q + 1));
-    CUDA_TRY(cudaMemcpyAsync(din + z0 * nxy, h_in + z0 * nxy, (z1 - z0) * nxy * sizeof(R),
-                             cudaMemcpyHostToDevice, p->s_in));
-    CUDA_TRY(cudaEventRecord(p->ev_in[q], p->s_in));
-  }
+  int uploaded = 0;
+  auto upload_through = [&](int q) -> mgrg_status {
+    for (; uploaded <= q; ++uploaded) {
+      const int u = uploaded;
+      const uint32_t z0 = fplane(chunk0(u)), z1 = u == G - 1 ? n2 : fplane(chunk0(u + 1));
+      CUDA_TRY(X.upload(din + z0 * nxy, hin, z0 * nxy, (z1 - z0) * nxy, p->s_in));
+      CUDA_TRY(cudaEventRecord(p->ev_in[u], p->s_in));
+    }
+    return MGRG_OK;
+  };
   for (int q = 0; q < G; ++q) {
     const uint32_t c0 = chunk0(q), c1 = chunk0(q + 1);
     // the group reads fine planes up to 2*c1*zc: the next slab's first plane
-    CUDA_TRY(cudaStreamWaitEvent(sc, p->ev_in[std::min(q + 1, G - 1)], 0));
+    const int need = std::min(q + 1, G - 1);
+    if (mgrg_status st = upload_through(need))
+      return st;
+    CUDA_TRY(cudaStreamWaitEvent(sc, p->ev_in[need], 0));
     LeanTiles tg = t;
     tg.tz0 = c0;
     tg.ntz = c1 - c0;
     const unsigned blocks = unsigned((tg.warps() + kLeanWPB - 1) / kLeanWPB);
-    lean_dec_kernel<R, true, true><<<blocks, 32 * kLeanWPB, lean_dec_smem<R>(), sc>>>(
+    auto k = p->fast ? lean_dec_kernel<R, true, true> : lean_dec_kernel<R, true, false>;
+    k<<<blocks, 32 * kLeanWPB, lean_dec_smem<R>(), sc>>>(
         g, P.lean[L][0], P.lean[L][1], P.lean[L][2], P.sten[L][0], P.sten[L][1], P.sten[L][2],
         din, clsL, Pout, F, tg);
     CUDA_TRY(cudaGetLastError());
     CUDA_TRY(cudaEventRecord(p->ev_dec[q], sc));
-    CUDA_TRY(cudaStreamWaitEvent(p->s_out, p->ev_dec[q], 0));
     // class-L pieces of coarse z planes [c0*zc, c1*zc): even-z types (1..3)
     // have m2 z ranks, odd-z types (4..7) m2 - 1
     const uint32_t zr0 = c0 * t.zc;
@@ -1812,18 +1914,15 @@ mgrg_status decompose_host_pipelined(mgrg_plan *p, const R *h_in, R *h_cls) {
         continue;
       const uint64_t S = uint64_t(g.tex[ty]) * g.tey[ty];
       const uint64_t off = p->nodes[L - 1] + g.tbase[ty] + S * a;
-      CUDA_TRY(cudaMemcpyAsync(h_cls + off, dcls + off, S * (b - a) * sizeof(R),
-                               cudaMemcpyDeviceToHost, p->s_out));
+      CUDA_TRY(X.download(hcls, off, S * (b - a), dcls + off, p->ev_dec[q]));
     }
   }
   // finest level's solves + coarser levels, then classes 0..L-1
   if (mgrg_status st = run_decompose<R>(p, din, dcls, sc, /*top_done=*/true))
     return st;
   CUDA_TRY(cudaEventRecord(p->ev_done, sc));
-  CUDA_TRY(cudaStreamWaitEvent(p->s_out, p->ev_done, 0));
-  CUDA_TRY(cudaMemcpyAsync(h_cls, dcls, p->nodes[L - 1] * sizeof(R), cudaMemcpyDeviceToHost,
-                           p->s_out));
-  CUDA_TRY(cudaStreamSynchronize(p->s_out));
+  CUDA_TRY(X.download(hcls, 0, p->nodes[L - 1], dcls, p->ev_done));
+  CUDA_TRY(X.drain());
   CUDA_TRY(cudaStreamSynchronize(sc));
   return MGRG_OK;
 }
@@ -1835,47 +1934,54 @@ mgrg_status decompose_host_pipelined(mgrg_plan *p, const R *h_in, R *h_cls) {
 // written per group and each group's output planes go down while later
 // groups are still being interpolated.
 template <typename R>
-mgrg_status recompose_host_pipelined(mgrg_plan *p, const R *h_cls, R *h_out) {
+mgrg_status recompose_host_pipelined(mgrg_plan *p, const HostView &hcls, const HostView &hout) {
   PlanT<R> &P = pt<R>(p);
+  HostXfer &X = *p->xfer;
   const int L = p->H.L;
   const LevelGeom<R> &g = P.geom[L];
-  const uint64_t N = p->nodes[L], nxy = uint64_t(g.n[0]) * g.n[1];
+  const uint64_t nxy = uint64_t(g.n[0]) * g.n[1];
   R *dcls = static_cast<R *>(p->d_stage), *dout = dcls + stage_half(p);
   R *F = ws<R>(p, p->offF);
   const R *prev = L == 1 ? dcls : level_buf<R>(p, L - 1);
   const R *clsL = dcls + p->nodes[L - 1];
   const uint32_t m2 = g.m[2], n2 = g.n[2];
   cudaStream_t sc = p->own_stream;
-  // uploads: classes 0..L-1, then class L by rload chunk groups
-  CUDA_TRY(cudaMemcpyAsync(dcls, h_cls, p->nodes[L - 1] * sizeof(R), cudaMemcpyHostToDevice,
-                           p->s_in));
+  // classes 0..L-1 first; the coarse levels run as soon as they are resident
+  CUDA_TRY(X.upload(dcls, hcls, 0, p->nodes[L - 1], p->s_in));
   CUDA_TRY(cudaEventRecord(p->ev_done, p->s_in));
-  const LeanTiles tr = lean_rtiles<R>(g.m[0], g.m[1], m2, true);
-  const int G = int(std::min<uint32_t>(tr.ntz, 16));
-  auto rchunk0 = [&](int q) { return uint32_t((uint64_t(q) * tr.ntz) / G); };
-  for (int q = 0; q < G; ++q) {
-    const uint32_t zr0 = rchunk0(q) * tr.zc, zr1 = q == G - 1 ? m2 : rchunk0(q + 1) * tr.zc;
-    for (unsigned ty = 1; ty < 8; ++ty) {
-      const uint32_t nz = (ty & 4) ? m2 - 1 : m2;
-      const uint32_t a = std::min(zr0, nz), b = q == G - 1 ? nz : std::min(zr1, nz);
-      if (b <= a)
-        continue;
-      const uint64_t S = uint64_t(g.tex[ty]) * g.tey[ty];
-      const uint64_t off = p->nodes[L - 1] + g.tbase[ty] + S * a;
-      CUDA_TRY(cudaMemcpyAsync(dcls + off, h_cls + off, S * (b - a) * sizeof(R),
-                               cudaMemcpyHostToDevice, p->s_in));
-    }
-    CUDA_TRY(cudaEventRecord(p->ev_in[q], p->s_in));
-  }
-  // coarse levels as soon as classes 0..L-1 are resident
   CUDA_TRY(cudaStreamWaitEvent(sc, p->ev_done, 0));
   if (L > 1)
     if (mgrg_status st = run_recompose<R>(p, dcls, L, dout, sc, L - 1))
       return st;
-  // finest load vector per group: chunk range [c0, c1) reads class ranks
-  // c0-1 .. c1 (the next group's first rank)
+  // class L by rload chunk groups, each uploaded one group ahead of the
+  // finest load-vector kernel that reads it: chunk range [c0, c1) reads class
+  // ranks c0-1 .. c1 (the next group's first rank)
+  const LeanTiles tr = lean_rtiles<R>(g.m[0], g.m[1], m2, true);
+  const int G = int(std::min<uint32_t>(tr.ntz, 16));
+  auto rchunk0 = [&](int q) { return uint32_t((uint64_t(q) * tr.ntz) / G); };
+  int uploaded = 0;
+  auto upload_through = [&](int q) -> mgrg_status {
+    for (; uploaded <= q; ++uploaded) {
+      const int u = uploaded;
+      const uint32_t zr0 = rchunk0(u) * tr.zc, zr1 = u == G - 1 ? m2 : rchunk0(u + 1) * tr.zc;
+      for (unsigned ty = 1; ty < 8; ++ty) {
+        const uint32_t nz = (ty & 4) ? m2 - 1 : m2;
+        const uint32_t a = std::min(zr0, nz), b = u == G - 1 ? nz : std::min(zr1, nz);
+        if (b <= a)
+          continue;
+        const uint64_t S = uint64_t(g.tex[ty]) * g.tey[ty];
+        const uint64_t off = p->nodes[L - 1] + g.tbase[ty] + S * a;
+        CUDA_TRY(X.upload(dcls + off, hcls, off, S * (b - a), p->s_in));
+      }
+      CUDA_TRY(cudaEventRecord(p->ev_in[u], p->s_in));
+    }
+    return MGRG_OK;
+  };
   for (int q = 0; q < G; ++q) {
-    CUDA_TRY(cudaStreamWaitEvent(sc, p->ev_in[std::min(q + 1, G - 1)], 0));
+    const int need = std::min(q + 1, G - 1);
+    if (mgrg_status st = upload_through(need))
+      return st;
+    CUDA_TRY(cudaStreamWaitEvent(sc, p->ev_in[need], 0));
     LeanTiles t = tr;
     t.tz0 = rchunk0(q);
     t.ntz = rchunk0(q + 1) - rchunk0(q);
@@ -1909,28 +2015,84 @@ mgrg_status recompose_host_pipelined(mgrg_plan *p, const R *h_cls, R *h_out) {
                                         dout, t);
     CUDA_TRY(cudaGetLastError());
     CUDA_TRY(cudaEventRecord(p->ev_dec[q], sc));
-    CUDA_TRY(cudaStreamWaitEvent(p->s_out, p->ev_dec[q], 0));
     const uint32_t z0 = std::min<uint32_t>(2 * t.tz0 * tg.zc, n2);
     const uint32_t z1 = q == H - 1 ? n2 : std::min<uint32_t>(2 * gchunk0(q + 1) * tg.zc, n2);
     if (z1 > z0)
-      CUDA_TRY(cudaMemcpyAsync(h_out + z0 * nxy, dout + z0 * nxy, (z1 - z0) * nxy * sizeof(R),
-                               cudaMemcpyDeviceToHost, p->s_out));
+      CUDA_TRY(X.download(hout, z0 * nxy, (z1 - z0) * nxy, dout + z0 * nxy, p->ev_dec[q]));
   }
-  CUDA_TRY(cudaStreamSynchronize(p->s_out));
+  CUDA_TRY(X.drain());
   CUDA_TRY(cudaStreamSynchronize(sc));
   return MGRG_OK;
 }
 
-template <typename R> bool pipelined_ok(mgrg_plan *p, bool need_fast = true) {
+template <typename R> bool pipelined_ok(mgrg_plan *p) {
   if (p->gen)
     return false;
   const int L = p->H.L;
   const LevelGeom<R> &g = pt<R>(p).geom[L];
-  return (p->fast || !need_fast) && p->lean && p->refine == 7u && lean_level(g) && g.n[2] > 1 &&
+  return p->lean && p->refine == 7u && lean_level(g) && g.n[2] > 1 &&
          p->nodes[L] >= (uint64_t(1) << 22) && g_pipelined_host;
+}
+
+// class offsets of the plan's class buffer (class l: [off[l], off[l+1]))
+static std::vector<uint64_t> class_offsets(const mgrg_plan *p) {
+  std::vector<uint64_t> off(size_t(p->H.L) + 2, 0);
+  for (int l = 0; l <= p->H.L; ++l)
+    off[size_t(l) + 1] = p->nodes[l];
+  return off;
+}
+
+static mgrg_status host_decompose(mgrg_plan *p, const HostView &hin, const HostView &hcls) {
+  DeviceGuard guard(p->device);
+  if (mgrg_status st = ensure_stage(p))
+    return st;
+  if (p->deferred)
+    return fail(p->deferred, p->deferred_msg);
+  if (p->dtype == MGRG_F32 ? pipelined_ok<float>(p) : pipelined_ok<double>(p))
+    return p->dtype == MGRG_F32 ? decompose_host_pipelined<float>(p, hin, hcls)
+                                : decompose_host_pipelined<double>(p, hin, hcls);
+  HostXfer &X = *p->xfer;
+  const uint64_t n = p->nodes[p->H.L];
+  char *din = static_cast<char *>(p->d_stage), *dout = din + stage_half(p) * p->esize;
+  CUDA_TRY(X.upload(din, hin, 0, n, p->own_stream));
+  if (mgrg_status st = mgrg_decompose(p, din, dout, p->own_stream))
+    return st;
+  CUDA_TRY(cudaEventRecord(p->ev_done, p->own_stream));
+  CUDA_TRY(X.download(hcls, 0, n, dout, p->ev_done));
+  CUDA_TRY(X.drain());
+  CUDA_TRY(cudaStreamSynchronize(p->own_stream));
+  return MGRG_OK;
+}
+
+static mgrg_status host_recompose(mgrg_plan *p, const HostView &hcls, int32_t k,
+                                  const HostView &hout) {
+  DeviceGuard guard(p->device);
+  if (mgrg_status st = ensure_stage(p))
+    return st;
+  if (k == p->H.L && (p->dtype == MGRG_F32 ? pipelined_ok<float>(p) : pipelined_ok<double>(p)))
+    return p->dtype == MGRG_F32 ? recompose_host_pipelined<float>(p, hcls, hout)
+                                : recompose_host_pipelined<double>(p, hcls, hout);
+  HostXfer &X = *p->xfer;
+  char *din = static_cast<char *>(p->d_stage), *dout = din + stage_half(p) * p->esize;
+  // only classes 0..k are read (refactor.hpp:483-485): copy that prefix
+  CUDA_TRY(X.upload(din, hcls, 0, p->nodes[k], p->own_stream));
+  if (mgrg_status st = mgrg_recompose(p, din, k, dout, p->own_stream))
+    return st;
+  CUDA_TRY(cudaEventRecord(p->ev_done, p->own_stream));
+  CUDA_TRY(X.download(hout, 0, p->nodes[p->H.L], dout, p->ev_done));
+  CUDA_TRY(X.drain());
+  CUDA_TRY(cudaStreamSynchronize(p->own_stream));
+  return MGRG_OK;
 }
 } // extern "C++"
 
+static mgrg_status check_level_arg(const mgrg_plan *p, int32_t k) {
+  if (k < 0 || k > p->H.L)
+    return fail(MGRG_INVALID_LEVEL, "requested " + std::to_string(k) +
+                                        " classes; container has " +
+                                        std::to_string(p->H.L));
+  return MGRG_OK;
+}
 
 mgrg_status mgrg_decompose_host(mgrg_plan *p, const void *h_values, void *h_classes) {
   g_last_error.clear();
@@ -1939,24 +2101,23 @@ mgrg_status mgrg_decompose_host(mgrg_plan *p, const void *h_values, void *h_clas
   if (!h_values || !h_classes)
     return fail(MGRG_INVALID_ARGUMENT, "null host buffer");
   DeviceGuard guard(p->device);
-  if (mgrg_status st = ensure_stage(p))
+  return host_decompose(p, HostView::of(h_values, p->esize), HostView::of(h_classes, p->esize));
+}
+
+mgrg_status mgrg_decompose_host_classes(mgrg_plan *p, const void *h_values,
+                                        void *const *h_classes) {
+  g_last_error.clear();
+  if (mgrg_status st = check_plan(p))
     return st;
-  if (p->deferred)
-    return fail(p->deferred, p->deferred_msg);
-  if (p->dtype == MGRG_F32 ? pipelined_ok<float>(p) : pipelined_ok<double>(p))
-    return p->dtype == MGRG_F32
-               ? decompose_host_pipelined<float>(p, static_cast<const float *>(h_values),
-                                                 static_cast<float *>(h_classes))
-               : decompose_host_pipelined<double>(p, static_cast<const double *>(h_values),
-                                                  static_cast<double *>(h_classes));
-  const uint64_t bytes = p->nodes[p->H.L] * p->esize;
-  char *din = static_cast<char *>(p->d_stage), *dout = din + stage_half(p) * p->esize;
-  CUDA_TRY(cudaMemcpyAsync(din, h_values, bytes, cudaMemcpyHostToDevice, p->own_stream));
-  if (mgrg_status st = mgrg_decompose(p, din, dout, p->own_stream))
-    return st;
-  CUDA_TRY(cudaMemcpyAsync(h_classes, dout, bytes, cudaMemcpyDeviceToHost, p->own_stream));
-  CUDA_TRY(cudaStreamSynchronize(p->own_stream));
-  return MGRG_OK;
+  if (!h_values || !h_classes)
+    return fail(MGRG_INVALID_ARGUMENT, "null host buffer");
+  const std::vector<uint64_t> off = class_offsets(p);
+  for (int l = 0; l <= p->H.L; ++l)
+    if (!h_classes[l] && off[size_t(l) + 1] > off[size_t(l)])
+      return fail(MGRG_INVALID_ARGUMENT, "null class buffer " + std::to_string(l));
+  DeviceGuard guard(p->device);
+  return host_decompose(p, HostView::of(h_values, p->esize),
+                        HostView::classes(h_classes, off.data(), p->H.L + 1, p->esize));
 }
 
 mgrg_status mgrg_recompose_host(mgrg_plan *p, const void *h_classes, int32_t k,
@@ -1966,30 +2127,29 @@ mgrg_status mgrg_recompose_host(mgrg_plan *p, const void *h_classes, int32_t k,
     return st;
   if (!h_values || !h_classes)
     return fail(MGRG_INVALID_ARGUMENT, "null host buffer");
-  if (k < 0 || k > p->H.L)
-    return fail(MGRG_INVALID_LEVEL, "requested " + std::to_string(k) +
-                                        " classes; container has " +
-                                        std::to_string(p->H.L));
+  if (mgrg_status st = check_level_arg(p, k))
+    return st;
   DeviceGuard guard(p->device);
-  if (mgrg_status st = ensure_stage(p))
+  return host_recompose(p, HostView::of(h_classes, p->esize), k,
+                        HostView::of(h_values, p->esize));
+}
+
+mgrg_status mgrg_recompose_host_classes(mgrg_plan *p, const void *const *h_classes, int32_t k,
+                                        void *h_values) {
+  g_last_error.clear();
+  if (mgrg_status st = check_plan(p))
     return st;
-  const uint64_t bytes = p->nodes[p->H.L] * p->esize;
-  char *din = static_cast<char *>(p->d_stage), *dout = din + stage_half(p) * p->esize;
-  if (k == p->H.L && p->lean && !p->gen &&
-      (p->dtype == MGRG_F32 ? pipelined_ok<float>(p, false) : pipelined_ok<double>(p, false)))
-    return p->dtype == MGRG_F32
-               ? recompose_host_pipelined<float>(p, static_cast<const float *>(h_classes),
-                                                 static_cast<float *>(h_values))
-               : recompose_host_pipelined<double>(p, static_cast<const double *>(h_classes),
-                                                  static_cast<double *>(h_values));
-  // only classes 0..k are read (refactor.hpp:483-485): copy that prefix
-  const uint64_t used = p->nodes[k] * p->esize;
-  CUDA_TRY(cudaMemcpyAsync(din, h_classes, used, cudaMemcpyHostToDevice, p->own_stream));
-  if (mgrg_status st = mgrg_recompose(p, din, k, dout, p->own_stream))
+  if (!h_values || !h_classes)
+    return fail(MGRG_INVALID_ARGUMENT, "null host buffer");
+  if (mgrg_status st = check_level_arg(p, k))
     return st;
-  CUDA_TRY(cudaMemcpyAsync(h_values, dout, bytes, cudaMemcpyDeviceToHost, p->own_stream));
-  CUDA_TRY(cudaStreamSynchronize(p->own_stream));
-  return MGRG_OK;
+  const std::vector<uint64_t> off = class_offsets(p);
+  for (int l = 0; l <= k; ++l)
+    if (!h_classes[l] && off[size_t(l) + 1] > off[size_t(l)])
+      return fail(MGRG_INVALID_ARGUMENT, "null class buffer " + std::to_string(l));
+  DeviceGuard guard(p->device);
+  return host_recompose(p, HostView::classes(h_classes, off.data(), k + 1, p->esize), k,
+                        HostView::of(h_values, p->esize));
 }
 
 // ---- unit-level kernels ------------------------------------------------

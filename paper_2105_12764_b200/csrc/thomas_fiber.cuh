@@ -34,22 +34,28 @@ namespace mgrg {
 
 constexpr int kTfThreads = 512; // threads per CTA = fibers x chunks
 
-// Fiber-group shape for a fiber length m: NF fibers x NCH = 512/NF chunks
-// per CTA with chunks of at most 33 positions.  Short fibers (m <= 528,
-// every 3-D level here) use 32 fibers per CTA (a warp = one chunk of 32
-// fibers: coalesced position rows); long 2-D fibers (m <= 4224) 4 fibers
-// x 128 chunks.  0 = not handled (the streaming kernels take over).
-__host__ __device__ inline int tf_nf(uint32_t m) {
-  return m <= 16u * 33u ? 32 : (m <= 128u * 33u ? 4 : 0);
+// Fiber-group shape for a fiber length m: 32 fibers per CTA (a warp = one
+// chunk of 32 fibers: coalesced position rows), 16 chunks of at most 33
+// positions per CTA.  Fibers longer than 16 x 33 = 528 positions (the long
+// 2-D levels, e.g. 8193^2) are spread over a thread-block cluster of
+// tf_cl(m) = 2, 4 or 8 CTAs, each holding a 16-chunk segment of the same 32
+// fibers, with the chunk carries exchanged through distributed shared memory
+// (thomas_cluster_kernel).  0 = not handled (the streaming kernels take over).
+__host__ __device__ inline int tf_cl(uint32_t m) {
+  if (m <= 16u * 33u)
+    return 1;
+  for (int cl = 2; cl <= 8; cl *= 2)
+    if (m <= uint32_t(16 * 33 * cl))
+      return cl;
+  return 0;
 }
-__host__ __device__ inline int tf_nch(uint32_t m) {
-  const int nf = tf_nf(m);
-  return nf ? kTfThreads / nf : 0;
-}
+__host__ __device__ inline int tf_nf(uint32_t m) { return tf_cl(m) ? 32 : 0; }
+__host__ __device__ inline int tf_nch(uint32_t m) { return 16 * tf_cl(m); }
 
 // Tables: q8[i] = {fwd_i, ip_i, g_i, PF_i, PB_i, 0, 0, 0}, then the chunk
 // multipliers pfend[w] (PF at the chunk end), pbstart[w] (PB at its start),
-// w < tf_nch(m).
+// w < tf_nch(m), then the cluster-segment multipliers mf[r] (product of the
+// segment's pfend), mb[r] (product of its pbstart), r < tf_cl(m).
 template <typename R> struct ThomasLean {
   const R *tab; // [8m] q8, [nch] pfend, [nch] pbstart
   uint32_t m;
@@ -72,10 +78,10 @@ __host__ __device__ inline uint32_t tf_padded(uint32_t m) {
   return uint32_t(tf_nch(m)) * uint32_t(tf_ch(m));
 }
 template <typename R> __host__ __device__ inline size_t tf_tab_elems(uint32_t m) {
-  return 8 * size_t(tf_padded(m) > m ? tf_padded(m) : m) + 2 * size_t(tf_nch(m));
+  return 8 * size_t(tf_padded(m) > m ? tf_padded(m) : m) + 2 * size_t(tf_nch(m)) +
+         2 * size_t(tf_cl(m));
 }
-// the coefficient table is staged in shared memory when it fits beside the
-// tile (every 3-D level); long 2-D fibers read it through L1
+// the coefficient table is staged in shared memory beside the tile
 template <typename R> __host__ __device__ inline bool tf_tab_smem(uint32_t m) {
   return tf_nf(m) == 32;
 }
@@ -303,6 +309,286 @@ __global__ void __launch_bounds__(kTfThreads, sizeof(R) == 4 ? 2 : 1)
       }
     }
   }
+}
+
+// ---- long fibers: thread-block clusters over 32-fiber groups -------------
+//
+// Fibers of m > 528 positions (tf_cl(m) = CL > 1) do not fit one CTA's
+// registers: CTA r of a CL-CTA cluster holds positions [r*SEG, (r+1)*SEG),
+// SEG = 16 * CH, of a group of 32 fibers -- 16 chunks in registers as in
+// thomas_fiber_kernel -- so every element is still read once and written
+// once.  The chunk carries of the sequential pass cross the segment
+// boundaries through distributed shared memory: after its zero-carry-in
+// pass every CTA publishes its segment's end value (forward: e_r, the value
+// at the segment end; backward: b_r, at the segment start), the cluster
+// barrier makes them visible, and CTA r composes the carry into its segment
+// from its neighbours' published values with the host-precomputed segment
+// multipliers mf / mb (c_{r+1} = mf_r * c_r + e_r; d_{r-1} = mb_r * d_r + b_r)
+// before its own 16-chunk pass.
+//
+// One CTA per SM holds a whole register file of fiber values, so the
+// kernel is persistent: the grid is the number of co-resident clusters,
+// each cluster walks the fiber groups, and the shared-memory tile of the
+// NEXT group is loaded (cp.async) as soon as the current group is in
+// registers -- the load overlaps this group's solve, carry exchange and
+// stores.  Results and epilogue bases go straight between registers and
+// HBM (y / z fibers: position rows of 32 consecutive x nodes, coalesced;
+// x fibers: each thread's chunk is a contiguous run, written sector by
+// sector).  The segment's coefficient slice is staged once per CTA.
+template <typename R, int DIM, int CH>
+__host__ __device__ inline size_t tc_tile_elems() {
+  constexpr size_t SEG = size_t(kTfThreads / 32) * CH;
+  return ((DIM == 0 ? 32 * (SEG + 1) : SEG * 32) + 3) & ~size_t(3);
+}
+// x fibers: per-warp output staging, 32 fibers x 8 positions (pitch 9)
+constexpr int kTcStg = 32 * 9;
+template <typename R, int DIM, int CH> __host__ __device__ inline size_t tc_smem() {
+  constexpr size_t SEG = size_t(kTfThreads / 32) * CH;
+  // tile, carries, q8 slice + pfend / pbstart slices, published e / b,
+  // x-fiber output staging
+  return (tc_tile_elems<R, DIM, CH>() + size_t(kTfThreads) + 8 * SEG + 2 * 16 + 2 * 32 +
+          (DIM == 0 ? size_t(kTfThreads / 32) * kTcStg : 0)) *
+         sizeof(R);
+}
+
+__device__ __forceinline__ void prefetch_l2(const void *p) {
+  asm volatile("prefetch.global.L2 [%0];\n" ::"l"(p));
+}
+__device__ __forceinline__ void cluster_arrive() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n" ::: "memory");
+}
+__device__ __forceinline__ void cluster_wait() {
+  asm volatile("barrier.cluster.wait.acquire.aligned;\n" ::: "memory");
+}
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;\n" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ uint32_t cluster_id_x() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%clusterid.x;\n" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ uint32_t cluster_count_x() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%nclusterid.x;\n" : "=r"(r));
+  return r;
+}
+// generic address of the same shared-memory variable in CTA `rank` of the
+// cluster (DSMEM)
+template <typename R> __device__ __forceinline__ const R *cluster_peer(const R *p, uint32_t rank) {
+  uint64_t out;
+  asm volatile("mapa.u64 %0, %1, %2;\n" : "=l"(out) : "l"(p), "r"(rank));
+  return reinterpret_cast<const R *>(out);
+}
+
+template <typename R, int DIM, int CH, int CL>
+__global__ void __launch_bounds__(kTfThreads, 1)
+    thomas_cluster_kernel(R *__restrict__ f, ThomasLean<R> t, uint64_t nfib, uint32_t m0,
+                          uint32_t m1, Epi epi, const R *base, R *out) {
+  pdl_wait();
+  constexpr int NF = 32, NW = kTfThreads / NF, NCH = NW * CL;
+  constexpr uint32_t SEG = uint32_t(NW) * CH, P0 = SEG + 1;
+  extern __shared__ __align__(16) unsigned char tc_raw[];
+  R *tile = reinterpret_cast<R *>(tc_raw);
+  R *carry = tile + tc_tile_elems<R, DIM, CH>();
+  R *sq = carry + kTfThreads;     // q8 of the segment's positions
+  R *spf = sq + 8 * SEG;          // pfend of the segment's chunks
+  R *spb = spf + NW;              // pbstart of the segment's chunks
+  R *pub_e = spb + NW;            // published forward end values [NF]
+  R *pub_b = pub_e + NF;          // published backward start values [NF]
+  R *ostg = pub_b + NF;           // x fibers: per-warp output staging
+  const uint32_t m = t.m;
+  const uint32_t mp = uint32_t(NCH) * CH;
+  const R *gq = t.tab, *gpf = gq + 8 * size_t(mp), *gpb = gpf + NCH, *gmf = gpb + NCH,
+          *gmb = gmf + CL;
+  const int tid = threadIdx.x, fi = tid % NF, w = tid / NF, lane = tid & 31;
+  const uint32_t r = cluster_rank();
+  const uint64_t ngroups = (nfib + NF - 1) / NF;
+  const uint64_t gstep = cluster_count_x();
+  const uint32_t pa0 = r * SEG;
+  const uint32_t plen = pa0 >= m ? 0u : (m - pa0 < SEG ? m - pa0 : SEG);
+  const uint32_t a = uint32_t(w) * CH; // local chunk start
+  const uint32_t len = a >= plen ? 0u : (plen - a < uint32_t(CH) ? plen - a : uint32_t(CH));
+  const uint64_t m01 = uint64_t(m0) * m1;
+  const uint64_t ps = DIM == 1 ? m0 : m01; // position stride (DIM 1, 2)
+  // position-0 address of fiber `fi` of group `gi` (DIM 1, 2; fibers past the
+  // end repeat the last)
+  auto fiber_addr = [&](uint64_t gi) -> uint64_t {
+    const uint64_t F0 = gi * NF;
+    const uint64_t F = F0 + min(uint64_t(fi), nfib - 1 - F0);
+    return DIM == 1 ? (F % m0) + m01 * (F / m0) : F;
+  };
+  auto stage = [&](uint64_t gi) {
+    const uint64_t F0 = gi * NF;
+    const int nf = int(nfib - F0 < uint64_t(NF) ? nfib - F0 : uint64_t(NF));
+    if (DIM == 0) {
+      for (int row = w; row < nf; row += NW) {
+        const R *src = f + (F0 + row) * m + pa0;
+        for (uint32_t j = lane; j < plen; j += 32)
+          cp_async(tile + size_t(row) * P0 + j, src + j);
+      }
+    } else {
+      const uint64_t fa = fiber_addr(gi);
+      for (uint32_t i = w; i < plen; i += NW)
+        cp_async(tile + size_t(i) * NF + fi, f + fa + ps * (pa0 + i));
+    }
+    cp_async_commit();
+  };
+
+  uint64_t gi = cluster_id_x();
+  tf_copy_in(sq, gq + 8 * size_t(pa0), 8 * SEG, tid); // 8*pa0*sizeof(R): 16-byte multiple
+  if (tid < NW) {
+    spf[tid] = gpf[r * NW + tid];
+    spb[tid] = gpb[r * NW + tid];
+  }
+  if (gi < ngroups)
+    stage(gi);
+  const R *qa = sq + 8 * size_t(a);
+  for (; gi < ngroups; gi += gstep) {
+    const uint64_t F0 = gi * NF;
+    const int nf = int(nfib - F0 < uint64_t(NF) ? nfib - F0 : uint64_t(NF));
+    cp_async_wait<0>();
+    __syncthreads();
+    R v[CH];
+    {
+      const uint32_t ln = (DIM == 0 && fi >= nf) ? 0u : len;
+#pragma unroll
+      for (int k = 0; k < CH; ++k)
+        v[k] = uint32_t(k) < ln ? (DIM == 0 ? tile[size_t(fi) * P0 + a + k]
+                                            : tile[size_t(a + k) * NF + fi])
+                                : R(0);
+    }
+    __syncthreads(); // the tile is free: the next group's rows go in now
+    if (gi + gstep < ngroups)
+      stage(gi + gstep);
+    // x fibers: the epilogue's base values pulled into L2 now, read after
+    // the solve (y / z fibers: measured slower -- 33 prefetches per thread)
+    if (DIM == 0 && epi != Epi::none && fi < nf) {
+      const R *bp = base + (F0 + fi) * m + pa0 + a;
+#pragma unroll
+      for (int k = 0; k < CH; k += 32 / int(sizeof(R)))
+        if (uint32_t(k) < len)
+          prefetch_l2(bp + k);
+    }
+
+    // ---- forward, zero carry-in; publish the segment's end value
+    R acc = R(0);
+#pragma unroll
+    for (int k = 0; k < CH; ++k) {
+      acc = fma(qa[8 * k], acc, v[k]);
+      v[k] = acc;
+    }
+    carry[w * NF + fi] = acc;
+    __syncthreads();
+    if (w == 0) {
+      R e = R(0);
+#pragma unroll
+      for (int k = 0; k < NW; ++k)
+        e = fma(spf[k], e, carry[k * NF + fi]);
+      pub_e[fi] = e;
+    }
+    cluster_arrive();
+    cluster_wait();
+    R c = R(0);
+#pragma unroll
+    for (int q = 0; q < CL - 1; ++q)
+      if (uint32_t(q) < r)
+        c = fma(gmf[q], c, cluster_peer(pub_e, uint32_t(q))[fi]);
+    for (int k = 0; k < w; ++k)
+      c = fma(spf[k], c, carry[k * NF + fi]);
+
+    // ---- forward fix-up + backward, zero carry-in; publish the segment start
+    R x = R(0);
+#pragma unroll
+    for (int k = CH - 1; k >= 0; --k) {
+      const R *q = qa + 8 * k;
+      const R vj = fma(q[3], c, v[k]);
+      x = fma(q[2], x, q[1] * vj);
+      v[k] = x;
+    }
+    __syncthreads(); // every thread has read the forward carries
+    carry[w * NF + fi] = x;
+    __syncthreads();
+    if (w == 0) {
+      R b = R(0);
+#pragma unroll
+      for (int k = NW - 1; k >= 0; --k)
+        b = fma(spb[k], b, carry[k * NF + fi]);
+      pub_b[fi] = b;
+    }
+    cluster_arrive();
+    cluster_wait();
+    R d = R(0);
+#pragma unroll
+    for (int q = CL - 1; q > 0; --q)
+      if (uint32_t(q) > r)
+        d = fma(gmb[q], d, cluster_peer(pub_b, uint32_t(q))[fi]);
+    for (int k = NW - 1; k > w; --k)
+      d = fma(spb[k], d, carry[k * NF + fi]);
+
+    // ---- backward fix-up, epilogue, store (registers -> HBM)
+#pragma unroll
+    for (int k = 0; k < CH; ++k)
+      v[k] = fma(qa[8 * k + 4], d, v[k]);
+    if (DIM == 0) {
+      // through the warp's staging, 8 positions at a time: a store
+      // instruction then covers 4 fibers x 8 consecutive positions (4
+      // 8-element runs) instead of 32 scattered elements
+      R *stg = ostg + w * kTcStg;
+      const int pos = lane & 7, fq = lane >> 3;
+#pragma unroll
+      for (int k0 = 0; k0 < CH; k0 += 8) {
+#pragma unroll
+        for (int j = 0; j < 8; ++j)
+          if (k0 + j < CH)
+            stg[fi * 9 + j] = v[k0 + j];
+        __syncwarp();
+        if (uint32_t(k0 + pos) < len) {
+#pragma unroll
+          for (int it = 0; it < 8; ++it) {
+            const int fb = it * 4 + fq;
+            if (fb < nf) {
+              const uint64_t g = (F0 + fb) * m + pa0 + a + k0 + pos;
+              const R z = stg[fb * 9 + pos];
+              if (epi == Epi::none)
+                f[g] = z;
+              else
+                out[g] = epi == Epi::add ? base[g] + z : base[g] - z;
+            }
+          }
+        }
+        __syncwarp();
+      }
+    } else if (fi < nf) {
+      const uint64_t p0 = fiber_addr(gi) + ps * (pa0 + a), st = ps;
+      R *o = (epi == Epi::none ? f : out) + p0;
+      if (epi == Epi::none) {
+#pragma unroll
+        for (int k = 0; k < CH; ++k)
+          if (uint32_t(k) < len)
+            o[k * st] = v[k];
+      } else {
+        const R *bp = base + p0;
+        constexpr int B = 8; // base loads in flight per batch
+#pragma unroll
+        for (int k0 = 0; k0 < CH; k0 += B) {
+          R bv[B];
+#pragma unroll
+          for (int k = 0; k < B; ++k)
+            if (k0 + k < CH && uint32_t(k0 + k) < len)
+              bv[k] = __ldcs(bp + (k0 + k) * st);
+#pragma unroll
+          for (int k = 0; k < B; ++k)
+            if (k0 + k < CH && uint32_t(k0 + k) < len)
+              o[(k0 + k) * st] = epi == Epi::add ? bv[k] + v[k0 + k] : bv[k] - v[k0 + k];
+        }
+      }
+    }
+  }
+  cluster_arrive();
+  cluster_wait(); // no CTA leaves while a peer may still read its carries
 }
 
 } // namespace mgrg

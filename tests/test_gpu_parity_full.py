@@ -186,12 +186,20 @@ def test_config5_block_1025sq_513_f64_full(oracle_mod):
 # ---- cheap shapes that reach the headline configs' kernel instantiations ----
 # (17, 9, 1025): 513-long z fibers -> the z solve fused with apply / unapply
 #   (thomas_fiber_kernel<R, 2, 33, 32>), as at 1025^3 level 10;
-# (8193, 9) / (9, 8193): 4097-long x / y fibers (thomas_fiber_kernel<double,
-#   {0,1}, 33, 4>), as at 8193^2 level 13;
+# (8193, 9) / (9, 8193): 4097-long x / y fibers (thomas_cluster_kernel<R,
+#   {0,1}, 33, 8>: 8-CTA clusters), as at 8193^2 level 13;
+# (4097, 65) / (65, 4097): 2049-long fibers, 4-CTA clusters, 33 fibers (a
+#   full and a 1-fiber cluster group);
+# (1073, 9) / (9, 1073) / (9, 5, 1073): 537-long fibers, 2-CTA clusters
+#   with 17-position chunks (x / y / z);
+# (5, 3, 4097): 2049-long z fibers (cluster, DIM 2);
 # (1025, 9, 17) / (9, 1025, 17): 513-long x / y fibers.
 TARGETED = [((17, 9, 1025), "float32"), ((17, 9, 1025), "float64"),
             ((8193, 9), "float64"), ((9, 8193), "float64"),
             ((8193, 9), "float32"), ((9, 8193), "float32"),
+            ((4097, 65), "float64"), ((65, 4097), "float32"),
+            ((1073, 9), "float32"), ((9, 1073), "float64"), ((9, 5, 1073), "float64"),
+            ((5, 3, 4097), "float32"),
             ((1025, 9, 17), "float32"), ((9, 1025, 17), "float32"),
             ((33, 17, 2049), "float32"), ((2049, 17, 9), "float64"),
             ((9, 2049, 17), "float64")]
