@@ -652,7 +652,9 @@ def run_ours(args, rank, world, local_rank):
                                "decompose_ms": r["decompose_ms"],
                                "recompose_ms": r["recompose_ms"], "steps": r["steps"],
                                "alloc_vector_ms": r.get("alloc_vector_ms"),
-                               "alloc_prefaulted_ms": r.get("alloc_prefaulted_ms")}
+                               "alloc_prefaulted_ms": r.get("alloc_prefaulted_ms"),
+                               "capi_reused_buffers_ms_per_step":
+                                   r.get("capi_reused_buffers_ms_per_step")}
             dropin["how"] = ("C++ drop-in include/mgr_b200/refactor.hpp: pageable std::vector "
                              "in, per-class std::vector out (mgr::decompose + mgr::recompose, "
                              "host wall clock incl. output allocation); tests/cpp/bench_dropin.cpp")
