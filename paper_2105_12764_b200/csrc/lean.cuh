@@ -35,7 +35,13 @@ namespace mgrg {
 #ifndef LEAN_DEC_MINB
 #define LEAN_DEC_MINB 3
 #endif
-template <typename R> __host__ __device__ constexpr int lean_ty() { return sizeof(R) == 4 ? LEAN_TY_F32 : 2; } // coarse y rows per warp band
+#ifndef LEAN_TY_F64
+#define LEAN_TY_F64 3 // measured (1025^2 x 513 f64, L9): TY 2 / MINB 3 2.59 ms, 2 / 2 2.33, 3 / 2 1.93, 4 / 2 2.41
+#endif
+#ifndef LEAN_DEC_MINB_F64
+#define LEAN_DEC_MINB_F64 2
+#endif
+template <typename R> __host__ __device__ constexpr int lean_ty() { return sizeof(R) == 4 ? LEAN_TY_F32 : LEAN_TY_F64; } // coarse y rows per warp band
 #ifndef LEAN_ZC_MAX
 #define LEAN_ZC_MAX 32
 #endif
@@ -184,6 +190,35 @@ template <typename R> __device__ __forceinline__ R flerp(R a, R b, R t) {
   return fma(t, b - a, a);
 }
 
+// Paired (even, odd) node updates.  FAST f32: Blackwell's packed FP32x2
+// instructions (FADD2 / FFMA2) do both lanes of the pair in one issue slot;
+// each component is the same round-to-nearest operation as the scalar
+// policy, so results are bit-identical to plerp / psub per component.
+template <typename R, bool FAST>
+__device__ __forceinline__ typename Vec2<R>::T plerp2(typename Vec2<R>::T a,
+                                                      typename Vec2<R>::T b, R t) {
+  if constexpr (FAST && sizeof(R) == 4) {
+    return __ffma2_rn(make_float2(t, t), __fadd2_rn(b, make_float2(-a.x, -a.y)), a);
+  } else {
+    typename Vec2<R>::T r;
+    r.x = plerp<R, FAST>(a.x, b.x, t);
+    r.y = plerp<R, FAST>(a.y, b.y, t);
+    return r;
+  }
+}
+template <typename R, bool FAST>
+__device__ __forceinline__ typename Vec2<R>::T psub2(typename Vec2<R>::T a,
+                                                     typename Vec2<R>::T b) {
+  if constexpr (FAST && sizeof(R) == 4) {
+    return __fadd2_rn(a, make_float2(-b.x, -b.y));
+  } else {
+    typename Vec2<R>::T r;
+    r.x = psub<R, FAST>(a.x, b.x);
+    r.y = psub<R, FAST>(a.y, b.y);
+    return r;
+  }
+}
+
 template <typename R, bool ALIGNED>
 __device__ __forceinline__ Pair<R> lean_pair(const typename Vec2<R>::T &v) {
   if constexpr (ALIGNED)
@@ -273,9 +308,8 @@ __device__ __forceinline__ void lean_plane(
     const R *__restrict__ slot, int q, const int *rowoff, R txr, const R *tyr,
     const W5r<R> &wx, const W5r<R> *wy, const Stencil<R> &sx,
     const Stencil<R> *__restrict__ sy, int cy0, int m1, bool ve, bool vo, uint32_t stmask_e,
-    uint32_t stmask_o, const PlaneOut<R> &po, R *__restrict__ cls, int ex_e, int ex_o, R *We,
-    R *Wo,
-    const R *WLe, const R *WLo, R tz, R *Y) {
+    uint32_t stmask_o, const PlaneOut<R> &po, R *__restrict__ cls, int ex_e, int ex_o,
+    typename Vec2<R>::T *W, const typename Vec2<R>::T *WL, R tz, R *Y) {
   constexpr int NR = 2 * TY + 3;
   constexpr int RP = LeanStage<R>::RP;
   using V = typename Vec2<R>::T;
@@ -294,41 +328,44 @@ __device__ __forceinline__ void lean_plane(
     else
       raw[r] = *reinterpret_cast<const V *>(p - 1);
   }
-  Pair<R> u[NR];
+  // u[r] = (even node, odd node) of the lane's pair on band row r
+  V u[NR];
 #pragma unroll
-  for (int r = 0; r < NR; ++r)
-    u[r] = (((r & 1) == 0) == EVEN) ? lean_pair<R, true>(raw[r]) : lean_pair<R, false>(raw[r]);
+  for (int r = 0; r < NR; ++r) {
+    if (((r & 1) == 0) == EVEN) {
+      u[r] = raw[r];
+    } else {
+      u[r].x = raw[r].y;
+      u[r].y = __shfl_down_sync(0xffffffffu, raw[r].x, 1);
+    }
+  }
   R X[NR];
   if constexpr (EVEN) {
 #pragma unroll
     for (int r = 0; r < NR; r += 2) {
-      const R un = __shfl_down_sync(0xffffffffu, u[r].e, 1);
-      We[r] = u[r].e;
-      Wo[r] = plerp<R, FAST>(u[r].e, un, txr);
+      const R un = __shfl_down_sync(0xffffffffu, u[r].x, 1);
+      W[r].x = u[r].x;
+      W[r].y = plerp<R, FAST>(u[r].x, un, txr);
     }
 #pragma unroll
-    for (int r = 1; r < NR; r += 2) {
-      We[r] = plerp<R, FAST>(We[r - 1], We[r + 1], tyr[r >> 1]);
-      Wo[r] = plerp<R, FAST>(Wo[r - 1], Wo[r + 1], tyr[r >> 1]);
-    }
+    for (int r = 1; r < NR; r += 2)
+      W[r] = plerp2<R, FAST>(W[r - 1], W[r + 1], tyr[r >> 1]);
   }
 #pragma unroll
   for (int r = 0; r < NR; ++r) {
-    R we, wo;
-    if constexpr (EVEN) {
-      we = We[r];
-      wo = Wo[r];
-    } else {
-      we = plerp<R, FAST>(WLe[r], We[r], tz);
-      wo = plerp<R, FAST>(WLo[r], Wo[r], tz);
-    }
+    V w;
+    if constexpr (EVEN)
+      w = W[r];
+    else
+      w = plerp2<R, FAST>(WL[r], W[r], tz);
+    const V c = psub2<R, FAST>(u[r], w);
     const bool kept = EVEN && !(r & 1); // even node coarse in every dim
-    const R ce = (kept || !ve) ? R(0) : psub<R, FAST>(u[r].e, we);
-    const R co = vo ? psub<R, FAST>(u[r].o, wo) : R(0);
+    const R ce = (kept || !ve) ? R(0) : c.x;
+    const R co = vo ? c.y : R(0);
     const int rr = r >> 1;
     if ((stmask_e >> r) & 1u)
       ((r & 1) ? cls : po.pe0)[((r & 1) ? po.ie1 : po.ie0) + uint32_t(ex_e * rr)] =
-          kept ? u[r].e : ce;
+          kept ? u[r].x : ce;
     if ((stmask_o >> r) & 1u)
       cls[((r & 1) ? po.io1 : po.io0) + uint32_t(ex_o * rr)] = co;
     X[r] = kept ? lean_xpass_odd<R, FAST>(wx, sx, co) : lean_xpass<R, FAST>(wx, sx, ce, co);
@@ -345,7 +382,7 @@ template <typename R> __host__ __device__ constexpr size_t lean_dec_smem() {
 }
 
 template <typename R, bool Z3, bool FAST>
-__global__ void __launch_bounds__(32 * kLeanWPB, LEAN_DEC_MINB)
+__global__ void __launch_bounds__(32 * kLeanWPB, sizeof(R) == 4 ? LEAN_DEC_MINB : LEAN_DEC_MINB_F64)
     lean_dec_kernel(LevelGeom<R> g, const LeanW<R> *__restrict__ lx,
                     const LeanW<R> *__restrict__ ly, const LeanW<R> *__restrict__ lz,
                     const Stencil<R> *__restrict__ sxt, const Stencil<R> *__restrict__ syt,
@@ -443,10 +480,11 @@ __global__ void __launch_bounds__(32 * kLeanWPB, LEAN_DEC_MINB)
   };
   auto q_of = [&](int p) -> int { return int((int64_t(p) * nxy) & (V - 1)); };
 
-  R WLe[NR], WLo[NR];
+  using V2 = typename Vec2<R>::T;
+  V2 WL[NR]; // the previous even plane's interpolant (even, odd node)
 #pragma unroll
   for (int r = 0; r < NR; ++r)
-    WLe[r] = WLo[r] = R(0);
+    WL[r].x = WL[r].y = R(0);
   R accM[TY], acc0[TY]; // FAST: partial f of outputs k-1 and k at step k
   R YEm2[TY], YOm1[TY], YEm1[TY]; // exact: carried q-1 term; y results of planes 2k-3, 2k-2
 #pragma unroll
@@ -460,7 +498,7 @@ __global__ void __launch_bounds__(32 * kLeanWPB, LEAN_DEC_MINB)
   int j = 0, js = 0; // plane counter and its ring slot (j % 3)
   for (int k = kbeg; k <= kend; ++k) {
     R YE[TY], YO[TY];
-    R We[NR], Wo[NR];
+    V2 W[NR];
     // ================= even plane 2k =================
     {
       const int pe = 2 * k;
@@ -478,12 +516,12 @@ __global__ void __launch_bounds__(32 * kLeanWPB, LEAN_DEC_MINB)
         po.io1 = uint32_t(g.tbase[3] + qc + int64_t(m0 - 1) * (yb + int64_t(m1 - 1) * k));
         lean_plane<R, TY, true, FAST>(ring + js * SLOT, q_of(pe), rowoff, txr, tyr, wx, wy, sx,
                                       syt, cy0, m1, ve,
-                                vo, own ? st_e : 0u, own ? st_o : 0u, po, cls, m0, m0 - 1, We, Wo,
-                                nullptr, nullptr, R(0), YE);
+                                vo, own ? st_e : 0u, own ? st_o : 0u, po, cls, m0, m0 - 1, W,
+                                nullptr, R(0), YE);
       } else {
 #pragma unroll
         for (int r = 0; r < NR; ++r)
-          We[r] = Wo[r] = R(0);
+          W[r].x = W[r].y = R(0);
 #pragma unroll
         for (int i = 0; i < TY; ++i)
           YE[i] = R(0);
@@ -518,8 +556,8 @@ __global__ void __launch_bounds__(32 * kLeanWPB, LEAN_DEC_MINB)
         po.io1 = uint32_t(g.tbase[7] + qc + int64_t(m0 - 1) * (yb + int64_t(m1 - 1) * zr));
         lean_plane<R, TY, false, FAST>(ring + js * SLOT, q_of(pz), rowoff, txr, tyr, wx, wy, sx,
                                        syt, cy0, m1, ve,
-                                 vo, own ? st_e : 0u, own ? st_o : 0u, po, cls, m0, m0 - 1, We,
-                                 Wo, WLe, WLo, __ldg(&lzk->t), YO);
+                                 vo, own ? st_e : 0u, own ? st_o : 0u, po, cls, m0, m0 - 1, W,
+                                 WL, __ldg(&lzk->t), YO);
       } else {
 #pragma unroll
         for (int i = 0; i < TY; ++i)
@@ -534,10 +572,8 @@ __global__ void __launch_bounds__(32 * kLeanWPB, LEAN_DEC_MINB)
         YO[i] = R(0);
     }
 #pragma unroll
-    for (int r = 0; r < NR; ++r) {
-      WLe[r] = We[r];
-      WLo[r] = Wo[r];
-    }
+    for (int r = 0; r < NR; ++r)
+      WL[r] = W[r];
     // ================= z pass =================
     const bool emit = outl && k - 1 >= cz0 && k - 1 < cz1;
     if constexpr (FAST) { // rolling accumulators
@@ -579,12 +615,18 @@ __global__ void __launch_bounds__(32 * kLeanWPB, LEAN_DEC_MINB)
 // class buffer of level l (coarse-in-every-dim nodes are zero).  Same warp
 // tiling and band walk as lean_dec_kernel; the class rows are coalesced
 // 4/8-byte loads (lane qc of a type row is element qc).
+#ifndef LEAN_RL_TY_F64
+#define LEAN_RL_TY_F64 4
+#endif
+#ifndef LEAN_RL_MINB_F64
+#define LEAN_RL_MINB_F64 2 // measured (1025^2 x 513 f64, L9): MINB 3 (168 regs, spills) 1.13 ms, 2 (246) 1.07
+#endif
 template <typename R> __host__ __device__ constexpr int lean_ty_rl() {
-  return sizeof(R) == 4 ? LEAN_RL_TY : 4; // taller band: fewer halo rows (no W registers here)
+  return sizeof(R) == 4 ? LEAN_RL_TY : LEAN_RL_TY_F64; // taller band: fewer halo rows (no W registers here)
 }
 
 template <typename R, bool Z3, bool FAST>
-__global__ void __launch_bounds__(32 * kLeanWPB, LEAN_RL_MINB)
+__global__ void __launch_bounds__(32 * kLeanWPB, sizeof(R) == 4 ? LEAN_RL_MINB : LEAN_RL_MINB_F64)
     lean_rload_kernel(LevelGeom<R> g, const LeanW<R> *__restrict__ lx,
                       const LeanW<R> *__restrict__ ly, const LeanW<R> *__restrict__ lz,
                       const Stencil<R> *__restrict__ sxt, const Stencil<R> *__restrict__ syt,
@@ -765,8 +807,14 @@ __global__ void __launch_bounds__(32 * kLeanWPB, LEAN_RL_MINB)
 #ifndef LEAN_RG_PF
 #define LEAN_RG_PF 1 // the loads of step k+1 are issued before step k computes
 #endif
+#ifndef LEAN_RG_TG_F64
+#define LEAN_RG_TG_F64 2
+#endif
+#ifndef LEAN_RG_MINB_F64
+#define LEAN_RG_MINB_F64 LEAN_RG_MINB
+#endif
 template <typename R> __host__ __device__ constexpr int lean_tg() {
-  return sizeof(R) == 4 ? LEAN_RG_TG : 2;
+  return sizeof(R) == 4 ? LEAN_RG_TG : LEAN_RG_TG_F64;
 }
 constexpr int kLeanGOut = 31;
 
@@ -790,7 +838,7 @@ __device__ __forceinline__ void lean_store_pair(R *p, R e, R o, bool we, bool wo
 }
 
 template <typename R, bool Z3, bool CLS, bool FAST>
-__global__ void __launch_bounds__(32 * kLeanWPB, LEAN_RG_MINB)
+__global__ void __launch_bounds__(32 * kLeanWPB, sizeof(R) == 4 ? LEAN_RG_MINB : LEAN_RG_MINB_F64)
     lean_rgpk_kernel(LevelGeom<R> g, const LeanW<R> *__restrict__ lx,
                      const LeanW<R> *__restrict__ ly, const LeanW<R> *__restrict__ lz,
                      const R *__restrict__ coarse, const R *__restrict__ cls,

@@ -731,6 +731,11 @@ template <typename R, int CY, bool FAST> void set_pair_attrs_t() {
 template <typename R, int CY> void set_pair_attrs() {
   set_pair_attrs_t<R, CY, false>();
   set_pair_attrs_t<R, CY, true>();
+  // the lean decompose ring (f64 bands above 2 coarse rows exceed 48 KB)
+  for (auto k : {lean_dec_kernel<R, true, true>, lean_dec_kernel<R, true, false>,
+                 lean_dec_kernel<R, false, true>, lean_dec_kernel<R, false, false>})
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         int(lean_dec_smem<R>()));
   cudaFuncSetAttribute(dec4_kernel<R, cy4<R>(), false>,
                        cudaFuncAttributeMaxDynamicSharedMemorySize, int(dec4_smem<R, cy4<R>()>()));
   cudaFuncSetAttribute(dec4_kernel<R, cy4<R>(), true>,

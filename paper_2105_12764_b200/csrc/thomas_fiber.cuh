@@ -87,11 +87,11 @@ template <typename R> __host__ __device__ inline bool tf_tab_smem(uint32_t m) {
 }
 // shared memory: [tile NF x m][carries NCH x NF][tables], 16-byte aligned parts
 template <typename R> __host__ __device__ inline size_t tf_tile_elems(int dim, uint32_t m) {
-  // NF fibers per position; z fibers in 32-fiber groups are staged with
+  // NF fibers per position; y / z fibers in 32-fiber groups are staged with
   // 16-byte chunks of a superset (pitch (32 + 2V - 2) / V * V, V = 16/sizeof(R))
   const int nf = tf_nf(m), v = 16 / int(sizeof(R));
   const size_t pitch =
-      (nf == 32 && dim == 2) ? size_t((32 + 2 * v - 2) / v * v) : size_t(nf);
+      (nf == 32 && dim != 0) ? size_t((32 + 2 * v - 2) / v * v) : size_t(nf);
   return (pitch * m + 3) & ~size_t(3);
 }
 template <typename R> __host__ __device__ inline size_t tf_smem(int dim, uint32_t m) {
@@ -158,12 +158,12 @@ __global__ void __launch_bounds__(kTfThreads, sizeof(R) == 4 ? 2 : 1)
   const bool contiguous = DIM == 2 || (F0 % m0) + uint64_t(nf) <= m0;
   const uint64_t ntot = nfib * m;
 
-  // DIM 1, 2: position-major tile [i][fiber]; with 32 contiguous fibers of
-  // DIM 2 each position row is fetched as its 16-byte aligned superset (NCK
+  // DIM 1, 2: position-major tile [i][fiber]; with 32 contiguous fibers
+  // each position row is fetched as its 16-byte aligned superset (NCK
   // chunks, one LDGSTS.128 each: ~4x fewer copy operations than element
   // copies) and read back at the row's shift.  The same staging brings the
   // epilogue's base rows in while the solve runs.
-  constexpr bool SUPR = NF == 32 && DIM == 2;
+  constexpr bool SUPR = NF == 32 && DIM != 0;
   auto stage_rows = [&](const R *src) {
     if (SUPR && contiguous) {
       constexpr int RPR = 32 / NCK; // rows per warp copy instruction

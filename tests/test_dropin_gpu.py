@@ -168,3 +168,72 @@ def test_graph_replay_identical(shape, dt, fast):
     assert plan.last_launches > 0
     plan.set_graphs(False)
     plan.close()
+
+
+# ---- host-buffer entry points: pageable vs pinned, flat vs per-class ---------
+# (csrc/hostio.cuh).  (129, 129, 257) has 4.3M nodes: the pipelined host paths
+# (dyadic 3-D, >= 2^22 nodes) in both policies; (33, 17, 9) the plain path.
+@pytest.mark.parametrize("shape", [(129, 129, 257), (33, 17, 9)], ids=["pipelined", "plain"])
+@pytest.mark.parametrize("fast", [False, True], ids=["exact", "fast"])
+@pytest.mark.parametrize("dtype", ["float32", "float64"])
+def test_host_entry_points_pageable_pinned_per_class(shape, fast, dtype):
+    import ctypes
+
+    import torch
+
+    from paper_2105_12764_b200 import Plan, _lib
+
+    rng = np.random.default_rng(zlib.crc32(repr((shape, fast, dtype)).encode()))
+    v = rng.random(int(np.prod(shape))).astype(dtype)
+    plan = Plan(shape, dtype, fast=fast, device=0)
+    L = plan.levels
+    ref = plan.decompose(torch.from_numpy(v).cuda()).cpu().numpy()
+    ref_r = {k: plan.recompose(torch.from_numpy(ref).cuda(), k).cpu().numpy()
+             for k in (L - 1, L)}
+    lib = _lib.lib()
+    # pageable flat buffers
+    out = np.full_like(v, np.nan)
+    _lib.check(lib.mgrg_decompose_host(plan._h, v.ctypes.data, out.ctypes.data))
+    assert np.array_equal(out, ref)
+    # pinned flat buffers (torch pinned host tensors)
+    pin_in = torch.from_numpy(v).pin_memory()
+    pin_out = torch.empty_like(pin_in).pin_memory()
+    _lib.check(lib.mgrg_decompose_host(plan._h, pin_in.data_ptr(), pin_out.data_ptr()))
+    assert np.array_equal(pin_out.numpy(), ref)
+    # per-class pageable buffers, written in place
+    sl = plan.class_slices()
+    cls = [np.full(s.stop - s.start, np.nan, dtype=dtype) for s in sl]
+    ptrs = (ctypes.c_void_p * len(cls))(*[c.ctypes.data for c in cls])
+    _lib.check(lib.mgrg_decompose_host_classes(plan._h, v.ctypes.data, ptrs))
+    for s, c in zip(sl, cls):
+        assert np.array_equal(c, ref[s])
+    # recompose from per-class pageable buffers (k = L: pipelined; k = L-1: prefix)
+    for k in (L - 1, L):
+        back = np.full_like(v, np.nan)
+        _lib.check(lib.mgrg_recompose_host_classes(plan._h, ptrs, k, back.ctypes.data))
+        assert np.array_equal(back, ref_r[k]), f"recompose_host_classes k={k}"
+        back2 = np.full_like(v, np.nan)
+        _lib.check(lib.mgrg_recompose_host(plan._h, ref.ctypes.data, k, back2.ctypes.data))
+        assert np.array_equal(back2, ref_r[k]), f"recompose_host k={k}"
+    # classes above k are never read: null pointers there are accepted
+    ptrs_k = (ctypes.c_void_p * len(cls))(*([c.ctypes.data for c in cls[:L]] + [None]))
+    back = np.full_like(v, np.nan)
+    _lib.check(lib.mgrg_recompose_host_classes(plan._h, ptrs_k, L - 1, back.ctypes.data))
+    assert np.array_equal(back, ref_r[L - 1])
+    plan.close()
+
+
+def test_host_classes_entry_points_reject_null_class():
+    import ctypes
+
+    from paper_2105_12764_b200 import Plan, _lib, errors
+
+    shape = (17, 9, 9)
+    plan = Plan(shape, "float64", device=0)
+    v = np.random.default_rng(3).random(int(np.prod(shape)))
+    sl = plan.class_slices()
+    cls = [np.empty(s.stop - s.start) for s in sl]
+    ptrs = (ctypes.c_void_p * len(cls))(*([c.ctypes.data for c in cls[:-1]] + [None]))
+    with pytest.raises(errors.Error):
+        _lib.check(_lib.lib().mgrg_decompose_host_classes(plan._h, v.ctypes.data, ptrs))
+    plan.close()
