@@ -435,8 +435,8 @@ template <typename R> mgrg_status upload_geometry(mgrg_plan *p) {
           // per position (8-padded), PFend, PBstart [tf_nch]; products in
           // fp64 from the working-precision factors, rounded once
           const uint32_t mm = uint32_t(tf.size());
-          std::vector<R> tl(tf_tab_elems<R>(mm), R(0));
-          const int nch = std::max(tf_nch(mm), 1), ch = std::max(tf_ch(mm), 1);
+          std::vector<R> tl(tf_tab_elems<R>(mm, kd), R(0));
+          const int nch = std::max(tf_nch<R>(mm, kd), 1), ch = std::max(tf_ch<R>(mm, kd), 1);
           const uint32_t mp = std::max<uint32_t>(uint32_t(nch) * uint32_t(ch), mm);
           R *Q = tl.data(), *Tpe = Q + 8 * size_t(mp), *Tps = Tpe + nch;
           for (uint32_t i = 0; i < mp; ++i) { // padding: fwd = g = 0, ip = 1
@@ -445,7 +445,7 @@ template <typename R> mgrg_status upload_geometry(mgrg_plan *p) {
             Q[8 * i + 1] = real ? ti[i] : R(1);
             Q[8 * i + 2] = (i + 1 < mm) ? R(-double(ti[i]) * double(th[i])) : R(0);
           }
-          for (int w = 0; w < tf_nch(mm); ++w) {
+          for (int w = 0; w < tf_nch<R>(mm, kd); ++w) {
             const uint32_t a = uint32_t(w) * uint32_t(ch), b = a + uint32_t(ch);
             double pr = 1.0;
             for (uint32_t i = a; i < b; ++i) {
@@ -461,10 +461,10 @@ template <typename R> mgrg_status upload_geometry(mgrg_plan *p) {
             Tps[w] = R(pr);
           }
           // cluster-segment multipliers (thomas_cluster_kernel): products of
-          // the per-position factors over each 16-chunk segment
-          if (tf_cl(mm) > 1) {
-            const int cl = tf_cl(mm);
-            const uint32_t seg = 16u * uint32_t(ch);
+          // the per-position factors over each CTA's segment
+          if (tf_cl<R>(mm, kd) > 1) {
+            const int cl = tf_cl<R>(mm, kd);
+            const uint32_t seg = uint32_t(tf_nw<R>(mm, kd)) * uint32_t(ch);
             R *Tmf = Tps + nch, *Tmb = Tmf + cl;
             for (int r = 0; r < cl; ++r) {
               double pf = 1.0, pb = 1.0;
@@ -911,38 +911,47 @@ void (*tf_pick(int ch))(R *, ThomasLean<R>, uint64_t, uint32_t, uint32_t, Epi, c
   default: return tf_kernel<R, DIM, 33>();
   }
 }
-// long fibers: cluster of cl CTAs, chunk length 17 or 33
-template <typename R, int DIM, int CH>
+// the cluster kernel: cl CTAs of nw warps, chunk length 17 or 33
+template <typename R, int DIM, int CH, int NW>
 void (*tc_pick_cl(int cl))(R *, ThomasLean<R>, uint64_t, uint32_t, uint32_t, Epi, const R *,
                            R *) {
   switch (cl) {
-  case 2: return thomas_cluster_kernel<R, DIM, CH, 2>;
-  case 4: return thomas_cluster_kernel<R, DIM, CH, 4>;
-  default: return thomas_cluster_kernel<R, DIM, CH, 8>;
+  case 1: return thomas_cluster_kernel<R, DIM, CH, 1, NW>;
+  case 2: return thomas_cluster_kernel<R, DIM, CH, 2, NW>;
+  case 4: return thomas_cluster_kernel<R, DIM, CH, 4, NW>;
+  default: return thomas_cluster_kernel<R, DIM, CH, 8, NW>;
   }
 }
 template <typename R, int DIM>
-void (*tc_pick(int ch, int cl))(R *, ThomasLean<R>, uint64_t, uint32_t, uint32_t, Epi,
-                                const R *, R *) {
-  return ch <= 17 ? tc_pick_cl<R, DIM, 17>(cl) : tc_pick_cl<R, DIM, 33>(cl);
+void (*tc_pick(int ch, int cl, int nw))(R *, ThomasLean<R>, uint64_t, uint32_t, uint32_t, Epi,
+                                        const R *, R *) {
+  if constexpr (sizeof(R) == 8)
+    if (nw == 8)
+      return ch <= 17 ? tc_pick_cl<R, DIM, 17, 8>(cl) : tc_pick_cl<R, DIM, 33, 8>(cl);
+  return ch <= 17 ? tc_pick_cl<R, DIM, 17, 16>(cl) : tc_pick_cl<R, DIM, 33, 16>(cl);
 }
-template <typename R> size_t tc_smem_of(int kd, int ch) {
-  if (ch <= 17)
-    return kd == 0 ? tc_smem<R, 0, 17>() : (kd == 1 ? tc_smem<R, 1, 17>() : tc_smem<R, 2, 17>());
-  return kd == 0 ? tc_smem<R, 0, 33>() : (kd == 1 ? tc_smem<R, 1, 33>() : tc_smem<R, 2, 33>());
+template <typename R, int CH, int NW> size_t tc_smem_dim(int kd) {
+  return kd == 0 ? tc_smem<R, 0, CH, NW>() : (kd == 1 ? tc_smem<R, 1, CH, NW>()
+                                                       : tc_smem<R, 2, CH, NW>());
+}
+template <typename R> size_t tc_smem_of(int kd, int ch, int nw) {
+  if (nw == 8)
+    return ch <= 17 ? tc_smem_dim<R, 17, 8>(kd) : tc_smem_dim<R, 33, 8>(kd);
+  return ch <= 17 ? tc_smem_dim<R, 17, 16>(kd) : tc_smem_dim<R, 33, 16>(kd);
 }
 // smem of the chunked-Thomas launch for a fiber length (either kernel)
 template <typename R> size_t tf_launch_smem(int kd, uint32_t m) {
-  return tf_cl(m) > 1 ? tc_smem_of<R>(kd, tf_ch(m)) : tf_smem<R>(kd, m);
+  return tf_clustered<R>(m, kd) ? tc_smem_of<R>(kd, tf_ch<R>(m, kd), tf_nw<R>(m, kd))
+                            : tf_smem<R>(kd, m);
 }
 template <typename R>
 void launch_tf(int kd, const ThomasLean<R> &tl, uint64_t nfib, uint32_t mx, uint32_t my,
                Epi epi, const R *base, R *out, R *f, cudaStream_t s) {
-  const int ch = tf_ch(tl.m), cl = tf_cl(tl.m);
+  const int ch = tf_ch<R>(tl.m, kd), cl = tf_cl<R>(tl.m, kd), nw = tf_nw<R>(tl.m, kd);
   const unsigned groups = unsigned((nfib + 31) / 32);
-  if (cl > 1) {
-    auto k = kd == 0 ? tc_pick<R, 0>(ch, cl)
-                     : (kd == 1 ? tc_pick<R, 1>(ch, cl) : tc_pick<R, 2>(ch, cl));
+  if (tf_clustered<R>(tl.m, kd)) {
+    auto k = kd == 0 ? tc_pick<R, 0>(ch, cl, nw)
+                     : (kd == 1 ? tc_pick<R, 1>(ch, cl, nw) : tc_pick<R, 2>(ch, cl, nw));
     cudaLaunchConfig_t cfg = {};
     // persistent: as many clusters as are co-resident (queried once per
     // instantiation), each walking the 32-fiber groups
@@ -955,8 +964,8 @@ void launch_tf(int kd, const ThomasLean<R> &tl, uint64_t nfib, uint32_t mx, uint
       if (it == resident.end()) {
         cudaLaunchConfig_t q = {};
         q.gridDim = dim3(unsigned(cl));
-        q.blockDim = dim3(kTfThreads);
-        q.dynamicSmemBytes = tc_smem_of<R>(kd, ch);
+        q.blockDim = dim3(unsigned(32 * nw));
+        q.dynamicSmemBytes = tc_smem_of<R>(kd, ch, nw);
         cudaLaunchAttribute qa[1];
         qa[0].id = cudaLaunchAttributeClusterDimension;
         qa[0].val.clusterDim.x = unsigned(cl);
@@ -974,8 +983,8 @@ void launch_tf(int kd, const ThomasLean<R> &tl, uint64_t nfib, uint32_t mx, uint
       }
     }
     cfg.gridDim = dim3(std::min<unsigned>(groups, unsigned(nres)) * unsigned(cl));
-    cfg.blockDim = dim3(kTfThreads);
-    cfg.dynamicSmemBytes = tc_smem_of<R>(kd, ch);
+    cfg.blockDim = dim3(unsigned(32 * nw));
+    cfg.dynamicSmemBytes = tc_smem_of<R>(kd, ch, nw);
     cfg.stream = s;
     cudaLaunchAttribute at[2];
     at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
@@ -999,15 +1008,16 @@ template <typename R> void set_tf_attrs() {
     cudaFuncSetAttribute(tf_pick<R, 1>(ch), cudaFuncAttributeMaxDynamicSharedMemorySize, lim);
     cudaFuncSetAttribute(tf_pick<R, 2>(ch), cudaFuncAttributeMaxDynamicSharedMemorySize, lim);
   }
-  for (int ch : {17, 33})
-    for (int cl : {2, 4, 8}) {
-      cudaFuncSetAttribute(tc_pick<R, 0>(ch, cl), cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           lim);
-      cudaFuncSetAttribute(tc_pick<R, 1>(ch, cl), cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           lim);
-      cudaFuncSetAttribute(tc_pick<R, 2>(ch, cl), cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           lim);
-    }
+  for (int nw : {8, 16})
+    for (int ch : {17, 33})
+      for (int cl : {1, 2, 4, 8}) {
+        cudaFuncSetAttribute(tc_pick<R, 0>(ch, cl, nw),
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, lim);
+        cudaFuncSetAttribute(tc_pick<R, 1>(ch, cl, nw),
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, lim);
+        cudaFuncSetAttribute(tc_pick<R, 2>(ch, cl, nw),
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, lim);
+      }
 }
 
 template <typename R>
@@ -1015,7 +1025,7 @@ void launch_thomas(bool fast, const LevelGeom<R> &g, const ThomasGeom<R> &t,
                    const ThomasLean<R> &tl, int kd, R *f, Epi epi, const R *base, R *out,
                    cudaStream_t s) {
   const uint64_t mx = g.m[0], my = g.m[1], mz = g.m[2];
-  if (fast && tl.tab && tf_ch(tl.m) && tf_launch_smem<R>(kd, tl.m) <= tf_limit<R>() &&
+  if (fast && tl.tab && tf_ch<R>(tl.m, kd) && tf_launch_smem<R>(kd, tl.m) <= tf_limit<R>() &&
       g_thomas_fiber) {
     const uint64_t nfib = kd == 0 ? my * mz : (kd == 1 ? mx * mz : mx * my);
     launch_tf<R>(kd, tl, nfib, uint32_t(mx), uint32_t(my), epi, base, out, f, s);

@@ -35,22 +35,42 @@ namespace mgrg {
 constexpr int kTfThreads = 512; // threads per CTA = fibers x chunks
 
 // Fiber-group shape for a fiber length m: 32 fibers per CTA (a warp = one
-// chunk of 32 fibers: coalesced position rows), 16 chunks of at most 33
-// positions per CTA.  Fibers longer than 16 x 33 = 528 positions (the long
-// 2-D levels, e.g. 8193^2) are spread over a thread-block cluster of
-// tf_cl(m) = 2, 4 or 8 CTAs, each holding a 16-chunk segment of the same 32
-// fibers, with the chunk carries exchanged through distributed shared memory
-// (thomas_cluster_kernel).  0 = not handled (the streaming kernels take over).
-__host__ __device__ inline int tf_cl(uint32_t m) {
-  if (m <= 16u * 33u)
-    return 1;
-  for (int cl = 2; cl <= 8; cl *= 2)
-    if (m <= uint32_t(16 * 33 * cl))
+// chunk of 32 fibers: coalesced position rows), tf_nw(m) chunks of at most
+// 33 positions per CTA.  16-warp CTAs by default; f64 fibers of 73..2112
+// positions use 8-warp CTAs (33 doubles per thread fill 128 registers, so a
+// 16-warp CTA is alone on its SM and its load, solve and store phases never
+// overlap; two 8-warp CTAs per SM do).  Fibers longer than one CTA's
+// tf_nw x 33 positions (the long 2-D levels, e.g. 8193^2) are spread over a
+// thread-block cluster of tf_cl(m) = 2, 4 or 8 CTAs, each holding a segment
+// of the same 32 fibers, with the chunk carries exchanged through
+// distributed shared memory (thomas_cluster_kernel).  0 = not handled (the
+// streaming kernels take over).
+#ifndef TF_NW8_F64
+#define TF_NW8_F64 1
+#endif
+template <typename R> __host__ __device__ inline int tf_nw(uint32_t m, int dim) {
+  return (TF_NW8_F64 && sizeof(R) == 8 && dim != 0 && m > 8u * 9u && m <= 8u * 33u * 8u)
+             ? 8
+             : 16;
+}
+template <typename R> __host__ __device__ inline int tf_cl(uint32_t m, int dim) {
+  const uint32_t seg = uint32_t(tf_nw<R>(m, dim)) * 33u;
+  for (int cl = 1; cl <= 8; cl *= 2)
+    if (m <= seg * uint32_t(cl))
       return cl;
   return 0;
 }
-__host__ __device__ inline int tf_nf(uint32_t m) { return tf_cl(m) ? 32 : 0; }
-__host__ __device__ inline int tf_nch(uint32_t m) { return 16 * tf_cl(m); }
+template <typename R> __host__ __device__ inline int tf_nf(uint32_t m, int dim) {
+  return tf_cl<R>(m, dim) ? 32 : 0;
+}
+template <typename R> __host__ __device__ inline int tf_nch(uint32_t m, int dim) {
+  return tf_nw<R>(m, dim) * tf_cl<R>(m, dim);
+}
+// served by thomas_cluster_kernel (clusters or 8-warp CTAs), else by
+// thomas_fiber_kernel (one 16-warp CTA per fiber group)
+template <typename R> __host__ __device__ inline bool tf_clustered(uint32_t m, int dim) {
+  return tf_cl<R>(m, dim) > 1 || tf_nw<R>(m, dim) == 8;
+}
 
 // Tables: q8[i] = {fwd_i, ip_i, g_i, PF_i, PB_i, 0, 0, 0}, then the chunk
 // multipliers pfend[w] (PF at the chunk end), pbstart[w] (PB at its start),
@@ -61,8 +81,8 @@ template <typename R> struct ThomasLean {
   uint32_t m;
 };
 // chunk length of a fiber length (the kernel instantiation), 0 = not handled
-__host__ __device__ inline int tf_ch(uint32_t m) {
-  const int nch = tf_nch(m);
+template <typename R> __host__ __device__ inline int tf_ch(uint32_t m, int dim) {
+  const int nch = tf_nch<R>(m, dim);
   if (!nch)
     return 0;
   const uint32_t c = (m + nch - 1) / nch;
@@ -74,40 +94,40 @@ __host__ __device__ inline int tf_ch(uint32_t m) {
 }
 // positions covered by the chunks (every chunk exactly CH long; positions
 // m .. mp-1 are padding: fwd = g = 0, so they decouple and solve to 0)
-__host__ __device__ inline uint32_t tf_padded(uint32_t m) {
-  return uint32_t(tf_nch(m)) * uint32_t(tf_ch(m));
+template <typename R> __host__ __device__ inline uint32_t tf_padded(uint32_t m, int dim) {
+  return uint32_t(tf_nch<R>(m, dim)) * uint32_t(tf_ch<R>(m, dim));
 }
-template <typename R> __host__ __device__ inline size_t tf_tab_elems(uint32_t m) {
-  return 8 * size_t(tf_padded(m) > m ? tf_padded(m) : m) + 2 * size_t(tf_nch(m)) +
-         2 * size_t(tf_cl(m));
+template <typename R> __host__ __device__ inline size_t tf_tab_elems(uint32_t m, int dim) {
+  return 8 * size_t(tf_padded<R>(m, dim) > m ? tf_padded<R>(m, dim) : m) + 2 * size_t(tf_nch<R>(m, dim)) +
+         2 * size_t(tf_cl<R>(m, dim));
 }
 // the coefficient table is staged in shared memory beside the tile
-template <typename R> __host__ __device__ inline bool tf_tab_smem(uint32_t m) {
-  return tf_nf(m) == 32;
+template <typename R> __host__ __device__ inline bool tf_tab_smem(uint32_t m, int dim) {
+  return tf_nf<R>(m, dim) == 32;
 }
 // shared memory: [tile NF x m][carries NCH x NF][tables], 16-byte aligned parts
 template <typename R> __host__ __device__ inline size_t tf_tile_elems(int dim, uint32_t m) {
   // NF fibers per position; y / z fibers in 32-fiber groups are staged with
   // 16-byte chunks of a superset (pitch (32 + 2V - 2) / V * V, V = 16/sizeof(R))
-  const int nf = tf_nf(m), v = 16 / int(sizeof(R));
+  const int nf = tf_nf<R>(m, dim), v = 16 / int(sizeof(R));
   const size_t pitch =
       (nf == 32 && dim != 0) ? size_t((32 + 2 * v - 2) / v * v) : size_t(nf);
   return (pitch * m + 3) & ~size_t(3);
 }
 template <typename R> __host__ __device__ inline size_t tf_smem(int dim, uint32_t m) {
   return (tf_tile_elems<R>(dim, m) + size_t(kTfThreads) +
-          (tf_tab_smem<R>(m) ? tf_tab_elems<R>(m) : 0)) *
+          (tf_tab_smem<R>(m, dim) ? tf_tab_elems<R>(m, dim) : 0)) *
          sizeof(R);
 }
 
 // 16-byte async copy of n elements (src, dst 16-byte aligned) by the CTA.
-template <typename R>
+template <typename R, int NT = kTfThreads>
 __device__ __forceinline__ void tf_copy_in(R *dst, const R *src, uint32_t n, int tid) {
   constexpr int V = 16 / sizeof(R);
   const uint32_t nv = n / V;
-  for (uint32_t e = tid; e < nv; e += kTfThreads)
+  for (uint32_t e = tid; e < nv; e += NT)
     cp_async16(dst + e * V, src + e * V);
-  for (uint32_t e = nv * V + tid; e < n; e += kTfThreads)
+  for (uint32_t e = nv * V + tid; e < n; e += NT)
     cp_async(dst + e, src + e);
 }
 
@@ -197,7 +217,7 @@ __global__ void __launch_bounds__(kTfThreads, sizeof(R) == 4 ? 2 : 1)
   };
 
   if (TSM)
-    tf_copy_in(stab, t.tab, tf_tab_elems<R>(m), tid);
+    tf_copy_in(stab, t.tab, tf_tab_elems<R>(m, DIM), tid);
   R v[CH];
   if (DIM == 0) {
     tf_copy_in(tile, f + F0 * m, uint32_t(nf) * m, tid);
@@ -313,21 +333,22 @@ __global__ void __launch_bounds__(kTfThreads, sizeof(R) == 4 ? 2 : 1)
 
 // ---- long fibers: thread-block clusters over 32-fiber groups -------------
 //
-// Fibers of m > 528 positions (tf_cl(m) = CL > 1) do not fit one CTA's
-// registers: CTA r of a CL-CTA cluster holds positions [r*SEG, (r+1)*SEG),
-// SEG = 16 * CH, of a group of 32 fibers -- 16 chunks in registers as in
-// thomas_fiber_kernel -- so every element is still read once and written
-// once.  The chunk carries of the sequential pass cross the segment
-// boundaries through distributed shared memory: after its zero-carry-in
-// pass every CTA publishes its segment's end value (forward: e_r, the value
-// at the segment end; backward: b_r, at the segment start), the cluster
-// barrier makes them visible, and CTA r composes the carry into its segment
-// from its neighbours' published values with the host-precomputed segment
-// multipliers mf / mb (c_{r+1} = mf_r * c_r + e_r; d_{r-1} = mb_r * d_r + b_r)
-// before its own 16-chunk pass.
+// Fibers longer than one CTA's NW x 33 positions (tf_cl(m) = CL > 1) do not
+// fit its registers: CTA r of a CL-CTA cluster holds positions
+// [r*SEG, (r+1)*SEG), SEG = NW * CH, of a group of 32 fibers -- NW chunks in
+// registers as in thomas_fiber_kernel -- so every element is still read once
+// and written once.  The chunk carries of the sequential pass cross the
+// segment boundaries through distributed shared memory: after its
+// zero-carry-in pass every CTA publishes its segment's end value (forward:
+// e_r, the value at the segment end; backward: b_r, at the segment start),
+// the cluster barrier makes them visible, and CTA r composes the carry into
+// its segment from its neighbours' published values with the
+// host-precomputed segment multipliers mf / mb (c_{r+1} = mf_r * c_r + e_r;
+// d_{r-1} = mb_r * d_r + b_r) before its own NW-chunk pass.  NW = 8 (f64,
+// tf_nw) keeps two CTAs per SM; CL = 1 is the plain (cluster-free) case.
 //
-// One CTA per SM holds a whole register file of fiber values, so the
-// kernel is persistent: the grid is the number of co-resident clusters,
+// A CTA holds (half) a register file of fiber values, so the kernel is
+// persistent: the grid is the number of co-resident clusters,
 // each cluster walks the fiber groups, and the shared-memory tile of the
 // NEXT group is loaded (cp.async) as soon as the current group is in
 // registers -- the load overlaps this group's solve, carry exchange and
@@ -335,19 +356,19 @@ __global__ void __launch_bounds__(kTfThreads, sizeof(R) == 4 ? 2 : 1)
 // HBM (y / z fibers: position rows of 32 consecutive x nodes, coalesced;
 // x fibers: each thread's chunk is a contiguous run, written sector by
 // sector).  The segment's coefficient slice is staged once per CTA.
-template <typename R, int DIM, int CH>
+template <typename R, int DIM, int CH, int NW>
 __host__ __device__ inline size_t tc_tile_elems() {
-  constexpr size_t SEG = size_t(kTfThreads / 32) * CH;
+  constexpr size_t SEG = size_t(NW) * CH;
   return ((DIM == 0 ? 32 * (SEG + 1) : SEG * 32) + 3) & ~size_t(3);
 }
 // x fibers: per-warp output staging, 32 fibers x 8 positions (pitch 9)
 constexpr int kTcStg = 32 * 9;
-template <typename R, int DIM, int CH> __host__ __device__ inline size_t tc_smem() {
-  constexpr size_t SEG = size_t(kTfThreads / 32) * CH;
+template <typename R, int DIM, int CH, int NW> __host__ __device__ inline size_t tc_smem() {
+  constexpr size_t SEG = size_t(NW) * CH;
   // tile, carries, q8 slice + pfend / pbstart slices, published e / b,
   // x-fiber output staging
-  return (tc_tile_elems<R, DIM, CH>() + size_t(kTfThreads) + 8 * SEG + 2 * 16 + 2 * 32 +
-          (DIM == 0 ? size_t(kTfThreads / 32) * kTcStg : 0)) *
+  return (tc_tile_elems<R, DIM, CH, NW>() + size_t(32 * NW) + 8 * SEG + 2 * NW + 2 * 32 +
+          (DIM == 0 ? size_t(NW) * kTcStg : 0)) *
          sizeof(R);
 }
 
@@ -383,17 +404,17 @@ template <typename R> __device__ __forceinline__ const R *cluster_peer(const R *
   return reinterpret_cast<const R *>(out);
 }
 
-template <typename R, int DIM, int CH, int CL>
-__global__ void __launch_bounds__(kTfThreads, 1)
+template <typename R, int DIM, int CH, int CL, int NW>
+__global__ void __launch_bounds__(32 * NW, NW == 8 ? 2 : 1)
     thomas_cluster_kernel(R *__restrict__ f, ThomasLean<R> t, uint64_t nfib, uint32_t m0,
                           uint32_t m1, Epi epi, const R *base, R *out) {
   pdl_wait();
-  constexpr int NF = 32, NW = kTfThreads / NF, NCH = NW * CL;
+  constexpr int NF = 32, NT = 32 * NW, NCH = NW * CL;
   constexpr uint32_t SEG = uint32_t(NW) * CH, P0 = SEG + 1;
   extern __shared__ __align__(16) unsigned char tc_raw[];
   R *tile = reinterpret_cast<R *>(tc_raw);
-  R *carry = tile + tc_tile_elems<R, DIM, CH>();
-  R *sq = carry + kTfThreads;     // q8 of the segment's positions
+  R *carry = tile + tc_tile_elems<R, DIM, CH, NW>();
+  R *sq = carry + NT;             // q8 of the segment's positions
   R *spf = sq + 8 * SEG;          // pfend of the segment's chunks
   R *spb = spf + NW;              // pbstart of the segment's chunks
   R *pub_e = spb + NW;            // published forward end values [NF]
@@ -438,7 +459,7 @@ __global__ void __launch_bounds__(kTfThreads, 1)
   };
 
   uint64_t gi = cluster_id_x();
-  tf_copy_in(sq, gq + 8 * size_t(pa0), 8 * SEG, tid); // 8*pa0*sizeof(R): 16-byte multiple
+  tf_copy_in<R, NT>(sq, gq + 8 * size_t(pa0), 8 * SEG, tid); // 8*pa0*sizeof(R): 16-byte multiple
   if (tid < NW) {
     spf[tid] = gpf[r * NW + tid];
     spb[tid] = gpb[r * NW + tid];
