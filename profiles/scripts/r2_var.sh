@@ -1,6 +1,6 @@
-TAG=${1:-r2o}
+TAG=${1:-r2q}
 O=gpurun_out/$TAG; mkdir -p $O
-timeout 1500 python -m pytest tests -m gpu -x -q -p no:cacheprovider > $O/gputest.log 2>&1; echo rc=$? >> $O/gputest.log
-timeout 300 python profiles/scripts/levels.py --shape 1025,1025,513 --dtype float64 > $O/levels_c5.txt 2>&1
-timeout 300 python profiles/scripts/levels.py --shape 8193,8193 --dtype float64 > $O/levels_c2.txt 2>&1
-timeout 300 python profiles/scripts/levels.py --shape 513,513,513 > $O/levels_c3u.txt 2>&1
+for v in base pf3m3 pf4m2 pf6m2 pf4m3; do
+  if [ $v = base ]; then L=""; else L=$PWD/paper_2105_12764_b200/variants/libmgrg_$v.so; fi
+  MGRG_LIB=$L timeout 300 python profiles/scripts/levels.py > $O/levels_c4_$v.txt 2>&1
+done
