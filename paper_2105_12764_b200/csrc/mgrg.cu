@@ -925,7 +925,7 @@ void (*tc_pick_cl(int cl))(R *, ThomasLean<R>, uint64_t, uint32_t, uint32_t, Epi
 template <typename R, int DIM>
 void (*tc_pick(int ch, int cl, int nw))(R *, ThomasLean<R>, uint64_t, uint32_t, uint32_t, Epi,
                                         const R *, R *) {
-  if constexpr (sizeof(R) == 8)
+  if constexpr (sizeof(R) == 8 || TF_NW8_F32)
     if (nw == 8)
       return ch <= 17 ? tc_pick_cl<R, DIM, 17, 8>(cl) : tc_pick_cl<R, DIM, 33, 8>(cl);
   return ch <= 17 ? tc_pick_cl<R, DIM, 17, 16>(cl) : tc_pick_cl<R, DIM, 33, 16>(cl);

@@ -48,10 +48,12 @@ constexpr int kTfThreads = 512; // threads per CTA = fibers x chunks
 #ifndef TF_NW8_F64
 #define TF_NW8_F64 1
 #endif
+#ifndef TF_NW8_F32
+#define TF_NW8_F32 0
+#endif
 template <typename R> __host__ __device__ inline int tf_nw(uint32_t m, int dim) {
-  return (TF_NW8_F64 && sizeof(R) == 8 && dim != 0 && m > 8u * 9u && m <= 8u * 33u * 8u)
-             ? 8
-             : 16;
+  const bool on = sizeof(R) == 8 ? TF_NW8_F64 : TF_NW8_F32;
+  return (on && dim != 0 && m > 8u * 9u && m <= 8u * 33u * 8u) ? 8 : 16;
 }
 template <typename R> __host__ __device__ inline int tf_cl(uint32_t m, int dim) {
   const uint32_t seg = uint32_t(tf_nw<R>(m, dim)) * 33u;
@@ -372,6 +374,9 @@ template <typename R, int DIM, int CH, int NW> __host__ __device__ inline size_t
          sizeof(R);
 }
 
+#ifndef TC_EPI_B
+#define TC_EPI_B 8
+#endif
 __device__ __forceinline__ void prefetch_l2(const void *p) {
   asm volatile("prefetch.global.L2 [%0];\n" ::"l"(p));
 }
@@ -405,7 +410,7 @@ template <typename R> __device__ __forceinline__ const R *cluster_peer(const R *
 }
 
 template <typename R, int DIM, int CH, int CL, int NW>
-__global__ void __launch_bounds__(32 * NW, NW == 8 ? 2 : 1)
+__global__ void __launch_bounds__(32 * NW, NW == 8 ? (sizeof(R) == 4 ? 4 : 2) : 1)
     thomas_cluster_kernel(R *__restrict__ f, ThomasLean<R> t, uint64_t nfib, uint32_t m0,
                           uint32_t m1, Epi epi, const R *base, R *out) {
   pdl_wait();
@@ -592,7 +597,7 @@ __global__ void __launch_bounds__(32 * NW, NW == 8 ? 2 : 1)
             o[k * st] = v[k];
       } else {
         const R *bp = base + p0;
-        constexpr int B = 8; // base loads in flight per batch
+        constexpr int B = TC_EPI_B; // base loads in flight per batch
 #pragma unroll
         for (int k0 = 0; k0 < CH; k0 += B) {
           R bv[B];
