@@ -915,6 +915,9 @@ void (*tf_pick(int ch))(R *, ThomasLean<R>, uint64_t, uint32_t, uint32_t, Epi, c
 template <typename R, int DIM, int CH, int NW>
 void (*tc_pick_cl(int cl))(R *, ThomasLean<R>, uint64_t, uint32_t, uint32_t, Epi, const R *,
                            R *) {
+  if constexpr (TF_CL16 && NW == 8 && sizeof(R) == 8)
+    if (cl == 16)
+      return thomas_cluster_kernel<R, DIM, CH, 16, NW>;
   switch (cl) {
   case 1: return thomas_cluster_kernel<R, DIM, CH, 1, NW>;
   case 2: return thomas_cluster_kernel<R, DIM, CH, 2, NW>;
@@ -1008,9 +1011,14 @@ template <typename R> void set_tf_attrs() {
     cudaFuncSetAttribute(tf_pick<R, 1>(ch), cudaFuncAttributeMaxDynamicSharedMemorySize, lim);
     cudaFuncSetAttribute(tf_pick<R, 2>(ch), cudaFuncAttributeMaxDynamicSharedMemorySize, lim);
   }
+  if (TF_CL16)
+    for (int ch : {17, 33})
+      for (auto k : {tc_pick<R, 0>(ch, 16, 8), tc_pick<R, 1>(ch, 16, 8),
+                     tc_pick<R, 2>(ch, 16, 8)})
+        cudaFuncSetAttribute(k, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
   for (int nw : {8, 16})
     for (int ch : {17, 33})
-      for (int cl : {1, 2, 4, 8}) {
+      for (int cl : {1, 2, 4, 8, 16}) {
         cudaFuncSetAttribute(tc_pick<R, 0>(ch, cl, nw),
                              cudaFuncAttributeMaxDynamicSharedMemorySize, lim);
         cudaFuncSetAttribute(tc_pick<R, 1>(ch, cl, nw),

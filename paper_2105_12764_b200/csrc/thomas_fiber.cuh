@@ -51,13 +51,22 @@ constexpr int kTfThreads = 512; // threads per CTA = fibers x chunks
 #ifndef TF_NW8_F32
 #define TF_NW8_F32 0
 #endif
+// TF_CL16: 8-warp CTAs in non-portable 16-CTA clusters for f64 y / z fibers
+// up to 4224 positions (else 16-warp CTAs in 8-CTA clusters there)
+#ifndef TF_CL16
+#define TF_CL16 0
+#endif
+template <typename R> __host__ __device__ inline int tf_maxcl(int nw) {
+  return (TF_CL16 && sizeof(R) == 8 && nw == 8) ? 16 : 8;
+}
 template <typename R> __host__ __device__ inline int tf_nw(uint32_t m, int dim) {
   const bool on = sizeof(R) == 8 ? TF_NW8_F64 : TF_NW8_F32;
-  return (on && dim != 0 && m > 8u * 9u && m <= 8u * 33u * 8u) ? 8 : 16;
+  return (on && dim != 0 && m > 8u * 9u && m <= 8u * 33u * uint32_t(tf_maxcl<R>(8))) ? 8 : 16;
 }
 template <typename R> __host__ __device__ inline int tf_cl(uint32_t m, int dim) {
-  const uint32_t seg = uint32_t(tf_nw<R>(m, dim)) * 33u;
-  for (int cl = 1; cl <= 8; cl *= 2)
+  const int nw = tf_nw<R>(m, dim);
+  const uint32_t seg = uint32_t(nw) * 33u;
+  for (int cl = 1; cl <= tf_maxcl<R>(nw); cl *= 2)
     if (m <= seg * uint32_t(cl))
       return cl;
   return 0;
