@@ -35,6 +35,25 @@ namespace mgrg {
 #ifndef LEAN_DEC_MINB
 #define LEAN_DEC_MINB 3
 #endif
+// CTAs per SM of the exact-policy instantiations (no FMA contraction: more
+// live temporaries), measured (profiles/r2/tuning): decompose f32 4 (3.94 ->
+// 3.54 ms at 1025^3 L10), f64 2 (5.23 -> 3.68 ms at 1025^2 x 513 L9); load
+// vector f32 3, f64 2 (2.93 -> 2.73 ms); GPK inverse 3
+#ifndef LEAN_EXACT_MINB_DEC_F32
+#define LEAN_EXACT_MINB_DEC_F32 4
+#endif
+#ifndef LEAN_EXACT_MINB_DEC_F64
+#define LEAN_EXACT_MINB_DEC_F64 2
+#endif
+#ifndef LEAN_EXACT_MINB_RL_F32
+#define LEAN_EXACT_MINB_RL_F32 3
+#endif
+#ifndef LEAN_EXACT_MINB_RL_F64
+#define LEAN_EXACT_MINB_RL_F64 2
+#endif
+#ifndef LEAN_EXACT_MINB_RG
+#define LEAN_EXACT_MINB_RG 3
+#endif
 #ifndef LEAN_TY_F64
 #define LEAN_TY_F64 3 // measured (1025^2 x 513 f64, L9): TY 2 / MINB 3 2.59 ms, 2 / 2 2.33, 3 / 2 1.93, 4 / 2 2.41
 #endif
@@ -382,7 +401,7 @@ template <typename R> __host__ __device__ constexpr size_t lean_dec_smem() {
 }
 
 template <typename R, bool Z3, bool FAST>
-__global__ void __launch_bounds__(32 * kLeanWPB, sizeof(R) == 4 ? LEAN_DEC_MINB : LEAN_DEC_MINB_F64)
+__global__ void __launch_bounds__(32 * kLeanWPB, !FAST ? (sizeof(R) == 4 ? LEAN_EXACT_MINB_DEC_F32 : LEAN_EXACT_MINB_DEC_F64) : (sizeof(R) == 4 ? LEAN_DEC_MINB : LEAN_DEC_MINB_F64))
     lean_dec_kernel(LevelGeom<R> g, const LeanW<R> *__restrict__ lx,
                     const LeanW<R> *__restrict__ ly, const LeanW<R> *__restrict__ lz,
                     const Stencil<R> *__restrict__ sxt, const Stencil<R> *__restrict__ syt,
@@ -626,7 +645,7 @@ template <typename R> __host__ __device__ constexpr int lean_ty_rl() {
 }
 
 template <typename R, bool Z3, bool FAST>
-__global__ void __launch_bounds__(32 * kLeanWPB, sizeof(R) == 4 ? LEAN_RL_MINB : LEAN_RL_MINB_F64)
+__global__ void __launch_bounds__(32 * kLeanWPB, !FAST ? (sizeof(R) == 4 ? LEAN_EXACT_MINB_RL_F32 : LEAN_EXACT_MINB_RL_F64) : (sizeof(R) == 4 ? LEAN_RL_MINB : LEAN_RL_MINB_F64))
     lean_rload_kernel(LevelGeom<R> g, const LeanW<R> *__restrict__ lx,
                       const LeanW<R> *__restrict__ ly, const LeanW<R> *__restrict__ lz,
                       const Stencil<R> *__restrict__ sxt, const Stencil<R> *__restrict__ syt,
@@ -838,7 +857,7 @@ __device__ __forceinline__ void lean_store_pair(R *p, R e, R o, bool we, bool wo
 }
 
 template <typename R, bool Z3, bool CLS, bool FAST>
-__global__ void __launch_bounds__(32 * kLeanWPB, sizeof(R) == 4 ? LEAN_RG_MINB : LEAN_RG_MINB_F64)
+__global__ void __launch_bounds__(32 * kLeanWPB, !FAST ? LEAN_EXACT_MINB_RG : (sizeof(R) == 4 ? LEAN_RG_MINB : LEAN_RG_MINB_F64))
     lean_rgpk_kernel(LevelGeom<R> g, const LeanW<R> *__restrict__ lx,
                      const LeanW<R> *__restrict__ ly, const LeanW<R> *__restrict__ lz,
                      const R *__restrict__ coarse, const R *__restrict__ cls,
