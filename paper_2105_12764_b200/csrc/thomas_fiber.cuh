@@ -146,8 +146,19 @@ __device__ __forceinline__ void tf_copy_in(R *dst, const R *src, uint32_t n, int
 // DIM 1: fiber id F = x + m0 * z, position i at x + m0 * (i + m1 * z);
 // DIM 2: fiber id F = x + m0 * y, position i at F + m0 * m1 * i.
 // Thread t: fiber t % NF, chunk t / NF.
+// CTAs per SM: x fibers of <= 17-position chunks run one more CTA per SM
+// (measured at 1025^3 L9 f32 44.5 -> 37.9 us, 1025^2 x 513 L8 f64 46.7 ->
+// 38.4 us; y / z fibers gain nothing and spill)
+#ifndef TF_MINB_F32_SHORT
+#define TF_MINB_F32_SHORT 3
+#endif
+#ifndef TF_MINB_F64_SHORT
+#define TF_MINB_F64_SHORT 2
+#endif
 template <typename R, int DIM, int CH, int NF>
-__global__ void __launch_bounds__(kTfThreads, sizeof(R) == 4 ? 2 : 1)
+__global__ void __launch_bounds__(kTfThreads,
+                                  sizeof(R) == 4 ? (DIM == 0 && CH <= 17 ? TF_MINB_F32_SHORT : 2)
+                                                 : (DIM == 0 && CH <= 17 ? TF_MINB_F64_SHORT : 1))
     thomas_fiber_kernel(R *__restrict__ f, ThomasLean<R> t, uint64_t nfib, uint32_t m0,
                         uint32_t m1, Epi epi, const R *base, R *out) {
   pdl_wait();
