@@ -1,7 +1,6 @@
-TAG=${1:-r2z}
+TAG=${1:-r2aa}
 O=gpurun_out/$TAG; mkdir -p $O
-timeout 900 python -m pytest tests/test_gpu_parity.py tests/test_coop.py -x -q -p no:cacheprovider > $O/parity.log 2>&1; echo rc=$? >> $O/parity.log
-timeout 300 python profiles/scripts/levels.py > $O/levels_c4.txt 2>&1
-timeout 300 python profiles/scripts/levels.py --shape 1025,1025,513 --dtype float64 > $O/levels_c5.txt 2>&1
-timeout 300 python profiles/scripts/levels.py --exact > $O/levels_c4x.txt 2>&1
-bash profiles/scripts/ncu_one.sh lean_dec 0 ${TAG}_ldec
+for v in base rl4m4 rl3m4 rl5m3 rl7m3; do
+  if [ $v = base ]; then L=""; else L=$PWD/paper_2105_12764_b200/variants/libmgrg_$v.so; fi
+  MGRG_LIB=$L timeout 300 python profiles/scripts/levels.py > $O/levels_c4_$v.txt 2>&1
+done
