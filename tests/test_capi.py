@@ -2,6 +2,7 @@
 symbol, and its host-side validation behaves like the reference's
 (errors.hpp codes) -- all without a GPU (no compute calls here)."""
 import ctypes
+import os
 import re
 
 import numpy as np
@@ -90,3 +91,21 @@ def test_python_plan_errors_are_reference_types():
         Plan((9, 9), "float32", levels=0)
     with pytest.raises(errors.InvalidArgument):
         Plan((9,), "int32")
+
+
+def test_hostio_views_and_copy_pool(tmp_path):
+    """The host side of the host-buffer entry points (csrc/hostio.cuh): the
+    per-class HostView splits every flat range into exactly the right class
+    pieces, and the parallel copy pool copies correctly (no device calls)."""
+    import subprocess
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    cuda = os.environ.get("CUDA_HOME", "/usr/local/cuda")
+    exe = str(tmp_path / "test_hostio")
+    subprocess.run(["g++", "-std=c++17", "-O2", "-I", os.path.join(cuda, "include"),
+                    os.path.join(root, "tests", "cpp", "test_hostio.cpp"),
+                    "-L", os.path.join(cuda, "lib64"), "-lcudart", "-pthread",
+                    f"-Wl,-rpath,{os.path.join(cuda, 'lib64')}", "-o", exe], check=True)
+    out = subprocess.run([exe], capture_output=True, text=True, timeout=120)
+    assert out.returncode == 0, out.stderr
+    assert "hostio ok" in out.stdout
