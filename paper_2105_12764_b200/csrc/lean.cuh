@@ -209,15 +209,18 @@ template <typename R> __device__ __forceinline__ R flerp(R a, R b, R t) {
   return fma(t, b - a, a);
 }
 
-// Paired (even, odd) node updates.  FAST f32: Blackwell's packed FP32x2
-// instructions (FADD2 / FFMA2) do both lanes of the pair in one issue slot;
-// each component is the same round-to-nearest operation as the scalar
-// policy, so results are bit-identical to plerp / psub per component.
+// Paired (even, odd) node updates.  f32: Blackwell's packed FP32x2
+// instructions (FADD2 / FMUL2 / FFMA2) do both lanes of the pair in one issue
+// slot; each component is the same round-to-nearest operation as the scalar
+// code of the policy (exact: a + t*(b - a) unfused, kernels.hpp:219), so
+// results are bit-identical to plerp / psub per component.
 template <typename R, bool FAST>
 __device__ __forceinline__ typename Vec2<R>::T plerp2(typename Vec2<R>::T a,
                                                       typename Vec2<R>::T b, R t) {
   if constexpr (FAST && sizeof(R) == 4) {
     return __ffma2_rn(make_float2(t, t), __fadd2_rn(b, make_float2(-a.x, -a.y)), a);
+  } else if constexpr (sizeof(R) == 4) {
+    return __fadd2_rn(a, __fmul2_rn(make_float2(t, t), __fadd2_rn(b, make_float2(-a.x, -a.y))));
   } else {
     typename Vec2<R>::T r;
     r.x = plerp<R, FAST>(a.x, b.x, t);
@@ -228,7 +231,7 @@ __device__ __forceinline__ typename Vec2<R>::T plerp2(typename Vec2<R>::T a,
 template <typename R, bool FAST>
 __device__ __forceinline__ typename Vec2<R>::T psub2(typename Vec2<R>::T a,
                                                      typename Vec2<R>::T b) {
-  if constexpr (FAST && sizeof(R) == 4) {
+  if constexpr (sizeof(R) == 4) {
     return __fadd2_rn(a, make_float2(-b.x, -b.y));
   } else {
     typename Vec2<R>::T r;
