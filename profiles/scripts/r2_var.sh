@@ -1,6 +1,4 @@
-TAG=${1:-r2aa}
+TAG=${1:-r2ac}
 O=gpurun_out/$TAG; mkdir -p $O
-for v in base rl4m4 rl3m4 rl5m3 rl7m3; do
-  if [ $v = base ]; then L=""; else L=$PWD/paper_2105_12764_b200/variants/libmgrg_$v.so; fi
-  MGRG_LIB=$L timeout 300 python profiles/scripts/levels.py > $O/levels_c4_$v.txt 2>&1
-done
+timeout 900 python -m pytest tests/test_gpu_parity.py tests/test_gpu_parity_full.py tests/test_cpp_shim.py -x -q -p no:cacheprovider > $O/parity.log 2>&1; echo rc=$? >> $O/parity.log
+timeout 300 python profiles/scripts/levels.py --exact > $O/levels_c4x.txt 2>&1
