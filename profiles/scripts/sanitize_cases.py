@@ -45,6 +45,14 @@ CASES = [
     ((9, 2049), "float64", False, True),
     ((9, 7, 5, 5), "float32", False, False),
     ((9, 9, 5, 3), "float64", True, True),
+    # round 2: long fibers on thread-block clusters (DSMEM carries), 8-warp
+    # f64 y / z CTAs
+    ((8193, 9), "float64", False, True),
+    ((9, 4097), "float32", True, True),
+    ((9, 1073), "float64", False, True),
+    ((9, 5, 1073), "float64", True, True),
+    ((5, 3, 4097), "float32", False, True),
+    ((33, 65, 257), "float64", False, True),
 ]
 if quick:
     CASES = CASES[:4] + CASES[8:9] + CASES[17:18]
@@ -100,9 +108,38 @@ def run_coop():
     assert np.array_equal(flat, ref_c)
 
 
+def run_host(shape, dt, fast):
+    """Host-buffer entry points: pageable (pinned rings + download worker,
+    csrc/hostio.cuh) and per-class buffers; the pipelined path at >= 2^22
+    nodes."""
+    import ctypes
+
+    from paper_2105_12764_b200 import _lib
+
+    v = rng.random(int(np.prod(shape))).astype(dt)
+    plan = Plan(shape, dt, device=0, fast=fast)
+    ref = plan.decompose(torch.from_numpy(v).to(dev)).cpu().numpy()
+    sl = plan.class_slices()
+    cls = [np.empty(s.stop - s.start, dtype=dt) for s in sl]
+    ptrs = (ctypes.c_void_p * len(cls))(*[c.ctypes.data for c in cls])
+    _lib.check(_lib.lib().mgrg_decompose_host_classes(plan._h, v.ctypes.data, ptrs))
+    assert np.array_equal(np.concatenate(cls), ref)
+    back = np.empty_like(v)
+    _lib.check(_lib.lib().mgrg_recompose_host_classes(plan._h, ptrs, plan.levels,
+                                                      back.ctypes.data))
+    flat = np.empty_like(v)
+    _lib.check(_lib.lib().mgrg_decompose_host(plan._h, v.ctypes.data, flat.ctypes.data))
+    assert np.array_equal(flat, ref)
+    plan.close()
+
+
 for c in CASES:
     run_case(*c)
     print("ok", c, flush=True)
+for shp, dt, fast in (((129, 129, 257), "float32", True), ((129, 129, 257), "float32", False),
+                      ((33, 17, 9), "float64", True)):
+    run_host(shp, dt, fast)
+    print("ok host", shp, dt, fast, flush=True)
 run_coop()
 print("ok coop", flush=True)
 print("sanitize cases done", flush=True)
