@@ -209,18 +209,17 @@ template <typename R> __device__ __forceinline__ R flerp(R a, R b, R t) {
   return fma(t, b - a, a);
 }
 
-// Paired (even, odd) node updates.  f32: Blackwell's packed FP32x2
-// instructions (FADD2 / FMUL2 / FFMA2) do both lanes of the pair in one issue
-// slot; each component is the same round-to-nearest operation as the scalar
-// code of the policy (exact: a + t*(b - a) unfused, kernels.hpp:219), so
-// results are bit-identical to plerp / psub per component.
+// Paired (even, odd) node updates.  FAST f32: Blackwell's packed FP32x2
+// instructions (FADD2 / FFMA2) do both lanes of the pair in one issue slot;
+// each component is the same round-to-nearest operation as the scalar FAST
+// code, so results are bit-identical to plerp / psub per component.  (Not
+// used for the exact policy: ptxas fuses a packed multiply and add into
+// FFMA2 even for .rn operations, which would break bit-identity.)
 template <typename R, bool FAST>
 __device__ __forceinline__ typename Vec2<R>::T plerp2(typename Vec2<R>::T a,
                                                       typename Vec2<R>::T b, R t) {
   if constexpr (FAST && sizeof(R) == 4) {
     return __ffma2_rn(make_float2(t, t), __fadd2_rn(b, make_float2(-a.x, -a.y)), a);
-  } else if constexpr (sizeof(R) == 4) {
-    return __fadd2_rn(a, __fmul2_rn(make_float2(t, t), __fadd2_rn(b, make_float2(-a.x, -a.y))));
   } else {
     typename Vec2<R>::T r;
     r.x = plerp<R, FAST>(a.x, b.x, t);
@@ -231,7 +230,7 @@ __device__ __forceinline__ typename Vec2<R>::T plerp2(typename Vec2<R>::T a,
 template <typename R, bool FAST>
 __device__ __forceinline__ typename Vec2<R>::T psub2(typename Vec2<R>::T a,
                                                      typename Vec2<R>::T b) {
-  if constexpr (sizeof(R) == 4) {
+  if constexpr (FAST && sizeof(R) == 4) {
     return __fadd2_rn(a, make_float2(-b.x, -b.y));
   } else {
     typename Vec2<R>::T r;
