@@ -1,7 +1,5 @@
-TAG=${1:-r2ak}
+TAG=${1:-r2an}
 O=gpurun_out/$TAG; mkdir -p $O
-for v in base half half5; do
-  if [ $v = base ]; then L=""; else L=$PWD/paper_2105_12764_b200/variants/libmgrg_$v.so; fi
-  MGRG_LIB=$L timeout 300 python profiles/scripts/levels.py > $O/levels_c4_$v.txt 2>&1
-  MGRG_LIB=$L timeout 300 python profiles/scripts/levels.py --shape 1025,1025,513 --dtype float64 > $O/levels_c5_$v.txt 2>&1
-done
+timeout 900 python -m pytest tests/test_gpu_parity.py tests/test_gpu_units.py tests/test_container.py tests/test_compress.py -x -q -p no:cacheprovider > $O/parity.log 2>&1; echo rc=$? >> $O/parity.log
+timeout 300 python profiles/scripts/levels.py --shape 129,129,129,9 > $O/levels_4d.txt 2>&1
+timeout 300 python profiles/scripts/bench_widen.py > $O/widen.json 2>&1
