@@ -35,9 +35,36 @@ namespace mgrg {
 
 constexpr int kGenDims = 4;
 
+// Division by a fixed extent as a multiply-high (the decode of a flat index
+// is the element-parallel kernels' main cost: three 32-bit divisions by
+// runtime divisors are ~60 instructions, these ~12): with l = ceil(log2 d),
+// m = floor(2^32 (2^l - d) / d) + 1, n / d = (t + ((n - t) >> 1)) >> (l - 1),
+// t = umulhi(m, n), exact for every 32-bit n (d = 1: identity).
+struct FastDiv {
+  uint32_t d, m, sh;
+};
+inline FastDiv make_fastdiv(uint32_t d) {
+  FastDiv f{d, 0u, 0u};
+  if (d > 1) {
+    uint32_t l = 0;
+    while ((uint64_t(1) << l) < d)
+      ++l;
+    f.m = uint32_t(((uint64_t(1) << 32) * ((uint64_t(1) << l) - d)) / d + 1);
+    f.sh = l - 1;
+  }
+  return f;
+}
+__device__ __forceinline__ uint32_t fdiv(uint32_t n, const FastDiv &f) {
+  if (f.d == 1)
+    return n;
+  const uint32_t t = __umulhi(f.m, n);
+  return (t + ((n - t) >> 1)) >> f.sh;
+}
+
 template <typename R> struct Gen4Geom {
   uint32_t n[kGenDims];            // level-l extents
   uint32_t m[kGenDims];            // level-(l-1) extents
+  FastDiv fn[kGenDims], fm[kGenDims]; // their fast divisors
   const R *h[kGenDims];            // level-l spacings (grid.cpp:60-65)
   const R *r[kGenDims];            // level-l ratios (grid.cpp:66-71)
   const R *th[kGenDims];           // level-(l-1) Thomas factors (kernels.hpp:107-135),
@@ -53,6 +80,26 @@ template <typename R> struct Gen4Geom {
     return uint64_t(m[0]) * m[1] * m[2] * m[3];
   }
 };
+
+// flat index -> lattice position with fast divisors (32-bit indices)
+__device__ __forceinline__ void gen_decode_f(uint64_t i, const FastDiv *f, uint32_t *p) {
+  if ((i >> 32) == 0) {
+    uint32_t j = uint32_t(i);
+#pragma unroll
+    for (int d = 0; d < kGenDims - 1; ++d) {
+      const uint32_t qd = fdiv(j, f[d]);
+      p[d] = j - qd * f[d].d;
+      j = qd;
+    }
+    p[kGenDims - 1] = j;
+    return;
+  }
+#pragma unroll
+  for (int d = 0; d < kGenDims; ++d) {
+    p[d] = uint32_t(i % f[d].d);
+    i /= f[d].d;
+  }
+}
 
 __device__ __forceinline__ void gen_decode(uint64_t i, const uint32_t *e, uint32_t *p) {
   if ((i >> 32) == 0) { // 32-bit divisions (a 64-bit one is a long call)
@@ -143,7 +190,7 @@ __global__ void gen_coef_kernel(Gen4Geom<R> g, const R *__restrict__ a, R *__res
   if (i >= g.nodes())
     return;
   uint32_t p[kGenDims];
-  gen_decode(i, g.n, p);
+  gen_decode_f(i, g.fn, p);
   const unsigned mask = gen_mask(g, p);
   if (!mask) {
     W[i] = R(0);
@@ -162,7 +209,7 @@ __global__ void gen_load_kernel(Gen4Geom<R> g, const R *__restrict__ cls, R *__r
   if (i >= g.nodes())
     return;
   uint32_t p[kGenDims];
-  gen_decode(i, g.n, p);
+  gen_decode_f(i, g.fn, p);
   const unsigned mask = gen_mask(g, p);
   W[i] = (mask && cls) ? cls[gen_slot(g, p, mask)] : R(0);
 }
@@ -181,7 +228,12 @@ __global__ void gen_mass_kernel(Gen4Geom<R> g, int d, uint4 e4, const R *__restr
   if (o >= total)
     return;
   uint32_t p[kGenDims];
-  gen_decode(o, oe, p);
+  // output extents: dims <= d at level l-1, dims > d at level l
+  FastDiv fo[kGenDims];
+#pragma unroll
+  for (int k = 0; k < kGenDims; ++k)
+    fo[k] = k <= d ? g.fm[k] : g.fn[k];
+  gen_decode_f(o, fo, p);
   uint64_t base = 0, str = 1, sd = 1;
 #pragma unroll
   for (int k = 0; k < kGenDims; ++k) {
@@ -203,7 +255,7 @@ __global__ void gen_apply_kernel(Gen4Geom<R> g, const R *__restrict__ a,
   if (i >= g.coarse_nodes())
     return;
   uint32_t c[kGenDims], q[kGenDims];
-  gen_decode(i, g.m, c);
+  gen_decode_f(i, g.fm, c);
 #pragma unroll
   for (int d = 0; d < kGenDims; ++d)
     q[d] = coarse_pos(c[d], g.n[d]);
@@ -227,7 +279,7 @@ __global__ void gen_rgpk_kernel(Gen4Geom<R> g, const R *__restrict__ cz,
   if (i >= g.nodes())
     return;
   uint32_t p[kGenDims];
-  gen_decode(i, g.n, p);
+  gen_decode_f(i, g.fn, p);
   const unsigned mask = gen_mask(g, p);
   auto at = [&](const uint32_t *q) {
     return cz[coarse_rank(q[0]) +
@@ -251,7 +303,7 @@ __global__ void gen_gpk_inplace_kernel(Gen4Geom<R> g, R *a, int inverse) {
   if (i >= g.nodes())
     return;
   uint32_t p[kGenDims];
-  gen_decode(i, g.n, p);
+  gen_decode_f(i, g.fn, p);
   const unsigned mask = gen_mask(g, p);
   if (!mask)
     return;
@@ -268,7 +320,7 @@ __global__ void gen_vecc_kernel(Gen4Geom<R> g, const R *__restrict__ in, R *__re
   if (i >= g.nodes())
     return;
   uint32_t p[kGenDims];
-  gen_decode(i, g.n, p);
+  gen_decode_f(i, g.fn, p);
   const unsigned mask = gen_mask(g, p);
   const R x = in[i];
   W[i] = mask ? x : R(0);
@@ -285,7 +337,7 @@ __global__ void gen_reorder_kernel(Gen4Geom<R> g, int to_natural, const R *__res
   if (i >= g.nodes())
     return;
   uint32_t p[kGenDims];
-  gen_decode(i, g.n, p);
+  gen_decode_f(i, g.fn, p);
   const unsigned mask = gen_mask(g, p);
   const uint64_t k =
       mask ? g.coarse_nodes() + gen_slot(g, p, mask)

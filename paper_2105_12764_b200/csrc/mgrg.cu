@@ -601,6 +601,8 @@ template <typename R> mgrg_status upload_geometry_gen(mgrg_plan *p) {
     for (int d = 0; d < kGenDims; ++d) {
       g.n[d] = uint32_t(H.ext[l][d]);
       g.m[d] = uint32_t(H.ext[l - 1][d]);
+      g.fn[d] = make_fastdiv(g.n[d]);
+      g.fm[d] = make_fastdiv(g.m[d]);
       g.h[d] = at(refs[l].h[d]);
       g.r[d] = at(refs[l].r[d]);
       g.th[d] = at(refs[l].th[d]);
