@@ -362,9 +362,10 @@ inline void fill_stats(PassStats &stats, mgrg_plan *p, std::size_t nd, bool reco
 }
 
 // An n-element value-initialised std::vector<Real> (the reference's output
-// type) whose pages are first faulted in by all host threads: a fresh
-// multi-GB std::vector otherwise spends ~0.4 s per GB page-faulting inside
-// its single-threaded zero fill (profiles/r2/host_probe.json).  Populating
+// type) whose pages are first faulted in (2 MiB pages where THP allows, by 4
+// host threads): a fresh multi-GB std::vector otherwise spends ~0.3 s per GB
+// page-faulting inside its single-threaded zero fill
+// (profiles/r2/host_probe.json, profiles/r2/alloc_probe.json).  Populating
 // the reserved storage is a kernel operation on memory the vector owns; no
 // element is touched before resize() constructs it.
 inline void prefault(void *p, std::size_t bytes) {
@@ -380,7 +381,10 @@ inline void prefault(void *p, std::size_t bytes) {
 #ifdef MADV_HUGEPAGE
   (void)madvise(reinterpret_cast<void *>(a), e - a, MADV_HUGEPAGE); // 2 MiB faults where THP allows
 #endif
-  const unsigned T = std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
+  // 4 threads: measured on the B200 host (profiles/r2/alloc_probe.json, 4.3 GB
+  // with MADV_HUGEPAGE): 1 thread 441 ms, 4 threads 119 ms, 16 threads 386 ms
+  // (fault-path contention)
+  const unsigned T = std::max(1u, std::min(4u, std::thread::hardware_concurrency()));
   const std::size_t per = ((e - a) / T + (2u << 20) - 1) & ~std::size_t((2u << 20) - 1);
   std::vector<std::thread> th;
   for (unsigned t = 0; t < T; ++t) {

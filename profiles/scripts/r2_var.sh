@@ -1,5 +1,6 @@
-TAG=${1:-r2ao}
+TAG=${1:-r2av}
 O=gpurun_out/$TAG; mkdir -p $O
-timeout 900 python -m pytest tests/test_gpu_parity.py tests/test_gpu_units.py tests/test_container.py tests/test_compress.py tests/test_cpp_shim.py -x -q -p no:cacheprovider > $O/parity.log 2>&1; echo rc=$? >> $O/parity.log
-timeout 300 python profiles/scripts/levels.py --shape 129,129,129,9 > $O/levels_4d.txt 2>&1
-timeout 300 python profiles/scripts/bench_widen.py > $O/widen.json 2>&1
+g++ -std=c++17 -O2 -Iinclude tests/cpp/bench_dropin.cpp -Lpaper_2105_12764_b200 -lmgrg -pthread -Wl,-rpath,$PWD/paper_2105_12764_b200 -o /tmp/bench_dropin
+timeout 300 /tmp/bench_dropin 1025 2 1 0 > $O/dropin.jsonl 2>&1
+timeout 300 /tmp/bench_dropin 1025 2 1 1 >> $O/dropin.jsonl 2>&1
+timeout 600 python -m pytest tests/test_cpp_shim.py -x -q -p no:cacheprovider > $O/shim.log 2>&1; echo rc=$? >> $O/shim.log
