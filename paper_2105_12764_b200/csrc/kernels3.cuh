@@ -65,9 +65,4 @@ template <typename R> struct W5 {
   }
 };
 
-// ---------------------------------------------------------------------------
-// Decompose, one level: GPK forward on `in`, class-order store into `cls`,
-// packed kept-node values into P, merged R*M of vec(C) into f
-// (refactor.hpp:165-175 minus the solves; kernels.hpp:231-279, 158-185).
-// ---------------------------------------------------------------------------
 } // namespace mgrg
