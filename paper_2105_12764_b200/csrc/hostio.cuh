@@ -151,6 +151,15 @@ inline bool host_pinned(const void *p) {
   }
   return a.type == cudaMemoryTypeHost;
 }
+// device memory passed where the host-buffer entry points expect host memory
+inline bool is_device_ptr(const void *p) {
+  cudaPointerAttributes a;
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return a.type == cudaMemoryTypeDevice;
+}
 
 // ---- the caller's host buffer as a flat element range -------------------
 struct HostView {
@@ -159,12 +168,14 @@ struct HostView {
   std::vector<char *> seg;        // ... or one per class
   std::vector<uint64_t> off;      // class offsets (seg.size() + 1 entries)
   bool pinned = false;
+  bool device = false; // a device pointer: rejected by the entry points
 
   static HostView of(const void *p, size_t es) {
     HostView v;
     v.es = es;
     v.flat = static_cast<char *>(const_cast<void *>(p));
     v.pinned = host_pinned(p);
+    v.device = !v.pinned && is_device_ptr(p);
     return v;
   }
   static HostView classes(const void *const *ptrs, const uint64_t *offs, int nclass, size_t es) {
@@ -174,8 +185,11 @@ struct HostView {
     for (int l = 0; l < nclass; ++l) {
       v.seg.push_back(static_cast<char *>(const_cast<void *>(ptrs[l])));
       v.off.push_back(offs[l]);
-      if (offs[l + 1] > offs[l] && !host_pinned(ptrs[l]))
+      if (offs[l + 1] > offs[l] && !host_pinned(ptrs[l])) {
         v.pinned = false;
+        if (is_device_ptr(ptrs[l]))
+          v.device = true;
+      }
     }
     v.off.push_back(offs[nclass]);
     return v;

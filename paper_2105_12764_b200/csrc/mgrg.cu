@@ -2067,7 +2067,17 @@ static std::vector<uint64_t> class_offsets(const mgrg_plan *p) {
   return off;
 }
 
+static mgrg_status host_views_ok(const HostView &a, const HostView &b) {
+  if (a.device || b.device)
+    return fail(MGRG_INVALID_ARGUMENT,
+                "device pointer passed to a host-buffer entry point (use mgrg_decompose / "
+                "mgrg_recompose for device buffers)");
+  return MGRG_OK;
+}
+
 static mgrg_status host_decompose(mgrg_plan *p, const HostView &hin, const HostView &hcls) {
+  if (mgrg_status st = host_views_ok(hin, hcls))
+    return st;
   DeviceGuard guard(p->device);
   if (mgrg_status st = ensure_stage(p))
     return st;
@@ -2091,6 +2101,8 @@ static mgrg_status host_decompose(mgrg_plan *p, const HostView &hin, const HostV
 
 static mgrg_status host_recompose(mgrg_plan *p, const HostView &hcls, int32_t k,
                                   const HostView &hout) {
+  if (mgrg_status st = host_views_ok(hcls, hout))
+    return st;
   DeviceGuard guard(p->device);
   if (mgrg_status st = ensure_stage(p))
     return st;

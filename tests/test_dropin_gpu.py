@@ -237,3 +237,20 @@ def test_host_classes_entry_points_reject_null_class():
     with pytest.raises(errors.Error):
         _lib.check(_lib.lib().mgrg_decompose_host_classes(plan._h, v.ctypes.data, ptrs))
     plan.close()
+
+
+def test_host_entry_points_reject_device_pointers():
+    import torch
+
+    from paper_2105_12764_b200 import Plan, _lib, errors
+
+    shape = (17, 9, 9)
+    plan = Plan(shape, "float32", device=0)
+    d = torch.rand(int(np.prod(shape)), device="cuda")
+    h = np.empty(int(np.prod(shape)), dtype=np.float32)
+    with pytest.raises(errors.Error, match="device pointer"):
+        _lib.check(_lib.lib().mgrg_decompose_host(plan._h, d.data_ptr(), h.ctypes.data))
+    with pytest.raises(errors.Error, match="device pointer"):
+        _lib.check(_lib.lib().mgrg_recompose_host(plan._h, h.ctypes.data, plan.levels,
+                                                  d.data_ptr()))
+    plan.close()
