@@ -2075,10 +2075,8 @@ static mgrg_status host_views_ok(const HostView &a, const HostView &b) {
   return MGRG_OK;
 }
 
-static mgrg_status host_decompose(mgrg_plan *p, const HostView &hin, const HostView &hcls) {
-  if (mgrg_status st = host_views_ok(hin, hcls))
-    return st;
-  DeviceGuard guard(p->device);
+static mgrg_status host_decompose_impl(mgrg_plan *p, const HostView &hin,
+                                       const HostView &hcls) {
   if (mgrg_status st = ensure_stage(p))
     return st;
   if (p->deferred)
@@ -2099,11 +2097,8 @@ static mgrg_status host_decompose(mgrg_plan *p, const HostView &hin, const HostV
   return MGRG_OK;
 }
 
-static mgrg_status host_recompose(mgrg_plan *p, const HostView &hcls, int32_t k,
-                                  const HostView &hout) {
-  if (mgrg_status st = host_views_ok(hcls, hout))
-    return st;
-  DeviceGuard guard(p->device);
+static mgrg_status host_recompose_impl(mgrg_plan *p, const HostView &hcls, int32_t k,
+                                       const HostView &hout) {
   if (mgrg_status st = ensure_stage(p))
     return st;
   if (k == p->H.L && (p->dtype == MGRG_F32 ? pipelined_ok<float>(p) : pipelined_ok<double>(p)))
@@ -2120,6 +2115,44 @@ static mgrg_status host_recompose(mgrg_plan *p, const HostView &hcls, int32_t k,
   CUDA_TRY(X.drain());
   CUDA_TRY(cudaStreamSynchronize(p->own_stream));
   return MGRG_OK;
+}
+// On failure nothing queued may still touch the caller's buffers after the
+// call returns: queued downloads are drained and the copy streams synced
+// (their own errors are secondary to the one reported).
+static void host_quiesce(mgrg_plan *p) {
+  if (p->xfer)
+    (void)p->xfer->drain();
+  for (cudaStream_t q : {p->s_in, p->s_out, p->own_stream})
+    if (q)
+      (void)cudaStreamSynchronize(q);
+  cudaGetLastError();
+}
+
+static mgrg_status host_decompose(mgrg_plan *p, const HostView &hin, const HostView &hcls) {
+  if (mgrg_status st = host_views_ok(hin, hcls))
+    return st;
+  DeviceGuard guard(p->device);
+  const mgrg_status st = host_decompose_impl(p, hin, hcls);
+  if (st != MGRG_OK) {
+    const std::string msg = g_last_error;
+    host_quiesce(p);
+    g_last_error = msg;
+  }
+  return st;
+}
+
+static mgrg_status host_recompose(mgrg_plan *p, const HostView &hcls, int32_t k,
+                                  const HostView &hout) {
+  if (mgrg_status st = host_views_ok(hcls, hout))
+    return st;
+  DeviceGuard guard(p->device);
+  const mgrg_status st = host_recompose_impl(p, hcls, k, hout);
+  if (st != MGRG_OK) {
+    const std::string msg = g_last_error;
+    host_quiesce(p);
+    g_last_error = msg;
+  }
+  return st;
 }
 } // extern "C++"
 
