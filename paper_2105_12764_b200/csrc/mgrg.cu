@@ -886,9 +886,12 @@ bool try_scan(int kd, const ThomasGeom<R> &t, uint64_t S, uint64_t inner, uint64
 template <typename R> constexpr size_t tf_limit() { return 224 * 1024; }
 
 // small coarse lattices: one CTA solves every dimension (thomas_small_kernel)
+#ifndef TS_SMEM_KB
+#define TS_SMEM_KB 96
+#endif
 template <typename R> bool ts_fits(const LevelGeom<R> &g) {
   return g_thomas_small &&
-         ts_smem<R>(g.coarse_nodes(), uint64_t(g.m[0]) + g.m[1] + g.m[2]) <= 96 * 1024;
+         ts_smem<R>(g.coarse_nodes(), uint64_t(g.m[0]) + g.m[1] + g.m[2]) <= size_t(TS_SMEM_KB) * 1024;
 }
 template <typename R>
 void launch_thomas_small(const LevelGeom<R> &g, const std::array<ThomasGeom<R>, 3> &t, R *f,
@@ -1104,7 +1107,7 @@ template <typename R> void set_thomas_attrs() {
   for (auto k : {thomas_exact_kernel<R, 0>, thomas_exact_kernel<R, 1>, thomas_exact_kernel<R, 2>})
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 74 * 1024);
   cudaFuncSetAttribute(thomas_small_kernel<R>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                       96 * 1024);
+                       TS_SMEM_KB * 1024);
 }
 
 template <typename R> R *ws(mgrg_plan *p, uint64_t off) {

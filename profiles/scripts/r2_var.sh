@@ -1,3 +1,6 @@
-TAG=${1:-r2aw}
+TAG=${1:-r2az}
 O=gpurun_out/$TAG; mkdir -p $O
-timeout 900 python -m pytest tests/test_dropin_gpu.py tests/test_capi.py tests/test_gpu_parity.py tests/test_cpp_shim.py -x -q -p no:cacheprovider > $O/t.log 2>&1; echo rc=$? >> $O/t.log
+timeout 300 python profiles/scripts/tail_probe.py > $O/tail_base.json 2>&1
+for v in ts24 ts8 ts0; do
+MGRG_LIB=$PWD/paper_2105_12764_b200/variants/libmgrg_$v.so timeout 300 python profiles/scripts/tail_probe.py > $O/tail_$v.json 2>&1
+done
