@@ -430,14 +430,21 @@ RefactoredData<Real> decompose(const TensorGrid<Real> &grid,
   out.shape = grid.shape;
   out.coords = grid.coords;
   out.levels = std::size_t(L);
-  // the classes are written in place, one host buffer per class
+  // upload + device work first, the class vectors allocated meanwhile, then
+  // the classes written in place, one host buffer per class
+  b200_detail::check(mgrg_decompose_host_begin(p, grid.values.data()));
   std::vector<void *> dst(std::size_t(L) + 1);
-  out.classes.resize(std::size_t(L) + 1);
-  for (int l = 0; l <= L; ++l) {
-    out.classes[l] = b200_detail::make_output_vector<Real>(off[l + 1] - off[l]);
-    dst[l] = out.classes[l].data();
+  try {
+    out.classes.resize(std::size_t(L) + 1);
+    for (int l = 0; l <= L; ++l) {
+      out.classes[l] = b200_detail::make_output_vector<Real>(off[l + 1] - off[l]);
+      dst[l] = out.classes[l].data();
+    }
+  } catch (...) {
+    mgrg_host_abort(p);
+    throw;
   }
-  b200_detail::check(mgrg_decompose_host_classes(p, grid.values.data(), dst.data()));
+  b200_detail::check(mgrg_decompose_host_end(p, dst.data()));
   if (opt.stats)
     b200_detail::fill_stats(*opt.stats, p, grid.shape.size(), false);
   return out;
@@ -470,12 +477,17 @@ TensorGrid<Real> recompose(const RefactoredData<Real> &r, std::size_t classes_us
                        std::to_string(off[l + 1] - off[l]));
     src[l] = r.classes[l].data();
   }
+  b200_detail::check(mgrg_recompose_host_begin(p, src.data(), int32_t(classes_used)));
   TensorGrid<Real> g;
-  g.shape = r.shape;
-  g.coords = r.coords;
-  g.values = b200_detail::make_output_vector<Real>(num_elements(r.shape));
-  b200_detail::check(mgrg_recompose_host_classes(p, src.data(), int32_t(classes_used),
-                                                 g.values.data()));
+  try {
+    g.shape = r.shape;
+    g.coords = r.coords;
+    g.values = b200_detail::make_output_vector<Real>(num_elements(r.shape));
+  } catch (...) {
+    mgrg_host_abort(p);
+    throw;
+  }
+  b200_detail::check(mgrg_recompose_host_end(p, g.values.data()));
   if (opt.stats)
     b200_detail::fill_stats(*opt.stats, p, r.shape.size(), true);
   return g;

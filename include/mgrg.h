@@ -133,6 +133,19 @@ mgrg_status mgrg_decompose_host_classes(mgrg_plan *plan, const void *h_values,
                                         void *const *h_classes);
 mgrg_status mgrg_recompose_host_classes(mgrg_plan *plan, const void *const *h_classes,
                                         int32_t classes_used, void *h_values);
+/* Split forms for callers that allocate their outputs while the device works:
+ * _begin uploads the inputs and enqueues the device path into the plan's
+ * staging, then returns; _end writes the outputs (same buffer conventions as
+ * the _classes / flat forms above) and waits.  One split call per plan at a
+ * time (a second _begin, or an _end without its _begin, is
+ * MGRG_INVALID_ARGUMENT); no other call may use the plan in between. */
+mgrg_status mgrg_decompose_host_begin(mgrg_plan *plan, const void *h_values);
+mgrg_status mgrg_decompose_host_end(mgrg_plan *plan, void *const *h_classes);
+mgrg_status mgrg_recompose_host_begin(mgrg_plan *plan, const void *const *h_classes,
+                                      int32_t classes_used);
+mgrg_status mgrg_recompose_host_end(mgrg_plan *plan, void *h_values);
+/* Abandon a split call between _begin and _end (waits for its device work). */
+mgrg_status mgrg_host_abort(mgrg_plan *plan);
 
 /* ---- unit-level kernels (kernels.hpp), device buffers, for parity ---------
  * compute_coefficients / restore_coefficients (kernels.hpp:284-310): in place

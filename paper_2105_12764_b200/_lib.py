@@ -22,7 +22,9 @@ EXPORTS = (
     "mgrg_plan_create", "mgrg_plan_destroy", "mgrg_plan_levels",
     "mgrg_plan_class_offsets", "mgrg_plan_level_shape", "mgrg_plan_sizes",
     "mgrg_decompose", "mgrg_recompose", "mgrg_decompose_host",
-    "mgrg_recompose_host", "mgrg_decompose_host_classes", "mgrg_recompose_host_classes", "mgrg_gpk", "mgrg_masstrans", "mgrg_solve",
+    "mgrg_recompose_host", "mgrg_decompose_host_classes", "mgrg_recompose_host_classes",
+    "mgrg_decompose_host_begin", "mgrg_decompose_host_end", "mgrg_recompose_host_begin",
+    "mgrg_recompose_host_end", "mgrg_host_abort", "mgrg_gpk", "mgrg_masstrans", "mgrg_solve",
     "mgrg_apply_correction", "mgrg_reorder", "mgrg_last_error",
     "mgrg_coop_level", "mgrg_coop_thomas_z", "mgrg_plan_level_buffer",
     "mgrg_cooperative_decompose_host",
@@ -108,6 +110,11 @@ def lib() -> ctypes.CDLL:
             "mgrg_recompose_host": [vp, vp, i32, vp],
             "mgrg_decompose_host_classes": [vp, vp, vp],
             "mgrg_recompose_host_classes": [vp, vp, i32, vp],
+            "mgrg_decompose_host_begin": [vp, vp],
+            "mgrg_decompose_host_end": [vp, vp],
+            "mgrg_recompose_host_begin": [vp, vp, i32],
+            "mgrg_recompose_host_end": [vp, vp],
+            "mgrg_host_abort": [vp],
             "mgrg_gpk": [vp, i32, i32, vp, vp],
             "mgrg_masstrans": [vp, i32, i32, vp, vp, i32, vp, vp],
             "mgrg_solve": [vp, i32, i32, vp, vp],

@@ -239,6 +239,7 @@ struct mgrg_plan {
   size_t prof_used = 0;
   // CUDA-graph replay of the level loop (mgrg_plan_set_graphs): one
   // instantiated graph per (operation, buffers, k), most recent last
+  int split_op = 0; // host begin/end pair in flight: 1 decompose, 2 recompose
   bool graphs = false;
   struct Graph {
     int op; // 0 decompose, 1 recompose
@@ -2223,6 +2224,167 @@ mgrg_status mgrg_recompose_host_classes(mgrg_plan *p, const void *const *h_class
   DeviceGuard guard(p->device);
   return host_recompose(p, HostView::classes(h_classes, off.data(), k + 1, p->esize), k,
                         HostView::of(h_values, p->esize));
+}
+
+// ---- split host calls (begin / end) --------------------------------------
+// The caller allocates its outputs between the two: _begin uploads the
+// inputs (pageable ones through the plan's rings, by the calling thread) and
+// enqueues the device path into the plan's staging; _end downloads into the
+// caller's buffers and waits.  The drop-in overlaps the reference API's
+// output allocation with the upload and the device work this way.
+static mgrg_status split_begin_check(mgrg_plan *p) {
+  if (p->split_op)
+    return fail(MGRG_INVALID_ARGUMENT, "a split host call is already in flight on this plan");
+  return MGRG_OK;
+}
+
+mgrg_status mgrg_decompose_host_begin(mgrg_plan *p, const void *h_values) {
+  g_last_error.clear();
+  if (mgrg_status st = check_plan(p))
+    return st;
+  if (mgrg_status st = split_begin_check(p))
+    return st;
+  if (!h_values)
+    return fail(MGRG_INVALID_ARGUMENT, "null host buffer");
+  const HostView hin = HostView::of(h_values, p->esize);
+  if (mgrg_status st = host_views_ok(hin, hin))
+    return st;
+  DeviceGuard guard(p->device);
+  if (mgrg_status st = ensure_stage(p))
+    return st;
+  if (p->deferred)
+    return fail(p->deferred, p->deferred_msg);
+  const uint64_t n = p->nodes[p->H.L];
+  char *din = static_cast<char *>(p->d_stage), *dout = din + stage_half(p) * p->esize;
+  mgrg_status st = MGRG_OK;
+  if (cudaError_t e = p->xfer->upload(din, hin, 0, n, p->own_stream))
+    st = fail(MGRG_CUDA_ERROR, cudaGetErrorString(e));
+  if (!st)
+    st = mgrg_decompose(p, din, dout, p->own_stream);
+  if (!st)
+    if (cudaError_t e = cudaEventRecord(p->ev_done, p->own_stream))
+      st = fail(MGRG_CUDA_ERROR, cudaGetErrorString(e));
+  if (st) {
+    const std::string msg = g_last_error;
+    host_quiesce(p);
+    g_last_error = msg;
+    return st;
+  }
+  p->split_op = 1;
+  return MGRG_OK;
+}
+
+mgrg_status mgrg_decompose_host_end(mgrg_plan *p, void *const *h_classes) {
+  g_last_error.clear();
+  if (mgrg_status st = check_plan(p))
+    return st;
+  if (p->split_op != 1)
+    return fail(MGRG_INVALID_ARGUMENT, "no mgrg_decompose_host_begin in flight on this plan");
+  if (!h_classes)
+    return fail(MGRG_INVALID_ARGUMENT, "null host buffer");
+  const std::vector<uint64_t> off = class_offsets(p);
+  for (int l = 0; l <= p->H.L; ++l)
+    if (!h_classes[l] && off[size_t(l) + 1] > off[size_t(l)])
+      return fail(MGRG_INVALID_ARGUMENT, "null class buffer " + std::to_string(l));
+  const HostView hcls = HostView::classes(h_classes, off.data(), p->H.L + 1, p->esize);
+  if (mgrg_status st = host_views_ok(hcls, hcls))
+    return st;
+  DeviceGuard guard(p->device);
+  p->split_op = 0;
+  const char *dout = static_cast<const char *>(p->d_stage) + stage_half(p) * p->esize;
+  mgrg_status st = MGRG_OK;
+  cudaError_t e = p->xfer->download(hcls, 0, p->nodes[p->H.L], dout, p->ev_done);
+  if (!e)
+    e = p->xfer->drain();
+  if (!e)
+    e = cudaStreamSynchronize(p->own_stream);
+  if (e) {
+    st = fail(MGRG_CUDA_ERROR, cudaGetErrorString(e));
+    const std::string msg = g_last_error;
+    host_quiesce(p);
+    g_last_error = msg;
+  }
+  return st;
+}
+
+mgrg_status mgrg_recompose_host_begin(mgrg_plan *p, const void *const *h_classes, int32_t k) {
+  g_last_error.clear();
+  if (mgrg_status st = check_plan(p))
+    return st;
+  if (mgrg_status st = split_begin_check(p))
+    return st;
+  if (!h_classes)
+    return fail(MGRG_INVALID_ARGUMENT, "null host buffer");
+  if (mgrg_status st = check_level_arg(p, k))
+    return st;
+  const std::vector<uint64_t> off = class_offsets(p);
+  for (int l = 0; l <= k; ++l)
+    if (!h_classes[l] && off[size_t(l) + 1] > off[size_t(l)])
+      return fail(MGRG_INVALID_ARGUMENT, "null class buffer " + std::to_string(l));
+  const HostView hcls = HostView::classes(h_classes, off.data(), k + 1, p->esize);
+  if (mgrg_status st = host_views_ok(hcls, hcls))
+    return st;
+  DeviceGuard guard(p->device);
+  if (mgrg_status st = ensure_stage(p))
+    return st;
+  char *din = static_cast<char *>(p->d_stage), *dout = din + stage_half(p) * p->esize;
+  mgrg_status st = MGRG_OK;
+  // only classes 0..k are read (refactor.hpp:483-485)
+  if (cudaError_t e = p->xfer->upload(din, hcls, 0, p->nodes[k], p->own_stream))
+    st = fail(MGRG_CUDA_ERROR, cudaGetErrorString(e));
+  if (!st)
+    st = mgrg_recompose(p, din, k, dout, p->own_stream);
+  if (!st)
+    if (cudaError_t e = cudaEventRecord(p->ev_done, p->own_stream))
+      st = fail(MGRG_CUDA_ERROR, cudaGetErrorString(e));
+  if (st) {
+    const std::string msg = g_last_error;
+    host_quiesce(p);
+    g_last_error = msg;
+    return st;
+  }
+  p->split_op = 2;
+  return MGRG_OK;
+}
+
+mgrg_status mgrg_recompose_host_end(mgrg_plan *p, void *h_values) {
+  g_last_error.clear();
+  if (mgrg_status st = check_plan(p))
+    return st;
+  if (p->split_op != 2)
+    return fail(MGRG_INVALID_ARGUMENT, "no mgrg_recompose_host_begin in flight on this plan");
+  if (!h_values)
+    return fail(MGRG_INVALID_ARGUMENT, "null host buffer");
+  const HostView hout = HostView::of(h_values, p->esize);
+  if (mgrg_status st = host_views_ok(hout, hout))
+    return st;
+  DeviceGuard guard(p->device);
+  p->split_op = 0;
+  const char *dout = static_cast<const char *>(p->d_stage) + stage_half(p) * p->esize;
+  mgrg_status st = MGRG_OK;
+  cudaError_t e = p->xfer->download(hout, 0, p->nodes[p->H.L], dout, p->ev_done);
+  if (!e)
+    e = p->xfer->drain();
+  if (!e)
+    e = cudaStreamSynchronize(p->own_stream);
+  if (e) {
+    st = fail(MGRG_CUDA_ERROR, cudaGetErrorString(e));
+    const std::string msg = g_last_error;
+    host_quiesce(p);
+    g_last_error = msg;
+  }
+  return st;
+}
+
+mgrg_status mgrg_host_abort(mgrg_plan *p) {
+  g_last_error.clear();
+  if (mgrg_status st = check_plan(p))
+    return st;
+  DeviceGuard guard(p->device);
+  if (p->split_op)
+    host_quiesce(p);
+  p->split_op = 0;
+  return MGRG_OK;
 }
 
 // ---- unit-level kernels ------------------------------------------------

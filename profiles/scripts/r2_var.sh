@@ -1,6 +1,6 @@
-TAG=${1:-r2az}
+TAG=${1:-r2ba}
 O=gpurun_out/$TAG; mkdir -p $O
-timeout 300 python profiles/scripts/tail_probe.py > $O/tail_base.json 2>&1
-for v in ts24 ts8 ts0; do
-MGRG_LIB=$PWD/paper_2105_12764_b200/variants/libmgrg_$v.so timeout 300 python profiles/scripts/tail_probe.py > $O/tail_$v.json 2>&1
-done
+timeout 900 python -m pytest tests/test_dropin_gpu.py tests/test_capi.py tests/test_cpp_shim.py -x -q -p no:cacheprovider > $O/t.log 2>&1; echo rc=$? >> $O/t.log
+g++ -std=c++17 -O2 -Iinclude tests/cpp/bench_dropin.cpp -Lpaper_2105_12764_b200 -lmgrg -pthread -Wl,-rpath,$PWD/paper_2105_12764_b200 -o /tmp/bench_dropin
+timeout 300 /tmp/bench_dropin 1025 2 1 0 > $O/dropin.jsonl 2>&1
+timeout 300 /tmp/bench_dropin 1025 2 1 1 >> $O/dropin.jsonl 2>&1

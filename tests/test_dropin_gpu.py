@@ -254,3 +254,43 @@ def test_host_entry_points_reject_device_pointers():
         _lib.check(_lib.lib().mgrg_recompose_host(plan._h, h.ctypes.data, plan.levels,
                                                   d.data_ptr()))
     plan.close()
+
+
+@pytest.mark.parametrize("shape", [(129, 129, 257), (33, 17, 9)], ids=["large", "small"])
+def test_split_host_calls(shape):
+    """mgrg_*_host_begin / _end (the drop-in allocates its outputs in between)
+    equal the one-shot host calls; misuse is InvalidArgument; abort clears."""
+    import ctypes
+
+    import torch
+
+    from paper_2105_12764_b200 import Plan, _lib, errors
+
+    lib = _lib.lib()
+    rng = np.random.default_rng(11)
+    v = rng.random(int(np.prod(shape))).astype(np.float32)
+    plan = Plan(shape, "float32", fast=True, device=0)
+    L = plan.levels
+    ref = plan.decompose(torch.from_numpy(v).cuda()).cpu().numpy()
+    sl = plan.class_slices()
+    cls = [np.full(s.stop - s.start, np.nan, dtype=np.float32) for s in sl]
+    ptrs = (ctypes.c_void_p * len(cls))(*[c.ctypes.data for c in cls])
+    _lib.check(lib.mgrg_decompose_host_begin(plan._h, v.ctypes.data))
+    with pytest.raises(errors.Error, match="already in flight"):
+        _lib.check(lib.mgrg_decompose_host_begin(plan._h, v.ctypes.data))
+    _lib.check(lib.mgrg_decompose_host_end(plan._h, ptrs))
+    assert np.array_equal(np.concatenate(cls), ref)
+    with pytest.raises(errors.Error, match="no mgrg_decompose_host_begin"):
+        _lib.check(lib.mgrg_decompose_host_end(plan._h, ptrs))
+    for k in (L - 1, L):
+        want = plan.recompose(torch.from_numpy(ref).cuda(), k).cpu().numpy()
+        out = np.full_like(v, np.nan)
+        _lib.check(lib.mgrg_recompose_host_begin(plan._h, ptrs, k))
+        _lib.check(lib.mgrg_recompose_host_end(plan._h, out.ctypes.data))
+        assert np.array_equal(out, want)
+    # abandoned split call: abort, then the plan is usable again
+    _lib.check(lib.mgrg_recompose_host_begin(plan._h, ptrs, L))
+    _lib.check(lib.mgrg_host_abort(plan._h))
+    out = np.empty_like(v)
+    _lib.check(lib.mgrg_recompose_host(plan._h, ref.ctypes.data, L, out.ctypes.data))
+    plan.close()
