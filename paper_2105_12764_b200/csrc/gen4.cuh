@@ -101,25 +101,6 @@ __device__ __forceinline__ void gen_decode_f(uint64_t i, const FastDiv *f, uint3
   }
 }
 
-__device__ __forceinline__ void gen_decode(uint64_t i, const uint32_t *e, uint32_t *p) {
-  if ((i >> 32) == 0) { // 32-bit divisions (a 64-bit one is a long call)
-    uint32_t j = uint32_t(i);
-#pragma unroll
-    for (int d = 0; d < kGenDims - 1; ++d) {
-      const uint32_t qd = j / e[d];
-      p[d] = j - qd * e[d];
-      j = qd;
-    }
-    p[kGenDims - 1] = j;
-    return;
-  }
-#pragma unroll
-  for (int d = 0; d < kGenDims; ++d) {
-    p[d] = uint32_t(i % e[d]);
-    i /= e[d];
-  }
-}
-
 template <typename R>
 __device__ __forceinline__ unsigned gen_mask(const Gen4Geom<R> &g, const uint32_t *p) {
   unsigned mask = 0;

@@ -4,7 +4,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <vector>
-#include "../../../paper_2105_12764_b200/csrc/tma.cuh"
+#include "tma.cuh"
 using namespace mgrg;
 __global__ void k(const __grid_constant__ CUtensorMap m, int c, double *out) {
   __shared__ __align__(128) double buf[32];

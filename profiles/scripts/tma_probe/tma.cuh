@@ -1,4 +1,5 @@
-// tma.cuh -- Tensor Memory Accelerator plumbing for the lean level kernels.
+// tma.cuh -- Tensor Memory Accelerator plumbing of the TMA probe (probe.cu); not part of
+// the library: the probe showed why TMA does not fit the lean kernels.
 //
 // Every level array and class-type row of a dyadic hierarchy has an ODD
 // pitch (2^k + 1 or 2^k elements at arbitrary offsets), so 2-D/3-D tensor
