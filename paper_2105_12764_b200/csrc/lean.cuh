@@ -642,8 +642,13 @@ __global__ void __launch_bounds__(32 * kLeanWPB, !FAST ? (sizeof(R) == 4 ? LEAN_
 #ifndef LEAN_RL_MINB_F64
 #define LEAN_RL_MINB_F64 2 // measured (1025^2 x 513 f64, L9): MINB 3 (168 regs, spills) 1.13 ms, 2 (246) 1.07
 #endif
-template <typename R> __host__ __device__ constexpr int lean_ty_rl() {
-  return sizeof(R) == 4 ? LEAN_RL_TY : LEAN_RL_TY_F64; // taller band: fewer halo rows (no W registers here)
+#ifndef LEAN_RL_TY_EXACT
+#define LEAN_RL_TY_EXACT 5 // exact f32 at 1025^3 L10: TY 6 3.41 ms (spills), 5 2.74, 4 2.82, 3 3.02
+#endif
+template <typename R, bool FAST = true> __host__ __device__ constexpr int lean_ty_rl() {
+  // taller band: fewer halo rows (no W registers here); the exact policy's
+  // unfused stencils keep more temporaries live
+  return sizeof(R) == 4 ? (FAST ? LEAN_RL_TY : LEAN_RL_TY_EXACT) : LEAN_RL_TY_F64;
 }
 
 template <typename R, bool Z3, bool FAST>
@@ -654,7 +659,7 @@ __global__ void __launch_bounds__(32 * kLeanWPB, !FAST ? (sizeof(R) == 4 ? LEAN_
                       const Stencil<R> *__restrict__ szt, const R *__restrict__ cls,
                       R *__restrict__ f, LeanTiles tl) {
   pdl_wait();
-  constexpr int TY = lean_ty_rl<R>(), NR = 2 * TY + 3;
+  constexpr int TY = lean_ty_rl<R, FAST>(), NR = 2 * TY + 3;
   const int lane = threadIdx.x & 31;
   const uint64_t wid = uint64_t(blockIdx.x) * kLeanWPB + (threadIdx.x >> 5);
   if (wid >= tl.warps())
@@ -1054,10 +1059,12 @@ template <typename R> LeanTiles lean_tiles(uint32_t m0, uint32_t m1, uint32_t m2
   return t;
 }
 
-template <typename R> LeanTiles lean_rtiles(uint32_t m0, uint32_t m1, uint32_t m2, bool z3) {
+template <typename R>
+LeanTiles lean_rtiles(uint32_t m0, uint32_t m1, uint32_t m2, bool z3, bool fast = true) {
   LeanTiles t;
   t.ntx = (m0 + kLeanOut - 1) / kLeanOut;
-  t.nty = (m1 + lean_ty_rl<R>() - 1) / lean_ty_rl<R>();
+  const int ty = fast ? lean_ty_rl<R, true>() : lean_ty_rl<R, false>();
+  t.nty = (m1 + ty - 1) / ty;
   // longer chunks for the load-vector kernel: fewer halo planes re-read
   // (measured 1.205 -> 1.172 ms at 1025^3 f32; the other two are faster at 32)
   t.zc = lean_zc(uint64_t(t.ntx) * t.nty, m2, z3, 2 * kLeanZC);

@@ -786,7 +786,7 @@ void launch_lean_rload(bool fast, const LevelGeom<R> &g,
                        const std::array<const Stencil<R> *, 3> &sc, const R *cls, R *f,
                        cudaStream_t s) {
   const bool z3 = g.n[2] > 1;
-  const LeanTiles t = lean_rtiles<R>(g.m[0], g.m[1], g.m[2], z3);
+  const LeanTiles t = lean_rtiles<R>(g.m[0], g.m[1], g.m[2], z3, fast);
   const unsigned blocks = unsigned((t.warps() + kLeanWPB - 1) / kLeanWPB);
   auto k = z3 ? (fast ? lean_rload_kernel<R, true, true> : lean_rload_kernel<R, true, false>)
               : (fast ? lean_rload_kernel<R, false, true> : lean_rload_kernel<R, false, false>);
@@ -1985,7 +1985,7 @@ mgrg_status recompose_host_pipelined(mgrg_plan *p, const HostView &hcls, const H
   // class L by rload chunk groups, each uploaded one group ahead of the
   // finest load-vector kernel that reads it: chunk range [c0, c1) reads class
   // ranks c0-1 .. c1 (the next group's first rank)
-  const LeanTiles tr = lean_rtiles<R>(g.m[0], g.m[1], m2, true);
+  const LeanTiles tr = lean_rtiles<R>(g.m[0], g.m[1], m2, true, p->fast);
   const int G = int(std::min<uint32_t>(tr.ntz, 16));
   auto rchunk0 = [&](int q) { return uint32_t((uint64_t(q) * tr.ntz) / G); };
   int uploaded = 0;

@@ -1,6 +1,6 @@
-TAG=${1:-r2be}
+TAG=${1:-r2bh}
 O=gpurun_out/$TAG; mkdir -p $O
-for v in base t3m4 t2m4 t2m5; do
-  if [ $v = base ]; then L=""; else L=$PWD/paper_2105_12764_b200/variants/libmgrg_$v.so; fi
-  MGRG_LIB=$L timeout 300 python profiles/scripts/levels.py > $O/levels_c4_$v.txt 2>&1
-done
+timeout 1500 python -m pytest tests -m gpu -x -q -p no:cacheprovider > $O/gputest.log 2>&1; echo rc=$? >> $O/gputest.log
+timeout 300 python profiles/scripts/levels.py --exact > $O/levels_c4x.txt 2>&1
+timeout 300 python profiles/scripts/levels.py --exact --shape 1025,1025,513 --dtype float64 > $O/levels_c5x.txt 2>&1
+timeout 300 python profiles/scripts/levels.py > $O/levels_c4.txt 2>&1
