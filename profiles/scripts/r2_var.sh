@@ -1,6 +1,6 @@
-TAG=${1:-r2bh}
+TAG=${1:-r2bi}
 O=gpurun_out/$TAG; mkdir -p $O
-timeout 1500 python -m pytest tests -m gpu -x -q -p no:cacheprovider > $O/gputest.log 2>&1; echo rc=$? >> $O/gputest.log
-timeout 300 python profiles/scripts/levels.py --exact > $O/levels_c4x.txt 2>&1
-timeout 300 python profiles/scripts/levels.py --exact --shape 1025,1025,513 --dtype float64 > $O/levels_c5x.txt 2>&1
-timeout 300 python profiles/scripts/levels.py > $O/levels_c4.txt 2>&1
+for v in base e2m4 e2m5 e4m3 e4m4; do
+  if [ $v = base ]; then L=""; else L=$PWD/paper_2105_12764_b200/variants/libmgrg_$v.so; fi
+  MGRG_LIB=$L timeout 300 python profiles/scripts/levels.py --exact > $O/levels_c4x_$v.txt 2>&1
+done
