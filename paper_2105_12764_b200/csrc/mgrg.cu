@@ -35,6 +35,7 @@
 #include "lean.cuh"
 #include "thomas_fiber.cuh"
 #include "thomas_exact.cuh"
+#include "thomas_2pass.cuh"
 #include "gen4.cuh"
 #include "hostio.cuh"
 
@@ -187,6 +188,7 @@ template <typename R> struct PlanT {
   std::vector<std::array<const Stencil<R> *, 3>> sten; // [l][kd] merged R*M tables
   std::vector<std::array<const LeanW<R> *, 3>> lean;   // [l][kd] lean tables (padded)
   std::vector<std::array<ThomasLean<R>, 3>> tlean;     // [l][kd] chunked Thomas tables
+  std::vector<std::array<ThomasTP<R>, 3>> ttp;         // [l][kd] two-pass long-fiber tables
   std::vector<Gen4Geom<R>> g4;                         // [l] 4-D levels (gen4.cuh)
   R *d_geom = nullptr;
 };
@@ -220,6 +222,7 @@ struct mgrg_plan {
   void *d_ws = nullptr; // [A: N_{L-1}][B: N_{L-2}][F: N_{L-1}]
   size_t ws_bytes = 0;
   uint64_t offA = 0, offB = 0, offF = 0; // element offsets inside d_ws
+  uint64_t offTP = 0;                    // two-pass Thomas scratch (thomas_2pass.cuh)
   void *d_stage = nullptr;               // host-API staging (2N elements), lazy
   cudaStream_t own_stream = nullptr;
   cudaStream_t s_in = nullptr, s_out = nullptr; // host-API copy streams (pipelined path)
@@ -391,13 +394,21 @@ Stencil<R> make_stencil(const std::vector<double> &hd, const std::vector<double>
   return s;
 }
 
+int knob(const char *name, int dflt);
+// two-pass long-fiber Thomas (thomas_2pass.cuh) for FAST strided (y / z)
+// fibers of at least this many positions; the cluster kernel serves x fibers
+// and shorter ones.  Measured (profiles/r2/tuning/README.md, 8193^2 f64):
+// y at m = 4097 150 -> 112 us; at m = 2049 35 -> 40 us and x fibers at m =
+// 4097 124 -> 135 us (the DIM-0 passes transpose through shared memory).
+int g_tp_min = knob("MGRG_TP_MIN", 4097);
+
 template <typename R> mgrg_status upload_geometry(mgrg_plan *p) {
   const Hierarchy &H = p->H;
   const int L = H.L;
   // host staging of every per-level array in R, then one upload
   std::vector<R> buf;
   struct Ref {
-    size_t h[3], r[3], th[3], tf[3], ti[3], st[3], lw[3], tl[3];
+    size_t h[3], r[3], th[3], tf[3], ti[3], st[3], lw[3], tl[3], tp[3];
   };
   std::vector<Ref> refs(L + 1);
   auto push = [&](const std::vector<R> &v) {
@@ -410,7 +421,7 @@ template <typename R> mgrg_status upload_geometry(mgrg_plan *p) {
   for (int l = 1; l <= L; ++l) {
     for (int kd = 0; kd < 3; ++kd) {
       refs[l].h[kd] = refs[l].r[kd] = refs[l].th[kd] = refs[l].tf[kd] =
-          refs[l].ti[kd] = refs[l].st[kd] = refs[l].lw[kd] = refs[l].tl[kd] = size_t(-1);
+          refs[l].ti[kd] = refs[l].st[kd] = refs[l].lw[kd] = refs[l].tl[kd] = refs[l].tp[kd] = size_t(-1);
       const int ud = p->kmap[kd];
       if (ud < 0)
         continue;
@@ -479,6 +490,37 @@ template <typename R> mgrg_status upload_geometry(mgrg_plan *p) {
           }
           refs[l].tl[kd] = push(tl);
         }
+        if (kd != 0 && tf.size() >= size_t(g_tp_min) && tf.size() <= size_t(kTpC) * kTpMaxK) {
+          // two-pass long-fiber tables (thomas_2pass.cuh): {fwd, ip, g, 0} per
+          // position, {PF, Q, PB, 0} per 32-position chunk; products in fp64
+          // from the working-precision factors, rounded once
+          const uint32_t mm = uint32_t(tf.size()), K = (mm + kTpC - 1) / kTpC;
+          std::vector<R> tq(4 * size_t(mm) + 4 * size_t(K), R(0));
+          R *Q = tq.data(), *Ck = Q + 4 * size_t(mm);
+          for (uint32_t i = 0; i < mm; ++i) {
+            Q[4 * i] = tf[i];
+            Q[4 * i + 1] = ti[i];
+            Q[4 * i + 2] = (i + 1 < mm) ? R(-double(ti[i]) * double(th[i])) : R(0);
+          }
+          for (uint32_t k = 0; k < K; ++k) {
+            const uint32_t a = k * kTpC, b = std::min(mm, a + kTpC);
+            double pf = 1.0, pb = 1.0, x = 0.0;
+            std::vector<double> pfi(b - a);
+            for (uint32_t i = a; i < b; ++i) {
+              pf *= double(Q[4 * i]);
+              pfi[i - a] = pf;
+            }
+            for (uint32_t i = b; i > a; --i) {
+              const uint32_t j = i - 1;
+              x = double(Q[4 * j + 1]) * pfi[j - a] + (j + 1 < b ? double(Q[4 * j + 2]) * x : 0.0);
+              pb *= double(Q[4 * j + 2]);
+            }
+            Ck[4 * k] = R(pf);
+            Ck[4 * k + 1] = R(x);
+            Ck[4 * k + 2] = R(pb);
+          }
+          refs[l].tp[kd] = push(tq);
+        }
         // stencil table (raw bytes of Stencil<R>, a whole number of R's)
         const uint64_t n = H.ext[l][ud], m = H.ext[l - 1][ud];
         std::vector<R> raw(m * (sizeof(Stencil<R>) / sizeof(R)));
@@ -514,6 +556,7 @@ template <typename R> mgrg_status upload_geometry(mgrg_plan *p) {
   P.sten.assign(L + 1, {nullptr, nullptr, nullptr});
   P.lean.assign(L + 1, {nullptr, nullptr, nullptr});
   P.tlean.assign(L + 1, {});
+  P.ttp.assign(L + 1, {});
   for (int l = 1; l <= L; ++l) {
     LevelGeom<R> &g = P.geom[l];
     g.refine = 0;
@@ -538,6 +581,13 @@ template <typename R> mgrg_status upload_geometry(mgrg_plan *p) {
         const R *b0 = base + refs[l].tl[kd];
         q.m = mm;
         q.tab = b0;
+      }
+      if (refs[l].tp[kd] != size_t(-1)) {
+        ThomasTP<R> &q = P.ttp[l][kd];
+        q.m = g.m[kd];
+        q.K = (q.m + kTpC - 1) / kTpC;
+        q.q = base + refs[l].tp[kd];
+        q.ck = q.q + 4 * size_t(q.m);
       }
       P.lean[l][kd] = refs[l].lw[kd] == size_t(-1)
                           ? nullptr
@@ -1010,6 +1060,40 @@ void launch_tf(int kd, const ThomasLean<R> &tl, uint64_t nfib, uint32_t mx, uint
   auto k = kd == 0 ? tf_pick<R, 0>(ch) : (kd == 1 ? tf_pick<R, 1>(ch) : tf_pick<R, 2>(ch));
   launch_pdl(k, groups, kTfThreads, tf_smem<R>(kd, tl.m), s, f, tl, nfib, mx, my, epi, base, out);
 }
+template <typename R> uint64_t tp_scratch_elems(mgrg_plan *p) {
+  PlanT<R> &P = pt<R>(p);
+  uint64_t need = 0;
+  for (size_t l = 1; l < P.ttp.size(); ++l)
+    for (int kd = 0; kd < 3; ++kd)
+      if (P.ttp[l][kd].q) {
+        const LevelGeom<R> &g = P.geom[l];
+        const uint64_t nfib = g.coarse_nodes() / g.m[kd];
+        need = std::max(need, 2 * nfib * P.ttp[l][kd].K);
+      }
+  return need;
+}
+template <typename R> void tp_bind_scratch(mgrg_plan *p) {
+  PlanT<R> &P = pt<R>(p);
+  for (size_t l = 1; l < P.ttp.size(); ++l)
+    for (int kd = 0; kd < 3; ++kd)
+      if (P.ttp[l][kd].q)
+        P.ttp[l][kd].scratch = static_cast<R *>(p->d_ws) + p->offTP;
+}
+// Two-pass long-fiber solve: pass 1 (chunk summaries), carry scans, pass 2
+// (chunk re-solve + epilogue); E / S scratch = 2 * nfib * K elements.
+template <typename R>
+void launch_tp(int kd, const ThomasTP<R> &tp, R *scratch, uint64_t nfib, uint32_t mx,
+               uint32_t my, Epi epi, const R *base, R *out, R *f, cudaStream_t s) {
+  R *E = scratch, *S = scratch + nfib * tp.K;
+  const dim3 grid(unsigned((nfib + 32 * kTpWarps - 1) / (32 * kTpWarps)), tp.K);
+  auto k1 = kd == 1 ? tp_pass1_kernel<R, 1> : tp_pass1_kernel<R, 2>;
+  launch_pdl(k1, grid, 32 * kTpWarps, 0, s, static_cast<const R *>(f), tp, nfib, mx, my, E, S);
+  launch_pdl(tp_carry_kernel<R>, unsigned((nfib + 31) / 32), 32 * kTcWarps, 0, s, tp, nfib, E,
+             S);
+  auto k2 = kd == 1 ? tp_pass2_kernel<R, 1> : tp_pass2_kernel<R, 2>;
+  launch_pdl(k2, grid, 32 * kTpWarps, 0, s, f, tp, nfib, mx, my, static_cast<const R *>(E),
+             static_cast<const R *>(S), epi, base, out);
+}
 template <typename R> void set_tf_attrs() {
   const int lim = int(tf_limit<R>());
   for (int ch : {1, 2, 3, 5, 9, 17, 33}) {
@@ -1037,8 +1121,13 @@ template <typename R> void set_tf_attrs() {
 template <typename R>
 void launch_thomas(bool fast, const LevelGeom<R> &g, const ThomasGeom<R> &t,
                    const ThomasLean<R> &tl, int kd, R *f, Epi epi, const R *base, R *out,
-                   cudaStream_t s) {
+                   cudaStream_t s, const ThomasTP<R> *tp = nullptr) {
   const uint64_t mx = g.m[0], my = g.m[1], mz = g.m[2];
+  if (fast && kd != 0 && tp && tp->q && tp->scratch && tp->m >= uint32_t(g_tp_min)) {
+    const uint64_t nfib = kd == 0 ? my * mz : (kd == 1 ? mx * mz : mx * my);
+    launch_tp<R>(kd, *tp, tp->scratch, nfib, uint32_t(mx), uint32_t(my), epi, base, out, f, s);
+    return;
+  }
   if (fast && tl.tab && tf_ch<R>(tl.m, kd) && tf_launch_smem<R>(kd, tl.m) <= tf_limit<R>() &&
       g_thomas_fiber) {
     const uint64_t nfib = kd == 0 ? my * mz : (kd == 1 ? mx * mz : mx * my);
@@ -1338,7 +1427,7 @@ mgrg_status run_decompose(mgrg_plan *p, const R *d_in, R *d_cls, cudaStream_t s,
       if (mgrg_status st = rec.begin(MGRG_K_THOMAS_X + kd, l, es * Cn * (last ? 3 : 2)))
         return st;
       launch_thomas<R>(p->fast, g, P.thom[l][kd], P.tlean[l][kd], kd, F,
-                       last ? Epi::add : Epi::none, Pout, Pout, s);
+                       last ? Epi::add : Epi::none, Pout, Pout, s, &P.ttp[l][kd]);
       if (mgrg_status st = rec.end())
         return st;
     }
@@ -1392,7 +1481,7 @@ mgrg_status run_recompose(mgrg_plan *p, const R *d_cls, int k, R *d_out,
         if (mgrg_status st = rec.begin(MGRG_K_THOMAS_X + kd, l, es * Cn * (last ? 3 : 2)))
           return st;
         launch_thomas<R>(p->fast, g, P.thom[l][kd], P.tlean[l][kd], kd, F,
-                         last ? Epi::sub : Epi::none, prev, F, s);
+                         last ? Epi::sub : Epi::none, prev, F, s, &P.ttp[l][kd]);
         if (mgrg_status st = rec.end())
           return st;
       }
@@ -1564,12 +1653,22 @@ mgrg_status mgrg_plan_create(const mgrg_grid_desc *desc, mgrg_plan **out) {
   p->offA = 0;
   p->offB = al(nA);
   p->offF = p->offB + al(nB);
-  p->ws_bytes = (p->offF + al(nA)) * p->esize;
+  // two-pass long-fiber Thomas scratch: the largest 2 * fibers * chunks
+  const uint64_t nTP = p->dtype == MGRG_F32 ? tp_scratch_elems<float>(p.get())
+                                            : tp_scratch_elems<double>(p.get());
+  p->offTP = p->offF + al(nA);
+  p->ws_bytes = (p->offTP + al(nTP)) * p->esize;
   cudaError_t e = cudaMalloc(&p->d_ws, p->ws_bytes);
   if (e != cudaSuccess) {
     cudaFree(p->d_geom);
     return fail(e == cudaErrorMemoryAllocation ? MGRG_OUT_OF_MEMORY : MGRG_CUDA_ERROR,
                 std::string("workspace allocation: ") + cudaGetErrorString(e));
+  }
+  if (nTP) {
+    if (p->dtype == MGRG_F32)
+      tp_bind_scratch<float>(p.get());
+    else
+      tp_bind_scratch<double>(p.get());
   }
   if (p->dtype == MGRG_F32) {
     set_smem_attrs<float, 32, 8>();
@@ -2026,7 +2125,7 @@ mgrg_status recompose_host_pipelined(mgrg_plan *p, const HostView &hcls, const H
     const int kd = p->refine_dims[i];
     const bool last = i == p->nrefine - 1;
     launch_thomas<R>(p->fast, g, P.thom[L][kd], P.tlean[L][kd], kd, F,
-                     last ? Epi::sub : Epi::none, prev, F, sc);
+                     last ? Epi::sub : Epi::none, prev, F, sc, &P.ttp[L][kd]);
   }
   CUDA_TRY(cudaGetLastError());
   // finest level per group, each group's planes [2c0, 2c1) down at once

@@ -194,6 +194,8 @@ def test_config5_block_1025sq_513_f64_full(oracle_mod):
 #   with 17-position chunks (x / y / z);
 # (5, 3, 4097): 2049-long z fibers (cluster, DIM 2);
 # (1025, 9, 17) / (9, 1025, 17): 513-long x / y fibers.
+# FAST y / z fibers of >= 4097 positions go through the two-pass solve
+# (thomas_2pass.cuh) instead of the clusters.
 TARGETED = [((17, 9, 1025), "float32"), ((17, 9, 1025), "float64"),
             ((8193, 9), "float64"), ((9, 8193), "float64"),
             ((8193, 9), "float32"), ((9, 8193), "float32"),
@@ -202,7 +204,13 @@ TARGETED = [((17, 9, 1025), "float32"), ((17, 9, 1025), "float64"),
             ((5, 3, 4097), "float32"),
             ((1025, 9, 17), "float32"), ((9, 1025, 17), "float32"),
             ((33, 17, 2049), "float32"), ((2049, 17, 9), "float64"),
-            ((9, 2049, 17), "float64")]
+            ((9, 2049, 17), "float64"),
+            # non-dyadic long fibers (1501 / 1251 / 1101 coarse positions:
+            # partial last chunk of the two-pass solve, thomas_2pass.cuh)
+            ((3000, 7), "float64"), ((7, 2500), "float32"), ((5, 3, 2200), "float64"),
+            # >= 4097-long y / z fibers: the two-pass solve, incl. a partial
+            # last chunk (4501 positions)
+            ((7, 9000), "float32"), ((3, 3, 8193), "float64")]
 
 
 @pytest.mark.parametrize("shape,dtype", TARGETED,
