@@ -110,9 +110,13 @@ mgrg_status crc_tables_device(int device, const mgrg::CrcTables **out) {
   return MGRG_OK;
 }
 
+// lane-private-table segment kernel (crc_blocks2_kernel); MGRG_CRC_V2=0
+// selects the shared-table kernel (A/B)
+int g_crc_v2 = knob("MGRG_CRC_V2", 1);
+
 uint64_t crc_scratch_words(uint64_t n) {
   const uint64_t nblk = n / 512 + 1;
-  return (nblk + mgrg::kCrcSegBlocks - 1) / mgrg::kCrcSegBlocks + 1;
+  return (nblk >> mgrg::kCrcSegMinLog) + 2;
 }
 
 // CRC-32 of n device bytes at d into *d_out (device), stream-ordered;
@@ -122,14 +126,46 @@ mgrg_status crc32_launch(const uint8_t *d, uint64_t n, uint32_t *d_out, uint32_t
   const uint64_t head = std::min<uint64_t>(n, (16 - (reinterpret_cast<uintptr_t>(d) & 15)) & 15);
   const uint64_t nblk = (n - head) / 512;
   const uint64_t tail = n - head - nblk * 512;
-  const uint64_t nseg = (nblk + mgrg::kCrcSegBlocks - 1) / mgrg::kCrcSegBlocks;
-  if (nblk)
-    mgrg::crc_blocks_kernel<<<unsigned(std::min<uint64_t>(
-                                  (nseg + mgrg::kCrcWarps - 1) / mgrg::kCrcWarps, 148 * 6)),
-                              32 * mgrg::kCrcWarps, 0, s>>>(
-        reinterpret_cast<const uint4 *>(d + head), nblk, T, d_seg);
-  mgrg::crc_combine_kernel<<<1, mgrg::kCrcRuns, 0, s>>>(
-      d_seg, nseg, nblk, d, uint32_t(head), d + head + nblk * 512, uint32_t(tail),
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  // segment length: the largest power of two (8..256 blocks) that still gives
+  // every warp of a full wave a segment (small ranges: short serial Horner
+  // chains; large ones: few segment values to combine)
+  const bool v2 = g_crc_v2 && nblk >= (uint64_t(1) << 16);
+  const uint64_t warps = uint64_t(sms) * (v2 ? mgrg::kCrc2Warps : 6 * mgrg::kCrcWarps);
+  int seglog = mgrg::kCrcSegMaxLog;
+  while (seglog > mgrg::kCrcSegMinLog && (nblk >> seglog) < warps)
+    --seglog;
+  const uint64_t nseg = (nblk + (uint64_t(1) << seglog) - 1) >> seglog;
+  if (nblk) {
+    // (per call: the attribute belongs to the current device's context)
+    const bool attr = cudaFuncSetAttribute(mgrg::crc_blocks2_kernel,
+                                           cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           int(mgrg::crc2_smem())) == cudaSuccess;
+    // the lane-private tables cost ~10 us to stage per launch: small ranges
+    // keep the shared-table kernel
+    if (attr && v2) {
+      mgrg::crc_blocks2_kernel<<<unsigned(std::min<uint64_t>(
+                                     (nseg + mgrg::kCrc2Warps - 1) / mgrg::kCrc2Warps,
+                                     uint64_t(sms))),
+                                 32 * mgrg::kCrc2Warps, mgrg::crc2_smem(), s>>>(
+          reinterpret_cast<const uint4 *>(d + head), nblk, seglog, T, d_seg);
+    } else {
+      mgrg::crc_blocks_kernel<<<unsigned(std::min<uint64_t>(
+                                    (nseg + mgrg::kCrcWarps - 1) / mgrg::kCrcWarps,
+                                    uint64_t(sms) * 6)),
+                                32 * mgrg::kCrcWarps, 0, s>>>(
+          reinterpret_cast<const uint4 *>(d + head), nblk, seglog, T, d_seg);
+    }
+  }
+  const bool cattr =
+      cudaFuncSetAttribute(mgrg::crc_combine_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           int(mgrg::crc_combine_smem())) == cudaSuccess;
+  if (!cattr)
+    return fail(MGRG_CUDA_ERROR, "crc combine: shared memory attribute");
+  mgrg::crc_combine_kernel<<<1, mgrg::kCrcRuns, mgrg::crc_combine_smem(), s>>>(
+      d_seg, nseg, nblk, seglog, d, uint32_t(head), d + head + nblk * 512, uint32_t(tail),
       crc_zbytes(n, 0xFFFFFFFFu), T, d_out);
   CUDA_TRY(cudaGetLastError());
   return MGRG_OK;
