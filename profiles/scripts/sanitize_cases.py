@@ -53,7 +53,13 @@ CASES = [
     ((9, 5, 1073), "float64", True, True),
     ((5, 3, 4097), "float32", False, True),
     ((33, 65, 257), "float64", False, True),
+    # round 2 (late): two-pass long strided fibers (thomas_2pass.cuh), DIM 1
+    # and DIM 2, incl. a partial last chunk
+    ((9, 8193), "float64", False, True),
+    ((3, 3, 8193), "float32", True, True),
+    ((7, 9000), "float32", False, True),
 ]
+NEW = CASES[-3:]
 if quick:
     CASES = CASES[:4] + CASES[8:9] + CASES[17:18]
 
@@ -133,9 +139,27 @@ def run_host(shape, dt, fast):
     plan.close()
 
 
-for c in CASES:
+def run_crc():
+    """GPU CRC-32 on a range long enough for the lane-private-table kernel
+    (>= 2^16 blocks) plus the tree combine, against zlib."""
+    import zlib
+
+    from paper_2105_12764_b200 import crc32
+
+    n = (1 << 16) * 512 + 4 * 1000 + 12  # + a partial segment and a tail
+    x = torch.from_numpy(rng.integers(0, 256, n, dtype=np.uint8)).to(dev)
+    for a in (0, 5):
+        assert crc32(x[a:]) == zlib.crc32(x[a:].cpu().numpy().tobytes())
+
+
+only_new = os.environ.get("SAN_ONLY_NEW") == "1"
+for c in (NEW if only_new else CASES):
     run_case(*c)
     print("ok", c, flush=True)
+run_crc()
+print("ok crc", flush=True)
+if only_new:
+    sys.exit(0)
 for shp, dt, fast in (((129, 129, 257), "float32", True), ((129, 129, 257), "float32", False),
                       ((33, 17, 9), "float64", True)):
     run_host(shp, dt, fast)
