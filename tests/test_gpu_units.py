@@ -118,3 +118,28 @@ def test_spatiotemporal_matches_reference(case):
     err = np.abs(np.asarray(back.values).reshape(-1) - case["values"]).max()
     tol = 1e-4 if case["values"].dtype == np.float32 else 1e-12
     assert err <= tol * (np.ptp(case["values"]) or 1.0)
+
+
+@pytest.mark.parametrize("dtype", ["float64", "float32"])
+@pytest.mark.parametrize("n", [1, 255, 256, 257, 100003])
+def test_apply_correction_matches_reference(dtype, n):
+    """apply_correction (kernels.hpp:451-464): values += z for sign >= 0,
+    values -= z otherwise, one IEEE add / subtract per node (numpy's are the
+    same round-to-nearest operations); length mismatch is ShapeError."""
+    import torch
+
+    from paper_2105_12764_b200 import Plan
+    from paper_2105_12764_b200.errors import ShapeError
+
+    rng = np.random.default_rng(n)
+    plan = Plan((9, 9), dtype)
+    v = rng.standard_normal(n).astype(dtype)
+    z = rng.standard_normal(n).astype(dtype)
+    for sign, ref in ((1, v + z), (0, v + z), (-1, v - z), (-7, v - z)):
+        d = torch.from_numpy(v.copy()).cuda()
+        plan.apply_correction(d, torch.from_numpy(z).cuda(), sign)
+        assert np.array_equal(d.cpu().numpy(), ref), sign
+    with pytest.raises(ShapeError, match="does not match"):
+        plan.apply_correction(torch.from_numpy(v).cuda(), torch.from_numpy(z[:-1].copy()).cuda()
+                              if n > 1 else torch.zeros(2, dtype=getattr(torch, dtype)).cuda())
+    plan.close()
