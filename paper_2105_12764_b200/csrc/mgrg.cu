@@ -1121,11 +1121,14 @@ template <typename R> void set_tf_attrs() {
 template <typename R>
 void launch_thomas(bool fast, const LevelGeom<R> &g, const ThomasGeom<R> &t,
                    const ThomasLean<R> &tl, int kd, R *f, Epi epi, const R *base, R *out,
-                   cudaStream_t s, const ThomasTP<R> *tp = nullptr) {
+                   cudaStream_t s, const ThomasTP<R> *tp = nullptr,
+                   uint64_t *extra_launches = nullptr) {
   const uint64_t mx = g.m[0], my = g.m[1], mz = g.m[2];
   if (fast && kd != 0 && tp && tp->q && tp->scratch && tp->m >= uint32_t(g_tp_min)) {
     const uint64_t nfib = kd == 0 ? my * mz : (kd == 1 ? mx * mz : mx * my);
     launch_tp<R>(kd, *tp, tp->scratch, nfib, uint32_t(mx), uint32_t(my), epi, base, out, f, s);
+    if (extra_launches)
+      *extra_launches += 2; // three kernels for one counted solve
     return;
   }
   if (fast && tl.tab && tf_ch<R>(tl.m, kd) && tf_launch_smem<R>(kd, tl.m) <= tf_limit<R>() &&
@@ -1427,7 +1430,8 @@ mgrg_status run_decompose(mgrg_plan *p, const R *d_in, R *d_cls, cudaStream_t s,
       if (mgrg_status st = rec.begin(MGRG_K_THOMAS_X + kd, l, es * Cn * (last ? 3 : 2)))
         return st;
       launch_thomas<R>(p->fast, g, P.thom[l][kd], P.tlean[l][kd], kd, F,
-                       last ? Epi::add : Epi::none, Pout, Pout, s, &P.ttp[l][kd]);
+                       last ? Epi::add : Epi::none, Pout, Pout, s, &P.ttp[l][kd],
+                       &rec.launches);
       if (mgrg_status st = rec.end())
         return st;
     }
@@ -1481,7 +1485,8 @@ mgrg_status run_recompose(mgrg_plan *p, const R *d_cls, int k, R *d_out,
         if (mgrg_status st = rec.begin(MGRG_K_THOMAS_X + kd, l, es * Cn * (last ? 3 : 2)))
           return st;
         launch_thomas<R>(p->fast, g, P.thom[l][kd], P.tlean[l][kd], kd, F,
-                         last ? Epi::sub : Epi::none, prev, F, s, &P.ttp[l][kd]);
+                         last ? Epi::sub : Epi::none, prev, F, s, &P.ttp[l][kd],
+                         &rec.launches);
         if (mgrg_status st = rec.end())
           return st;
       }
