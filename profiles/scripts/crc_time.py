@@ -18,15 +18,18 @@ out = {"bytes": nbytes}
 for name, fn in (("class_crc32_all", lambda: plan.class_crc32(c)), ("crc32_one_range", lambda: crc32(c))):
     fn()
     torch.cuda.synchronize()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    reps = 10
-    e0.record()
-    for _ in range(reps):
+    ts = []
+    for _ in range(10):  # per call: each call ends in a host sync (CRCs to the host)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
         fn()
-    e1.record()
-    torch.cuda.synchronize()
-    ms = e0.elapsed_time(e1) / reps
-    out[name] = {"ms": round(ms, 3), "GBps": round(nbytes / ms / 1e6, 1)}
+        e1.record()
+        torch.cuda.synchronize()
+        ts.append(e0.elapsed_time(e1))
+    ts.sort()
+    ms = ts[len(ts) // 2]
+    out[name] = {"ms_median": round(ms, 3), "ms_min": round(ts[0], 3), "ms_max": round(ts[-1], 3),
+                 "GBps_median": round(nbytes / ms / 1e6, 1)}
 pre = c[: (64 << 20) // 4]
 out["zlib_match_64MiB"] = crc32(pre) == zlib.crc32(pre.cpu().numpy().tobytes())
 for a, b in ((0, 12345677), (0, 12345805), (3, 12345805), (1, 200), (0, 128 * 64 + 128)):
