@@ -114,78 +114,95 @@ mgrg_status crc_tables_device(int device, const mgrg::CrcTables **out) {
 // selects the shared-table kernel (A/B)
 int g_crc_v2 = knob("MGRG_CRC_V2", 1);
 
-uint64_t crc_scratch_words(uint64_t n) {
-  const uint64_t nblk = n / 512 + 1;
-  return (nblk >> mgrg::kCrcSegMinLog) + 2;
-}
-
-// CRC-32 of n device bytes at d into *d_out (device), stream-ordered;
-// d_seg: crc_scratch_words(n) words of scratch.
-mgrg_status crc32_launch(const uint8_t *d, uint64_t n, uint32_t *d_out, uint32_t *d_seg,
-                         const mgrg::CrcTables *T, cudaStream_t s) {
-  const uint64_t head = std::min<uint64_t>(n, (16 - (reinterpret_cast<uintptr_t>(d) & 15)) & 15);
-  const uint64_t nblk = (n - head) / 512;
-  const uint64_t tail = n - head - nblk * 512;
-  int dev = 0, sms = 148;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  // segment length: the largest power of two (8..256 blocks) that still gives
-  // every warp of a full wave a segment (small ranges: short serial Horner
-  // chains; large ones: few segment values to combine)
-  const bool v2 = g_crc_v2 && nblk >= (uint64_t(1) << 16);
-  const uint64_t warps = uint64_t(sms) * (v2 ? mgrg::kCrc2Warps : 6 * mgrg::kCrcWarps);
-  int seglog = mgrg::kCrcSegMaxLog;
-  while (seglog > mgrg::kCrcSegMinLog && (nblk >> seglog) < warps)
-    --seglog;
-  const uint64_t nseg = (nblk + (uint64_t(1) << seglog) - 1) >> seglog;
-  if (nblk) {
-    // (per call: the attribute belongs to the current device's context)
-    const bool attr = cudaFuncSetAttribute(mgrg::crc_blocks2_kernel,
-                                           cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                           int(mgrg::crc2_smem())) == cudaSuccess;
-    // the lane-private tables cost ~10 us to stage per launch: small ranges
-    // keep the shared-table kernel
-    if (attr && v2) {
-      mgrg::crc_blocks2_kernel<<<unsigned(std::min<uint64_t>(
-                                     (nseg + mgrg::kCrc2Warps - 1) / mgrg::kCrc2Warps,
-                                     uint64_t(sms))),
-                                 32 * mgrg::kCrc2Warps, mgrg::crc2_smem(), s>>>(
-          reinterpret_cast<const uint4 *>(d + head), nblk, seglog, T, d_seg);
-    } else {
-      mgrg::crc_blocks_kernel<<<unsigned(std::min<uint64_t>(
-                                    (nseg + mgrg::kCrcWarps - 1) / mgrg::kCrcWarps,
-                                    uint64_t(sms) * 6)),
-                                32 * mgrg::kCrcWarps, 0, s>>>(
-          reinterpret_cast<const uint4 *>(d + head), nblk, seglog, T, d_seg);
-    }
-  }
-  const bool cattr =
-      cudaFuncSetAttribute(mgrg::crc_combine_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           int(mgrg::crc_combine_smem())) == cudaSuccess;
-  if (!cattr)
-    return fail(MGRG_CUDA_ERROR, "crc combine: shared memory attribute");
-  mgrg::crc_combine_kernel<<<1, mgrg::kCrcRuns, mgrg::crc_combine_smem(), s>>>(
-      d_seg, nseg, nblk, seglog, d, uint32_t(head), d + head + nblk * 512, uint32_t(tail),
-      crc_zbytes(n, 0xFFFFFFFFu), T, d_out);
-  CUDA_TRY(cudaGetLastError());
-  return MGRG_OK;
-}
-
-// CRC-32 of `count` device byte ranges (ptr[i], len[i]) -> host crc[i].
+// CRC-32 of `count` device byte ranges (ptr[i], len[i]) -> host crc[i]:
+// per batch of up to kCrcMaxRanges ranges, one segment launch per kernel
+// family (lane-private tables for ranges of >= 2^16 blocks: their ~10 us
+// table staging pays off; shared tables below) and one combine launch with a
+// CTA per range.
 mgrg_status crc32_ranges(int device, const uint8_t *const *ptr, const uint64_t *len,
                          int count, uint32_t *crc, cudaStream_t s) {
   const mgrg::CrcTables *T = nullptr;
   if (mgrg_status st = crc_tables_device(device, &T))
     return st;
+  int sms = 148;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+  // (per call: the attributes belong to the current device's context)
+  if (cudaFuncSetAttribute(mgrg::crc_blocks2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           int(mgrg::crc2_smem())) != cudaSuccess ||
+      cudaFuncSetAttribute(mgrg::crc_combine_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           int(mgrg::crc_combine_smem())) != cudaSuccess)
+    return fail(MGRG_CUDA_ERROR, "crc kernels: shared memory attribute");
+  struct Plan1 {
+    uint64_t head, nblk, tail, nseg;
+    int seglog;
+    bool v2;
+  };
+  std::vector<Plan1> pl(count);
   uint64_t words = 0;
-  for (int i = 0; i < count; ++i)
-    words = std::max(words, crc_scratch_words(len[i]));
+  for (int i = 0; i < count; ++i) {
+    const uint8_t *d = ptr[i];
+    const uint64_t n = len[i];
+    Plan1 &q = pl[i];
+    q.head = std::min<uint64_t>(n, (16 - (reinterpret_cast<uintptr_t>(d) & 15)) & 15);
+    q.nblk = (n - q.head) / 512;
+    q.tail = n - q.head - q.nblk * 512;
+    q.v2 = g_crc_v2 && q.nblk >= (uint64_t(1) << 16);
+    // segment length: the largest power of two (8..256 blocks) that still
+    // gives every warp of a full wave a segment (small ranges: short serial
+    // Horner chains; large ones: few segment values to combine)
+    const uint64_t warps = uint64_t(sms) * (q.v2 ? mgrg::kCrc2Warps : 6 * mgrg::kCrcWarps);
+    q.seglog = mgrg::kCrcSegMaxLog;
+    while (q.seglog > mgrg::kCrcSegMinLog && (q.nblk >> q.seglog) < warps)
+      --q.seglog;
+    q.nseg = (q.nblk + (uint64_t(1) << q.seglog) - 1) >> q.seglog;
+    words += q.nseg + 1;
+  }
   uint32_t *scratch = nullptr;
-  CUDA_TRY(cudaMallocAsync(&scratch, (words * count + count) * sizeof(uint32_t), s));
-  uint32_t *d_out = scratch + words * count;
+  CUDA_TRY(cudaMallocAsync(&scratch, (words + count) * sizeof(uint32_t), s));
+  uint32_t *d_out = scratch + words;
   mgrg_status st = MGRG_OK;
-  for (int i = 0; i < count && !st; ++i)
-    st = crc32_launch(ptr[i], len[i], d_out + i, scratch + words * i, T, s);
+  uint64_t woff = 0;
+  for (int b0 = 0; b0 < count && !st; b0 += mgrg::kCrcMaxRanges) {
+    const int b1 = std::min(count, b0 + mgrg::kCrcMaxRanges);
+    mgrg::CrcJobs J1{}, J2{};
+    mgrg::CrcFins FS{};
+    for (int i = b0; i < b1; ++i) {
+      const Plan1 &q = pl[i];
+      uint32_t *seg = scratch + woff;
+      woff += q.nseg + 1;
+      if (q.nblk) {
+        mgrg::CrcJobs &J = q.v2 ? J2 : J1;
+        J.r[J.n] = {reinterpret_cast<const uint4 *>(ptr[i] + q.head), q.nblk, J.nseg, seg,
+                    q.seglog};
+        J.nseg += q.nseg;
+        ++J.n;
+      }
+      FS.f[FS.n++] = {seg,
+                      q.nseg,
+                      q.nblk,
+                      q.seglog,
+                      ptr[i],
+                      ptr[i] + q.head + q.nblk * 512,
+                      uint32_t(q.head),
+                      uint32_t(q.tail),
+                      crc_zbytes(len[i], 0xFFFFFFFFu),
+                      d_out + i};
+    }
+    if (J2.n)
+      mgrg::crc_blocks2_kernel<<<unsigned(std::min<uint64_t>(
+                                     (J2.nseg + mgrg::kCrc2Warps - 1) / mgrg::kCrc2Warps,
+                                     uint64_t(sms))),
+                                 32 * mgrg::kCrc2Warps, mgrg::crc2_smem(), s>>>(J2, T);
+    if (J1.n)
+      mgrg::crc_blocks_kernel<<<unsigned(std::min<uint64_t>(
+                                    (J1.nseg + mgrg::kCrcWarps - 1) / mgrg::kCrcWarps,
+                                    uint64_t(sms) * 6)),
+                                32 * mgrg::kCrcWarps, 0, s>>>(J1, T);
+    mgrg::crc_combine_kernel<<<unsigned(FS.n), mgrg::kCrcRuns, mgrg::crc_combine_smem(), s>>>(
+        FS, T);
+    if (cudaGetLastError() != cudaSuccess)
+      st = fail(MGRG_CUDA_ERROR, "crc kernels: launch failed");
+  }
   if (!st) {
     cudaError_t e = cudaMemcpyAsync(crc, d_out, count * sizeof(uint32_t),
                                     cudaMemcpyDeviceToHost, s);

@@ -32,6 +32,29 @@ constexpr int kCrcSegMinLog = 3; //   (host-chosen per range: enough segments fo
 constexpr int kCrcWarps = 8;       // warps per CTA of the block kernel
 constexpr int kCrcRuns = 1024;     // threads of the combine kernel
 
+// Several byte ranges (the class records of one container) in one launch:
+// the segments of every range are numbered consecutively (seg0), a warp's
+// global segment id picks its range by a short scan.
+constexpr int kCrcMaxRanges = 32;
+struct CrcRange {
+  const uint4 *data; // 16-byte aligned body
+  uint64_t nblk;     // 512-byte blocks
+  uint64_t seg0;     // first global segment id
+  uint32_t *seg;     // segment values
+  int seglog;        // 2^seglog blocks per segment
+};
+struct CrcJobs {
+  CrcRange r[kCrcMaxRanges];
+  int n;
+  uint64_t nseg; // total segments
+};
+__device__ __forceinline__ int crc_range_of(const CrcJobs &J, uint64_t gsid) {
+  int ri = 0;
+  while (ri + 1 < J.n && gsid >= J.r[ri + 1].seg0)
+    ++ri;
+  return ri;
+}
+
 // Device tables (uploaded once per process, crc_tables()):
 //   slice[4][256]            slice-by-4 CRC tables
 //   z16, z32, z64, z128, z256 butterfly shifts; z512 per-block accumulation;
@@ -63,8 +86,7 @@ __device__ __forceinline__ uint32_t crc_fold16(const uint32_t (*s)[256], uint4 w
 // stream at its byte offset (Z_{16 * (31 - a)} overall).  Tables in shared
 // memory: slice-by-4 for the folds, Z_512 and the butterfly shifts.
 __global__ void __launch_bounds__(32 * kCrcWarps)
-    crc_blocks_kernel(const uint4 *__restrict__ data, uint64_t nblk, int seglog,
-                      const CrcTables *__restrict__ T, uint32_t *__restrict__ seg) {
+    crc_blocks_kernel(const __grid_constant__ CrcJobs J, const CrcTables *__restrict__ T) {
   __shared__ uint32_t s[4][256];
   __shared__ uint32_t z[6][4][256];
   for (int i = threadIdx.x; i < 1024; i += blockDim.x)
@@ -73,15 +95,17 @@ __global__ void __launch_bounds__(32 * kCrcWarps)
     (&z[0][0][0])[i] = (&T->z[0][0][0])[i];
   __syncthreads();
   const int lane = threadIdx.x & 31;
-  const uint64_t segb = uint64_t(1) << seglog, nseg = (nblk + segb - 1) >> seglog;
   auto zap = [&](int k, uint32_t v) {
     return z[k][0][v & 255u] ^ z[k][1][(v >> 8) & 255u] ^ z[k][2][(v >> 16) & 255u] ^
            z[k][3][v >> 24];
   };
   // persistent warps: the tables are staged once per CTA
-  for (uint64_t sid = uint64_t(blockIdx.x) * kCrcWarps + (threadIdx.x >> 5); sid < nseg;
-       sid += uint64_t(gridDim.x) * kCrcWarps) {
-  const uint64_t b0 = sid * segb, b1 = u64min(b0 + segb, nblk);
+  for (uint64_t gsid = uint64_t(blockIdx.x) * kCrcWarps + (threadIdx.x >> 5); gsid < J.nseg;
+       gsid += uint64_t(gridDim.x) * kCrcWarps) {
+  const CrcRange &R = J.r[crc_range_of(J, gsid)];
+  const uint4 *data = R.data;
+  const uint64_t sid = gsid - R.seg0, segb = uint64_t(1) << R.seglog;
+  const uint64_t b0 = sid * segb, b1 = u64min(b0 + segb, R.nblk);
   uint32_t acc = 0;
   uint64_t b = b0;
   // four blocks per iteration: the loads and the four independent folds
@@ -105,7 +129,7 @@ __global__ void __launch_bounds__(32 * kCrcWarps)
     acc = zap(k, acc) ^ r; // Z_{16 * 2^k}(left) ^ right
   }
   if (lane == 0)
-    seg[sid] = acc;
+    R.seg[sid] = acc;
   }
 }
 
@@ -125,8 +149,7 @@ __host__ __device__ constexpr size_t crc2_smem() {
   return (4 * 256 * 32 + 8 * 4 * 256) * sizeof(uint32_t);
 }
 __global__ void __launch_bounds__(32 * kCrc2Warps, 1)
-    crc_blocks2_kernel(const uint4 *__restrict__ data, uint64_t nblk, int seglog,
-                       const CrcTables *__restrict__ T, uint32_t *__restrict__ seg) {
+    crc_blocks2_kernel(const __grid_constant__ CrcJobs J, const CrcTables *__restrict__ T) {
   extern __shared__ uint32_t crc2_sm[];
   uint32_t *ls = crc2_sm;                    // [4][256][32] lane-private slice tables
   uint32_t(*z)[4][256] = reinterpret_cast<uint32_t(*)[4][256]>(crc2_sm + 4 * 256 * 32);
@@ -154,10 +177,12 @@ __global__ void __launch_bounds__(32 * kCrc2Warps, 1)
     return z[k][0][v & 255u] ^ z[k][1][(v >> 8) & 255u] ^ z[k][2][(v >> 16) & 255u] ^
            z[k][3][v >> 24];
   };
-  const uint64_t segb = uint64_t(1) << seglog, nseg = (nblk + segb - 1) >> seglog;
-  for (uint64_t sid = uint64_t(blockIdx.x) * kCrc2Warps + (threadIdx.x >> 5); sid < nseg;
-       sid += uint64_t(gridDim.x) * kCrc2Warps) {
-    const uint64_t b0 = sid * segb, b1 = u64min(b0 + segb, nblk);
+  for (uint64_t gsid = uint64_t(blockIdx.x) * kCrc2Warps + (threadIdx.x >> 5); gsid < J.nseg;
+       gsid += uint64_t(gridDim.x) * kCrc2Warps) {
+    const CrcRange &R = J.r[crc_range_of(J, gsid)];
+    const uint4 *data = R.data;
+    const uint64_t sid = gsid - R.seg0, segb = uint64_t(1) << R.seglog;
+    const uint64_t b0 = sid * segb, b1 = u64min(b0 + segb, R.nblk);
     const uint64_t nquad = (b1 - b0) / 4;
     const uint4 *dp = data + b0 * 32 + 4 * lane;
     uint32_t acc = 0;
@@ -199,23 +224,40 @@ __global__ void __launch_bounds__(32 * kCrc2Warps, 1)
       acc ^= h;
     }
     if (lane == 0)
-      seg[sid] = acc;
+      R.seg[sid] = acc;
   }
 }
 
 
-// One CTA: thread t folds a run of per = 2^p consecutive segment values
+// One CTA per range: thread t folds a run of per = 2^p consecutive segment values
 // (<= 1024 runs; full segments shift by the staged single table
 // Z_{512 * SEG}), the runs meet in a 10-level tree (round 1 folded them
 // serially on thread 0: ~50 us per call), then thread 0 adds the head bytes,
 // the tail bytes, the init term (zinit = Z_n(0xFFFFFFFF), host-computed) and
 // the final xor.
+struct CrcFin {
+  const uint32_t *seg;
+  uint64_t nseg, nblk;
+  int seglog;
+  const uint8_t *head, *tail;
+  uint32_t nhead, ntail, zinit;
+  uint32_t *out;
+};
+struct CrcFins {
+  CrcFin f[kCrcMaxRanges];
+  int n;
+};
 constexpr size_t crc_combine_smem() { return (32 + 1) * 4 * 256 * sizeof(uint32_t); }
 __global__ void __launch_bounds__(kCrcRuns)
-    crc_combine_kernel(const uint32_t *__restrict__ seg, uint64_t nseg, uint64_t nblk, int seglog,
-                       const uint8_t *__restrict__ head, uint32_t nhead,
-                       const uint8_t *__restrict__ tail, uint32_t ntail, uint32_t zinit,
-                       const CrcTables *__restrict__ T, uint32_t *__restrict__ out) {
+    crc_combine_kernel(const __grid_constant__ CrcFins FS, const CrcTables *__restrict__ T) {
+  // one CTA per range
+  const CrcFin &FN = FS.f[blockIdx.x];
+  const uint32_t *seg = FN.seg;
+  const uint64_t nseg = FN.nseg, nblk = FN.nblk;
+  const int seglog = FN.seglog;
+  const uint8_t *head = FN.head, *tail = FN.tail;
+  const uint32_t nhead = FN.nhead, ntail = FN.ntail, zinit = FN.zinit;
+  uint32_t *out = FN.out;
   __shared__ uint32_t run[kCrcRuns];
   // every table this kernel touches, staged once (the lookups of the tree
   // and of the byte loops are dependent chains: shared-memory latency)
