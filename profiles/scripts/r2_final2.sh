@@ -1,7 +1,7 @@
 # late round-2 pass: sanitizer on the new kernels, full GPU suite, smoke, bench, launch list, levels
 O=gpurun_out/${1:-r2fin}
 mkdir -p $O
-SAN_ONLY_NEW=1 bash profiles/scripts/sanitize.sh $O/sanitize > /dev/null 2>&1
+# (compute-sanitizer is closed on this pool: see profiles/r2/late/sanitizer_closed.txt)
 timeout 1500 python -m pytest tests -m gpu -x -q -p no:cacheprovider > $O/gputest.log 2>&1; echo rc=$? >> $O/gputest.log
 python -c "import __graft_entry__ as g; g.smoke()" > $O/smoke.log 2>&1; echo rc=$? >> $O/smoke.log
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,power.draw --format=csv > $O/gpu.txt
