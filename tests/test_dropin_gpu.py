@@ -139,7 +139,8 @@ def test_coop_schedule_matches_runtime_rule():
 
 @pytest.mark.parametrize("shape,dt,fast", [((65, 33, 17), "float32", True),
                                            ((33, 17, 9), "float64", False),
-                                           ((257, 129), "float64", True)])
+                                           ((257, 129), "float64", True),
+                                           ((9, 8193), "float64", True)])  # two-pass solve
 def test_graph_replay_identical(shape, dt, fast):
     """mgrg_plan_set_graphs: captured-graph replay gives the same bits as the
     stream launches, for repeated calls, a second buffer set (new capture)
@@ -293,4 +294,26 @@ def test_split_host_calls(shape):
     _lib.check(lib.mgrg_host_abort(plan._h))
     out = np.empty_like(v)
     _lib.check(lib.mgrg_recompose_host(plan._h, ref.ctypes.data, L, out.ctypes.data))
+    plan.close()
+
+
+def test_two_pass_solve_launch_count():
+    """A FAST y solve of >= 4097 positions runs as three kernels (pass 1,
+    carry scan, pass 2: csrc/thomas_2pass.cuh) and the plan's launch count
+    includes them: one profile record per counted launch, plus two for the
+    (9, 8193) decompose's single two-pass solve (the top level's y fibers)."""
+    import torch
+
+    from paper_2105_12764_b200 import Plan
+
+    v = torch.rand(9 * 8193, dtype=torch.float64, device="cuda")
+    plan = Plan((9, 8193), "float64", fast=True)
+    c = plan.decompose(v)
+    plan.set_profiling(True)
+    plan.decompose(v, c)
+    torch.cuda.synchronize()
+    recs = plan.profile(reset=True)
+    # one profile record per counted solve / level kernel; the top level's y
+    # solve (m = 4097) adds two kernels to the count
+    assert plan.last_launches == len(recs) + 2
     plan.close()
